@@ -1,0 +1,232 @@
+/*
+ * mpm_capi.h -- C ABI of the B200-native MPM one-step operator Phi = G2P o U o P2G and
+ * its reverse-mode adjoint (libmpm_b200.so).
+ *
+ * The reference (/root/reference/proj, "arxiv/paper_2507_04192") is a header-only C++20
+ * template library in namespace mpm with no ABI (proj/CMakeLists.txt:13-15 builds a static
+ * lib holding only src/hash.cpp). Each entry point below is the plain-pointer form of one
+ * reference API; the C++ drop-in layer (include/mpm_gpu/) converts the reference's own
+ * Scene/SimState/StateCotangent/ParamGrads/Grid types into these views, so existing callers
+ * compile unchanged. The reference interface each call replaces is cited beside it.
+ *
+ * Conventions
+ *  - Scalars in views are T = float (MPM_F32) or double (MPM_F64), chosen at ctx creation.
+ *  - Host arrays use the reference's in-memory layout (std::vector<Eigen::Matrix>):
+ *      vectors   T[n][dim]
+ *      matrices  T[n][dim*dim], each matrix COLUMN-MAJOR (Eigen default)
+ *    so a std::vector<Vec<T,dim>>::data() / std::vector<Mat<T,dim>>::data() can be passed
+ *    directly (state.hpp:17-63, adjoint.hpp:10-72).
+ *  - Particles are addressed by their index in the host arrays (the reference's particle
+ *    id). The device keeps its own cell-sorted order and maps back at this boundary.
+ *  - Every call is synchronous at return (reference semantics); the context owns a CUDA
+ *    stream and all device buffers. One context per host thread.
+ *  - Errors: int status (below) + mpm_last_error(). The C++ layer rethrows the reference
+ *    exception types (common.hpp:22-36): 2 -> ValidationError, 3 -> NumericalError,
+ *    4 -> OutOfDomainError{particle}, 5 -> NumericalError("checkpoint mismatch ...").
+ *  - There is NO CPU fallback: without a usable sm_100 device, mpm_ctx_create fails with
+ *    MPM_ERR_CUDA.
+ */
+#ifndef MPM_CAPI_H
+#define MPM_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPM_CAPI_VERSION 1
+
+/* dtype tags */
+enum { MPM_F32 = 0, MPM_F64 = 1 };
+
+/* status codes (common.hpp:22-36 exit-code convention, extended) */
+enum {
+    MPM_OK = 0,
+    MPM_ERR_USAGE = 1,         /* bad arguments to this ABI */
+    MPM_ERR_VALIDATION = 2,    /* ValidationError */
+    MPM_ERR_NUMERICAL = 3,     /* NumericalError */
+    MPM_ERR_OUT_OF_DOMAIN = 4, /* OutOfDomainError{particle} */
+    MPM_ERR_CHECKPOINT = 5,    /* checkpoint replay mismatch (checkpoint.hpp:124-126) */
+    MPM_ERR_CUDA = 6           /* device / CUDA / NCCL failure */
+};
+
+/* config.hpp:13 SchemeKind, same order */
+enum { MPM_SCHEME_PIC = 0, MPM_SCHEME_FLIP = 1, MPM_SCHEME_BLEND = 2, MPM_SCHEME_APIC = 3, MPM_SCHEME_TPIC = 4 };
+/* config.hpp:34 WallKind, same order */
+enum { MPM_WALL_SLIP = 0, MPM_WALL_NO_SLIP = 1, MPM_WALL_FIXED = 2, MPM_WALL_COULOMB = 3 };
+/* material.hpp:97 Material variant index */
+enum { MPM_MAT_FLUID = 0, MPM_MAT_DRUCKER_PRAGER = 1 };
+
+/* Scene<T,dim> (scene.hpp:9-16) minus the init-only geometry. All reals are passed as
+ * double and converted to T once (exact when the caller's Scene<T> holds T values). */
+typedef struct mpm_scene_desc {
+    int dim;             /* 2 or 3 */
+    int dtype;           /* MPM_F32 / MPM_F64 */
+    double dh;           /* SimConfig::dh */
+    int cells[3];        /* SimConfig::cells */
+    double origin[3];    /* SimConfig::origin */
+    double dt;           /* SimConfig::dt */
+    double gravity[3];   /* SimConfig::gravity */
+    int scheme;          /* TransferScheme::kind */
+    double alpha_flip;   /* TransferScheme::alpha_flip */
+    int track_def_grad;  /* SimConfig::track_def_grad */
+    int material;        /* MPM_MAT_* */
+    /* FluidParams (material.hpp:13-29) */
+    double rho0, viscosity, sound_speed;
+    int rate_form;
+    /* DruckerPragerParams (material.hpp:52-95), derived constants passed as stored */
+    double K, nu, G, phi, psi, cohesion, sigma_t, q_phi, k_phi, q_psi, tau_P, alpha_P;
+    /* BoundarySpec (config.hpp:45-57) */
+    int band_layers;
+    int wall_kind[6];           /* w = 2*axis + side */
+    int n_friction[6];          /* Coulomb segments per wall */
+    const double* friction[6];  /* n_friction[w] coefficients */
+    /* Obstacles (config.hpp:61-88): n_obstacles * (lo[dim], hi[dim]) */
+    int n_obstacles;
+    const double* obstacles;
+    double mass_epsilon;        /* Scene::mass_epsilon (set by init_scene) */
+} mpm_scene_desc;
+
+/* SimState<T,dim> (state.hpp:17-87) as host arrays; NULL = field absent. */
+typedef struct mpm_state_view {
+    int64_t n;
+    void* x;        /* [n][dim] */
+    void* v;        /* [n][dim] */
+    void* mass;     /* [n] */
+    void* volume;   /* [n] */
+    void* rho;      /* [n] */
+    void* eps_eq;   /* [n] */
+    void* sigma_zz; /* [n] (2-D only) */
+    void* sigma;    /* [n][dim*dim] col-major, symmetric */
+    void* grad_v;   /* [n][dim*dim] col-major */
+    void* affine;   /* [n][dim*dim] col-major, APIC only */
+    void* def_grad; /* [n][dim*dim] col-major, track_def_grad only */
+    int64_t step;
+    double time;
+} mpm_state_view;
+
+/* StateCotangent<T,dim> (adjoint.hpp:10-72); sigma/grad_v/affine are full matrices. */
+typedef struct mpm_cot_view {
+    int64_t n;
+    void* x;        /* [n][dim] */
+    void* v;        /* [n][dim] */
+    void* rho;      /* [n] */
+    void* volume;   /* [n] */
+    void* eps_eq;   /* [n] (discarded on input, zero on output) */
+    void* sigma_zz; /* [n] (2-D) */
+    void* sigma;    /* [n][dim*dim] */
+    void* grad_v;   /* [n][dim*dim] */
+    void* affine;   /* [n][dim*dim] (APIC) */
+} mpm_cot_view;
+
+/* ParamGrads<T,dim> (adjoint.hpp:77-90); ACCUMULATED into (+=) like the reference. */
+typedef struct mpm_param_grads {
+    double sound_speed;
+    double viscosity;
+    double* wall_friction[6]; /* n_friction[w] entries each (may be NULL if 0) */
+} mpm_param_grads;
+
+/* Grid<T,dim> (state.hpp:91-173), dense, row-major node index (last axis fastest). */
+typedef struct mpm_grid_view {
+    int64_t num_nodes;
+    void* mass;     /* [nodes] */
+    void* momentum; /* [nodes][dim] */
+    void* v_old;    /* [nodes][dim] */
+    void* v;        /* [nodes][dim] */
+    void* force;    /* [nodes][dim] */
+} mpm_grid_view;
+
+/* Built-in loss seeders for backprop_trajectory (checkpoint.hpp:63-66 Seeder protocol):
+ * masked Lagrangian least squares (SPEC.md observe_lagrangian + loss):
+ *   L = sum_{k<n_obs} sum_{l<n_sel} || z_{sel[l]}(obs_steps[k]) - target[k][l] ||^2,
+ * z = x (field 0) or v (field 1); sel = NULL means all particles in id order. */
+enum { MPM_SEEDER_NONE = 0, MPM_SEEDER_LAGRANGIAN_LS = 1 };
+typedef struct mpm_seeder_desc {
+    int kind;
+    int field;               /* 0 = x, 1 = v */
+    int n_obs;               /* number of observed steps */
+    const int64_t* obs_steps;
+    int64_t n_sel;
+    const int64_t* sel;      /* particle ids, or NULL = all */
+    const void* target;      /* T[n_obs][n_sel][dim] */
+} mpm_seeder_desc;
+
+/* BackpropResult (checkpoint.hpp:53-61) counters */
+typedef struct mpm_backprop_result {
+    double loss;
+    int64_t checkpoints_stored;
+    int64_t peak_replay_states;
+} mpm_backprop_result;
+
+/* advance flags */
+enum { MPM_ADV_NAN_GUARD = 1u /* run(): abort on non-finite state (stepper.hpp:107-109) */ };
+
+typedef struct mpm_ctx mpm_ctx;
+
+/* ---- context ---------------------------------------------------------------------- */
+/* Stepper<T,dim>::Stepper(const Scene&) (stepper.hpp:66-70): validates the scene and
+ * allocates device state, grid blocks, sort and workspace buffers for up to max_particles. */
+int mpm_ctx_create(const mpm_scene_desc* scene, int64_t max_particles, int device, mpm_ctx** out);
+void mpm_ctx_destroy(mpm_ctx* ctx);
+/* last error: code, offending particle id (-1), step (-1), message */
+int mpm_last_error(const mpm_ctx* ctx, int* code, int64_t* particle, int64_t* step, char* msg, size_t msg_len);
+int mpm_version(void);
+/* human-readable device name for logs */
+int mpm_device_name(char* buf, size_t len);
+
+/* ---- state transfer ------------------------------------------------------------------ */
+int mpm_state_upload(mpm_ctx* ctx, const mpm_state_view* s);
+int mpm_state_download(mpm_ctx* ctx, mpm_state_view* s);
+/* order-independent 64-bit digest of the device state (replaces SimState::hash at the
+ * checkpoint replay check, state.hpp:152-167 / checkpoint.hpp:124) */
+int mpm_state_digest(mpm_ctx* ctx, uint64_t* out);
+/* max_particle_speed (stepper.hpp:491-498) */
+int mpm_max_speed(mpm_ctx* ctx, double* vmax);
+
+/* ---- forward ------------------------------------------------------------------------ */
+/* n x Stepper::advance (stepper.hpp:472-482); MPM_ADV_NAN_GUARD adds run()'s all_finite
+ * check after every step (stepper.hpp:519-522). */
+int mpm_advance(mpm_ctx* ctx, int64_t n_steps, uint32_t flags);
+/* phase functions (each backs one reference free function, for per-phase parity):
+ * p2g (transfer.hpp:402-434), grid_momentum_update (transfer.hpp:440-449),
+ * apply_grid_corrections (contact.hpp:394-411), g2p (transfer.hpp:457-486),
+ * constitutive_update (stepper.hpp:428-456). */
+int mpm_p2g(mpm_ctx* ctx);
+int mpm_grid_momentum_update(mpm_ctx* ctx);
+int mpm_grid_corrections(mpm_ctx* ctx);
+int mpm_g2p(mpm_ctx* ctx);
+int mpm_constitutive(mpm_ctx* ctx);
+/* Stepper::grid (stepper.hpp:464) as a dense host grid, and the reverse for tests that
+ * drive the phase functions on a prescribed grid (test_contact.cpp, test_transfer.cpp). */
+int mpm_grid_download(mpm_ctx* ctx, mpm_grid_view* g);
+int mpm_grid_upload(mpm_ctx* ctx, const mpm_grid_view* g);
+
+/* ---- adjoint ------------------------------------------------------------------------ */
+/* step_vjp (adjoint.hpp:328-525): cot_in is OVERWRITTEN, pg is ACCUMULATED. */
+int mpm_step_vjp(mpm_ctx* ctx, const mpm_state_view* state_in, const mpm_cot_view* cot_out,
+                 mpm_cot_view* cot_in, mpm_param_grads* pg);
+/* backprop_trajectory (checkpoint.hpp:72-143) with CheckpointPlan::make(total_steps,
+ * n_segments) (checkpoint.hpp:15-34) and a built-in device seeder. */
+int mpm_backprop(mpm_ctx* ctx, const mpm_state_view* initial, int64_t total_steps, int n_segments,
+                 const mpm_seeder_desc* seeder, mpm_cot_view* initial_state_cot,
+                 mpm_param_grads* pg, mpm_backprop_result* result);
+
+/* ---- instrumentation (bench / tests) --------------------------------------------------- */
+/* enable per-kernel CUDA-event timing on the context stream */
+int mpm_profile_enable(mpm_ctx* ctx, int enable);
+/* total device time (ms) and launch count of kernels whose name contains `name` since the
+ * last reset; name = "" sums all kernels of this library */
+int mpm_profile_query(mpm_ctx* ctx, const char* name, double* ms, int64_t* launches);
+int mpm_profile_reset(mpm_ctx* ctx);
+/* number of this library's kernels launched on the context so far */
+int64_t mpm_launch_count(const mpm_ctx* ctx);
+/* number of active grid nodes (m > mass_epsilon) of the last P2G, and occupied blocks */
+int mpm_grid_stats(mpm_ctx* ctx, int64_t* active_nodes, int64_t* occupied_blocks, int64_t* active_node_blocks);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPM_CAPI_H */
