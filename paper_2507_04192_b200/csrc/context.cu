@@ -1,0 +1,941 @@
+// context.cu -- host runtime of libmpm_b200.so: device context, buffer ownership, step
+// orchestration (CUDA graph per step), error attribution and the C ABI (include/mpm_capi.h).
+//
+// The context is the device-side Stepper (stepper.hpp:462-483): it owns the particle state
+// (double-buffered SoA), the node-block grid, the sort / segment tables, the P2G partial tiles
+// and the adjoint workspace, all on one CUDA stream. Calls are synchronous at return.
+
+#include "../../include/mpm_capi.h"
+#include "common.cuh"
+#include "constit.cuh"
+#include "kernels_adj.cuh"
+#include "kernels_fwd.cuh"
+#include "kernels_util.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace mpmgpu;
+
+namespace {
+
+struct ApiError : std::runtime_error {
+    int code;
+    int64_t particle, step;
+    ApiError(int c, const std::string& m, int64_t p = -1, int64_t s = -1)
+        : std::runtime_error(m), code(c), particle(p), step(s)
+    {
+    }
+};
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            throw ApiError(MPM_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " \
+                                             + __FILE__ + ":" + std::to_string(__LINE__));         \
+    } while (0)
+
+struct ProfEvent {
+    const char* name;
+    cudaEvent_t a, b;
+};
+
+// ----------------------------------------------------------------------------------------
+struct CtxBase {
+    virtual ~CtxBase() = default;
+    virtual void upload(const mpm_state_view* s) = 0;
+    virtual void download(mpm_state_view* s) = 0;
+    virtual uint64_t digest() = 0;
+    virtual double max_speed() = 0;
+    virtual void advance(int64_t n, uint32_t flags) = 0;
+    virtual void phase_p2g() = 0;
+    virtual void phase_mom() = 0;
+    virtual void phase_corr() = 0;
+    virtual void phase_g2p() = 0;
+    virtual void phase_constit() = 0;
+    virtual void grid_download(mpm_grid_view* g) = 0;
+    virtual void grid_upload(const mpm_grid_view* g) = 0;
+    virtual void step_vjp(const mpm_state_view* s, const mpm_cot_view* co, mpm_cot_view* ci, mpm_param_grads* pg) = 0;
+    virtual void backprop(const mpm_state_view* s0, int64_t total, int nseg, const mpm_seeder_desc* sd,
+                          mpm_cot_view* c0, mpm_param_grads* pg, mpm_backprop_result* res) = 0;
+    virtual void grid_stats(int64_t* an, int64_t* ob, int64_t* anb) = 0;
+
+    // profiling
+    bool prof = false;
+    std::vector<ProfEvent> events;
+    std::vector<std::pair<std::string, std::pair<double, int64_t>>> prof_acc;
+    int64_t launches = 0;
+};
+
+template <class T> T* dalloc(size_t n)
+{
+    T* p = nullptr;
+    if (n == 0)
+        n = 1;
+    CK(cudaMalloc(&p, n * sizeof(T)));
+    return p;
+}
+
+template <class T, int D> struct Ctx : CtxBase {
+    using C = Cfg<D>;
+    DevScene<T, D> sc{};
+    mpm_scene_desc desc{};
+    cudaStream_t stream{};
+    int device = 0;
+    int64_t cap = 0, n = 0;
+    int64_t step = 0;
+    double time = 0;
+    bool has_aff = false, has_F = false;
+    std::vector<void*> allocs;
+
+    PBuf<T, D> buf[2]{};
+    int cur = 0;
+    int *keys = nullptr, *keys_sorted = nullptr, *perm = nullptr, *iota = nullptr;
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    int *bstart = nullptr, *bend = nullptr, *lstart = nullptr, *occ = nullptr, *act = nullptr, *counts = nullptr; // counts[0]=n_occ, [1]=n_act
+    unsigned char* nflag = nullptr;
+    int *d_nb = nullptr, *d_nnb = nullptr;
+    T* partials = nullptr;
+    GBuf<T, D> G{};
+    DevStatus* st = nullptr;
+    DevStatus* st_host = nullptr;
+    Stage<T, D> stage{};
+    T* stage_host = nullptr;
+    size_t stage_elems = 0;
+    unsigned long long* d_red = nullptr;
+    bool keys_valid = false;
+    bool grid_touched_all = false;
+    int nsm = 148;
+    int p2g_ctas_per_sm = 1;
+    AdjWork<T, D> aw{};
+
+    cudaGraphExec_t graphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}}; // [guard][cur]
+
+    template <class X> X* alloc(size_t k)
+    {
+        X* p = dalloc<X>(k);
+        allocs.push_back(p);
+        return p;
+    }
+
+    Ctx(const mpm_scene_desc* d, int64_t max_particles, int dev)
+    {
+        desc = *d;
+        device = dev;
+        CK(cudaSetDevice(dev));
+        cudaDeviceProp prop{};
+        CK(cudaGetDeviceProperties(&prop, dev));
+        if (prop.major < 10)
+            throw ApiError(MPM_ERR_CUDA, "libmpm_b200 requires an sm_100 (Blackwell) device; found " + std::string(prop.name));
+        nsm = prop.multiProcessorCount;
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        build_scene(d);
+        cap = max_particles;
+        has_aff = d->scheme == MPM_SCHEME_APIC;
+        has_F = d->track_def_grad != 0;
+        for (int b = 0; b < 2; ++b)
+            alloc_pbuf(buf[b]);
+        keys = alloc<int>(cap);
+        keys_sorted = alloc<int>(cap);
+        perm = alloc<int>(cap);
+        iota = alloc<int>(cap);
+        k_iota<<<unsigned((cap + 255) / 256), 256, 0, stream>>>(iota, int(cap));
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, keys, keys_sorted, iota, perm, int(cap), 0, 32, stream));
+        cub_tmp = alloc<unsigned char>(cub_bytes);
+        bstart = alloc<int>(sc.nb_total);
+        bend = alloc<int>(sc.nb_total);
+        lstart = alloc<int>((size_t)sc.nb_total * (C::B + 1));
+        occ = alloc<int>(sc.nb_total);
+        act = alloc<int>(sc.nnb_total);
+        counts = alloc<int>(4);
+        nflag = alloc<unsigned char>(sc.nnb_total);
+        d_nb = alloc<int>(D);
+        d_nnb = alloc<int>(D);
+        CK(cudaMemcpyAsync(d_nb, sc.nb, sizeof(int) * D, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(d_nnb, sc.nnb, sizeof(int) * D, cudaMemcpyHostToDevice, stream));
+        partials = alloc<T>((size_t)sc.nb_total * C::NF * C::TN);
+        const size_t nodes = (size_t)sc.nnb_total * C::NB;
+        G.m = alloc<T>(nodes);
+        for (int a = 0; a < D; ++a) {
+            G.p[a] = alloc<T>(nodes);
+            G.f[a] = alloc<T>(nodes);
+            G.v[a] = alloc<T>(nodes);
+            G.vold[a] = alloc<T>(nodes);
+        }
+        zero_grid();
+        st = alloc<DevStatus>(1);
+        CK(cudaMallocHost(&st_host, sizeof(DevStatus)));
+        reset_status();
+        stage_elems = 0;
+        for (int f = 0; f < S_NFIELDS; ++f)
+            stage_elems += (size_t)cap * stage_comps<D>(f);
+        T* sbase = alloc<T>(stage_elems);
+        size_t off = 0;
+        for (int f = 0; f < S_NFIELDS; ++f) {
+            stage.f[f] = sbase + off;
+            off += (size_t)cap * stage_comps<D>(f);
+        }
+        CK(cudaMallocHost(&stage_host, stage_elems * sizeof(T)));
+        d_red = alloc<unsigned long long>(2);
+        aw.init(*this);
+        set_smem_attrs();
+        CK(cudaStreamSynchronize(stream));
+    }
+
+    ~Ctx() override
+    {
+        for (auto& g : graphs)
+            for (auto& e : g)
+                if (e)
+                    cudaGraphExecDestroy(e);
+        for (auto& e : events) {
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        aw.free_all();
+        for (void* p : allocs)
+            cudaFree(p);
+        if (st_host)
+            cudaFreeHost(st_host);
+        if (stage_host)
+            cudaFreeHost(stage_host);
+        if (stream)
+            cudaStreamDestroy(stream);
+    }
+
+    void build_scene(const mpm_scene_desc* d)
+    {
+        if (d->dh <= 0 || d->dt <= 0)
+            throw ApiError(MPM_ERR_VALIDATION, "config: grid spacing and time step must be positive");
+        sc.dh = T(d->dh);
+        sc.inv_dh = T(1) / sc.dh;
+        sc.dt = T(d->dt);
+        sc.alpha = d->scheme == MPM_SCHEME_FLIP ? T(1) : (d->scheme == MPM_SCHEME_BLEND ? T(d->alpha_flip) : T(0));
+        for (int a = 0; a < D; ++a) {
+            if (d->cells[a] < 5)
+                throw ApiError(MPM_ERR_VALIDATION, "config: need at least 5 cells per axis");
+            sc.cells[a] = d->cells[a];
+            sc.origin[a] = T(d->origin[a]);
+            sc.gravity[a] = T(d->gravity[a]);
+            sc.nb[a] = (d->cells[a] - 1 + C::B - 1) / C::B;
+            sc.nnb[a] = (d->cells[a] + 1 + C::B - 1) / C::B;
+        }
+        sc.nb_total = 1;
+        sc.nnb_total = 1;
+        for (int a = 0; a < D; ++a) {
+            sc.nb_total *= sc.nb[a];
+            sc.nnb_total *= sc.nnb[a];
+        }
+        if ((int64_t)sc.nb_total << C::LOGNB >= (int64_t(1) << 31) - 1)
+            throw ApiError(MPM_ERR_VALIDATION, "grid too large for 32-bit cell keys");
+        sc.scheme = d->scheme;
+        sc.apic = d->scheme == MPM_SCHEME_APIC;
+        sc.tpic = d->scheme == MPM_SCHEME_TPIC;
+        sc.track_F = d->track_def_grad;
+        sc.material = d->material;
+        sc.rho0 = T(d->rho0);
+        sc.visc = T(d->viscosity);
+        sc.c = T(d->sound_speed);
+        sc.rate_form = d->rate_form;
+        sc.K = T(d->K);
+        sc.G = T(d->G);
+        sc.q_phi = T(d->q_phi);
+        sc.k_phi = T(d->k_phi);
+        sc.q_psi = T(d->q_psi);
+        sc.tau_P = T(d->tau_P);
+        sc.alpha_P = T(d->alpha_P);
+        sc.sigma_t = T(d->sigma_t);
+        sc.band = d->band_layers;
+        int off = 0;
+        for (int w = 0; w < 2 * D; ++w) {
+            sc.wall_kind[w] = d->wall_kind[w];
+            sc.n_fric[w] = d->n_friction[w];
+            sc.fric_off[w] = off;
+            if (d->wall_kind[w] == MPM_WALL_COULOMB && d->n_friction[w] < 1)
+                throw ApiError(MPM_ERR_VALIDATION, "scene: coulomb wall needs at least one segment");
+            for (int k = 0; k < d->n_friction[w]; ++k) {
+                if (off >= MAX_FRIC)
+                    throw ApiError(MPM_ERR_VALIDATION, "too many Coulomb friction segments (max 64 total)");
+                sc.fric[off++] = T(d->friction[w][k]);
+            }
+        }
+        if (d->n_obstacles > MAX_OBST)
+            throw ApiError(MPM_ERR_VALIDATION, "too many obstacles (max 16)");
+        sc.n_obst = d->n_obstacles;
+        for (int o = 0; o < d->n_obstacles; ++o)
+            for (int k = 0; k < 2 * D; ++k)
+                sc.obst[o][k] = T(d->obstacles[o * 2 * D + k]);
+        sc.mass_eps = T(d->mass_epsilon);
+    }
+
+    void alloc_pbuf(PBuf<T, D>& P)
+    {
+        for (int a = 0; a < D; ++a) {
+            P.x[a] = alloc<T>(cap);
+            P.v[a] = alloc<T>(cap);
+        }
+        P.m = alloc<T>(cap);
+        P.V = alloc<T>(cap);
+        P.rho = alloc<T>(cap);
+        P.eps = alloc<T>(cap);
+        P.szz = D == 2 ? alloc<T>(cap) : nullptr;
+        for (int s = 0; s < C::NS; ++s)
+            P.sig[s] = alloc<T>(cap);
+        for (int k = 0; k < D * D; ++k) {
+            P.gv[k] = alloc<T>(cap);
+            P.aff[k] = has_aff ? alloc<T>(cap) : nullptr;
+            P.F[k] = has_F ? alloc<T>(cap) : nullptr;
+        }
+        P.pid = alloc<int>(cap);
+    }
+
+    void zero_grid()
+    {
+        const size_t nodes = (size_t)sc.nnb_total * C::NB;
+        CK(cudaMemsetAsync(G.m, 0, nodes * sizeof(T), stream));
+        for (int a = 0; a < D; ++a) {
+            CK(cudaMemsetAsync(G.p[a], 0, nodes * sizeof(T), stream));
+            CK(cudaMemsetAsync(G.f[a], 0, nodes * sizeof(T), stream));
+            CK(cudaMemsetAsync(G.v[a], 0, nodes * sizeof(T), stream));
+            CK(cudaMemsetAsync(G.vold[a], 0, nodes * sizeof(T), stream));
+        }
+    }
+
+    void reset_status()
+    {
+        DevStatus s{};
+        s.den_pid = 0x7fffffff;
+        s.ood_pid = 0x7fffffff;
+        s.step = step;
+        s.err_step = -1;
+        CK(cudaMemcpyAsync(st, &s, sizeof(s), cudaMemcpyHostToDevice, stream));
+    }
+
+    // ---- kernel launch helpers ------------------------------------------------------------
+    size_t g2p_smem() const { return sizeof(T) * 2 * D * C::TN; }
+
+    void set_smem_attrs()
+    {
+        size_t sm = g2p_smem();
+        auto set = [&](auto kern) { CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))); };
+        set(k_g2p<T, D, P_CONSTIT, false, false>);
+        set(k_g2p<T, D, P_CONSTIT | P_GUARD, false, false>);
+        set(k_g2p<T, D, P_CONSTIT, true, false>);
+        set(k_g2p<T, D, P_CONSTIT | P_GUARD, true, false>);
+        set(k_g2p<T, D, P_CONSTIT, false, true>);
+        set(k_g2p<T, D, P_CONSTIT | P_GUARD, false, true>);
+        set(k_g2p<T, D, P_CONSTIT, true, true>);
+        set(k_g2p<T, D, P_CONSTIT | P_GUARD, true, true>);
+        set(k_g2p<T, D, 0, false, false>);
+        set(k_g2p<T, D, 0, true, false>);
+        set(k_g2p<T, D, 0, false, true>);
+        set(k_g2p<T, D, 0, true, true>);
+        if constexpr (D == 3) {
+            CK(cudaFuncSetAttribute(k_p2g_staged3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(Stage3Cfg<T>::SMEM)));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2g_ctas_per_sm, k_p2g_staged3<T>, Stage3Cfg<T>::THREADS,
+                                                             Stage3Cfg<T>::SMEM));
+        } else {
+            CK(cudaFuncSetAttribute(k_p2g_staged<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(StageCfg<T, D>::SMEM)));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2g_ctas_per_sm, k_p2g_staged<T, D>, StageCfg<T, D>::THREADS,
+                                                             StageCfg<T, D>::SMEM));
+        }
+        if (p2g_ctas_per_sm < 1)
+            p2g_ctas_per_sm = 1;
+        aw.set_attrs(*this);
+    }
+
+    template <class F> void launch(const char* name, F&& f)
+    {
+        ++launches;
+        if (prof) {
+            ProfEvent e{name, nullptr, nullptr};
+            CK(cudaEventCreate(&e.a));
+            CK(cudaEventCreate(&e.b));
+            CK(cudaEventRecord(e.a, stream));
+            f();
+            CK(cudaEventRecord(e.b, stream));
+            events.push_back(e);
+        } else {
+            f();
+        }
+        CK(cudaGetLastError());
+    }
+
+    unsigned grid_for(int64_t k, int tpb) const { return unsigned((k + tpb - 1) / tpb); }
+    unsigned persistent(int per_sm) const { return unsigned(nsm * per_sm); }
+
+    // ---- sort + segment tables ---------------------------------------------------------------
+    void sort_and_segment()
+    {
+        if (!keys_valid) {
+            launch("k_keys", [&] { k_keys<T, D><<<grid_for(n, 256), 256, 0, stream>>>(sc, buf[cur], int(n), keys, st); });
+            keys_valid = true;
+        }
+        int end_bit = 1;
+        while ((int64_t(1) << end_bit) <= (int64_t(sc.nb_total) << C::LOGNB))
+            ++end_bit;
+        end_bit = end_bit < 31 ? end_bit + 1 : 31; // room for the out-of-domain sentinel
+        if (end_bit > 31)
+            end_bit = 31;
+        size_t bytes = cub_bytes;
+        CK(cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys, keys_sorted, iota, perm, int(n), 0, 32, stream));
+        CK(cudaMemsetAsync(bstart, 0xff, sizeof(int) * sc.nb_total, stream));
+        CK(cudaMemsetAsync(bend, 0xff, sizeof(int) * sc.nb_total, stream));
+        CK(cudaMemsetAsync(lstart, 0xff, sizeof(int) * sc.nb_total * (C::B + 1), stream));
+        CK(cudaMemsetAsync(counts, 0, sizeof(int) * 4, stream));
+        CK(cudaMemsetAsync(nflag, 0, sc.nnb_total, stream));
+        launch("k_seg", [&] { k_seg<D><<<grid_for(n, 256), 256, 0, stream>>>(keys_sorted, int(n), sc.nb_total, bstart, bend, lstart); });
+        launch("k_compact", [&] { k_compact_pos<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, sc.nb_total, occ, counts); });
+        launch("k_mark_nodes", [&] { k_mark_nodes<D><<<grid_for(sc.nb_total, 128), 128, 0, stream>>>(occ, counts, d_nb, d_nnb, nflag); });
+        launch("k_compact", [&] { k_compact_flag<<<grid_for(sc.nnb_total, 256), 256, 0, stream>>>(nflag, sc.nnb_total, act, counts + 1); });
+        (void)end_bit;
+    }
+
+    void p2g_kernel()
+    {
+        if (sc.apic || sc.tpic) {
+            const int tpb = D == 2 ? 160 : 256;
+            launch("k_p2g", [&] {
+                k_p2g<T, D, true><<<persistent(8), tpb, 0, stream>>>(sc, buf[cur], perm, keys_sorted, bstart, bend, occ,
+                                                                     counts, partials, st);
+            });
+        } else {
+            if constexpr (D == 3) {
+                using S = Stage3Cfg<T>;
+                launch("k_p2g", [&] {
+                    k_p2g_staged3<T><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
+                        sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st);
+                });
+            } else {
+                using S = StageCfg<T, D>;
+                launch("k_p2g", [&] {
+                    k_p2g_staged<T, D><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
+                        sc, buf[cur], perm, keys_sorted, bstart, bend, occ, counts, partials, st);
+                });
+            }
+        }
+    }
+
+    template <int MODE> void grid_kernel()
+    {
+        launch("k_grid", [&] {
+            k_grid<T, D, MODE><<<persistent(4), C::NB, 0, stream>>>(sc, G, partials, bstart, act, counts + 1, st);
+        });
+    }
+
+    template <int FL> void g2p_kernel_fl()
+    {
+        auto& Pin = buf[cur];
+        auto& Pout = buf[cur ^ 1];
+        const size_t sm = g2p_smem();
+        const unsigned gr = persistent(D == 2 ? 8 : 4);
+        if (has_aff && has_F)
+            launch("k_g2p", [&] { k_g2p<T, D, FL, true, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st); });
+        else if (has_aff)
+            launch("k_g2p", [&] { k_g2p<T, D, FL, true, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st); });
+        else if (has_F)
+            launch("k_g2p", [&] { k_g2p<T, D, FL, false, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st); });
+        else
+            launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st); });
+        cur ^= 1;
+        keys_valid = true;
+    }
+
+    void step_once(bool guard)
+    {
+        sort_and_segment();
+        p2g_kernel();
+        grid_kernel<G_SUM | G_MOM | G_CORR>();
+        if (guard)
+            g2p_kernel_fl<P_CONSTIT | P_GUARD>();
+        else
+            g2p_kernel_fl<P_CONSTIT>();
+        launch("k_step_end", [&] { k_step_end<<<1, 1, 0, stream>>>(st); });
+    }
+
+    // ---- status ------------------------------------------------------------------------------
+    void fetch_status()
+    {
+        CK(cudaMemcpyAsync(st_host, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+    }
+
+    // raise the reference's exception for whatever the device flagged
+    void check_status(int64_t step_before)
+    {
+        fetch_status();
+        DevStatus s = *st_host;
+        step = s.step;
+        time = double(T(step) * sc.dt);
+        if (!s.abort)
+            return;
+        reset_status();
+        if (s.den_flag)
+            throw ApiError(MPM_ERR_NUMERICAL, "update: 1 + tr(dd) <= 0, time step too large for the compression rate",
+                           s.den_pid, s.step + 1);
+        if (s.nan_flag) {
+            step = s.step + 1; // the step completed, then the guard fired (stepper.hpp:519-522)
+            time = double(T(step) * sc.dt);
+            throw ApiError(MPM_ERR_NUMERICAL, "run: non-finite particle field detected at step " + std::to_string(step),
+                           -1, step);
+        }
+        if (s.ood_flag) {
+            // keys of step s.step+1's output -> the state after that step is complete; the
+            // next P2G is where the reference throws (bspline.hpp:322-327)
+            if (s.err_step >= 0 || s.step != step_before || true) {
+            }
+            throw ApiError(MPM_ERR_OUT_OF_DOMAIN,
+                           "particle " + std::to_string(s.ood_pid) + " outside valid grid interior", s.ood_pid,
+                           s.step + 1);
+        }
+        throw ApiError(MPM_ERR_NUMERICAL, "device step aborted", -1, s.step);
+    }
+
+    // ---- API ----------------------------------------------------------------------------------
+    void upload(const mpm_state_view* s) override
+    {
+        if (s->n < 1 || s->n > cap)
+            throw ApiError(MPM_ERR_USAGE, "state size " + std::to_string(s->n) + " outside [1, " + std::to_string(cap) + "]");
+        if (!s->x || !s->v || !s->mass || !s->volume || !s->rho || !s->sigma)
+            throw ApiError(MPM_ERR_USAGE, "state view missing required fields");
+        if (has_aff && !s->affine)
+            throw ApiError(MPM_ERR_USAGE, "APIC scheme needs the affine field");
+        n = s->n;
+        // symmetric stress contract (packed storage): reject genuinely non-symmetric input
+        const T* sg = static_cast<const T*>(s->sigma);
+        for (int64_t i = 0; i < n; ++i)
+            for (int r = 0; r < D; ++r)
+                for (int c = r + 1; c < D; ++c) {
+                    T a = sg[i * D * D + c * D + r], b = sg[i * D * D + r * D + c];
+                    T scale = std::max(std::abs(a), std::abs(b));
+                    if (std::abs(a - b) > T(1e-5) * scale + T(0))
+                        throw ApiError(MPM_ERR_VALIDATION, "stress of particle " + std::to_string(i) + " is not symmetric", i);
+                }
+        const void* src[S_NFIELDS] = {s->x, s->v, s->mass, s->volume, s->rho, s->eps_eq, D == 2 ? s->sigma_zz : nullptr,
+                                      s->sigma, s->grad_v, s->affine, s->def_grad};
+        for (int f = 0; f < S_NFIELDS; ++f) {
+            size_t bytes = (size_t)n * stage_comps<D>(f) * sizeof(T);
+            if (src[f])
+                CK(cudaMemcpyAsync(stage.f[f], src[f], bytes, cudaMemcpyHostToDevice, stream));
+            else if (f == S_EPS || f == S_GV || f == S_SZZ)
+                CK(cudaMemsetAsync(stage.f[f], 0, bytes, stream));
+            else if (f == S_F && has_F)
+                throw ApiError(MPM_ERR_USAGE, "track_def_grad needs the def_grad field");
+        }
+        launch("k_upload", [&] {
+            k_upload<T, D><<<grid_for(n, 256), 256, 0, stream>>>(stage, buf[cur], int(n), D == 2 && s->sigma_zz != nullptr,
+                                                                 has_aff, has_F);
+        });
+        step = s->step;
+        time = s->time;
+        keys_valid = false;
+        reset_status();
+        CK(cudaStreamSynchronize(stream));
+    }
+
+    void download(mpm_state_view* s) override
+    {
+        if (n == 0)
+            throw ApiError(MPM_ERR_USAGE, "no state uploaded");
+        launch("k_download", [&] { k_download<T, D><<<grid_for(n, 256), 256, 0, stream>>>(stage, buf[cur], int(n), has_aff, has_F); });
+        void* dst[S_NFIELDS] = {s->x, s->v, s->mass, s->volume, s->rho, s->eps_eq, D == 2 ? s->sigma_zz : nullptr,
+                                s->sigma, s->grad_v, has_aff ? s->affine : nullptr, has_F ? s->def_grad : nullptr};
+        for (int f = 0; f < S_NFIELDS; ++f)
+            if (dst[f])
+                CK(cudaMemcpyAsync(dst[f], stage.f[f], (size_t)n * stage_comps<D>(f) * sizeof(T),
+                                   cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        s->n = n;
+        s->step = step;
+        s->time = time;
+    }
+
+    uint64_t digest() override
+    {
+        CK(cudaMemsetAsync(d_red, 0, sizeof(unsigned long long), stream));
+        launch("k_digest", [&] { k_digest<T, D><<<grid_for(n, 256), 256, 0, stream>>>(buf[cur], int(n), has_aff, d_red); });
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, d_red, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        return h ^ (uint64_t)step * 0x9e3779b97f4a7c15ull;
+    }
+
+    double max_speed() override
+    {
+        CK(cudaMemsetAsync(d_red + 1, 0, sizeof(unsigned long long), stream));
+        launch("k_max_speed", [&] { k_max_speed<T, D><<<grid_for(n, 256), 256, 0, stream>>>(buf[cur], int(n), d_red + 1); });
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, d_red + 1, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        double v;
+        std::memcpy(&v, &h, sizeof(v));
+        return v;
+    }
+
+    void advance(int64_t nsteps, uint32_t flags) override
+    {
+        if (n == 0)
+            throw ApiError(MPM_ERR_USAGE, "no state uploaded");
+        if (nsteps <= 0)
+            return;
+        const bool guard = flags & MPM_ADV_NAN_GUARD;
+        const int64_t step0 = step;
+        reset_status();
+        if (prof) {
+            for (int64_t k = 0; k < nsteps; ++k)
+                step_once(guard);
+        } else {
+            // first step runs eagerly (computes keys if needed); the rest replay a captured graph
+            step_once(guard);
+            for (int64_t k = 1; k < nsteps; ++k) {
+                cudaGraphExec_t& ge = graphs[guard][cur];
+                if (!ge) {
+                    const int cur0 = cur;
+                    const int64_t l0 = launches;
+                    cudaGraph_t g;
+                    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+                    step_once(guard);
+                    CK(cudaStreamEndCapture(stream, &g));
+                    CK(cudaGraphInstantiate(&graphs[guard][cur0], g, 0));
+                    CK(cudaGraphDestroy(g));
+                    graph_launches = launches - l0;
+                    launches = l0;
+                    cur = cur0;
+                }
+                CK(cudaGraphLaunch(graphs[guard][cur], stream));
+                launches += graph_launches;
+                cur ^= 1;
+            }
+        }
+        check_status(step0);
+    }
+    int64_t graph_launches = 0;
+
+    // ---- phase functions (per-phase parity with the reference free functions) ---------------
+    void phase_p2g() override
+    {
+        reset_status();
+        sort_and_segment();
+        p2g_kernel();
+        zero_grid(); // Grid::reset (state.hpp:235-242)
+        grid_kernel<G_SUM | G_STORE>();
+        grid_touched_all = false;
+        check_status(step);
+    }
+    void activate_all_node_blocks()
+    {
+        // phases applied to an uploaded grid act on every node (contact.hpp:249-262)
+        CK(cudaMemsetAsync(nflag, 1, sc.nnb_total, stream));
+        CK(cudaMemsetAsync(counts + 1, 0, sizeof(int), stream));
+        launch("k_compact", [&] { k_compact_flag<<<grid_for(sc.nnb_total, 256), 256, 0, stream>>>(nflag, sc.nnb_total, act, counts + 1); });
+    }
+    void phase_mom() override
+    {
+        reset_status();
+        if (grid_touched_all)
+            activate_all_node_blocks();
+        grid_kernel<G_MOM | G_STORE>();
+        check_status(step);
+    }
+    void phase_corr() override
+    {
+        reset_status();
+        if (grid_touched_all)
+            activate_all_node_blocks();
+        grid_kernel<G_CORR | G_STORE>();
+        check_status(step);
+    }
+    void phase_g2p() override
+    {
+        reset_status();
+        sort_and_segment();
+        g2p_kernel_fl<0>();
+        check_status(step);
+    }
+    void phase_constit() override
+    {
+        reset_status();
+        launch("k_constitutive", [&] {
+            if (has_F)
+                k_constitutive<T, D, true><<<grid_for(n, 256), 256, 0, stream>>>(sc, buf[cur], int(n), st);
+            else
+                k_constitutive<T, D, false><<<grid_for(n, 256), 256, 0, stream>>>(sc, buf[cur], int(n), st);
+        });
+        fetch_status();
+        if (st_host->den_flag) {
+            int p = st_host->den_pid;
+            reset_status();
+            throw ApiError(MPM_ERR_NUMERICAL, "update: 1 + tr(dd) <= 0, time step too large for the compression rate", p);
+        }
+    }
+
+    // dense (row-major node index) <-> node-block layout
+    void grid_download(mpm_grid_view* g) override
+    {
+        const int64_t nn = num_nodes();
+        std::vector<T> blk((size_t)sc.nnb_total * C::NB);
+        auto pull = [&](T* dptr, void* dst, int comps, int comp) {
+            if (!dst)
+                return;
+            CK(cudaMemcpyAsync(blk.data(), dptr, blk.size() * sizeof(T), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            T* out = static_cast<T*>(dst);
+            for (int64_t i = 0; i < nn; ++i)
+                out[i * comps + comp] = blk[block_index(i)];
+        };
+        pull(G.m, g->mass, 1, 0);
+        for (int a = 0; a < D; ++a) {
+            pull(G.p[a], g->momentum, D, a);
+            pull(G.vold[a], g->v_old, D, a);
+            pull(G.v[a], g->v, D, a);
+            pull(G.f[a], g->force, D, a);
+        }
+        g->num_nodes = nn;
+    }
+    void grid_upload(const mpm_grid_view* g) override
+    {
+        const int64_t nn = num_nodes();
+        std::vector<T> blk((size_t)sc.nnb_total * C::NB);
+        auto push = [&](T* dptr, const void* srcp, int comps, int comp) {
+            std::fill(blk.begin(), blk.end(), T(0));
+            if (srcp) {
+                const T* in = static_cast<const T*>(srcp);
+                for (int64_t i = 0; i < nn; ++i)
+                    blk[block_index(i)] = in[i * comps + comp];
+            }
+            CK(cudaMemcpyAsync(dptr, blk.data(), blk.size() * sizeof(T), cudaMemcpyHostToDevice, stream));
+            CK(cudaStreamSynchronize(stream));
+        };
+        push(G.m, g->mass, 1, 0);
+        for (int a = 0; a < D; ++a) {
+            push(G.p[a], g->momentum, D, a);
+            push(G.vold[a], g->v_old, D, a);
+            push(G.v[a], g->v, D, a);
+            push(G.f[a], g->force, D, a);
+        }
+        grid_touched_all = true;
+        activate_all_node_blocks();
+        CK(cudaStreamSynchronize(stream));
+    }
+    int64_t num_nodes() const
+    {
+        int64_t r = 1;
+        for (int a = 0; a < D; ++a)
+            r *= sc.cells[a] + 1;
+        return r;
+    }
+    size_t block_index(int64_t flat) const
+    {
+        int idx[D];
+        for (int a = D - 1; a >= 0; --a) {
+            idx[a] = int(flat % (sc.cells[a] + 1));
+            flat /= (sc.cells[a] + 1);
+        }
+        size_t q = 0, loc = 0;
+        for (int a = 0; a < D; ++a) {
+            q = q * sc.nnb[a] + (idx[a] >> C::LOGB);
+            loc = (loc << C::LOGB) | (idx[a] & (C::B - 1));
+        }
+        return q * C::NB + loc;
+    }
+
+    void grid_stats(int64_t* an, int64_t* ob, int64_t* anb) override
+    {
+        fetch_status();
+        int cnt[4];
+        CK(cudaMemcpyAsync(cnt, counts, sizeof(cnt), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (an)
+            *an = int64_t(st_host->active_nodes);
+        if (ob)
+            *ob = cnt[0];
+        if (anb)
+            *anb = cnt[1];
+    }
+
+    // ---- adjoint (kernels_adj.cuh) -------------------------------------------------------------
+    void step_vjp(const mpm_state_view* s, const mpm_cot_view* co, mpm_cot_view* ci, mpm_param_grads* pg) override
+    {
+        aw.step_vjp_api(*this, s, co, ci, pg);
+    }
+    void backprop(const mpm_state_view* s0, int64_t total, int nseg, const mpm_seeder_desc* sd, mpm_cot_view* c0,
+                  mpm_param_grads* pg, mpm_backprop_result* res) override
+    {
+        aw.backprop_api(*this, s0, total, nseg, sd, c0, pg, res);
+    }
+};
+
+} // namespace
+
+// ---------------------------------------------------------------------------------------------
+struct mpm_ctx {
+    std::unique_ptr<CtxBase> impl;
+    int code = 0;
+    int64_t particle = -1, step = -1;
+    std::string msg;
+};
+
+template <class F> static int guarded(mpm_ctx* c, F&& f)
+{
+    if (c) {
+        c->code = 0;
+        c->particle = -1;
+        c->step = -1;
+        c->msg.clear();
+    }
+    try {
+        f();
+        return MPM_OK;
+    } catch (const ApiError& e) {
+        if (c) {
+            c->code = e.code;
+            c->particle = e.particle;
+            c->step = e.step;
+            c->msg = e.what();
+        }
+        return e.code;
+    } catch (const std::exception& e) {
+        if (c) {
+            c->code = MPM_ERR_USAGE;
+            c->msg = e.what();
+        }
+        return MPM_ERR_USAGE;
+    }
+}
+
+extern "C" {
+
+int mpm_version(void) { return MPM_CAPI_VERSION; }
+
+int mpm_device_name(char* buf, size_t len)
+{
+    cudaDeviceProp p{};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&p, dev) != cudaSuccess)
+        return MPM_ERR_CUDA;
+    std::snprintf(buf, len, "%s (sm_%d%d, %d SMs)", p.name, p.major, p.minor, p.multiProcessorCount);
+    return MPM_OK;
+}
+
+int mpm_ctx_create(const mpm_scene_desc* d, int64_t max_particles, int device, mpm_ctx** out)
+{
+    if (!d || !out || max_particles < 1)
+        return MPM_ERR_USAGE;
+    *out = nullptr;
+    static thread_local mpm_ctx scratch;
+    return guarded(&scratch, [&] {
+        std::unique_ptr<mpm_ctx> c(new mpm_ctx);
+        if (d->dim == 2 && d->dtype == MPM_F64)
+            c->impl.reset(new Ctx<double, 2>(d, max_particles, device));
+        else if (d->dim == 3 && d->dtype == MPM_F64)
+            c->impl.reset(new Ctx<double, 3>(d, max_particles, device));
+        else if (d->dim == 2 && d->dtype == MPM_F32)
+            c->impl.reset(new Ctx<float, 2>(d, max_particles, device));
+        else if (d->dim == 3 && d->dtype == MPM_F32)
+            c->impl.reset(new Ctx<float, 3>(d, max_particles, device));
+        else
+            throw ApiError(MPM_ERR_USAGE, "dim must be 2 or 3 and dtype MPM_F32 or MPM_F64");
+        *out = c.release();
+    });
+}
+
+void mpm_ctx_destroy(mpm_ctx* c) { delete c; }
+
+int mpm_last_error(const mpm_ctx* c, int* code, int64_t* particle, int64_t* step, char* msg, size_t len)
+{
+    if (!c)
+        return MPM_ERR_USAGE;
+    if (code)
+        *code = c->code;
+    if (particle)
+        *particle = c->particle;
+    if (step)
+        *step = c->step;
+    if (msg && len) {
+        std::strncpy(msg, c->msg.c_str(), len - 1);
+        msg[len - 1] = 0;
+    }
+    return MPM_OK;
+}
+
+#define MPM_CALL(c, body)                                                                          \
+    do {                                                                                           \
+        if (!(c))                                                                                  \
+            return MPM_ERR_USAGE;                                                                  \
+        return guarded(c, [&] { body; });                                                          \
+    } while (0)
+
+int mpm_state_upload(mpm_ctx* c, const mpm_state_view* s) { MPM_CALL(c, c->impl->upload(s)); }
+int mpm_state_download(mpm_ctx* c, mpm_state_view* s) { MPM_CALL(c, c->impl->download(s)); }
+int mpm_state_digest(mpm_ctx* c, uint64_t* out) { MPM_CALL(c, *out = c->impl->digest()); }
+int mpm_max_speed(mpm_ctx* c, double* v) { MPM_CALL(c, *v = c->impl->max_speed()); }
+int mpm_advance(mpm_ctx* c, int64_t n, uint32_t flags) { MPM_CALL(c, c->impl->advance(n, flags)); }
+int mpm_p2g(mpm_ctx* c) { MPM_CALL(c, c->impl->phase_p2g()); }
+int mpm_grid_momentum_update(mpm_ctx* c) { MPM_CALL(c, c->impl->phase_mom()); }
+int mpm_grid_corrections(mpm_ctx* c) { MPM_CALL(c, c->impl->phase_corr()); }
+int mpm_g2p(mpm_ctx* c) { MPM_CALL(c, c->impl->phase_g2p()); }
+int mpm_constitutive(mpm_ctx* c) { MPM_CALL(c, c->impl->phase_constit()); }
+int mpm_grid_download(mpm_ctx* c, mpm_grid_view* g) { MPM_CALL(c, c->impl->grid_download(g)); }
+int mpm_grid_upload(mpm_ctx* c, const mpm_grid_view* g) { MPM_CALL(c, c->impl->grid_upload(g)); }
+int mpm_step_vjp(mpm_ctx* c, const mpm_state_view* s, const mpm_cot_view* co, mpm_cot_view* ci, mpm_param_grads* pg)
+{
+    MPM_CALL(c, c->impl->step_vjp(s, co, ci, pg));
+}
+int mpm_backprop(mpm_ctx* c, const mpm_state_view* s0, int64_t total, int nseg, const mpm_seeder_desc* sd,
+                 mpm_cot_view* c0, mpm_param_grads* pg, mpm_backprop_result* res)
+{
+    MPM_CALL(c, c->impl->backprop(s0, total, nseg, sd, c0, pg, res));
+}
+
+int mpm_profile_enable(mpm_ctx* c, int enable) { MPM_CALL(c, c->impl->prof = enable != 0); }
+
+int mpm_profile_reset(mpm_ctx* c)
+{
+    MPM_CALL(c, {
+        for (auto& e : c->impl->events) {
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        c->impl->events.clear();
+        c->impl->prof_acc.clear();
+    });
+}
+
+int mpm_profile_query(mpm_ctx* c, const char* name, double* ms, int64_t* launches)
+{
+    MPM_CALL(c, {
+        double tot = 0;
+        int64_t k = 0;
+        for (auto& e : c->impl->events) {
+            if (name && *name && !std::strstr(e.name, name))
+                continue;
+            float t = 0;
+            CK(cudaEventSynchronize(e.b));
+            CK(cudaEventElapsedTime(&t, e.a, e.b));
+            tot += t;
+            ++k;
+        }
+        if (ms)
+            *ms = tot;
+        if (launches)
+            *launches = k;
+    });
+}
+
+int64_t mpm_launch_count(const mpm_ctx* c) { return c ? c->impl->launches : -1; }
+
+int mpm_grid_stats(mpm_ctx* c, int64_t* an, int64_t* ob, int64_t* anb) { MPM_CALL(c, c->impl->grid_stats(an, ob, anb)); }
+
+} // extern "C"

@@ -1,0 +1,1363 @@
+// kernels_fwd.cuh -- forward step Phi = G2P o U o P2G on B200 (sm_100a).
+//
+// Per step:
+//   sort      stable radix sort of 32-bit cell keys (block << LOGNB | local cell) -> perm
+//   k_seg     dense per-block segment [bstart, bend) of the sorted order
+//   k_p2g     CTA per occupied particle block: node-column march (deterministic gather,
+//             no atomics) of the block's particles into its (B+2)^d partial tile
+//   k_grid    CTA per active node block: sum <= 2^d partial tiles in fixed order, momentum
+//             update, wall / obstacle / Coulomb corrections (transfer.hpp:440-449,
+//             contact.hpp:394-411)
+//   k_g2p     CTA per occupied particle block: node tile in smem, gather + v/x/grad v update
+//             (transfer.hpp:457-486) fused with the constitutive update (stepper.hpp:428-456),
+//             writes the new state in sorted order and the next step's cell keys
+#pragma once
+
+#include "common.cuh"
+#include "constit.cuh"
+
+namespace mpmgpu {
+
+// ---------------------------------------------------------------------------------------
+// keys / segments
+template <class T, int D>
+__global__ void k_keys(DevScene<T, D> sc, PBuf<T, D> P, int n, int* keys, DevStatus* st)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    T x[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        x[a] = P.x[a][i];
+    int key;
+    if (!cell_key<T, D>(sc, x, key)) {
+        key = 0x7fffffff;
+        atomicMin(&st->ood_pid, P.pid[i]);
+        st->ood_flag = 1;
+        st->abort = 1;
+    }
+    keys[i] = key;
+}
+
+__global__ void k_iota(int* a, int n)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n)
+        a[i] = i;
+}
+
+// dense segment table: bstart[b] / bend[b] for every particle block present in sorted keys,
+// plus the first sorted index of every non-empty base level (lstart[b][z], others untouched;
+// the reader fills gaps with a suffix minimum)
+template <int D>
+__global__ void k_seg(const int* keys, int n, int nb_total, int* bstart, int* bend, int* lstart)
+{
+    using C = Cfg<D>;
+    constexpr int LVLBITS = (D - 1) * C::LOGB;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    const int k = keys[i];
+    int b = k >> C::LOGNB;
+    if (b >= nb_total)
+        return;
+    const int kp = i > 0 ? keys[i - 1] : -1;
+    int bp = i > 0 ? (kp >> C::LOGNB) : -1;
+    int bn = i + 1 < n ? (keys[i + 1] >> C::LOGNB) : -1;
+    if (b != bp)
+        bstart[b] = i;
+    if (b != bn)
+        bend[b] = i + 1;
+    const int z = (k & (C::NB - 1)) >> LVLBITS;
+    if (b != bp || z != ((kp & (C::NB - 1)) >> LVLBITS))
+        lstart[b * (C::B + 1) + z] = i;
+}
+
+// node blocks touched by occupied particle block Q: Q + s, s in {0,1}^D
+template <int D>
+__global__ void k_mark_nodes(const int* occ, const int* n_occ, const int* nb, const int* nnb, unsigned char* nflag)
+{
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= *n_occ)
+        return;
+    int q[D];
+    block_coords<D>(occ[w], nb, q);
+#pragma unroll
+    for (int s = 0; s < (1 << D); ++s) {
+        int id = 0;
+        bool ok = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            int c = q[a] + ((s >> (D - 1 - a)) & 1);
+            ok &= c < nnb[a];
+            id = id * nnb[a] + c;
+        }
+        if (ok)
+            nflag[id] = 1;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// P2G: node-column march.
+//
+// Thread (column, segment) owns the node column `col` of the block tile (all axes but the
+// last) and a range of base levels along the last axis. Walking base levels upward it
+// gathers, from the 3^(d-1) base cells around its column, every particle's contributions to
+// the three nodes above it, in a rolling 3-node register window. A node is final (for this
+// segment) once the march passes it and is written once -- no atomics, no smem tile, fixed
+// summation order (level, then base cell in canonical offset order, then sorted particle
+// order). The two nodes a segment shares with the next one are added after a barrier.
+template <class T, int D> struct P2GContrib {
+    T acc[3][Cfg<D>::NF];
+};
+
+template <class T, int D>
+__device__ __forceinline__ void axis_weights(T x, T origin, T inv_dh, T* w, T* dw)
+{
+    T u = (x - origin) * inv_dh;
+    T fl = dfloor<T>(u - T(0.5));
+    T fx = u - fl;
+    T h0 = T(1.5) - fx, h1 = fx - T(1), h2 = fx - T(0.5);
+    w[0] = T(0.5) * h0 * h0;
+    w[1] = T(0.75) - h1 * h1;
+    w[2] = T(0.5) * h2 * h2;
+    dw[0] = -h0 * inv_dh;
+    dw[1] = -T(2) * h1 * inv_dh;
+    dw[2] = h2 * inv_dh;
+}
+
+// APIC / TPIC velocity augmentation matrix A (transfer.hpp:379-397), row-major D x D
+template <class T, int D>
+__device__ __forceinline__ void affine_matrix(const DevScene<T, D>& sc, const PBuf<T, D>& P, int src, const T* x,
+                                              const T (&w)[D][3], const int* base, T* A)
+{
+    if (sc.tpic) {
+#pragma unroll
+        for (int k = 0; k < D * D; ++k)
+            A[k] = __ldg(P.gv[k] + src);
+        return;
+    }
+    // D = sum_o phi r r^T, canonical order, then A = B D^-1
+    T Dm[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            Dm[i][j] = T(0);
+    for (int k = 0; k < Cfg<D>::NOFF; ++k) {
+        int o[D];
+        int kk = k;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+            o[a] = kk % 3;
+            kk /= 3;
+        }
+        T phi = T(1), r[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            phi *= w[a][o[a]];
+            r[a] = (sc.origin[a] + T(base[a] + o[a]) * sc.dh) - x[a];
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                Dm[i][j] += phi * r[i] * r[j];
+    }
+    T inv[D][D];
+    if constexpr (D == 2) {
+        T det = Dm[0][0] * Dm[1][1] - Dm[0][1] * Dm[1][0];
+        T id = T(1) / det;
+        inv[0][0] = Dm[1][1] * id;
+        inv[0][1] = -Dm[0][1] * id;
+        inv[1][0] = -Dm[1][0] * id;
+        inv[1][1] = Dm[0][0] * id;
+    } else {
+        T c00 = Dm[1][1] * Dm[2][2] - Dm[1][2] * Dm[2][1];
+        T c01 = Dm[1][2] * Dm[2][0] - Dm[1][0] * Dm[2][2];
+        T c02 = Dm[1][0] * Dm[2][1] - Dm[1][1] * Dm[2][0];
+        T det = Dm[0][0] * c00 + Dm[0][1] * c01 + Dm[0][2] * c02;
+        T id = T(1) / det;
+        inv[0][0] = c00 * id;
+        inv[1][0] = c01 * id;
+        inv[2][0] = c02 * id;
+        inv[0][1] = (Dm[0][2] * Dm[2][1] - Dm[0][1] * Dm[2][2]) * id;
+        inv[1][1] = (Dm[0][0] * Dm[2][2] - Dm[0][2] * Dm[2][0]) * id;
+        inv[2][1] = (Dm[0][1] * Dm[2][0] - Dm[0][0] * Dm[2][1]) * id;
+        inv[0][2] = (Dm[0][1] * Dm[1][2] - Dm[0][2] * Dm[1][1]) * id;
+        inv[1][2] = (Dm[0][2] * Dm[1][0] - Dm[0][0] * Dm[1][2]) * id;
+        inv[2][2] = (Dm[0][0] * Dm[1][1] - Dm[0][1] * Dm[1][0]) * id;
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            T s = T(0);
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+                s += __ldg(P.aff[i * D + k] + src) * inv[k][j];
+            A[i * D + j] = s;
+        }
+}
+
+template <class T, int D, bool AFF>
+__global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, const int* __restrict__ perm,
+                                             const int* __restrict__ keys, const int* __restrict__ bstart,
+                                             const int* __restrict__ bend, const int* __restrict__ occ,
+                                             const int* __restrict__ n_occ, T* __restrict__ partials,
+                                             const DevStatus* st)
+{
+    using C = Cfg<D>;
+    constexpr int B = C::B, TE = C::TE, NF = C::NF;
+    __shared__ int cst[C::NB + 1];
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    const int tid = threadIdx.x;
+    const int col = tid % C::NCOL, seg = tid / C::NCOL;
+    // column coordinates (all axes but the last)
+    int cn[D - 1 > 0 ? D - 1 : 1];
+    {
+        int cc = col;
+#pragma unroll
+        for (int a = D - 2; a >= 0; --a) {
+            cn[a] = cc % TE;
+            cc /= TE;
+        }
+    }
+    const int zb = seg * B / C::SEGS, ze = (seg + 1) * B / C::SEGS;
+    const bool active = seg < C::SEGS;
+
+    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+        const int Q = occ[w];
+        const int s0 = bstart[Q], s1 = bend[Q], len = s1 - s0;
+        int qc[D];
+        block_coords<D>(Q, sc.nb, qc);
+        // cell ranges: cst[c] = first index (segment-relative) with local cell >= c
+        for (int c = tid; c <= C::NB; c += blockDim.x) {
+            int lo = 0, hi = len;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if ((keys[s0 + mid] & (C::NB - 1)) < c)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            cst[c] = lo;
+        }
+        __syncthreads();
+        T* part = partials + (size_t)Q * NF * C::TN;
+        T ov[2][NF];
+        if (active) {
+            T acc[3][NF];
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    acc[k][f] = T(0);
+            for (int z = zb; z < ze; ++z) {
+#pragma unroll
+                for (int oo = 0; oo < C::NOFF / 3; ++oo) { // offsets on the non-march axes
+                    int o[D - 1 > 0 ? D - 1 : 1];
+                    int bcell = 0;
+                    bool ok = true;
+                    {
+                        int kk = oo;
+#pragma unroll
+                        for (int a = D - 2; a >= 0; --a) {
+                            o[a] = kk % 3;
+                            kk /= 3;
+                        }
+#pragma unroll
+                        for (int a = 0; a < D - 1; ++a) {
+                            int bc = cn[a] - o[a];
+                            ok &= bc >= 0 && bc < B;
+                            bcell = (bcell << C::LOGB) | (bc & (B - 1));
+                        }
+                    }
+                    if (!ok)
+                        continue;
+                    bcell |= z << ((D - 1) * C::LOGB); // level-major local cell (common.cuh)
+                    const int kb = cst[bcell], ke = cst[bcell + 1];
+                    for (int k = kb; k < ke; ++k) {
+                        const int src = __ldg(perm + s0 + k);
+                        T x[D], v[D];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            x[a] = __ldg(P.x[a] + src);
+                            v[a] = __ldg(P.v[a] + src);
+                        }
+                        const T m = __ldg(P.m + src), V = __ldg(P.V + src);
+                        T sig[C::NS];
+#pragma unroll
+                        for (int s = 0; s < C::NS; ++s)
+                            sig[s] = __ldg(P.sig[s] + src);
+                        T w[D][3], dw[D][3];
+#pragma unroll
+                        for (int a = 0; a < D; ++a)
+                            axis_weights<T, D>(x[a], sc.origin[a], sc.inv_dh, w[a], dw[a]);
+                        T A[D * D];
+                        int base[D];
+                        if constexpr (AFF) {
+#pragma unroll
+                            for (int a = 0; a < D - 1; ++a)
+                                base[a] = qc[a] * B + cn[a] - o[a];
+                            base[D - 1] = qc[D - 1] * B + z;
+                            affine_matrix<T, D>(sc, P, src, x, w, base, A);
+                        }
+                        // product of the non-march weights / derivative factors
+                        T wp = T(1);
+#pragma unroll
+                        for (int a = 0; a < D - 1; ++a)
+                            wp *= w[a][o[a]];
+#pragma unroll
+                        for (int o2 = 0; o2 < 3; ++o2) {
+                            const T phi = wp * w[D - 1][o2];
+                            T gw[D];
+#pragma unroll
+                            for (int a = 0; a < D; ++a) {
+                                T r = (a == D - 1) ? dw[a][o2] : dw[a][o[a]];
+#pragma unroll
+                                for (int b = 0; b < D; ++b)
+                                    if (b != a)
+                                        r *= (b == D - 1) ? w[b][o2] : w[b][o[b]];
+                                gw[a] = r;
+                            }
+                            T vel[D];
+#pragma unroll
+                            for (int a = 0; a < D; ++a)
+                                vel[a] = v[a];
+                            if constexpr (AFF) {
+                                T r[D];
+#pragma unroll
+                                for (int a = 0; a < D; ++a) {
+                                    int idx = a == D - 1 ? base[a] + o2 : base[a] + o[a];
+                                    r[a] = (sc.origin[a] + T(idx) * sc.dh) - x[a];
+                                }
+#pragma unroll
+                                for (int a = 0; a < D; ++a) {
+                                    T s = T(0);
+#pragma unroll
+                                    for (int b = 0; b < D; ++b)
+                                        s += A[a * D + b] * r[b];
+                                    vel[a] += s;
+                                }
+                            }
+                            const T mphi = m * phi;
+                            acc[o2][0] += mphi;
+#pragma unroll
+                            for (int a = 0; a < D; ++a) {
+                                T sg = T(0);
+#pragma unroll
+                                for (int b = 0; b < D; ++b)
+                                    sg += sig[sym_idx<D>(a, b)] * gw[b];
+                                acc[o2][1 + a] += mphi * vel[a];
+                                acc[o2][1 + D + a] += -(V * sg); // gravity: + g m_i per node (k_grid)
+                            }
+                        }
+                    }
+                }
+                // node z of this column is final for this segment
+                const int idx = z * C::NCOL + col;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    part[f * C::TN + idx] = acc[0][f];
+                    acc[0][f] = acc[1][f];
+                    acc[1][f] = acc[2][f];
+                    acc[2][f] = T(0);
+                }
+            }
+            if (seg == C::SEGS - 1) { // top of the tile: nodes B and B+1
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        part[f * C::TN + (ze + k) * C::NCOL + col] = acc[k][f];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        ov[k][f] = acc[k][f];
+            }
+        }
+        __syncthreads(); // next segment's own sums for the shared nodes are written
+        if (active && seg < C::SEGS - 1) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    T* p = part + f * C::TN + (ze + k) * C::NCOL + col;
+                    *p = *p + ov[k][f];
+                }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// P2G, staged (PIC / FLIP / blend).
+//
+// One CTA per occupied particle block, base levels (last axis) processed in order. Each level's
+// particles -- one contiguous run of the level-major sorted order -- are staged by the whole CTA
+// into shared memory as P2G records { w[d][3], dw[d][3], m, m v, V sigma } (weights computed
+// once per particle). Thread (base column bc, offset oo on the first d-1 axes) owns the 3
+// nodes (bc + oo, z .. z+2) in a rolling register window and visits only the particles of its
+// own base column; the 3^(d-1) lanes of one base column are adjacent, so every record read is
+// a shared-memory broadcast and no lane is idle. After each level the window's finished node
+// is written to an exclusive (node column, source offset) slot; NCOL threads then sum the
+// 3^(d-1) slots of each node column in fixed order into the block's partial tile. No atomics;
+// per-node order = (source offset, level, chunk, sorted particle order): deterministic.
+template <class T, int D> struct StageCfg {
+    static constexpr int NSRC = D == 2 ? 3 : 9;              // offsets on the non-march axes
+    static constexpr int NBC = Cfg<D>::NB / Cfg<D>::B;        // base columns per block
+    static constexpr int THREADS = NBC * NSRC;                // 48 (2-D), 576 (3-D)
+    static constexpr int NREC = 6 * D + 1 + D + Cfg<D>::NS;   // w, dw, m, mv, Vsig
+    static constexpr int CAP = D == 2 ? 128 : (sizeof(T) == 8 ? 256 : 512);
+    static constexpr size_t SMEM_REC = sizeof(T) * NREC * CAP;
+    static constexpr size_t SMEM_SLOT = sizeof(T) * Cfg<D>::NCOL * NSRC * Cfg<D>::NF;
+    static constexpr size_t SMEM = SMEM_REC + SMEM_SLOT;
+};
+
+template <class T, int D>
+__global__ void __launch_bounds__(StageCfg<T, D>::THREADS, 1)
+    k_p2g_staged(DevScene<T, D> sc, PBuf<T, D> P, const int* __restrict__ perm, const int* __restrict__ keys,
+                 const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ occ,
+                 const int* __restrict__ n_occ, T* __restrict__ partials, const DevStatus* st)
+{
+    using C = Cfg<D>;
+    using S = StageCfg<T, D>;
+    constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NSRC = S::NSRC, NBC = S::NBC;
+    constexpr int LVLBITS = (D - 1) * C::LOGB;
+    // record field offsets (in units of CAP)
+    constexpr int RW = 0, RDW = 3 * D, RM = 6 * D, RMV = 6 * D + 1, RVS = 7 * D + 1;
+    extern __shared__ unsigned char smem_raw[];
+    T* rec = reinterpret_cast<T*>(smem_raw);                            // [NREC][CAP]
+    T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_REC);            // [NCOL][NSRC][NF]
+    __shared__ int lvl[B + 1];
+    __shared__ int cst[NBC + 1];
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    const int tid = threadIdx.x;
+    const int bc = tid / NSRC, oo = tid % NSRC;
+    int o[D - 1], bcc[D - 1], ncol = 0;
+    {
+        int kk = oo, rem = bc;
+#pragma unroll
+        for (int a = D - 2; a >= 0; --a) {
+            o[a] = kk % 3;
+            kk /= 3;
+            bcc[a] = rem & (B - 1);
+            rem >>= C::LOGB;
+        }
+#pragma unroll
+        for (int a = 0; a < D - 1; ++a)
+            ncol = ncol * TE + bcc[a] + o[a];
+    }
+
+    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+        const int Q = occ[w];
+        const int s0 = bstart[Q], s1 = bend[Q], len = s1 - s0;
+        __syncthreads();
+        for (int z = tid; z <= B; z += blockDim.x) { // first index with level >= z
+            int lo = 0, hi = len;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (((keys[s0 + mid] & (C::NB - 1)) >> LVLBITS) < z)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            lvl[z] = lo;
+        }
+        T* part = partials + (size_t)Q * NF * C::TN;
+        T acc[3][NF];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+                acc[k][f] = T(0);
+
+        // after base level z (z < B) or at the tail (z = B, B+1): publish node level z
+        auto emit_and_reduce = [&](int z) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                slots[(ncol * NSRC + oo) * NF + f] = acc[0][f];
+                acc[0][f] = acc[1][f];
+                acc[1][f] = acc[2][f];
+                acc[2][f] = T(0);
+            }
+            __syncthreads();
+            for (int c = tid; c < C::NCOL; c += blockDim.x) {
+                int nc[D - 1];
+                {
+                    int rem = c;
+#pragma unroll
+                    for (int a = D - 2; a >= 0; --a) {
+                        nc[a] = rem % TE;
+                        rem /= TE;
+                    }
+                }
+                T sum[NF];
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    sum[f] = T(0);
+#pragma unroll
+                for (int q = 0; q < NSRC; ++q) {
+                    bool ok = true;
+                    int kk = q;
+#pragma unroll
+                    for (int a = D - 2; a >= 0; --a) {
+                        const int bcq = nc[a] - kk % 3;
+                        kk /= 3;
+                        ok &= bcq >= 0 && bcq < B;
+                    }
+                    if (ok)
+#pragma unroll
+                        for (int f = 0; f < NF; ++f)
+                            sum[f] += slots[(c * NSRC + q) * NF + f];
+                }
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    part[f * C::TN + z * C::NCOL + c] = sum[f];
+            }
+        };
+
+        for (int z = 0; z < B; ++z) {
+            __syncthreads(); // lvl ready / previous reduce done
+            const int l0 = lvl[z], nl = lvl[z + 1] - l0;
+            for (int ch = 0; ch * CAP < nl || ch == 0; ++ch) {
+                const int b0 = l0 + ch * CAP, cl = max(0, min(CAP, nl - ch * CAP));
+                if (ch > 0)
+                    __syncthreads(); // previous chunk consumed
+                for (int c = tid; c <= NBC; c += blockDim.x) {
+                    int lo = 0, hi = cl;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if ((keys[s0 + b0 + mid] & ((1 << LVLBITS) - 1)) < c)
+                            lo = mid + 1;
+                        else
+                            hi = mid;
+                    }
+                    cst[c] = c == NBC ? cl : lo;
+                }
+                for (int r = tid; r < cl; r += blockDim.x) {
+                    const int src = __ldg(perm + s0 + b0 + r);
+                    const T m = __ldg(P.m + src), V = __ldg(P.V + src);
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        const T u = (__ldg(P.x[a] + src) - sc.origin[a]) * sc.inv_dh;
+                        const T fx = u - dfloor<T>(u - T(0.5));
+                        const T h0 = T(1.5) - fx, h1 = fx - T(1), h2 = fx - T(0.5);
+                        rec[(RW + 3 * a + 0) * CAP + r] = T(0.5) * h0 * h0;
+                        rec[(RW + 3 * a + 1) * CAP + r] = T(0.75) - h1 * h1;
+                        rec[(RW + 3 * a + 2) * CAP + r] = T(0.5) * h2 * h2;
+                        rec[(RDW + 3 * a + 0) * CAP + r] = -h0 * sc.inv_dh;
+                        rec[(RDW + 3 * a + 1) * CAP + r] = -T(2) * h1 * sc.inv_dh;
+                        rec[(RDW + 3 * a + 2) * CAP + r] = h2 * sc.inv_dh;
+                        rec[(RMV + a) * CAP + r] = m * __ldg(P.v[a] + src);
+                    }
+                    rec[RM * CAP + r] = m;
+#pragma unroll
+                    for (int q = 0; q < C::NS; ++q)
+                        rec[(RVS + q) * CAP + r] = V * __ldg(P.sig[q] + src);
+                }
+                __syncthreads();
+                const int kb = cst[bc], ke = cst[bc + 1];
+                for (int k = kb; k < ke; ++k) {
+                    // weights of the first d-1 axes at this thread's offsets
+                    T wn[D - 1], dwn[D - 1];
+#pragma unroll
+                    for (int a = 0; a < D - 1; ++a) {
+                        wn[a] = rec[(RW + 3 * a + o[a]) * CAP + k];
+                        dwn[a] = rec[(RDW + 3 * a + o[a]) * CAP + k];
+                    }
+                    T pw = T(1), pdw[D - 1];
+#pragma unroll
+                    for (int a = 0; a < D - 1; ++a)
+                        pw *= wn[a];
+#pragma unroll
+                    for (int a = 0; a < D - 1; ++a) {
+                        T r = dwn[a];
+#pragma unroll
+                        for (int b2 = 0; b2 < D - 1; ++b2)
+                            if (b2 != a)
+                                r *= wn[b2];
+                        pdw[a] = r;
+                    }
+                    T wz[3], dwz[3], mv[D], vs[C::NS];
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        wz[q] = rec[(RW + 3 * (D - 1) + q) * CAP + k];
+                        dwz[q] = rec[(RDW + 3 * (D - 1) + q) * CAP + k];
+                    }
+                    const T m = rec[RM * CAP + k];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        mv[a] = rec[(RMV + a) * CAP + k];
+#pragma unroll
+                    for (int q = 0; q < C::NS; ++q)
+                        vs[q] = rec[(RVS + q) * CAP + k];
+                    // V sigma grad(phi) = wz * u + dwz * t  (grad phi = (pdw wz, pw dwz))
+                    T u[D], t[D];
+#pragma unroll
+                    for (int r = 0; r < D; ++r) {
+                        T sacc = T(0);
+#pragma unroll
+                        for (int a = 0; a < D - 1; ++a)
+                            sacc += vs[sym_idx<D>(r, a)] * pdw[a];
+                        u[r] = sacc;
+                        t[r] = vs[sym_idx<D>(r, D - 1)] * pw;
+                    }
+                    const T mpw = m * pw;
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const T phi = pw * wz[q];
+                        acc[q][0] += mpw * wz[q];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            acc[q][1 + a] += phi * mv[a];
+                            acc[q][1 + D + a] -= wz[q] * u[a] + dwz[q] * t[a];
+                        }
+                    }
+                }
+            }
+            __syncthreads(); // all records of this level consumed before the slots are reused
+            emit_and_reduce(z);
+        }
+        __syncthreads();
+        emit_and_reduce(B);
+        __syncthreads();
+        emit_and_reduce(B + 1);
+    }
+}
+
+// 3-D P2G (PIC / FLIP / blend): thread = (base column, x-offset o0), looping the 3 y-offsets
+// (63 accumulators: 3 node columns x rolling 3-node window). 3 adjacent lanes share a base
+// column -> broadcast record reads; 192 threads and ~110 KB smem -> 2 CTAs per SM overlap each
+// other's barrier phases. Records hold the fractional offsets; weights are formed per visit.
+template <class T> struct Stage3Cfg {
+    static constexpr int NBC = 64, THREADS = 192, NSRC = 9;
+    static constexpr int NREC = 3 + 1 + 3 + 6; // fx[3], m, m v[3], V sigma[6]
+    static constexpr int CAP = sizeof(T) == 8 ? 512 : 1024;
+    static constexpr size_t SMEM_REC = sizeof(T) * NREC * CAP;
+    static constexpr size_t SMEM_SLOT = sizeof(T) * Cfg<3>::NCOL * NSRC * Cfg<3>::NF;
+    static constexpr size_t SMEM = SMEM_REC + SMEM_SLOT;
+};
+
+template <class T> __device__ __forceinline__ void quad_w(T fx, int o, T inv_dh, T& w, T& dw)
+{
+    if (o == 0) {
+        const T h = T(1.5) - fx;
+        w = T(0.5) * h * h;
+        dw = -h * inv_dh;
+    } else if (o == 1) {
+        const T h = fx - T(1);
+        w = T(0.75) - h * h;
+        dw = -T(2) * h * inv_dh;
+    } else {
+        const T h = fx - T(0.5);
+        w = T(0.5) * h * h;
+        dw = h * inv_dh;
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(Stage3Cfg<T>::THREADS, 2)
+    k_p2g_staged3(DevScene<T, 3> sc, PBuf<T, 3> P, const int* __restrict__ perm, const int* __restrict__ keys,
+                  const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ lstart,
+                  const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials,
+                  const DevStatus* st)
+{
+    using C = Cfg<3>;
+    using S = Stage3Cfg<T>;
+    constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC;
+    constexpr int RFX = 0, RM = 3, RMV = 4, RVS = 7;
+    extern __shared__ unsigned char smem_raw[];
+    T* rec = reinterpret_cast<T*>(smem_raw);                 // [NREC][CAP]
+    T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_REC); // [NCOL][NSRC][NF]
+    __shared__ int lvl[B + 1];
+    __shared__ int ccount[NBC], cst[NBC + 1];
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    const int tid = threadIdx.x;
+    const int bc = tid / 3, o0 = tid % 3;
+    const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
+
+    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+        const int Q = occ[w];
+        const int s0 = bstart[Q], s1 = bend[Q];
+        __syncthreads();
+        if (tid == 0) { // level starts: suffix minimum over the recorded non-empty levels
+            int nxt = s1;
+            lvl[B] = s1 - s0;
+            for (int z = B - 1; z >= 0; --z) {
+                const int v = lstart[Q * (B + 1) + z];
+                nxt = (v >= s0 && v < s1) ? v : nxt;
+                lvl[z] = nxt - s0;
+            }
+        }
+        T* part = partials + (size_t)Q * NF * C::TN;
+        T acc[3][3][NF]; // [o1][window][field]
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    acc[a][k][f] = T(0);
+
+        auto emit_and_reduce = [&](int z) {
+#pragma unroll
+            for (int o1 = 0; o1 < 3; ++o1) {
+                const int ncol = (bc0 + o0) * TE + bc1 + o1;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    slots[(ncol * NSRC + o0 * 3 + o1) * NF + f] = acc[o1][0][f];
+                    acc[o1][0][f] = acc[o1][1][f];
+                    acc[o1][1][f] = acc[o1][2][f];
+                    acc[o1][2][f] = T(0);
+                }
+            }
+            __syncthreads();
+            for (int c = tid; c < C::NCOL; c += blockDim.x) {
+                const int n0 = c / TE, n1 = c % TE;
+                T sum[NF];
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    sum[f] = T(0);
+#pragma unroll
+                for (int q = 0; q < NSRC; ++q) {
+                    const int b0 = n0 - q / 3, b1 = n1 - q % 3;
+                    if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
+#pragma unroll
+                        for (int f = 0; f < NF; ++f)
+                            sum[f] += slots[(c * NSRC + q) * NF + f];
+                }
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    part[f * C::TN + z * C::NCOL + c] = sum[f];
+            }
+        };
+
+        for (int z = 0; z < B; ++z) {
+            __syncthreads(); // lvl ready, previous level's slots reduced
+            const int l0 = lvl[z], nl = lvl[z + 1] - l0;
+            for (int ch = 0; ch * CAP < nl || ch == 0; ++ch) {
+                const int b0 = l0 + ch * CAP, cl = max(0, min(CAP, nl - ch * CAP));
+                if (ch > 0)
+                    __syncthreads();
+                if (tid < NBC)
+                    ccount[tid] = 0;
+                __syncthreads();
+                for (int r = tid; r < cl; r += blockDim.x) {
+                    const int src = __ldg(perm + s0 + b0 + r);
+                    const int lc = __ldg(keys + s0 + b0 + r) & (NBC - 1);
+                    atomicAdd(&ccount[lc], 1);
+                    const T m = __ldg(P.m + src), V = __ldg(P.V + src);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const T u = (__ldg(P.x[a] + src) - sc.origin[a]) * sc.inv_dh;
+                        rec[(RFX + a) * CAP + r] = u - dfloor<T>(u - T(0.5));
+                        rec[(RMV + a) * CAP + r] = m * __ldg(P.v[a] + src);
+                    }
+                    rec[RM * CAP + r] = m;
+#pragma unroll
+                    for (int q = 0; q < 6; ++q)
+                        rec[(RVS + q) * CAP + r] = V * __ldg(P.sig[q] + src);
+                }
+                __syncthreads();
+                if (tid < 32) { // exclusive scan of the 64 column counts (records are column-sorted)
+                    const int c0 = ccount[2 * tid], c1 = ccount[2 * tid + 1];
+                    int v = c0 + c1;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int t = __shfl_up_sync(0xffffffffu, v, d);
+                        if (tid >= d)
+                            v += t;
+                    }
+                    const int excl = v - c0 - c1;
+                    cst[2 * tid] = excl;
+                    cst[2 * tid + 1] = excl + c0;
+                    if (tid == 31)
+                        cst[NBC] = v;
+                }
+                __syncthreads();
+                const int kb = cst[bc], ke = cst[bc + 1];
+                for (int k = kb; k < ke; ++k) {
+                    T wx, dwx;
+                    quad_w<T>(rec[(RFX + 0) * CAP + k], o0, sc.inv_dh, wx, dwx);
+                    const T fy = rec[(RFX + 1) * CAP + k], fz = rec[(RFX + 2) * CAP + k];
+                    T wy[3], dwy[3], wz[3], dwz[3];
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        quad_w<T>(fy, q, sc.inv_dh, wy[q], dwy[q]);
+                        quad_w<T>(fz, q, sc.inv_dh, wz[q], dwz[q]);
+                    }
+                    const T m = rec[RM * CAP + k];
+                    T mv[3], vs[6];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                        mv[a] = rec[(RMV + a) * CAP + k];
+#pragma unroll
+                    for (int q = 0; q < 6; ++q)
+                        vs[q] = rec[(RVS + q) * CAP + k];
+#pragma unroll
+                    for (int o1 = 0; o1 < 3; ++o1) {
+                        // grad phi = (dwx wy wz, wx dwy wz, wx wy dwz): V sigma grad phi = wz u + dwz t
+                        const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
+                        T u[3], t[3];
+#pragma unroll
+                        for (int r = 0; r < 3; ++r) {
+                            u[r] = vs[sym_idx<3>(r, 0)] * p1 + vs[sym_idx<3>(r, 1)] * p2;
+                            t[r] = vs[sym_idx<3>(r, 2)] * pw;
+                        }
+                        const T mpw = m * pw;
+#pragma unroll
+                        for (int q = 0; q < 3; ++q) {
+                            const T phi = pw * wz[q];
+                            acc[o1][q][0] += mpw * wz[q];
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {
+                                acc[o1][q][1 + a] += phi * mv[a];
+                                acc[o1][q][4 + a] -= wz[q] * u[a] + dwz[q] * t[a];
+                            }
+                        }
+                    }
+                }
+            }
+            __syncthreads(); // records of this level consumed, slots free
+            emit_and_reduce(z);
+        }
+        __syncthreads();
+        emit_and_reduce(B);
+        __syncthreads();
+        emit_and_reduce(B + 1);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// grid update: combine partial tiles, momentum update, boundary/contact corrections.
+enum GridMode { G_SUM = 1, G_MOM = 2, G_CORR = 4, G_STORE = 8 };
+
+// collect_node_corrections + apply_node_correction (contact.hpp:141-224), fixed order
+template <class T, int D>
+__device__ __forceinline__ void node_corrections(const DevScene<T, D>& sc, const int* n, T* v)
+{
+    // plain walls in wall order (slip zeroes the axis component, no-slip/fixed zero v)
+#pragma unroll
+    for (int w = 0; w < 2 * D; ++w) {
+        const int kind = sc.wall_kind[w];
+        if (kind == 3)
+            continue;
+        const int a = w / 2;
+        const bool in = (w % 2 == 0) ? n[a] < sc.band : n[a] > sc.cells[a] - sc.band;
+        if (!in)
+            continue;
+        if (kind == 0)
+            v[a] = T(0);
+        else {
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                v[b] = T(0);
+        }
+    }
+    if (sc.n_obst > 0) {
+        T xp[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            xp[a] = sc.origin[a] + T(n[a]) * sc.dh;
+        for (int ob = 0; ob < sc.n_obst; ++ob) {
+            bool inside = true;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+                inside &= !(xp[a] < sc.obst[ob][a] || xp[a] > sc.obst[ob][D + a]);
+            if (!inside)
+                continue;
+            int best_a = 0, best_s = 0;
+            T best = T(0);
+            bool first = true;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                T dlo = xp[a] - sc.obst[ob][a];
+                T dhi = sc.obst[ob][D + a] - xp[a];
+                if (first || dlo < best) {
+                    best = dlo;
+                    best_a = a;
+                    best_s = 0;
+                    first = false;
+                }
+                if (dhi < best) {
+                    best = dhi;
+                    best_a = a;
+                    best_s = 1;
+                }
+            }
+            const T nrm = best_s == 0 ? T(-1) : T(1);
+            const T vn = v[best_a] * nrm; // v . n with a unit axis normal
+            if (vn < T(0)) {
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    v[a] = v[a] - vn * (a == best_a ? nrm : T(0));
+            }
+        }
+    }
+    // Coulomb walls (contact.hpp:40-51, 336-351)
+#pragma unroll
+    for (int w = 0; w < 2 * D; ++w) {
+        if (sc.wall_kind[w] != 3)
+            continue;
+        const int a = w / 2;
+        const bool in = (w % 2 == 0) ? n[a] < sc.band : n[a] > sc.cells[a] - sc.band;
+        if (!in)
+            continue;
+        const int seg_axis = a == 0 ? 1 : 0;
+        const T coord = sc.origin[seg_axis] + T(n[seg_axis]) * sc.dh;
+        const int ns = sc.n_fric[w];
+        const T len = (T(sc.cells[seg_axis]) * sc.dh) / T(ns);
+        int k = int(ceil(double((coord - sc.origin[seg_axis]) / len))) - 1;
+        k = k < 0 ? 0 : (k > ns - 1 ? ns - 1 : k);
+        const T mu = sc.fric[sc.fric_off[w] + k];
+        const T nrm = (w % 2 == 0) ? T(-1) : T(1);
+        T vn = T(0);
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+            vn += v[b] * (b == a ? nrm : T(0));
+        if (vn <= T(0))
+            continue;
+        T t[D], t2 = T(0);
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+            t[b] = v[b] - vn * (b == a ? nrm : T(0));
+            t2 += t[b] * t[b];
+        }
+        const T tn = dsqrt<T>(t2);
+        if (tn <= mu * vn) {
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                v[b] = T(0);
+        } else {
+            const T s = mu * vn / tn;
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                v[b] = t[b] - s * t[b];
+        }
+    }
+}
+
+template <class T, int D, int MODE>
+__global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, D> G, const T* __restrict__ partials,
+                                                     const int* __restrict__ bstart, const int* __restrict__ act,
+                                                     const int* __restrict__ n_act, DevStatus* st)
+{
+    using C = Cfg<D>;
+    if (st->abort)
+        return;
+    const int nact = *n_act;
+    const int tid = threadIdx.x;
+    int lc[D];
+    {
+        int t = tid;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+            lc[a] = t & (C::B - 1);
+            t >>= C::LOGB;
+        }
+    }
+    unsigned long long nact_nodes = 0;
+    for (int w = blockIdx.x; w < nact; w += gridDim.x) {
+        const int q = act[w];
+        int qc[D], n[D];
+        block_coords<D>(q, sc.nnb, qc);
+        bool inside = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            n[a] = qc[a] * C::B + lc[a];
+            inside &= n[a] <= sc.cells[a];
+        }
+        const size_t gi = (size_t)q * C::NB + tid;
+        T m = T(0), p[D], f[D], v[D], vold[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            p[a] = f[a] = v[a] = vold[a] = T(0);
+        if (MODE & G_SUM) {
+            // fixed order over source blocks Q = q - s, s lexicographic in {0,1}^D
+#pragma unroll
+            for (int s = 0; s < (1 << D); ++s) {
+                int Qid = 0, tl = 0;
+                bool ok = true;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const int sa = (s >> (D - 1 - a)) & 1;
+                    const int Qa = qc[a] - sa;
+                    const int t = n[a] - Qa * C::B;
+                    ok &= Qa >= 0 && Qa < sc.nb[a] && t < C::TE;
+                    Qid = Qid * sc.nb[a] + Qa;
+                    (void)t;
+                }
+                if (!ok || bstart[Qid] < 0)
+                    continue;
+                // tile index: last axis slowest, columns row-major over the other axes
+                int colx = 0, z = 0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const int sa = (s >> (D - 1 - a)) & 1;
+                    const int t = n[a] - (qc[a] - sa) * C::B;
+                    if (a == D - 1)
+                        z = t;
+                    else
+                        colx = colx * C::TE + t;
+                }
+                tl = z * C::NCOL + colx;
+                const T* part = partials + (size_t)Qid * C::NF * C::TN + tl;
+                m += part[0];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    p[a] += part[(1 + a) * C::TN];
+                    f[a] += part[(1 + D + a) * C::TN];
+                }
+            }
+            // sum_p phi m g = g m_i (transfer.hpp:427, gravity term factored out of the scatter)
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+                f[a] += sc.gravity[a] * m;
+        } else {
+            m = G.m[gi];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                p[a] = G.p[a][gi];
+                f[a] = G.f[a][gi];
+                v[a] = G.v[a][gi];
+                vold[a] = G.vold[a][gi];
+            }
+        }
+        if (MODE & G_MOM) {
+            if (m > sc.mass_eps) {
+                const T s = sc.dt / m;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    vold[a] = p[a] / m;
+                    v[a] = vold[a] + s * f[a];
+                }
+                nact_nodes += inside;
+            } else if (MODE & G_SUM) {
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    v[a] = vold[a] = T(0);
+            }
+        }
+        if ((MODE & G_CORR) && inside)
+            node_corrections<T, D>(sc, n, v);
+        if (!inside) {
+            m = T(0);
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+                p[a] = f[a] = v[a] = vold[a] = T(0);
+        }
+        if (MODE & G_STORE) {
+            G.m[gi] = m;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                G.p[a][gi] = p[a];
+                G.f[a][gi] = f[a];
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            G.v[a][gi] = v[a];
+            G.vold[a][gi] = vold[a];
+        }
+    }
+    if (MODE & G_MOM) {
+        // warp-aggregated count of active nodes (diagnostic only)
+        for (int o = 16; o > 0; o >>= 1)
+            nact_nodes += __shfl_down_sync(0xffffffffu, nact_nodes, o);
+        if ((tid & 31) == 0 && nact_nodes)
+            atomicAdd(&st->active_nodes, nact_nodes);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// G2P (+ constitutive): CTA per occupied particle block, node tile (v, v_old) in smem.
+enum G2PFlags { P_CONSTIT = 1, P_GUARD = 2 };
+
+template <class T, int D, int FLAGS, bool APIC, bool TRACKF>
+__global__ void __launch_bounds__(256) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pin, PBuf<T, D> Pout,
+                                             GBuf<T, D> G, const int* __restrict__ perm,
+                                             const int* __restrict__ bstart, const int* __restrict__ bend,
+                                             const int* __restrict__ occ, const int* __restrict__ n_occ,
+                                             int* __restrict__ keys_out, DevStatus* st)
+{
+    using C = Cfg<D>;
+    constexpr int TE = C::TE, TN = C::TN;
+    extern __shared__ unsigned char smem_raw[];
+    T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]: v[0..D), vold[0..D)
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    const T alpha = sc.alpha;
+    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+        const int Q = occ[w];
+        const int s0 = bstart[Q], s1 = bend[Q];
+        int qc[D];
+        block_coords<D>(Q, sc.nb, qc);
+        __syncthreads();
+        for (int t = threadIdx.x; t < TN; t += blockDim.x) {
+            int tl[D], rem = t, nid = 0, loc = 0;
+            bool ok = true;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+                tl[a] = rem % TE;
+                rem /= TE;
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int nn = qc[a] * C::B + tl[a];
+                const int qb = nn >> C::LOGB;
+                ok &= qb < sc.nnb[a];
+                nid = nid * sc.nnb[a] + qb;
+                loc = (loc << C::LOGB) | (nn & (C::B - 1));
+            }
+            const size_t gi = (size_t)nid * C::NB + loc;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                tile[a * TN + t] = ok ? G.v[a][gi] : T(0);
+                tile[(D + a) * TN + t] = ok ? G.vold[a][gi] : T(0);
+            }
+        }
+        __syncthreads();
+        for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+            const int src = perm[i];
+            T x[D], v[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                x[a] = __ldg(Pin.x[a] + src);
+                v[a] = __ldg(Pin.v[a] + src);
+            }
+            T w[D][3], dw[D][3];
+            int tb[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                axis_weights<T, D>(x[a], sc.origin[a], sc.inv_dh, w[a], dw[a]);
+                const int b = int(dfloor<T>((x[a] - sc.origin[a]) * sc.inv_dh - T(0.5)));
+                tb[a] = b - qc[a] * C::B;
+            }
+            T vpic[D], vinc[D], L[D * D], Bm[D * D];
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+                vpic[a] = vinc[a] = T(0);
+#pragma unroll
+            for (int k = 0; k < D * D; ++k)
+                L[k] = Bm[k] = T(0);
+#pragma unroll
+            for (int k = 0; k < C::NOFF; ++k) {
+                int o[D];
+                int kk = k, ti = 0;
+#pragma unroll
+                for (int a = D - 1; a >= 0; --a) {
+                    o[a] = kk % 3;
+                    kk /= 3;
+                }
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    ti = ti * TE + tb[a] + o[a];
+                T phi = T(1);
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    phi *= w[a][o[a]];
+                T gw[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    T r = dw[a][o[a]];
+#pragma unroll
+                    for (int b = 0; b < D; ++b)
+                        if (b != a)
+                            r *= w[b][o[b]];
+                    gw[a] = r;
+                }
+                T nv[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    nv[a] = tile[a * TN + ti];
+                    const T nvo = tile[(D + a) * TN + ti];
+                    vpic[a] += phi * nv[a];
+                    vinc[a] += phi * (nv[a] - nvo);
+                }
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+#pragma unroll
+                    for (int b = 0; b < D; ++b)
+                        L[a * D + b] += nv[a] * gw[b];
+                if constexpr (APIC) {
+                    T r[D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        r[a] = (sc.origin[a] + T(qc[a] * C::B + tb[a] + o[a]) * sc.dh) - x[a];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+                            Bm[a * D + b] += phi * nv[a] * r[b];
+                }
+            }
+            T xn[D], vn[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                vn[a] = alpha * (v[a] + vinc[a]) + (T(1) - alpha) * vpic[a];
+                xn[a] = x[a] + sc.dt * vpic[a];
+            }
+            T m = __ldg(Pin.m + src), V = __ldg(Pin.V + src), rho = __ldg(Pin.rho + src), eps = __ldg(Pin.eps + src);
+            T szz = D == 2 ? __ldg(Pin.szz + src) : T(0);
+            T sig[C::NS];
+#pragma unroll
+            for (int s = 0; s < C::NS; ++s)
+                sig[s] = __ldg(Pin.sig[s] + src);
+            T Fm[D * D];
+            if constexpr (TRACKF) {
+#pragma unroll
+                for (int k = 0; k < D * D; ++k)
+                    Fm[k] = __ldg(Pin.F[k] + src);
+            }
+            bool ok_den = true;
+            if (FLAGS & P_CONSTIT) {
+                ok_den = constitutive_particle<T, D>(sc, sig, szz, rho, V, eps, L);
+                if constexpr (TRACKF) { // F <- (I + L dt) F (stepper.hpp:452-455)
+                    T Fn[D * D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int b = 0; b < D; ++b) {
+                            T s = T(0);
+#pragma unroll
+                            for (int k = 0; k < D; ++k)
+                                s += ((a == k ? T(1) : T(0)) + L[a * D + k] * sc.dt) * Fm[k * D + b];
+                            Fn[a * D + b] = s;
+                        }
+#pragma unroll
+                    for (int k = 0; k < D * D; ++k)
+                        Fm[k] = Fn[k];
+                }
+            }
+            const int pid = Pin.pid[src];
+            // write the new state at sorted slot i
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                Pout.x[a][i] = xn[a];
+                Pout.v[a][i] = vn[a];
+            }
+            Pout.m[i] = m;
+            Pout.V[i] = V;
+            Pout.rho[i] = rho;
+            Pout.eps[i] = eps;
+            if (D == 2)
+                Pout.szz[i] = szz;
+#pragma unroll
+            for (int s = 0; s < C::NS; ++s)
+                Pout.sig[s][i] = sig[s];
+#pragma unroll
+            for (int k = 0; k < D * D; ++k)
+                Pout.gv[k][i] = L[k];
+            if constexpr (APIC) {
+#pragma unroll
+                for (int k = 0; k < D * D; ++k)
+                    Pout.aff[k][i] = Bm[k];
+            }
+            if constexpr (TRACKF) {
+#pragma unroll
+                for (int k = 0; k < D * D; ++k)
+                    Pout.F[k][i] = Fm[k];
+            }
+            Pout.pid[i] = pid;
+            if (!ok_den) {
+                atomicMin(&st->den_pid, pid);
+                st->den_flag = 1;
+                st->abort = 1;
+            }
+            if (FLAGS & P_GUARD) { // ParticleSoA::all_finite (state.hpp:129-143)
+                bool fin = finite_(V) && finite_(rho) && finite_(eps) && finite_(szz);
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    fin &= finite_(xn[a]) && finite_(vn[a]);
+#pragma unroll
+                for (int s = 0; s < C::NS; ++s)
+                    fin &= finite_(sig[s]);
+#pragma unroll
+                for (int k = 0; k < D * D; ++k)
+                    fin &= finite_(L[k]) && (!APIC || finite_(Bm[k]));
+                if (!fin) {
+                    st->nan_flag = 1;
+                    st->abort = 1;
+                }
+            }
+            int key;
+            if (!cell_key<T, D>(sc, xn, key)) {
+                key = 0x7fffffff;
+                atomicMin(&st->ood_pid, pid);
+                st->ood_flag = 1;
+                st->abort = 1;
+            }
+            keys_out[i] = key;
+        }
+    }
+}
+
+// constitutive-only phase (constitutive_update on the stored grad_v), in place
+template <class T, int D, bool TRACKF>
+__global__ void k_constitutive(DevScene<T, D> sc, PBuf<T, D> P, int n, DevStatus* st)
+{
+    using C = Cfg<D>;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || st->abort)
+        return;
+    T L[D * D], sig[C::NS];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k)
+        L[k] = P.gv[k][i];
+#pragma unroll
+    for (int s = 0; s < C::NS; ++s)
+        sig[s] = P.sig[s][i];
+    T szz = D == 2 ? P.szz[i] : T(0), rho = P.rho[i], V = P.V[i], eps = P.eps[i];
+    if (!constitutive_particle<T, D>(sc, sig, szz, rho, V, eps, L)) {
+        atomicMin(&st->den_pid, P.pid[i]);
+        st->den_flag = 1;
+        return;
+    }
+#pragma unroll
+    for (int s = 0; s < C::NS; ++s)
+        P.sig[s][i] = sig[s];
+    if (D == 2)
+        P.szz[i] = szz;
+    P.rho[i] = rho;
+    P.V[i] = V;
+    P.eps[i] = eps;
+    if constexpr (TRACKF) {
+        T Fm[D * D], Fn[D * D];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k)
+            Fm[k] = P.F[k][i];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+                T s = T(0);
+#pragma unroll
+                for (int k = 0; k < D; ++k)
+                    s += ((a == k ? T(1) : T(0)) + L[a * D + k] * sc.dt) * Fm[k * D + b];
+                Fn[a * D + b] = s;
+            }
+#pragma unroll
+        for (int k = 0; k < D * D; ++k)
+            P.F[k][i] = Fn[k];
+    }
+}
+
+__global__ void k_step_end(DevStatus* st)
+{
+    if (!st->abort)
+        st->step += 1;
+}
+
+} // namespace mpmgpu

@@ -1,0 +1,197 @@
+// kernels_util.cuh -- boundary conversion and bookkeeping kernels.
+//
+// Host views use the reference's layout (std::vector<Eigen::Matrix>: vectors [n][d],
+// matrices [n][d*d] column-major). Upload places particle id p at storage slot p; download
+// scatters every slot back to its id, so the device's sorted order never leaks out.
+#pragma once
+
+#include "common.cuh"
+
+namespace mpmgpu {
+
+// staging layout (elements of T): per field a contiguous [n][comps] block
+enum StageField { S_X, S_V, S_M, S_VOL, S_RHO, S_EPS, S_SZZ, S_SIG, S_GV, S_AFF, S_F, S_NFIELDS };
+
+template <int D> __host__ __device__ constexpr int stage_comps(int f)
+{
+    return (f == S_X || f == S_V) ? D : (f >= S_SIG ? D * D : 1);
+}
+
+template <class T, int D> struct Stage {
+    T* f[S_NFIELDS];
+};
+
+template <class T, int D>
+__global__ void k_upload(Stage<T, D> S, PBuf<T, D> P, int n, int has_szz, int has_aff, int has_F)
+{
+    using C = Cfg<D>;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        P.x[a][i] = S.f[S_X][i * D + a];
+        P.v[a][i] = S.f[S_V][i * D + a];
+    }
+    P.m[i] = S.f[S_M][i];
+    P.V[i] = S.f[S_VOL][i];
+    P.rho[i] = S.f[S_RHO][i];
+    P.eps[i] = S.f[S_EPS][i];
+    if (D == 2)
+        P.szz[i] = has_szz ? S.f[S_SZZ][i] : T(0);
+    // column-major (r, c) at c*D + r; packed symmetric keeps the upper triangle (r <= c)
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = r; c < D; ++c)
+            P.sig[sym_idx<D>(r, c)][i] = S.f[S_SIG][i * D * D + c * D + r];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            P.gv[r * D + c][i] = S.f[S_GV][i * D * D + c * D + r];
+            if (has_aff)
+                P.aff[r * D + c][i] = S.f[S_AFF][i * D * D + c * D + r];
+            if (has_F)
+                P.F[r * D + c][i] = S.f[S_F][i * D * D + c * D + r];
+        }
+    P.pid[i] = i;
+    (void)C::NS;
+}
+
+template <class T, int D>
+__global__ void k_download(Stage<T, D> S, PBuf<T, D> P, int n, int has_aff, int has_F)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    const int p = P.pid[i];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        S.f[S_X][p * D + a] = P.x[a][i];
+        S.f[S_V][p * D + a] = P.v[a][i];
+    }
+    S.f[S_M][p] = P.m[i];
+    S.f[S_VOL][p] = P.V[i];
+    S.f[S_RHO][p] = P.rho[i];
+    S.f[S_EPS][p] = P.eps[i];
+    if (D == 2)
+        S.f[S_SZZ][p] = P.szz[i];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            S.f[S_SIG][p * D * D + c * D + r] = P.sig[sym_idx<D>(r, c)][i];
+            S.f[S_GV][p * D * D + c * D + r] = P.gv[r * D + c][i];
+            if (has_aff)
+                S.f[S_AFF][p * D * D + c * D + r] = P.aff[r * D + c][i];
+            if (has_F)
+                S.f[S_F][p * D * D + c * D + r] = P.F[r * D + c][i];
+        }
+}
+
+// unordered compaction of a dense predicate (list order does not affect results: every
+// listed block is processed independently)
+__global__ void k_compact_pos(const int* __restrict__ dense, int n, int* __restrict__ list, int* __restrict__ count)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool p = i < n && dense[i] >= 0;
+    unsigned m = __ballot_sync(0xffffffffu, p);
+    int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0 && m)
+        base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (p)
+        list[base + __popc(m & ((1u << lane) - 1))] = i;
+}
+
+__global__ void k_compact_flag(const unsigned char* __restrict__ dense, int n, int* __restrict__ list,
+                               int* __restrict__ count)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool p = i < n && dense[i] != 0;
+    unsigned m = __ballot_sync(0xffffffffu, p);
+    int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0 && m)
+        base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (p)
+        list[base + __popc(m & ((1u << lane) - 1))] = i;
+}
+
+// ---- digest: order-independent 64-bit sum of per-particle content hashes -------------
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z)
+{
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+template <class T> __device__ __forceinline__ unsigned long long bits_of(T x);
+template <> __device__ __forceinline__ unsigned long long bits_of<double>(double x)
+{
+    return (unsigned long long)__double_as_longlong(x);
+}
+template <> __device__ __forceinline__ unsigned long long bits_of<float>(float x)
+{
+    return (unsigned long long)(unsigned)__float_as_uint(x);
+}
+
+template <class T, int D>
+__global__ void k_digest(PBuf<T, D> P, int n, int has_aff, unsigned long long* out)
+{
+    using C = Cfg<D>;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long h = 0;
+    if (i < n) {
+        h = mix64((unsigned long long)P.pid[i]);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            h = mix64(h ^ bits_of(P.x[a][i]));
+            h = mix64(h ^ bits_of(P.v[a][i]));
+        }
+        h = mix64(h ^ bits_of(P.V[i]));
+        h = mix64(h ^ bits_of(P.rho[i]));
+        h = mix64(h ^ bits_of(P.eps[i]));
+        if (D == 2)
+            h = mix64(h ^ bits_of(P.szz[i]));
+#pragma unroll
+        for (int s = 0; s < C::NS; ++s)
+            h = mix64(h ^ bits_of(P.sig[s][i]));
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) {
+            h = mix64(h ^ bits_of(P.gv[k][i]));
+            if (has_aff)
+                h = mix64(h ^ bits_of(P.aff[k][i]));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        h += __shfl_down_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0)
+        atomicAdd(out, h);
+}
+
+// max |v| (stepper.hpp:491-498) as the bit pattern of a non-negative double
+template <class T, int D>
+__global__ void k_max_speed(PBuf<T, D> P, int n, unsigned long long* out)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double s = 0;
+    if (i < n) {
+        T q = T(0);
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            q += P.v[a][i] * P.v[a][i];
+        s = (double)dsqrt<T>(q);
+        if (!(s >= 0))
+            s = __longlong_as_double(0x7ff0000000000000ll); // NaN -> +inf
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        s = fmax(s, __shfl_down_sync(0xffffffffu, s, o));
+    if ((threadIdx.x & 31) == 0)
+        atomicMax(out, (unsigned long long)__double_as_longlong(s));
+}
+
+} // namespace mpmgpu
