@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MPM step (BASELINE.json metric: particle-steps/s, fwd, with HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C4] [--dtype f64]
+
+Workload (N=1): C4 -- 3-D granular column collapse, Drucker-Prager sand, FLIP, 128x64x64-cell
+column = 4,194,304 particles on a 256^3 grid, f64 (the reference's precision), synthetic input
+from init_scene. A "step" is one forward MPM step Phi over all particles.
+  value      particle-steps/s over K steps timed with CUDA events on the library's stream,
+             state resident in HBM (1.4 GB >> 126 MB L2: no flush needed), max over ranks.
+  e2e        the same metric through the reference-facing C ABI with HOST buffers: one
+             `run`-style call = mpm_state_upload (pinned host -> device) + mpm_advance(K) +
+             mpm_state_download, wall-clock, so host<->device copies are inside the region.
+  roofline   dominant kernel (largest share of the step) measured live with CUDA events:
+             algorithmic bytes per launch / mean launch time vs MEASURED_PEAKS.json hbm_gbs;
+             plus the whole-step figure N_p * B_fwd / t_step (B_fwd from SURVEY.md §8d).
+  cpu_baseline  the reference compiled unmodified (oracle/_ref, "reference") -- or the oracle
+             restatement ("port") if absent -- on a bounded sample of the same workload, one
+             process per host core.
+N>1 (torchrun): weak scaling, one C4 replica per rank (replicas only in this revision: the NCCL
+slab decomposition of §8e is not yet on this path), max-over-ranks device time.
+--impl reference: the reference's own CPU implementation of the step on all host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "particle-steps/sec (fwd)"
+UNIT = "particle-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---- algorithmic bytes ------------------------------------------------------
+def bytes_model(scene, n_particles, active_nodes):
+    """B_fwd = (IN + OUT) s + (A/N_p) 2 (1 + 2d) s, IN/OUT per SURVEY §8d (D-P adds eps, 2-D sigma_zz)."""
+    d = scene.dim
+    s = 8 if scene.dtype == "f64" else 4
+    ns = 3 if d == 2 else 6
+    dp = scene.material.__class__.__name__ == "DruckerPragerParams"
+    IN = 2 * d + 2 + 1 + ns + (1 if dp else 0) + (1 if (dp and d == 2) else 0)    # x v m V rho sig (+eps, +szz)
+    OUT = 2 * d + 2 + ns + d * d + (1 if dp else 0) + (1 if (dp and d == 2) else 0)  # x v V rho sig gradv (+eps, +szz)
+    per_particle = (IN + OUT) * s
+    grid = 2 * (1 + 2 * d) * s * active_nodes / n_particles
+    return per_particle + grid, IN, OUT
+
+
+def kernel_bytes(scene, n, active_nodes, occupied_blocks):
+    """Compulsory bytes per launch of the two particle kernels."""
+    d = scene.dim
+    s = 8 if scene.dtype == "f64" else 4
+    ns = 3 if d == 2 else 6
+    dp = scene.material.__class__.__name__ == "DruckerPragerParams"
+    B = 16 if d == 2 else 8
+    tile = (B + 2) ** d
+    nf = 1 + 2 * d
+    # k_p2g: read x v m V sigma (+ perm, keys) per particle; write one partial tile per block
+    p2g = n * ((2 * d + 2 + ns) * s + 8) + occupied_blocks * tile * nf * s
+    # k_g2p: read + write the whole particle record (+ perm, pid, key) and the node tiles (v, v_old)
+    rec_in = 2 * d + 4 + ns + (1 if (dp and d == 2) else 0)
+    rec_out = rec_in + d * d
+    g2p = n * ((rec_in + rec_out) * s + 4 * 4) + occupied_blocks * tile * 2 * d * s
+    return {"k_p2g": p2g, "k_g2p": g2p}
+
+
+# ---- clocks sampler -------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm = [float(p[0]) for p in self.samples if p[0].replace(".", "").isdigit()]
+        mx = [float(p[1]) for p in self.samples if p[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for p in self.samples:
+            for k, nme in enumerate(names):
+                if p[3 + k].lower() in ("active", "1"):
+                    reasons.add(nme)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---- CPU baseline (the reference on host cores) --------------------------------------------
+def _cpu_worker(args):
+    """One host core: the reference's own run() timer (stepper.hpp:504-535) on the full scene."""
+    cfg, dtype, kind, steps = args
+    sys.path.insert(0, str(ROOT))
+    from oracle import CpuOracle  # test infrastructure: the CPU baseline, never the product path
+    from paper_2507_04192_b200.presets import CONFIGS
+    s = CONFIGS[cfg](dtype)
+    o = CpuOracle(kind)
+    st = o.init_scene(s)
+    secs = o.run_seconds_per_1000(s, st, steps) / 1000.0 * steps
+    return st.particles.size() * steps, secs
+
+
+def _mem_available_gb():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) / 1e6
+    except Exception:
+        pass
+    return 16.0
+
+
+def cpu_baseline(cfg, dtype, steps=1):
+    """The reference (or the restatement) on the same scene, `steps` steps, one process per core
+    (independent replicas are the reference's only sanctioned concurrency), capped
+    by host memory. Value = sum of the per-process rates."""
+    import multiprocessing as mp
+    import oracle
+    kind = "ref" if oracle.available("ref") else "orc"
+    cores = os.cpu_count() or 1
+    per_proc_gb = {"C4": 6.0, "C5": 40.0}.get(cfg, 1.0) * (0.5 if dtype == "f32" else 1.0)
+    procs = max(1, min(cores, int(_mem_available_gb() * 0.6 / per_proc_gb)))
+    with mp.get_context("spawn").Pool(procs) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, [(cfg, dtype, kind, steps)] * procs)
+        wall = time.perf_counter() - t0
+    per_proc = [r[0] / r[1] for r in res]
+    value = sum(per_proc)
+    n = int(res[0][0] / steps)
+    sample = (f"{procs} concurrent replicas (one per host core, of {cores}) of the full {cfg} scene "
+              f"({n} particles), {steps} step(s) each, timed by the reference's run() timer; "
+              f"value = sum of per-process particle-steps/s")
+    return {"value": value, "unit": UNIT, "cores": procs, "host_cores": cores,
+            "kind": "reference" if kind == "ref" else "port", "sample": sample,
+            "single_process": per_proc[0], "wall_s": wall,
+            "label": "reference compiled against the Eigen-API shim (C++20 -O3 -DNDEBUG, serial)"
+            if kind == "ref" else "oracle restatement (C++20 -O3, serial)"}
+
+
+# ---- GPU arm -----------------------------------------------------------------------------------
+def bench_b200(a, rank, world, local):
+    import ctypes as C
+
+    import torch
+    from paper_2507_04192_b200 import capi, init_scene
+    from paper_2507_04192_b200.presets import CONFIGS
+    from paper_2507_04192_b200.solver import Context
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    s = CONFIGS[a.config](a.dtype)
+    st = init_scene(s)
+    n = st.particles.size()
+    ctx = Context(s, n, device=local)
+    ctx.upload(st)
+    ctx.advance(a.warmup)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = ctx.launch_count()
+    barrier()
+    ms = ctx.advance_timed(a.steps)
+    barrier()
+    launches = ctx.launch_count() - l0
+    ck = clocks.stop()
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / a.steps
+    value = n * world * a.steps / (ms / 1e3)
+
+    active_nodes, occ_blocks, act_blocks = ctx.grid_stats()
+    active_nodes_step = active_nodes / a.steps
+    B_fwd, IN, OUT = bytes_model(s, n, active_nodes_step)
+
+    # ---- per-kernel profile (CUDA events around each launch on the library stream)
+    ctx.profile(True)
+    ctx.profile_reset()
+    ctx.advance(3)
+    prof = {}
+    for k in ("k_p2g", "k_grid", "k_g2p", "k_seg", "k_compact", "k_mark_nodes", "k_step_end", "k_keys"):
+        t_ms, cnt = ctx.profile_query(k)
+        if cnt:
+            prof[k] = {"ms_per_launch": t_ms / cnt, "launches": cnt}
+    total_ms, _ = ctx.profile_query("")
+    ctx.profile(False)
+    kb = kernel_bytes(s, n, active_nodes_step, occ_blocks)
+    dom = max(("k_p2g", "k_g2p"), key=lambda k: prof.get(k, {}).get("ms_per_launch", 0))
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    dom_ms = prof[dom]["ms_per_launch"]
+    achieved = kb[dom] / (dom_ms / 1e3) / 1e9
+    step_gbs = n * B_fwd / (ms_per_step / 1e3) / 1e9
+
+    # ---- e2e through the C ABI with pinned host buffers (upload + K steps + download)
+    e2e = None
+    if rank == 0:
+        e2e = bench_e2e(ctx, s, st, a.steps)
+
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    if rank != 0:
+        return None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": a.dtype, "data": "synthetic (init_scene seeding of the named scene, deterministic)",
+        "config": {"workload": f"{a.config}: 3-D D-P granular column collapse, FLIP, 128x64x64-cell column on 256^3 "
+                               f"grid, dt 1e-5" if a.config == "C4" else a.config,
+                   "particles_per_gpu": n, "grid_cells": s.config.cells, "parallelism": f"replicas x{world}",
+                   "l2_policy": "inputs (state ~1.4 GB f64) larger than the 126 MB L2; no flush",
+                   "algorithmic_bytes_per_particle_step": B_fwd, "active_nodes_per_particle": active_nodes_step / n},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "algorithmic_bytes_per_launch": kb[dom], "mean_launch_ms": dom_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
+                     "step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak,
+                              "bytes_per_particle_step": B_fwd}},
+        "kernels": prof, "profiled_step_ms": total_ms / 3,
+        "clocks": ck, "gpu_launches": launches, "e2e": e2e,
+    }
+    return line
+
+
+def bench_e2e(ctx, s, st, steps):
+    """One reference-style run call through the C ABI on pinned host buffers."""
+    import ctypes as C
+
+    import torch
+    from paper_2507_04192_b200 import capi
+
+    p = st.particles
+    d = s.dim
+    T = p.dtype
+    n = p.size()
+
+    def pinned(shape):
+        t = torch.empty(shape, dtype=torch.float64 if T == np.float64 else torch.float32, pin_memory=True)
+        return t.numpy()
+
+    host = {"x": pinned((n, d)), "v": pinned((n, d)), "mass": pinned((n,)), "volume": pinned((n,)),
+            "rho": pinned((n,)), "eps_eq": pinned((n,)), "sigma": pinned((n, d * d)), "grad_v": pinned((n, d * d))}
+    if d == 2:
+        host["sigma_zz"] = pinned((n,))
+    host["x"][...] = p.x
+    host["v"][...] = p.v
+    host["mass"][...] = p.mass
+    host["volume"][...] = p.volume
+    host["rho"][...] = p.rho
+    host["eps_eq"][...] = p.eps_eq
+    host["sigma"][...] = np.transpose(p.sigma, (0, 2, 1)).reshape(n, d * d)
+    host["grad_v"][...] = np.transpose(p.grad_v, (0, 2, 1)).reshape(n, d * d)
+    if d == 2:
+        host["sigma_zz"][...] = p.sigma_zz
+    view = capi.StateView()
+    view.n = n
+    for k, arr in host.items():
+        setattr(view, k, arr.ctypes.data)
+    view.step = 0
+    view.time = 0.0
+    out = capi.StateView()
+    outb = {k: pinned(v.shape) for k, v in host.items()}
+    out.n = n
+    for k, arr in outb.items():
+        setattr(out, k, arr.ctypes.data)
+    lib = ctx.lib
+    nbytes_in = sum(v.nbytes for v in host.values())
+    nbytes_out = sum(v.nbytes for v in outb.values())
+    # warm path once
+    ctx.check(lib.mpm_state_upload(ctx.h, C.byref(view)))
+    ctx.check(lib.mpm_advance(ctx.h, 1, 0))
+    ctx.check(lib.mpm_state_download(ctx.h, C.byref(out)))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.check(lib.mpm_state_upload(ctx.h, C.byref(view)))
+    ctx.check(lib.mpm_advance(ctx.h, steps, 0))
+    ctx.check(lib.mpm_state_download(ctx.h, C.byref(out)))
+    t1 = time.perf_counter()
+    return {"value": n * steps / (t1 - t0), "unit": UNIT, "h2d_bytes_per_step": nbytes_in / steps,
+            "d2h_bytes_per_step": nbytes_out / steps,
+            "call": f"mpm_state_upload (pinned host) + mpm_advance({steps}) + mpm_state_download, wall clock",
+            "seconds": t1 - t0}
+
+
+def bench_reference(a, rank, world):
+    """--impl reference: the reference's own CPU implementation of the step (oracle/_ref, compiled
+    unmodified against the Eigen shim) on all host cores, rank 0 only; each process runs
+    the full scene for 2 steps (a bounded sample: ~10-30 s per step per core at C4)."""
+    if rank != 0:
+        return None
+    res = cpu_baseline(a.config, a.dtype, 2)
+    value = res["value"]
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": a.dtype, "data": "synthetic (init_scene seeding)",
+            "config": {"workload": a.config, "sample": res["sample"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
+                             "sample": res["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    a = parse()
+    rank, world, local = dist_env()
+    if a.impl == "reference":
+        line = bench_reference(a, rank, world)
+        if line:
+            print(json.dumps(line), flush=True)
+        return
+    line = bench_b200(a, rank, world, local)
+    if line is not None:
+        if not a.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(a.config, a.dtype, 1)
+            except Exception as e:  # the baseline is reported, never the target
+                line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

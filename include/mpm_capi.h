@@ -189,6 +189,9 @@ int mpm_max_speed(mpm_ctx* ctx, double* vmax);
 /* n x Stepper::advance (stepper.hpp:472-482); MPM_ADV_NAN_GUARD adds run()'s all_finite
  * check after every step (stepper.hpp:519-522). */
 int mpm_advance(mpm_ctx* ctx, int64_t n_steps, uint32_t flags);
+/* mpm_advance with CUDA events recorded on the context stream around the n steps:
+ * *device_ms = device time of the steps (bench / instrumentation) */
+int mpm_advance_timed(mpm_ctx* ctx, int64_t n_steps, uint32_t flags, double* device_ms);
 /* phase functions (each backs one reference free function, for per-phase parity):
  * p2g (transfer.hpp:402-434), grid_momentum_update (transfer.hpp:440-449),
  * apply_grid_corrections (contact.hpp:394-411), g2p (transfer.hpp:457-486),

@@ -166,6 +166,7 @@ _PROTOS = {
     "mpm_state_digest": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "mpm_max_speed": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "mpm_advance": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint32]),
+    "mpm_advance_timed": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint32, C.POINTER(C.c_double)]),
     "mpm_p2g": (C.c_int, [C.c_void_p]),
     "mpm_grid_momentum_update": (C.c_int, [C.c_void_p]),
     "mpm_grid_corrections": (C.c_int, [C.c_void_p]),

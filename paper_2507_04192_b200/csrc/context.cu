@@ -57,6 +57,7 @@ struct CtxBase {
     virtual uint64_t digest() = 0;
     virtual double max_speed() = 0;
     virtual void advance(int64_t n, uint32_t flags) = 0;
+    virtual double advance_timed(int64_t n, uint32_t flags) = 0;
     virtual void phase_p2g() = 0;
     virtual void phase_mom() = 0;
     virtual void phase_corr() = 0;
@@ -590,8 +591,18 @@ template <class T, int D> struct Ctx : CtxBase {
             throw ApiError(MPM_ERR_USAGE, "no state uploaded");
         if (nsteps <= 0)
             return;
-        const bool guard = flags & MPM_ADV_NAN_GUARD;
         const int64_t step0 = step;
+        advance_enqueue(nsteps, flags);
+        check_status(step0);
+    }
+
+    void advance_enqueue(int64_t nsteps, uint32_t flags)
+    {
+        if (n == 0)
+            throw ApiError(MPM_ERR_USAGE, "no state uploaded");
+        if (nsteps <= 0)
+            return;
+        const bool guard = flags & MPM_ADV_NAN_GUARD;
         reset_status();
         if (prof) {
             for (int64_t k = 0; k < nsteps; ++k)
@@ -619,9 +630,25 @@ template <class T, int D> struct Ctx : CtxBase {
                 cur ^= 1;
             }
         }
-        check_status(step0);
     }
     int64_t graph_launches = 0;
+
+    double advance_timed(int64_t nsteps, uint32_t flags) override
+    {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, stream));
+        advance_enqueue(nsteps, flags);
+        CK(cudaEventRecord(b, stream));
+        CK(cudaEventSynchronize(b));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        check_status(step);
+        return ms;
+    }
 
     // ---- phase functions (per-phase parity with the reference free functions) ---------------
     void phase_p2g() override
@@ -882,6 +909,14 @@ int mpm_state_download(mpm_ctx* c, mpm_state_view* s) { MPM_CALL(c, c->impl->dow
 int mpm_state_digest(mpm_ctx* c, uint64_t* out) { MPM_CALL(c, *out = c->impl->digest()); }
 int mpm_max_speed(mpm_ctx* c, double* v) { MPM_CALL(c, *v = c->impl->max_speed()); }
 int mpm_advance(mpm_ctx* c, int64_t n, uint32_t flags) { MPM_CALL(c, c->impl->advance(n, flags)); }
+int mpm_advance_timed(mpm_ctx* c, int64_t n, uint32_t flags, double* ms)
+{
+    MPM_CALL(c, {
+        double t = c->impl->advance_timed(n, flags);
+        if (ms)
+            *ms = t;
+    });
+}
 int mpm_p2g(mpm_ctx* c) { MPM_CALL(c, c->impl->phase_p2g()); }
 int mpm_grid_momentum_update(mpm_ctx* c) { MPM_CALL(c, c->impl->phase_mom()); }
 int mpm_grid_corrections(mpm_ctx* c) { MPM_CALL(c, c->impl->phase_corr()); }

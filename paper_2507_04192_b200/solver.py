@@ -75,6 +75,13 @@ class Context:
     def advance(self, n: int, nan_guard: bool = False):
         self.check(self.lib.mpm_advance(self.h, int(n), capi.MPM_ADV_NAN_GUARD if nan_guard else 0))
 
+    def advance_timed(self, n: int, nan_guard: bool = False) -> float:
+        """advance n steps; returns the device time (ms) from CUDA events on the context stream"""
+        ms = C.c_double()
+        self.check(self.lib.mpm_advance_timed(self.h, int(n), capi.MPM_ADV_NAN_GUARD if nan_guard else 0,
+                                              C.byref(ms)))
+        return ms.value
+
     def digest(self) -> int:
         d = C.c_uint64()
         self.check(self.lib.mpm_state_digest(self.h, C.byref(d)))
