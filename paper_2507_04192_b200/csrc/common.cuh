@@ -106,7 +106,7 @@ struct DevStatus {
     int den_pid;
     int ood_pid;
     int far_flag;
-    int pad;
+    int ood_counted;      // the completed step whose output left the domain was counted
     long long step;       // absolute step index of the state currently in the buffers
     long long err_step;   // step during which a den/nan error occurred
     unsigned long long active_nodes;

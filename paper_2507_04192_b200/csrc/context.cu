@@ -495,8 +495,6 @@ template <class T, int D> struct Ctx : CtxBase {
         if (s.ood_flag) {
             // keys of step s.step+1's output -> the state after that step is complete; the
             // next P2G is where the reference throws (bspline.hpp:322-327)
-            if (s.err_step >= 0 || s.step != step_before || true) {
-            }
             throw ApiError(MPM_ERR_OUT_OF_DOMAIN,
                            "particle " + std::to_string(s.ood_pid) + " outside valid grid interior", s.ood_pid,
                            s.step + 1);
@@ -689,6 +687,13 @@ template <class T, int D> struct Ctx : CtxBase {
         reset_status();
         sort_and_segment();
         g2p_kernel_fl<0>();
+        fetch_status();
+        if (st_host->abort && st_host->ood_flag == 2 && !st_host->den_flag && !st_host->nan_flag) {
+            // g2p itself does not check the domain (transfer.hpp:457-486): the next p2g throws
+            reset_status();
+            keys_valid = false;
+            return;
+        }
         check_status(step);
     }
     void phase_constit() override
@@ -792,7 +797,218 @@ template <class T, int D> struct Ctx : CtxBase {
             *anb = cnt[1];
     }
 
+    // ---- small transfer helpers (used by the adjoint workspace) ---------------------------------
+    void h2d(T* dst, const T* src, int64_t k) { CK(cudaMemcpyAsync(dst, src, k * sizeof(T), cudaMemcpyHostToDevice, stream)); CK(cudaStreamSynchronize(stream)); }
+    void d2h(T* dst, const T* src, int64_t k) { CK(cudaMemcpyAsync(dst, src, k * sizeof(T), cudaMemcpyDeviceToHost, stream)); CK(cudaStreamSynchronize(stream)); }
+    void zero(T* dst, int64_t k) { if (dst) CK(cudaMemsetAsync(dst, 0, k * sizeof(T), stream)); }
+    void h2d_raw(void* dst, const void* src, size_t b) { CK(cudaMemcpyAsync(dst, src, b, cudaMemcpyHostToDevice, stream)); CK(cudaStreamSynchronize(stream)); }
+    void d2h_raw(void* dst, const void* src, size_t b) { CK(cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToHost, stream)); CK(cudaStreamSynchronize(stream)); }
+
+    // every device array of a particle buffer, for slot copies
+    std::vector<std::pair<void*, size_t>> pbuf_arrays(const PBuf<T, D>& P)
+    {
+        std::vector<std::pair<void*, size_t>> v;
+        for (int a = 0; a < D; ++a) {
+            v.push_back({P.x[a], sizeof(T)});
+            v.push_back({P.v[a], sizeof(T)});
+        }
+        v.push_back({P.m, sizeof(T)});
+        v.push_back({P.V, sizeof(T)});
+        v.push_back({P.rho, sizeof(T)});
+        v.push_back({P.eps, sizeof(T)});
+        if (D == 2)
+            v.push_back({P.szz, sizeof(T)});
+        for (int q = 0; q < C::NS; ++q)
+            v.push_back({P.sig[q], sizeof(T)});
+        for (int k = 0; k < D * D; ++k) {
+            v.push_back({P.gv[k], sizeof(T)});
+            if (has_aff)
+                v.push_back({P.aff[k], sizeof(T)});
+            if (has_F)
+                v.push_back({P.F[k], sizeof(T)});
+        }
+        v.push_back({P.pid, sizeof(int)});
+        return v;
+    }
+    void pbuf_copy(const PBuf<T, D>& dst, const PBuf<T, D>& src)
+    {
+        auto d = pbuf_arrays(dst), s = pbuf_arrays(src);
+        for (size_t i = 0; i < d.size(); ++i)
+            CK(cudaMemcpyAsync(d[i].first, s[i].first, n * s[i].second, cudaMemcpyDeviceToDevice, stream));
+    }
+    PBuf<T, D> pbuf_alloc(std::vector<void*>& owned)
+    {
+        PBuf<T, D> P{};
+        const size_t before = allocs.size();
+        alloc_pbuf(P);
+        for (size_t i = before; i < allocs.size(); ++i)
+            owned.push_back(allocs[i]);
+        allocs.resize(before); // owned by the caller
+        return P;
+    }
+    uint64_t digest_of(const PBuf<T, D>& P)
+    {
+        CK(cudaMemsetAsync(d_red, 0, sizeof(unsigned long long), stream));
+        launch("k_digest", [&] { k_digest<T, D><<<grid_for(n, 256), 256, 0, stream>>>(P, int(n), has_aff, d_red); });
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, d_red, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        return h;
+    }
+
     // ---- adjoint (kernels_adj.cuh) -------------------------------------------------------------
+    // backprop_trajectory (checkpoint.hpp:72-143): forward sweep keeping segment-start states in
+    // HBM slots (+ a device digest at every boundary), then per segment (reversed): replay into
+    // L+1 slots, digest check against the sweep (checkpoint.hpp:124-126), seed + step_vjp per step.
+    void backprop_run(AdjWork<T, D>& aw, const mpm_state_view* s0, int64_t total, int nseg, const mpm_seeder_desc* sd,
+                      mpm_cot_view* c0, mpm_param_grads* pg, mpm_backprop_result* res)
+    {
+        if (total < 1)
+            throw ApiError(MPM_ERR_VALIDATION, "checkpoint plan: need at least one step");
+        if (nseg < 1 || int64_t(nseg) > total)
+            throw ApiError(MPM_ERR_VALIDATION, "checkpoint plan: n_segments must lie in [1, N_t]");
+        std::vector<int64_t> bnd(nseg + 1, 0);
+        {
+            const int64_t base = total / nseg, rem = total % nseg;
+            int64_t at = 0;
+            for (int k = 0; k < nseg; ++k) {
+                at += base + (k < rem ? 1 : 0);
+                bnd[k + 1] = at;
+            }
+        }
+        int64_t Lmax = 0;
+        for (int k = 0; k < nseg; ++k)
+            Lmax = std::max(Lmax, bnd[k + 1] - bnd[k]);
+        upload(s0);
+        aw.ensure(*this);
+        const int64_t step0 = step;
+        const PBuf<T, D> own0 = buf[0], own1 = buf[1];
+        const int cur0 = cur;
+        // seeder tables on the device
+        const bool seeding = sd && sd->kind == MPM_SEEDER_LAGRANGIAN_LS && sd->n_obs > 0;
+        const int64_t nsel = seeding ? (sd->sel ? sd->n_sel : n) : 0;
+        std::vector<void*> owned;
+        long long* d_sel = nullptr;
+        T* d_tgt = nullptr;
+        if (seeding) {
+            if (sd->sel) {
+                CK(cudaMalloc(&d_sel, nsel * sizeof(long long)));
+                owned.push_back(d_sel);
+                std::vector<long long> hs(sd->sel, sd->sel + nsel);
+                for (long long p : hs)
+                    if (p < 0 || p >= n)
+                        throw ApiError(MPM_ERR_VALIDATION, "seeder: particle index out of range");
+                h2d_raw(d_sel, hs.data(), nsel * sizeof(long long));
+            }
+            CK(cudaMalloc(&d_tgt, (size_t)sd->n_obs * nsel * D * sizeof(T)));
+            owned.push_back(d_tgt);
+            h2d_raw(d_tgt, sd->target, (size_t)sd->n_obs * nsel * D * sizeof(T));
+        }
+        auto obs_index = [&](int64_t t) {
+            if (!seeding)
+                return -1;
+            for (int k = 0; k < sd->n_obs; ++k)
+                if (sd->obs_steps[k] == t)
+                    return k;
+            return -1;
+        };
+        auto seed = [&](const PBuf<T, D>& P, int k, int cb, int do_cot) {
+            launch("k_slot_of_pid", [&] { k_slot_of_pid<T, D><<<grid_for(n, 256), 256, 0, stream>>>(P, int(n), aw.slot_of_pid); });
+            launch("k_seed", [&] {
+                k_seed_lagrangian<T, D><<<1, 1024, 0, stream>>>(P, int(n), aw.slot_of_pid, d_sel, nsel,
+                                                                d_tgt + (size_t)k * nsel * D, sd->field, aw.cot[cb],
+                                                                do_cot, aw.loss_acc);
+            });
+        };
+        try {
+            std::vector<PBuf<T, D>> ckpt(nseg), replay(Lmax + 1);
+            for (auto& P : ckpt)
+                P = pbuf_alloc(owned);
+            for (auto& P : replay)
+                P = pbuf_alloc(owned);
+            std::vector<uint64_t> bhash(nseg + 1);
+            CK(cudaMemsetAsync(aw.loss_acc, 0, sizeof(double), stream));
+            // forward sweep
+            reset_status();
+            if (obs_index(0) >= 0)
+                seed(buf[cur], obs_index(0), 0, 0);
+            for (int k = 0; k < nseg; ++k) {
+                pbuf_copy(ckpt[k], buf[cur]);
+                bhash[k] = digest_of(buf[cur]);
+                for (int64_t t = bnd[k]; t < bnd[k + 1]; ++t) {
+                    step_once(false);
+                    if (obs_index(t + 1) >= 0)
+                        seed(buf[cur], obs_index(t + 1), 0, 0);
+                }
+            }
+            bhash[nseg] = digest_of(buf[cur]);
+            check_status(step0);
+            double loss = 0;
+            d2h_raw(&loss, aw.loss_acc, sizeof(double));
+            // backward sweep
+            aw.cot_zero(*this, 0);
+            aw.pg_reset(*this, pg);
+            int cb = 0;
+            int64_t peak = 0;
+            for (int k = nseg - 1; k >= 0; --k) {
+                const int64_t b0 = bnd[k], b1 = bnd[k + 1], len = b1 - b0;
+                pbuf_copy(replay[0], ckpt[k]);
+                for (int64_t j = 0; j < len; ++j) {
+                    buf[0] = replay[j];
+                    buf[1] = replay[j + 1];
+                    cur = 0;
+                    keys_valid = false;
+                    step_once(false);
+                }
+                peak = std::max(peak, len + 1);
+                if (digest_of(replay[len]) != bhash[k + 1])
+                    throw ApiError(MPM_ERR_CHECKPOINT,
+                                   "checkpoint mismatch: recomputed segment end differs from the recorded state at step "
+                                       + std::to_string(step0 + b1));
+                for (int64_t t = b1; t > b0; --t) {
+                    if (obs_index(t) >= 0)
+                        seed(replay[t - b0], obs_index(t), cb, 1);
+                    buf[0] = replay[t - b0 - 1];
+                    buf[1] = replay[t - b0];
+                    cur = 0;
+                    keys_valid = false;
+                    aw.vjp_enqueue(*this, cb, cb ^ 1);
+                    cb ^= 1;
+                }
+                check_status(step);
+            }
+            if (obs_index(0) >= 0)
+                seed(ckpt[0], obs_index(0), cb, 1);
+            CK(cudaStreamSynchronize(stream));
+            aw.cot_download(*this, c0, cb);
+            aw.pg_download(*this, pg);
+            if (res) {
+                res->loss = loss;
+                res->checkpoints_stored = nseg;
+                res->peak_replay_states = peak;
+            }
+            // restore the context's own buffers holding S0
+            buf[0] = own0;
+            buf[1] = own1;
+            cur = cur0;
+            pbuf_copy(buf[cur], ckpt[0]);
+            step = step0;
+            keys_valid = false;
+            CK(cudaStreamSynchronize(stream));
+        } catch (...) {
+            buf[0] = own0;
+            buf[1] = own1;
+            cur = cur0;
+            keys_valid = false;
+            cudaStreamSynchronize(stream);
+            for (void* p : owned)
+                cudaFree(p);
+            throw;
+        }
+        for (void* p : owned)
+            cudaFree(p);
+    }
+
     void step_vjp(const mpm_state_view* s, const mpm_cot_view* co, mpm_cot_view* ci, mpm_param_grads* pg) override
     {
         aw.step_vjp_api(*this, s, co, ci, pg);

@@ -1,26 +1,1761 @@
-// kernels_adj.cuh -- reverse-mode adjoint of the step (adjoint.hpp) -- placeholder.
+// kernels_adj.cuh -- reverse-mode adjoint of the step (adjoint.hpp:328-525) and the segmented
+// checkpoint driver (checkpoint.hpp:72-143) on B200.
+//
+// Cotangents are stored in particle-id order (pid-indexed), so the per-step cell re-sort of the
+// forward state never has to be inverted: step t's cotangent and step t-1's state meet through
+// pid. step_vjp = forward replay (sort, P2G, grid with stored m/p/f) then
+//   K5a k_adj_g2pT_gather  per particle: G2P gather of grad v (forward), constitutive VJP
+//                          (fluid_vjp adjoint.hpp:153-184 / dp_vjp :188-293), the gather half of
+//                          the G2P transpose (x cotangent, :429-434); writes per-particle scatter
+//                          records in sorted order
+//   K5b k_adj_scatter      G2P transpose scatter (:427-428, 436) of gv_cot / gvold_cot into
+//                          per-block partial tiles: the deterministic node-column march of P2G
+//   K6  k_adj_grid         per node: fixed-order partial sum, correction-chain VJP replayed
+//                          from v_tilde (:441-460, node_correction_vjp :114-150), momentum
+//                          update transpose (:462-477)
+//   K7  k_adj_p2gT         per particle: P2G transpose gather (:479-524)
+// Parameter gradients (c, mu, friction segments) are reduced per block and then over blocks
+// in a fixed order: adjoints are bit-reproducible run to run.
 #pragma once
 
 #include "common.cuh"
+#include "constit.cuh"
+#include "kernels_fwd.cuh"
+#include "kernels_util.cuh"
 
 #include <stdexcept>
+#include <vector>
 
 namespace mpmgpu {
 
-template <class T, int D> struct AdjWork {
-    template <class Ctx> void init(Ctx&) {}
-    void free_all() {}
-    template <class Ctx> void set_attrs(Ctx&) {}
-    template <class Ctx>
-    void step_vjp_api(Ctx&, const mpm_state_view*, const mpm_cot_view*, mpm_cot_view*, mpm_param_grads*)
-    {
-        throw std::runtime_error("step_vjp: adjoint kernels not built yet");
+constexpr int PG_SLOTS = 2 + MAX_FRIC; // c, mu, friction[fric_off[w] + k]
+
+// pid-indexed cotangent arrays (StateCotangent, adjoint.hpp:10-72); matrices full, row-major
+template <class T, int D> struct CBuf {
+    T* x[D];
+    T* v[D];
+    T* rho;
+    T* V;
+    T* eps;
+    T* szz;
+    T* sig[D * D];
+    T* gv[D * D];
+    T* aff[D * D];
+};
+
+// per-particle scatter records of the G2P transpose, sorted-slot order
+template <class T, int D> struct SBuf {
+    T* a[D];       // pic_cot + inc_cot
+    T* inc[D];     // inc_cot
+    T* L[D * D];   // grad v_new cotangent
+    T* Bc[D * D];  // APIC: affine cotangent (cot_out.affine)
+};
+
+// cotangent grid (node blocks): gv_cot / gvold_cot sums are transient; these are the outputs of K6
+template <class T, int D> struct GCBuf {
+    T* gm;
+    T* gmom[D];
+    T* gf[D];
+};
+
+// ---- device VJP math ----------------------------------------------------------------------
+// detail::fluid_vjp (adjoint.hpp:152-184); L row-major; sc_ (sigma cotangent) full row-major
+template <class T, int D>
+__device__ __forceinline__ void fluid_vjp_dev(const DevScene<T, D>& sc, T rho, T V, const T* L, const T* sgc, T rho_c,
+                                              T V_c, T* gvn_c, T& rho_in_c, T& V_in_c, T& c_acc, T& mu_acc)
+{
+    T dd[D][D];
+    T trd = T(0);
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            dd[i][j] = T(0.5) * (L[i * D + j] + L[j * D + i]) * sc.dt;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        trd += dd[i][i];
+    const T den = T(1) + trd;
+    const T rho_new = rho / den;
+    const T c = sc.c;
+    const T k = sc.rate_form ? sc.visc / sc.dt : sc.visc;
+    T trs = T(0);
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        trs += sgc[i * D + i];
+    const T p_c = -trs;
+    T mu_sum = T(0);
+    const T vis = -(T(2) / T(3)) * trd;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+            mu_sum += sgc[i * D + j] * (vis * (i == j ? T(1) : T(0)) + T(2) * dd[i][j]);
+    mu_acc += mu_sum * (sc.rate_form ? T(1) / sc.dt : T(1));
+    T trd_c = -(T(2) / T(3)) * k * trs;
+    T dd_c[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            dd_c[i][j] = T(2) * k * sgc[i * D + j];
+    c_acc += T(2) * c * (rho_new - sc.rho0) * p_c;
+    const T rho_new_c = rho_c + c * c * p_c;
+    rho_in_c += rho_new_c / den;
+    T den_c = -(rho / (den * den)) * rho_new_c;
+    V_in_c += den * V_c;
+    den_c += V * V_c;
+    trd_c += den_c;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        dd_c[i][i] += trd_c;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            gvn_c[i * D + j] += sc.dt * T(0.5) * (dd_c[i][j] + dd_c[j][i]);
+}
+
+// detail::dp_vjp (adjoint.hpp:186-293). S: input stress (3x3 embedding); sgc: sigma cotangent
+// (D x D full, row-major). Outputs accumulate into gvn_c (D x D), sig_in_c (D x D), szz_in_c.
+template <class T, int D>
+__device__ __forceinline__ void dp_vjp_dev(const DevScene<T, D>& sc, const T (&S)[3][3], const T* L, const T* sgc,
+                                           T szz_c, T rho_c, T V_c, T rho_in, T V_in, T* gvn_c, T* sig_in_c,
+                                           T& szz_in_c, T& rho_in_c, T& V_in_c)
+{
+    DpTrial<T, D> t;
+    dp_trial<T, D>(sc, S, L, t);
+    T oc[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            oc[i][j] = (i < D && j < D) ? sgc[i * D + j] : T(0);
+    if (D == 2)
+        oc[2][2] += szz_c;
+    T tc[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            tc[i][j] = T(0);
+    auto assemble = [&](const T (&dc)[3][3], T sm_c) {
+        T trdc = T(0);
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                tc[i][j] += dc[i][j];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            trdc += dc[i][i];
+        const T sm_total = sm_c - trdc;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            tc[i][i] += sm_total / T(3);
+    };
+    auto contract_dev = [&]() { // (out_cot .* dev).sum(), column-major order
+        T s = T(0);
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                s += oc[i][j] * t.dev[i][j];
+        return s;
+    };
+    if (t.zone == 1) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                tc[i][j] = oc[i][j];
+    } else if (t.zone == 2) {
+        const T denom = sc.G + sc.K * sc.q_phi * sc.q_psi;
+        const T dlam = t.fs / denom;
+        const T sm_new = t.sm - sc.K * sc.q_psi * dlam;
+        const T tau_new = sc.k_phi - sc.q_phi * sm_new;
+        if (!(t.tau <= T(0) || tau_new < T(0))) {
+            const bool capped = sm_new > sc.sigma_t;
+            const T ratio = tau_new / t.tau;
+            T dc[3][3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    dc[i][j] = ratio * oc[i][j];
+            const T ratio_c = contract_dev();
+            T sm_new_c = capped ? T(0) : (oc[0][0] + oc[1][1] + oc[2][2]);
+            const T tau_new_c = ratio_c / t.tau;
+            T tau_c = -ratio_c * tau_new / (t.tau * t.tau);
+            sm_new_c += -sc.q_phi * tau_new_c;
+            T sm_c = sm_new_c;
+            const T dlam_c = -sc.K * sc.q_psi * sm_new_c;
+            const T fs_c = dlam_c / denom;
+            tau_c += fs_c;
+            sm_c += sc.q_phi * fs_c;
+            if (t.tau > T(0))
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        dc[i][j] += (tau_c / (T(2) * t.tau)) * t.dev[i][j];
+            assemble(dc, sm_c);
+        }
+    } else {
+        if (t.tau > sc.tau_P) {
+            const T ratio = sc.tau_P / t.tau;
+            T dc[3][3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    dc[i][j] = ratio * oc[i][j];
+            const T ratio_c = contract_dev();
+            const T tau_c = -ratio_c * sc.tau_P / (t.tau * t.tau);
+            if (t.tau > T(0))
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        dc[i][j] += (tau_c / (T(2) * t.tau)) * t.dev[i][j];
+            assemble(dc, T(0));
+        } else {
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    tc[i][j] = oc[i][j];
+            const T sm_c = -(oc[0][0] + oc[1][1] + oc[2][2]);
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                tc[i][i] += sm_c / T(3);
+        }
     }
-    template <class Ctx>
-    void backprop_api(Ctx&, const mpm_state_view*, int64_t, int, const mpm_seeder_desc*, mpm_cot_view*,
-                      mpm_param_grads*, mpm_backprop_result*)
+    // trial = sR + 2G dd + (K - 2G/3) tr(dd) I
+    const T lam = sc.K - T(2) * sc.G / T(3);
+    const T ttr = tc[0][0] + tc[1][1] + tc[2][2];
+    T dd_c[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            dd_c[i][j] = T(2) * sc.G * tc[i][j] + (i == j ? lam * ttr : T(0));
+    const T den = T(1) + t.trd;
+    const T den_c = V_in * V_c - (rho_in / (den * den)) * rho_c;
+    V_in_c += den * V_c;
+    rho_in_c += rho_c / den;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        dd_c[i][i] += den_c;
+    // sR = S + S dw^T + dw S^T
+    T S_c[3][3], dw_c[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            T a1 = T(0), a2 = T(0), b1 = T(0), b2 = T(0);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                a1 += tc[i][k] * t.dw[k][j];
+                a2 += t.dw[k][i] * tc[k][j];
+                b1 += tc[k][i] * S[k][j];
+                b2 += tc[i][k] * S[k][j];
+            }
+            S_c[i][j] = tc[i][j] + a1 + a2;
+            dw_c[i][j] = b1 + b2;
+        }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            gvn_c[i * D + j] += sc.dt * (T(0.5) * (dd_c[i][j] + dd_c[j][i]) + T(0.5) * (dw_c[i][j] - dw_c[j][i]));
+            sig_in_c[i * D + j] += S_c[i][j];
+        }
+    if (D == 2)
+        szz_in_c += S_c[2][2];
+}
+
+// fixed-order CTA reduction of per-thread values -> out[slot] (deterministic)
+template <class T, int NT>
+__device__ __forceinline__ T block_sum_fixed(T v, T* scratch)
+{
+    scratch[threadIdx.x] = v;
+    __syncthreads();
+#pragma unroll
+    for (int s = NT / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s)
+            scratch[threadIdx.x] = scratch[threadIdx.x] + scratch[threadIdx.x + s];
+        __syncthreads();
+    }
+    T r = scratch[0];
+    __syncthreads();
+    return r;
+}
+
+// ---- K5a: G2P-transpose gather + constitutive VJP ------------------------------------------
+template <class T, int D, bool APIC>
+__global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf<T, D> Pin, GBuf<T, D> G,
+                                                         const int* __restrict__ perm, const int* __restrict__ bstart,
+                                                         const int* __restrict__ bend, const int* __restrict__ occ,
+                                                         const int* __restrict__ n_occ, CBuf<T, D> co, CBuf<T, D> ci,
+                                                         SBuf<T, D> S, T* __restrict__ pg_block, DevStatus* st)
+{
+    using C = Cfg<D>;
+    constexpr int TE = C::TE, TN = C::TN;
+    extern __shared__ unsigned char smem_raw[];
+    T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]
+    __shared__ T red[256];
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    const T alpha = sc.alpha;
+    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+        const int Q = occ[w];
+        const int s0 = bstart[Q], s1 = bend[Q];
+        int qc[D];
+        block_coords<D>(Q, sc.nb, qc);
+        __syncthreads();
+        for (int t = threadIdx.x; t < TN; t += blockDim.x) {
+            int tl[D], rem = t, nid = 0, loc = 0;
+            bool ok = true;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+                tl[a] = rem % TE;
+                rem /= TE;
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int nn = qc[a] * C::B + tl[a];
+                const int qb = nn >> C::LOGB;
+                ok &= qb < sc.nnb[a];
+                nid = nid * sc.nnb[a] + qb;
+                loc = (loc << C::LOGB) | (nn & (C::B - 1));
+            }
+            const size_t gi = (size_t)nid * C::NB + loc;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                tile[a * TN + t] = ok ? G.v[a][gi] : T(0);
+                tile[(D + a) * TN + t] = ok ? G.vold[a][gi] : T(0);
+            }
+        }
+        __syncthreads();
+        T c_acc = T(0), mu_acc = T(0);
+        // process the segment in rounds so every thread reaches the block reductions
+        for (int base = s0; base < s1; base += blockDim.x) {
+            const int i = base + threadIdx.x;
+            if (i < s1) {
+                const int src = perm[i];
+                const int pid = Pin.pid[src];
+                T x[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    x[a] = Pin.x[a][src];
+                T w[D][3], dw[D][3];
+                int tb[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const T u = (x[a] - sc.origin[a]) * sc.inv_dh;
+                    const T fl = dfloor<T>(u - T(0.5));
+                    const T fx = u - fl;
+                    const T h0 = T(1.5) - fx, h1 = fx - T(1), h2 = fx - T(0.5);
+                    w[a][0] = T(0.5) * h0 * h0;
+                    w[a][1] = T(0.75) - h1 * h1;
+                    w[a][2] = T(0.5) * h2 * h2;
+                    dw[a][0] = -h0 * sc.inv_dh;
+                    dw[a][1] = -T(2) * h1 * sc.inv_dh;
+                    dw[a][2] = h2 * sc.inv_dh;
+                    tb[a] = int(fl) - qc[a] * C::B;
+                }
+                // forward gather: grad v_new (transfer.hpp:476)
+                T L[D * D];
+#pragma unroll
+                for (int k = 0; k < D * D; ++k)
+                    L[k] = T(0);
+                for (int k = 0; k < C::NOFF; ++k) {
+                    int o[D], kk = k, ti = 0;
+#pragma unroll
+                    for (int a = D - 1; a >= 0; --a) {
+                        o[a] = kk % 3;
+                        kk /= 3;
+                    }
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        ti = ti * TE + tb[a] + o[a];
+                    T gw[D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        T r = dw[a][o[a]];
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+                            if (b != a)
+                                r *= w[b][o[b]];
+                        gw[a] = r;
+                    }
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        const T nv = tile[a * TN + ti];
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+                            L[a * D + b] += nv * gw[b];
+                    }
+                }
+                // (1) constitutive transpose (adjoint.hpp:374-400)
+                T sgc[D * D], gvn_c[D * D], sig_in_c[D * D];
+#pragma unroll
+                for (int k = 0; k < D * D; ++k) {
+                    sgc[k] = co.sig[k][pid];
+                    gvn_c[k] = T(0);
+                    sig_in_c[k] = T(0);
+                }
+                T rho_in_c = T(0), V_in_c = T(0), szz_in_c = T(0);
+                const T rho = Pin.rho[src], V = Pin.V[src];
+                if (sc.material == 0) {
+                    fluid_vjp_dev<T, D>(sc, rho, V, L, sgc, co.rho[pid], co.V[pid], gvn_c, rho_in_c, V_in_c, c_acc,
+                                        mu_acc);
+                } else {
+                    T Sm[3][3];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+#pragma unroll
+                        for (int b = 0; b < 3; ++b)
+                            Sm[a][b] = (a < D && b < D) ? Pin.sig[sym_idx<D>(a, b)][src] : T(0);
+                    if (D == 2)
+                        Sm[2][2] = Pin.szz[src];
+                    dp_vjp_dev<T, D>(sc, Sm, L, sgc, D == 2 ? co.szz[pid] : T(0), co.rho[pid], co.V[pid], rho, V,
+                                     gvn_c, sig_in_c, szz_in_c, rho_in_c, V_in_c);
+                }
+                // cot_out.grad_v joins (adjoint.hpp:398-400)
+#pragma unroll
+                for (int k = 0; k < D * D; ++k)
+                    gvn_c[k] += co.gv[k][pid];
+                // (2) G2P transpose, gather half (adjoint.hpp:405-439)
+                T vc[D], xc[D], pic[D], inc[D], xp[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    vc[a] = co.v[a][pid];
+                    xc[a] = co.x[a][pid];
+                    pic[a] = (T(1) - alpha) * vc[a] + sc.dt * xc[a];
+                    inc[a] = alpha * vc[a];
+                    xp[a] = T(0);
+                }
+                T Bc[D * D];
+                if constexpr (APIC) {
+#pragma unroll
+                    for (int k = 0; k < D * D; ++k)
+                        Bc[k] = co.aff[k][pid];
+                }
+                for (int k = 0; k < C::NOFF; ++k) {
+                    int o[D], kk = k, ti = 0;
+#pragma unroll
+                    for (int a = D - 1; a >= 0; --a) {
+                        o[a] = kk % 3;
+                        kk /= 3;
+                    }
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        ti = ti * TE + tb[a] + o[a];
+                    T phi = T(1);
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        phi *= w[a][o[a]];
+                    T gw[D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        T r = dw[a][o[a]];
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+                            if (b != a)
+                                r *= w[b][o[b]];
+                        gw[a] = r;
+                    }
+                    // Hessian of phi (stencil_hessian adjoint.hpp:95-110)
+                    T H[D][D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int b = a; b < D; ++b) {
+                            T r = a == b ? (o[a] == 1 ? -T(2) * sc.inv_dh * sc.inv_dh : sc.inv_dh * sc.inv_dh)
+                                         : dw[a][o[a]] * dw[b][o[b]];
+#pragma unroll
+                            for (int c = 0; c < D; ++c)
+                                if (c != a && c != b)
+                                    r *= w[c][o[c]];
+                            H[a][b] = r;
+                            H[b][a] = r;
+                        }
+                    T wv[D], uv[D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        wv[a] = tile[a * TN + ti];
+                        uv[a] = tile[(D + a) * TN + ti];
+                    }
+                    T s1 = T(0), s2 = T(0);
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        s1 += pic[a] * wv[a];
+                        s2 += inc[a] * (wv[a] - uv[a]);
+                    }
+                    T LTw[D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        T s = T(0);
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+                            s += gvn_c[b * D + a] * wv[b];
+                        LTw[a] = s;
+                    }
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        T hs = T(0);
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+                            hs += H[a][b] * LTw[b];
+                        xp[a] += gw[a] * (s1 + s2);
+                        xp[a] += hs;
+                    }
+                    if constexpr (APIC) {
+                        T r[D];
+#pragma unroll
+                        for (int a = 0; a < D; ++a)
+                            r[a] = (sc.origin[a] + T(qc[a] * C::B + tb[a] + o[a]) * sc.dh) - x[a];
+                        T Bcr[D], BcTw[D], wBr = T(0);
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            T s = T(0), s2b = T(0);
+#pragma unroll
+                            for (int b = 0; b < D; ++b) {
+                                s += Bc[a * D + b] * r[b];
+                                s2b += Bc[b * D + a] * wv[b];
+                            }
+                            Bcr[a] = s;
+                            BcTw[a] = s2b;
+                        }
+#pragma unroll
+                        for (int a = 0; a < D; ++a)
+                            wBr += wv[a] * Bcr[a];
+#pragma unroll
+                        for (int a = 0; a < D; ++a)
+                            xp[a] += gw[a] * wBr - phi * BcTw[a];
+                    }
+                }
+                // write cot_in (overwrites: this kernel is the first writer of every field)
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    ci.v[a][pid] = alpha * vc[a];
+                    ci.x[a][pid] = xc[a] + xp[a];
+                }
+                ci.rho[pid] = rho_in_c;
+                ci.V[pid] = V_in_c;
+                ci.eps[pid] = T(0);
+                if (D == 2)
+                    ci.szz[pid] = szz_in_c;
+#pragma unroll
+                for (int k = 0; k < D * D; ++k) {
+                    ci.sig[k][pid] = sig_in_c[k];
+                    ci.gv[k][pid] = T(0);
+                    if constexpr (APIC)
+                        ci.aff[k][pid] = T(0);
+                }
+                // scatter records (sorted slot i)
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    S.a[a][i] = pic[a] + inc[a];
+                    S.inc[a][i] = inc[a];
+                }
+#pragma unroll
+                for (int k = 0; k < D * D; ++k) {
+                    S.L[k][i] = gvn_c[k];
+                    if constexpr (APIC)
+                        S.Bc[k][i] = Bc[k];
+                }
+            }
+        }
+        // per-block c / mu partials (fixed-order tree) -> pg_block[Q][0..1]
+        if (sc.material == 0) {
+            const T cs = block_sum_fixed<T, 256>(c_acc, red);
+            const T ms = block_sum_fixed<T, 256>(mu_acc, red);
+            if (threadIdx.x == 0) {
+                pg_block[(size_t)Q * 2 + 0] = cs;
+                pg_block[(size_t)Q * 2 + 1] = ms;
+            }
+        }
+    }
+}
+
+// ---- K5b: G2P-transpose scatter (node-column march over the sorted records) ----------------
+// Contributions per node (adjoint.hpp:427-436): gv_cot += phi a + L grad(phi) (+ APIC phi Bc r),
+// gvold_cot -= phi inc. 2D fields per node, deterministic order as in k_p2g.
+template <class T, int D, bool APIC>
+__global__ void __launch_bounds__(256) k_adj_scatter(DevScene<T, D> sc, PBuf<T, D> Pin, SBuf<T, D> S,
+                                                     const int* __restrict__ perm, const int* __restrict__ keys,
+                                                     const int* __restrict__ bstart, const int* __restrict__ bend,
+                                                     const int* __restrict__ occ, const int* __restrict__ n_occ,
+                                                     T* __restrict__ partials, const DevStatus* st)
+{
+    using C = Cfg<D>;
+    constexpr int B = C::B, TE = C::TE, NF = 2 * D;
+    constexpr int LVLBITS = (D - 1) * C::LOGB;
+    __shared__ int cst[C::NB + 1];
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    const int tid = threadIdx.x;
+    const int col = tid % C::NCOL, seg = tid / C::NCOL;
+    int cn[D - 1 > 0 ? D - 1 : 1];
     {
-        throw std::runtime_error("backprop: adjoint kernels not built yet");
+        int cc = col;
+#pragma unroll
+        for (int a = D - 2; a >= 0; --a) {
+            cn[a] = cc % TE;
+            cc /= TE;
+        }
+    }
+    const int zb = seg * B / C::SEGS, ze = (seg + 1) * B / C::SEGS;
+    const bool active = seg < C::SEGS;
+    for (int wq = blockIdx.x; wq < nocc; wq += gridDim.x) {
+        const int Q = occ[wq];
+        const int s0 = bstart[Q], s1 = bend[Q], len = s1 - s0;
+        int qc[D];
+        block_coords<D>(Q, sc.nb, qc);
+        for (int c = tid; c <= C::NB; c += blockDim.x) {
+            int lo = 0, hi = len;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if ((keys[s0 + mid] & (C::NB - 1)) < c)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            cst[c] = lo;
+        }
+        __syncthreads();
+        T* part = partials + (size_t)Q * NF * C::TN;
+        T ov[2][NF];
+        if (active) {
+            T acc[3][NF];
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    acc[k][f] = T(0);
+            for (int z = zb; z < ze; ++z) {
+                for (int oo = 0; oo < C::NOFF / 3; ++oo) {
+                    int o[D - 1 > 0 ? D - 1 : 1];
+                    int bcell = 0;
+                    bool ok = true;
+                    {
+                        int kk = oo;
+#pragma unroll
+                        for (int a = D - 2; a >= 0; --a) {
+                            o[a] = kk % 3;
+                            kk /= 3;
+                        }
+#pragma unroll
+                        for (int a = 0; a < D - 1; ++a) {
+                            const int bc = cn[a] - o[a];
+                            ok &= bc >= 0 && bc < B;
+                            bcell = (bcell << C::LOGB) | (bc & (B - 1));
+                        }
+                    }
+                    if (!ok)
+                        continue;
+                    bcell |= z << LVLBITS;
+                    const int kb = cst[bcell], ke = cst[bcell + 1];
+                    for (int k = kb; k < ke; ++k) {
+                        const int i = s0 + k;
+                        const int src = __ldg(perm + i);
+                        T x[D], wgt[D][3], dwt[D][3];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            x[a] = __ldg(Pin.x[a] + src);
+                            const T u = (x[a] - sc.origin[a]) * sc.inv_dh;
+                            const T fx = u - dfloor<T>(u - T(0.5));
+                            const T h0 = T(1.5) - fx, h1 = fx - T(1), h2 = fx - T(0.5);
+                            wgt[a][0] = T(0.5) * h0 * h0;
+                            wgt[a][1] = T(0.75) - h1 * h1;
+                            wgt[a][2] = T(0.5) * h2 * h2;
+                            dwt[a][0] = -h0 * sc.inv_dh;
+                            dwt[a][1] = -T(2) * h1 * sc.inv_dh;
+                            dwt[a][2] = h2 * sc.inv_dh;
+                        }
+                        T av[D], iv[D], L[D * D];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            av[a] = S.a[a][i];
+                            iv[a] = S.inc[a][i];
+                        }
+#pragma unroll
+                        for (int q = 0; q < D * D; ++q)
+                            L[q] = S.L[q][i];
+#pragma unroll
+                        for (int o2 = 0; o2 < 3; ++o2) {
+                            T phi = wgt[D - 1][o2];
+#pragma unroll
+                            for (int a = 0; a < D - 1; ++a)
+                                phi *= wgt[a][o[a]];
+                            T gw[D];
+#pragma unroll
+                            for (int a = 0; a < D; ++a) {
+                                T r = (a == D - 1) ? dwt[a][o2] : dwt[a][o[a]];
+#pragma unroll
+                                for (int b = 0; b < D; ++b)
+                                    if (b != a)
+                                        r *= (b == D - 1) ? wgt[b][o2] : wgt[b][o[b]];
+                                gw[a] = r;
+                            }
+                            T add[D];
+#pragma unroll
+                            for (int a = 0; a < D; ++a) {
+                                T s = T(0);
+#pragma unroll
+                                for (int b = 0; b < D; ++b)
+                                    s += L[a * D + b] * gw[b];
+                                add[a] = phi * av[a] + s;
+                            }
+                            if constexpr (APIC) {
+                                T r[D];
+#pragma unroll
+                                for (int a = 0; a < D; ++a) {
+                                    const int idx = a == D - 1 ? qc[a] * B + z + o2 : qc[a] * B + cn[a];
+                                    r[a] = (sc.origin[a] + T(idx) * sc.dh) - x[a];
+                                }
+#pragma unroll
+                                for (int a = 0; a < D; ++a) {
+                                    T s = T(0);
+#pragma unroll
+                                    for (int b = 0; b < D; ++b)
+                                        s += S.Bc[a * D + b][i] * r[b];
+                                    add[a] += phi * s;
+                                }
+                            }
+#pragma unroll
+                            for (int a = 0; a < D; ++a) {
+                                acc[o2][a] += add[a];
+                                acc[o2][D + a] -= phi * iv[a];
+                            }
+                        }
+                    }
+                }
+                const int idx = z * C::NCOL + col;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    part[f * C::TN + idx] = acc[0][f];
+                    acc[0][f] = acc[1][f];
+                    acc[1][f] = acc[2][f];
+                    acc[2][f] = T(0);
+                }
+            }
+            if (seg == C::SEGS - 1) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        part[f * C::TN + (ze + k) * C::NCOL + col] = acc[k][f];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        ov[k][f] = acc[k][f];
+            }
+        }
+        __syncthreads();
+        if (active && seg < C::SEGS - 1) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    T* p = part + f * C::TN + (ze + k) * C::NCOL + col;
+                    *p = *p + ov[k][f];
+                }
+        }
+        __syncthreads();
+    }
+}
+
+// ---- K6: per node: sum partials, correction-chain VJP, momentum-update transpose ------------
+template <class T, int D>
+__device__ __forceinline__ void corr_vjp_chain(const DevScene<T, D>& sc, const int* n, const T* vtilde, T* cot,
+                                               T* fr_acc)
+{
+    // forward replay of the chain (contact.hpp:141-224): record inputs of each correction
+    constexpr int MAXC = 2 * D + MAX_OBST + 2 * D;
+    struct Rec {
+        int kind; // 0 slip, 1 zero, 2 obstacle, 3 coulomb
+        int axis;
+        T nrm;    // normal sign along `axis` (obstacle / coulomb normals are axis-aligned)
+        T mu;
+        int fidx;
+        T vin[D];
+    };
+    Rec rec[MAXC];
+    int nc = 0;
+    T v[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        v[a] = vtilde[a];
+    for (int w = 0; w < 2 * D; ++w) {
+        const int kind = sc.wall_kind[w];
+        if (kind == 3)
+            continue;
+        const int a = w / 2;
+        const bool in = (w % 2 == 0) ? n[a] < sc.band : n[a] > sc.cells[a] - sc.band;
+        if (!in)
+            continue;
+        Rec& r = rec[nc++];
+        r.kind = kind == 0 ? 0 : 1;
+        r.axis = a;
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+            r.vin[b] = v[b];
+        if (kind == 0)
+            v[a] = T(0);
+        else
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                v[b] = T(0);
+    }
+    if (sc.n_obst > 0) {
+        T xp[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            xp[a] = sc.origin[a] + T(n[a]) * sc.dh;
+        for (int ob = 0; ob < sc.n_obst; ++ob) {
+            bool inside = true;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+                inside &= !(xp[a] < sc.obst[ob][a] || xp[a] > sc.obst[ob][D + a]);
+            if (!inside)
+                continue;
+            int best_a = 0, best_s = 0;
+            T best = T(0);
+            bool first = true;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const T dlo = xp[a] - sc.obst[ob][a];
+                const T dhi = sc.obst[ob][D + a] - xp[a];
+                if (first || dlo < best) {
+                    best = dlo;
+                    best_a = a;
+                    best_s = 0;
+                    first = false;
+                }
+                if (dhi < best) {
+                    best = dhi;
+                    best_a = a;
+                    best_s = 1;
+                }
+            }
+            Rec& r = rec[nc++];
+            r.kind = 2;
+            r.axis = best_a;
+            r.nrm = best_s == 0 ? T(-1) : T(1);
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                r.vin[b] = v[b];
+            const T vn = v[best_a] * r.nrm;
+            if (vn < T(0))
+#pragma unroll
+                for (int b = 0; b < D; ++b)
+                    v[b] = v[b] - vn * (b == best_a ? r.nrm : T(0));
+        }
+    }
+    for (int w = 0; w < 2 * D; ++w) {
+        if (sc.wall_kind[w] != 3)
+            continue;
+        const int a = w / 2;
+        const bool in = (w % 2 == 0) ? n[a] < sc.band : n[a] > sc.cells[a] - sc.band;
+        if (!in)
+            continue;
+        const int seg_axis = a == 0 ? 1 : 0;
+        const T coord = sc.origin[seg_axis] + T(n[seg_axis]) * sc.dh;
+        const int ns = sc.n_fric[w];
+        const T len = (T(sc.cells[seg_axis]) * sc.dh) / T(ns);
+        int k = int(ceil(double((coord - sc.origin[seg_axis]) / len))) - 1;
+        k = k < 0 ? 0 : (k > ns - 1 ? ns - 1 : k);
+        Rec& r = rec[nc++];
+        r.kind = 3;
+        r.axis = a;
+        r.nrm = (w % 2 == 0) ? T(-1) : T(1);
+        r.mu = sc.fric[sc.fric_off[w] + k];
+        r.fidx = sc.fric_off[w] + k;
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+            r.vin[b] = v[b];
+        T vn = v[a] * r.nrm;
+        if (vn <= T(0))
+            continue;
+        T t[D], t2 = T(0);
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+            t[b] = v[b] - vn * (b == a ? r.nrm : T(0));
+            t2 += t[b] * t[b];
+        }
+        const T tn = dsqrt<T>(t2);
+        if (tn <= r.mu * vn) {
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                v[b] = T(0);
+        } else {
+            const T s = r.mu * vn / tn;
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                v[b] = t[b] - s * t[b];
+        }
+    }
+    // reverse (node_correction_vjp, adjoint.hpp:114-150)
+    for (int q = nc - 1; q >= 0; --q) {
+        const Rec& r = rec[q];
+        if (r.kind == 0) {
+            cot[r.axis] = T(0);
+        } else if (r.kind == 1) {
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                cot[b] = T(0);
+        } else if (r.kind == 2) {
+            const T vn = r.vin[r.axis] * r.nrm;
+            if (vn < T(0)) {
+                const T ncd = r.nrm * cot[r.axis];
+                cot[r.axis] = cot[r.axis] - r.nrm * ncd;
+            }
+        } else {
+            T vn = T(0);
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                vn += r.vin[b] * (b == r.axis ? r.nrm : T(0));
+            if (vn <= T(0))
+                continue;
+            T t[D], t2 = T(0);
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+                t[b] = r.vin[b] - vn * (b == r.axis ? r.nrm : T(0));
+                t2 += t[b] * t[b];
+            }
+            const T tn = dsqrt<T>(t2);
+            if (tn <= r.mu * vn) {
+#pragma unroll
+                for (int b = 0; b < D; ++b)
+                    cot[b] = T(0);
+                continue;
+            }
+            const T s = T(1) - r.mu * vn / tn;
+            T that[D], tc = T(0), ncd = T(0), thc = T(0);
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+                that[b] = t[b] / tn;
+                tc += t[b] * cot[b];
+                ncd += (b == r.axis ? r.nrm : T(0)) * cot[b];
+                thc += that[b] * cot[b];
+            }
+            T out[D];
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+                const T nb = b == r.axis ? r.nrm : T(0);
+                out[b] = s * (cot[b] - nb * ncd) + tc * (-(r.mu / tn) * nb + (r.mu * vn / (tn * tn)) * that[b]);
+            }
+            fr_acc[r.fidx] += -vn * thc;
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+                cot[b] = out[b];
+        }
+    }
+}
+
+template <class T, int D>
+__global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf<T, D> G, GCBuf<T, D> GC,
+                                                         const T* __restrict__ partials, const int* __restrict__ bstart,
+                                                         const int* __restrict__ act, const int* __restrict__ n_act,
+                                                         T* __restrict__ fr_block, const DevStatus* st)
+{
+    using C = Cfg<D>;
+    constexpr int NF = 2 * D;
+    __shared__ T red[C::NB];
+    if (st->abort)
+        return;
+    const int nact = *n_act;
+    const int tid = threadIdx.x;
+    int lc[D];
+    {
+        int t = tid;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) {
+            lc[a] = t & (C::B - 1);
+            t >>= C::LOGB;
+        }
+    }
+    int nfr = 0;
+    for (int w = 0; w < 2 * D; ++w)
+        nfr += sc.n_fric[w];
+    for (int wq = blockIdx.x; wq < nact; wq += gridDim.x) {
+        const int q = act[wq];
+        int qc[D], n[D];
+        block_coords<D>(q, sc.nnb, qc);
+        bool inside = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            n[a] = qc[a] * C::B + lc[a];
+            inside &= n[a] <= sc.cells[a];
+        }
+        const size_t gi = (size_t)q * C::NB + tid;
+        T gv[D], gvo[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            gv[a] = gvo[a] = T(0);
+#pragma unroll
+        for (int s = 0; s < (1 << D); ++s) {
+            int Qid = 0, colx = 0, z = 0;
+            bool ok = true;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int sa = (s >> (D - 1 - a)) & 1;
+                const int Qa = qc[a] - sa;
+                const int t = n[a] - Qa * C::B;
+                ok &= Qa >= 0 && Qa < sc.nb[a] && t < C::TE;
+                Qid = Qid * sc.nb[a] + Qa;
+                if (a == D - 1)
+                    z = t;
+                else
+                    colx = colx * C::TE + t;
+            }
+            if (!ok || bstart[Qid] < 0)
+                continue;
+            const T* part = partials + (size_t)Qid * NF * C::TN + z * C::NCOL + colx;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                gv[a] += part[a * C::TN];
+                gvo[a] += part[(D + a) * C::TN];
+            }
+        }
+        const T m = G.m[gi];
+        T fr_acc[MAX_FRIC];
+        for (int k = 0; k < nfr; ++k)
+            fr_acc[k] = T(0);
+        T gm = T(0), gmom[D], gf[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            gmom[a] = gf[a] = T(0);
+        if (inside && m > sc.mass_eps) {
+            T p[D], f[D], vt[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                p[a] = G.p[a][gi];
+                f[a] = G.f[a][gi];
+            }
+            // v_tilde = v_old + (dt/m) f, recomputed with the forward's arithmetic (k_grid)
+            const T sdt = sc.dt / m;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+                vt[a] = p[a] / m + sdt * f[a];
+            corr_vjp_chain<T, D>(sc, n, vt, gv, fr_acc);
+            T uc[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                uc[a] = gvo[a] + gv[a];
+                gf[a] = (sc.dt / m) * gv[a];
+                gmom[a] = uc[a] / m;
+            }
+            T pu = T(0), fv = T(0);
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                pu += p[a] * uc[a];
+                fv += f[a] * gv[a];
+            }
+            gm = -(pu) / (m * m) - sc.dt * (fv) / (m * m);
+        }
+        GC.gm[gi] = gm;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            GC.gmom[a][gi] = gmom[a];
+            GC.gf[a][gi] = gf[a];
+        }
+        // friction gradient partials per node block (fixed-order tree)
+        for (int k = 0; k < nfr; ++k) {
+            const T s = block_sum_fixed<T, C::NB>(fr_acc[k], red);
+            if (tid == 0)
+                fr_block[(size_t)q * MAX_FRIC + k] = s;
+        }
+    }
+}
+
+// ---- K7: P2G transpose gather (adjoint.hpp:479-524) -----------------------------------------
+template <class T, int D, bool AFF>
+__global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> Pin, GCBuf<T, D> GC,
+                                                  const int* __restrict__ perm, const int* __restrict__ bstart,
+                                                  const int* __restrict__ bend, const int* __restrict__ occ,
+                                                  const int* __restrict__ n_occ, CBuf<T, D> ci, const DevStatus* st)
+{
+    using C = Cfg<D>;
+    constexpr int TE = C::TE, TN = C::TN, NF = 1 + 2 * D;
+    extern __shared__ unsigned char smem_raw[];
+    T* tile = reinterpret_cast<T*>(smem_raw); // [NF][TN]: gm, gmom[D], gf[D]
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+        const int Q = occ[w];
+        const int s0 = bstart[Q], s1 = bend[Q];
+        int qc[D];
+        block_coords<D>(Q, sc.nb, qc);
+        __syncthreads();
+        for (int t = threadIdx.x; t < TN; t += blockDim.x) {
+            int tl[D], rem = t, nid = 0, loc = 0;
+            bool ok = true;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+                tl[a] = rem % TE;
+                rem /= TE;
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int nn = qc[a] * C::B + tl[a];
+                const int qb = nn >> C::LOGB;
+                ok &= qb < sc.nnb[a];
+                nid = nid * sc.nnb[a] + qb;
+                loc = (loc << C::LOGB) | (nn & (C::B - 1));
+            }
+            const size_t gi = (size_t)nid * C::NB + loc;
+            tile[t] = ok ? GC.gm[gi] : T(0);
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                tile[(1 + a) * TN + t] = ok ? GC.gmom[a][gi] : T(0);
+                tile[(1 + D + a) * TN + t] = ok ? GC.gf[a][gi] : T(0);
+            }
+        }
+        __syncthreads();
+        for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+            const int src = perm[i];
+            const int pid = Pin.pid[src];
+            T x[D], v[D], sig[D][D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                x[a] = Pin.x[a][src];
+                v[a] = Pin.v[a][src];
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = 0; b < D; ++b)
+                    sig[a][b] = Pin.sig[sym_idx<D>(a, b)][src];
+            const T mass = Pin.m[src], vol = Pin.V[src];
+            T w[D][3], dw[D][3];
+            int tb[D], base[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const T u = (x[a] - sc.origin[a]) * sc.inv_dh;
+                const T fl = dfloor<T>(u - T(0.5));
+                const T fx = u - fl;
+                const T h0 = T(1.5) - fx, h1 = fx - T(1), h2 = fx - T(0.5);
+                w[a][0] = T(0.5) * h0 * h0;
+                w[a][1] = T(0.75) - h1 * h1;
+                w[a][2] = T(0.5) * h2 * h2;
+                dw[a][0] = -h0 * sc.inv_dh;
+                dw[a][1] = -T(2) * h1 * sc.inv_dh;
+                dw[a][2] = h2 * sc.inv_dh;
+                base[a] = int(fl);
+                tb[a] = base[a] - qc[a] * C::B;
+            }
+            T A[D * D], Dinv[D * D];
+            if constexpr (AFF) {
+                if (sc.tpic) {
+#pragma unroll
+                    for (int k = 0; k < D * D; ++k)
+                        A[k] = Pin.gv[k][src];
+                } else {
+                    // D = sum phi r r^T (canonical order), Dinv, A = B Dinv (adjoint.hpp:346-362)
+                    T Dm[D][D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+                            Dm[a][b] = T(0);
+                    for (int k = 0; k < C::NOFF; ++k) {
+                        int o[D], kk = k;
+#pragma unroll
+                        for (int a = D - 1; a >= 0; --a) {
+                            o[a] = kk % 3;
+                            kk /= 3;
+                        }
+                        T phi = T(1), r[D];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            phi *= w[a][o[a]];
+                            r[a] = (sc.origin[a] + T(base[a] + o[a]) * sc.dh) - x[a];
+                        }
+#pragma unroll
+                        for (int a = 0; a < D; ++a)
+#pragma unroll
+                            for (int b = 0; b < D; ++b)
+                                Dm[a][b] += phi * r[a] * r[b];
+                    }
+                    if constexpr (D == 2) {
+                        const T det = Dm[0][0] * Dm[1][1] - Dm[0][1] * Dm[1][0];
+                        const T id = T(1) / det;
+                        Dinv[0] = Dm[1][1] * id;
+                        Dinv[1] = -Dm[0][1] * id;
+                        Dinv[2] = -Dm[1][0] * id;
+                        Dinv[3] = Dm[0][0] * id;
+                    } else {
+                        const T c00 = Dm[1][1] * Dm[2][2] - Dm[1][2] * Dm[2][1];
+                        const T c01 = Dm[1][2] * Dm[2][0] - Dm[1][0] * Dm[2][2];
+                        const T c02 = Dm[1][0] * Dm[2][1] - Dm[1][1] * Dm[2][0];
+                        const T det = Dm[0][0] * c00 + Dm[0][1] * c01 + Dm[0][2] * c02;
+                        const T id = T(1) / det;
+                        Dinv[0] = c00 * id;
+                        Dinv[3] = c01 * id;
+                        Dinv[6] = c02 * id;
+                        Dinv[1] = (Dm[0][2] * Dm[2][1] - Dm[0][1] * Dm[2][2]) * id;
+                        Dinv[4] = (Dm[0][0] * Dm[2][2] - Dm[0][2] * Dm[2][0]) * id;
+                        Dinv[7] = (Dm[0][1] * Dm[2][0] - Dm[0][0] * Dm[2][1]) * id;
+                        Dinv[2] = (Dm[0][1] * Dm[1][2] - Dm[0][2] * Dm[1][1]) * id;
+                        Dinv[5] = (Dm[0][2] * Dm[1][0] - Dm[0][0] * Dm[1][2]) * id;
+                        Dinv[8] = (Dm[0][0] * Dm[1][1] - Dm[0][1] * Dm[1][0]) * id;
+                    }
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int b = 0; b < D; ++b) {
+                            T s = T(0);
+#pragma unroll
+                            for (int k = 0; k < D; ++k)
+                                s += Pin.aff[a * D + k][src] * Dinv[k * D + b];
+                            A[a * D + b] = s;
+                        }
+                }
+            }
+            T vcot[D], xpc[D], sigc[D * D], Vc = T(0), Ac[D * D];
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+                vcot[a] = xpc[a] = T(0);
+#pragma unroll
+            for (int k = 0; k < D * D; ++k)
+                sigc[k] = Ac[k] = T(0);
+            for (int k = 0; k < C::NOFF; ++k) {
+                int o[D], kk = k, ti = 0;
+#pragma unroll
+                for (int a = D - 1; a >= 0; --a) {
+                    o[a] = kk % 3;
+                    kk /= 3;
+                }
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    ti = ti * TE + tb[a] + o[a];
+                T phi = T(1);
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    phi *= w[a][o[a]];
+                T gw[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    T r = dw[a][o[a]];
+#pragma unroll
+                    for (int b = 0; b < D; ++b)
+                        if (b != a)
+                            r *= w[b][o[b]];
+                    gw[a] = r;
+                }
+                T H[D][D];
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+#pragma unroll
+                    for (int b = a; b < D; ++b) {
+                        T r = a == b ? (o[a] == 1 ? -T(2) * sc.inv_dh * sc.inv_dh : sc.inv_dh * sc.inv_dh)
+                                     : dw[a][o[a]] * dw[b][o[b]];
+#pragma unroll
+                        for (int c = 0; c < D; ++c)
+                            if (c != a && c != b)
+                                r *= w[c][o[c]];
+                        H[a][b] = r;
+                        H[b][a] = r;
+                    }
+                const T gmc = tile[ti];
+                T mc[D], fc[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    mc[a] = tile[(1 + a) * TN + ti];
+                    fc[a] = tile[(1 + D + a) * TN + ti];
+                }
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    vcot[a] += mass * phi * mc[a];
+                T vel[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    vel[a] = v[a];
+                if constexpr (AFF) {
+                    T r[D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        r[a] = (sc.origin[a] + T(base[a] + o[a]) * sc.dh) - x[a];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        T s = T(0), sT = T(0);
+#pragma unroll
+                        for (int b = 0; b < D; ++b) {
+                            s += A[a * D + b] * r[b];
+                            sT += A[b * D + a] * mc[b];
+                        }
+                        vel[a] += s;
+                        xpc[a] -= mass * phi * sT;
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+                            Ac[a * D + b] += mass * phi * mc[a] * r[b];
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+#pragma unroll
+                    for (int b = 0; b < D; ++b)
+                        sigc[a * D + b] += -vol * fc[a] * gw[b];
+                T sg[D], sf[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    T s1 = T(0), s2 = T(0);
+#pragma unroll
+                    for (int b = 0; b < D; ++b) {
+                        s1 += sig[a][b] * gw[b];
+                        s2 += sig[a][b] * fc[b];
+                    }
+                    sg[a] = s1;
+                    sf[a] = s2;
+                }
+                T sgf = T(0), gdf = T(0), mdv = T(0);
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    sgf += sg[a] * fc[a];
+                    gdf += sc.gravity[a] * fc[a];
+                    mdv += mc[a] * vel[a];
+                }
+                Vc += -sgf;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    T hs = T(0);
+#pragma unroll
+                    for (int b = 0; b < D; ++b)
+                        hs += H[a][b] * sf[b];
+                    xpc[a] += mass * gmc * gw[a];
+                    xpc[a] += mass * mdv * gw[a];
+                    xpc[a] += mass * gdf * gw[a];
+                    xpc[a] += -vol * hs;
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                ci.v[a][pid] += vcot[a];
+                ci.x[a][pid] += xpc[a];
+            }
+            ci.V[pid] += Vc;
+#pragma unroll
+            for (int k = 0; k < D * D; ++k)
+                ci.sig[k][pid] += sigc[k];
+            if constexpr (AFF) {
+                if (sc.tpic) {
+#pragma unroll
+                    for (int k = 0; k < D * D; ++k)
+                        ci.gv[k][pid] += Ac[k];
+                } else {
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int b = 0; b < D; ++b) {
+                            T s = T(0);
+#pragma unroll
+                            for (int k = 0; k < D; ++k)
+                                s += Ac[a * D + k] * Dinv[k * D + b];
+                            ci.aff[a * D + b][pid] += s;
+                        }
+                }
+            }
+        }
+    }
+}
+
+// ---- parameter-gradient reductions (fixed order over dense block ids) ------------------------
+// pg_acc[0] += sum_Q c[Q], pg_acc[1] += sum_Q mu[Q] over occupied particle blocks;
+// pg_acc[2 + k] += sum_q fr[q][k] over active node blocks. One CTA, fixed chunking.
+template <class T>
+__global__ void __launch_bounds__(1024) k_pg_reduce(const T* __restrict__ pg_block, const int* __restrict__ bstart,
+                                                    int nb_total, const T* __restrict__ fr_block,
+                                                    const unsigned char* __restrict__ nflag, int nnb_total, int nfr,
+                                                    int fluid, double* pg_acc)
+{
+    __shared__ T red[1024];
+    const int nslot = 2 + nfr;
+    for (int s = 0; s < nslot; ++s) {
+        T acc = T(0);
+        if (s < 2) {
+            if (!fluid)
+                continue;
+            const int per = (nb_total + 1023) / 1024;
+            for (int j = 0; j < per; ++j) {
+                const int b = threadIdx.x * per + j;
+                if (b < nb_total && bstart[b] >= 0)
+                    acc += pg_block[(size_t)b * 2 + s];
+            }
+        } else {
+            const int per = (nnb_total + 1023) / 1024;
+            for (int j = 0; j < per; ++j) {
+                const int q = threadIdx.x * per + j;
+                if (q < nnb_total && nflag[q])
+                    acc += fr_block[(size_t)q * MAX_FRIC + (s - 2)];
+            }
+        }
+        const T tot = block_sum_fixed<T, 1024>(acc, red);
+        if (threadIdx.x == 0)
+            pg_acc[s] += double(tot);
+    }
+}
+
+// ---- Lagrangian least-squares seeder (SPEC observe_lagrangian + loss) -------------------------
+// loss += sum ||z - target||^2 (fixed-order), cot.z[pid] += 2 (z - target), z = x or v.
+template <class T, int D>
+__global__ void __launch_bounds__(1024) k_seed_lagrangian(PBuf<T, D> P, int n, const int* __restrict__ slot_of_pid,
+                                                          const long long* __restrict__ sel, long long nsel,
+                                                          const T* __restrict__ target, int field, CBuf<T, D> cot,
+                                                          int do_cot, double* loss_acc)
+{
+    __shared__ T red[1024];
+    T acc = T(0);
+    const long long per = (nsel + 1023) / 1024;
+    for (long long j = 0; j < per; ++j) {
+        const long long l = threadIdx.x * per + j;
+        if (l >= nsel)
+            break;
+        const int pid = sel ? int(sel[l]) : int(l);
+        const int s = slot_of_pid[pid];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const T z = field == 0 ? P.x[a][s] : P.v[a][s];
+            const T r = z - target[l * D + a];
+            acc += r * r;
+            if (do_cot) {
+                T* zc = field == 0 ? cot.x[a] : cot.v[a];
+                zc[pid] += T(2) * r;
+            }
+        }
+    }
+    const T tot = block_sum_fixed<T, 1024>(acc, red);
+    if (threadIdx.x == 0)
+        *loss_acc += double(tot);
+}
+
+template <class T, int D> __global__ void k_slot_of_pid(PBuf<T, D> P, int n, int* slot_of_pid)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n)
+        slot_of_pid[P.pid[i]] = i;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Adjoint workspace + drivers (host side, templated on the context type)
+template <class T, int D> struct AdjWork {
+    using C = Cfg<D>;
+    CBuf<T, D> cot[2]{};
+    SBuf<T, D> sb{};
+    GCBuf<T, D> gc{};
+    T* partials = nullptr;  // 2D fields per tile node
+    T* pg_block = nullptr;  // [nb_total][2]
+    T* fr_block = nullptr;  // [nnb_total][MAX_FRIC]
+    double* pg_acc = nullptr;
+    double* loss_acc = nullptr;
+    int* slot_of_pid = nullptr;
+    std::vector<void*> allocs;
+    bool ready = false;
+    int64_t cap = 0;
+
+    template <class X> X* al(size_t k)
+    {
+        X* p = nullptr;
+        if (cudaMalloc(&p, (k ? k : 1) * sizeof(X)) != cudaSuccess)
+            throw std::runtime_error("adjoint workspace: cudaMalloc failed (out of device memory)");
+        allocs.push_back(p);
+        return p;
+    }
+
+    template <class Ctx> void init(Ctx&) {}
+
+    template <class Ctx> void ensure(Ctx& c)
+    {
+        if (ready)
+            return;
+        cap = c.cap;
+        for (int b = 0; b < 2; ++b) {
+            auto& k = cot[b];
+            for (int a = 0; a < D; ++a) {
+                k.x[a] = al<T>(cap);
+                k.v[a] = al<T>(cap);
+            }
+            k.rho = al<T>(cap);
+            k.V = al<T>(cap);
+            k.eps = al<T>(cap);
+            k.szz = D == 2 ? al<T>(cap) : nullptr;
+            for (int q = 0; q < D * D; ++q) {
+                k.sig[q] = al<T>(cap);
+                k.gv[q] = al<T>(cap);
+                k.aff[q] = c.has_aff ? al<T>(cap) : nullptr;
+            }
+        }
+        for (int a = 0; a < D; ++a) {
+            sb.a[a] = al<T>(cap);
+            sb.inc[a] = al<T>(cap);
+        }
+        for (int q = 0; q < D * D; ++q) {
+            sb.L[q] = al<T>(cap);
+            sb.Bc[q] = c.has_aff ? al<T>(cap) : nullptr;
+        }
+        const size_t nodes = (size_t)c.sc.nnb_total * C::NB;
+        gc.gm = al<T>(nodes);
+        for (int a = 0; a < D; ++a) {
+            gc.gmom[a] = al<T>(nodes);
+            gc.gf[a] = al<T>(nodes);
+        }
+        partials = al<T>((size_t)c.sc.nb_total * 2 * D * C::TN);
+        pg_block = al<T>((size_t)c.sc.nb_total * 2);
+        fr_block = al<T>((size_t)c.sc.nnb_total * MAX_FRIC);
+        pg_acc = al<double>(PG_SLOTS);
+        loss_acc = al<double>(1);
+        slot_of_pid = al<int>(cap);
+        ready = true;
+        set_attrs(c);
+    }
+
+    void free_all()
+    {
+        for (void* p : allocs)
+            cudaFree(p);
+        allocs.clear();
+        ready = false;
+    }
+
+    template <class Ctx> void set_attrs(Ctx& c)
+    {
+        if (!ready)
+            return;
+        const int sm5 = int(sizeof(T) * 2 * D * C::TN), sm7 = int(sizeof(T) * (1 + 2 * D) * C::TN);
+        cudaFuncSetAttribute(k_adj_g2pT_gather<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm5);
+        cudaFuncSetAttribute(k_adj_g2pT_gather<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm5);
+        cudaFuncSetAttribute(k_adj_p2gT<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm7);
+        cudaFuncSetAttribute(k_adj_p2gT<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm7);
+        (void)c;
+    }
+
+    // upload / download a host cotangent view (reference layout, id order) <-> cot[b]
+    template <class Ctx> void cot_upload(Ctx& c, const mpm_cot_view* v, int b)
+    {
+        auto& k = cot[b];
+        const int64_t n = c.n;
+        std::vector<T> h((size_t)n);
+        auto put_vec = [&](T* const* dst, const void* srcp) {
+            for (int a = 0; a < D; ++a) {
+                if (srcp) {
+                    const T* s = static_cast<const T*>(srcp);
+                    for (int64_t i = 0; i < n; ++i)
+                        h[i] = s[i * D + a];
+                } else
+                    std::fill(h.begin(), h.end(), T(0));
+                c.h2d(dst[a], h.data(), n);
+            }
+        };
+        auto put_sc = [&](T* dst, const void* srcp) {
+            if (!dst)
+                return;
+            if (srcp)
+                c.h2d(dst, static_cast<const T*>(srcp), n);
+            else
+                c.zero(dst, n);
+        };
+        auto put_mat = [&](T* const* dst, const void* srcp) {
+            if (!dst[0])
+                return;
+            for (int r = 0; r < D; ++r)
+                for (int q = 0; q < D; ++q) {
+                    if (srcp) {
+                        const T* s = static_cast<const T*>(srcp);
+                        for (int64_t i = 0; i < n; ++i)
+                            h[i] = s[i * D * D + q * D + r]; // column-major (r, q)
+                    } else
+                        std::fill(h.begin(), h.end(), T(0));
+                    c.h2d(dst[r * D + q], h.data(), n);
+                }
+        };
+        put_vec(k.x, v->x);
+        put_vec(k.v, v->v);
+        put_sc(k.rho, v->rho);
+        put_sc(k.V, v->volume);
+        put_sc(k.eps, nullptr);
+        if (D == 2)
+            put_sc(k.szz, v->sigma_zz);
+        put_mat(k.sig, v->sigma);
+        put_mat(k.gv, v->grad_v);
+        if (c.has_aff)
+            put_mat(k.aff, v->affine);
+    }
+
+    template <class Ctx> void cot_zero(Ctx& c, int b)
+    {
+        auto& k = cot[b];
+        const int64_t n = c.n;
+        for (int a = 0; a < D; ++a) {
+            c.zero(k.x[a], n);
+            c.zero(k.v[a], n);
+        }
+        c.zero(k.rho, n);
+        c.zero(k.V, n);
+        c.zero(k.eps, n);
+        if (D == 2)
+            c.zero(k.szz, n);
+        for (int q = 0; q < D * D; ++q) {
+            c.zero(k.sig[q], n);
+            c.zero(k.gv[q], n);
+            if (c.has_aff)
+                c.zero(k.aff[q], n);
+        }
+    }
+
+    template <class Ctx> void cot_download(Ctx& c, mpm_cot_view* v, int b)
+    {
+        auto& k = cot[b];
+        const int64_t n = c.n;
+        std::vector<T> h((size_t)n);
+        auto get_vec = [&](T* const* srcd, void* dstp) {
+            if (!dstp)
+                return;
+            T* d = static_cast<T*>(dstp);
+            for (int a = 0; a < D; ++a) {
+                c.d2h(h.data(), srcd[a], n);
+                for (int64_t i = 0; i < n; ++i)
+                    d[i * D + a] = h[i];
+            }
+        };
+        auto get_sc = [&](T* srcd, void* dstp) {
+            if (dstp && srcd)
+                c.d2h(static_cast<T*>(dstp), srcd, n);
+        };
+        auto get_mat = [&](T* const* srcd, void* dstp) {
+            if (!dstp || !srcd[0])
+                return;
+            T* d = static_cast<T*>(dstp);
+            for (int r = 0; r < D; ++r)
+                for (int q = 0; q < D; ++q) {
+                    c.d2h(h.data(), srcd[r * D + q], n);
+                    for (int64_t i = 0; i < n; ++i)
+                        d[i * D * D + q * D + r] = h[i];
+                }
+        };
+        get_vec(k.x, v->x);
+        get_vec(k.v, v->v);
+        get_sc(k.rho, v->rho);
+        get_sc(k.V, v->volume);
+        get_sc(k.eps, v->eps_eq);
+        if (D == 2)
+            get_sc(k.szz, v->sigma_zz);
+        get_mat(k.sig, v->sigma);
+        get_mat(k.gv, v->grad_v);
+        if (c.has_aff)
+            get_mat(k.aff, v->affine);
+    }
+
+    // one reverse step on the state currently in c.buf[c.cur]: cot[bo] (out) -> cot[bi] (in)
+    template <class Ctx> void vjp_enqueue(Ctx& c, int bo, int bi)
+    {
+        ensure(c);
+        // forward replay with the full grid stored (m, p, f, v, v_old)
+        c.sort_and_segment();
+        c.p2g_kernel();
+        c.template grid_kernel<G_SUM | G_MOM | G_CORR | G_STORE>();
+        auto& Pin = c.buf[c.cur];
+        const unsigned gr = c.persistent(4);
+        const size_t sm5 = sizeof(T) * 2 * D * C::TN, sm7 = sizeof(T) * (1 + 2 * D) * C::TN;
+        if (c.has_aff)
+            c.launch("k_adj_g2pT_gather", [&] {
+                k_adj_g2pT_gather<T, D, true><<<gr, 256, sm5, c.stream>>>(c.sc, Pin, c.G, c.perm, c.bstart, c.bend,
+                                                                           c.occ, c.counts, cot[bo], cot[bi], sb,
+                                                                           pg_block, c.st);
+            });
+        else
+            c.launch("k_adj_g2pT_gather", [&] {
+                k_adj_g2pT_gather<T, D, false><<<gr, 256, sm5, c.stream>>>(c.sc, Pin, c.G, c.perm, c.bstart, c.bend,
+                                                                            c.occ, c.counts, cot[bo], cot[bi], sb,
+                                                                            pg_block, c.st);
+            });
+        const int tpb = D == 2 ? 160 : 256;
+        if (c.has_aff)
+            c.launch("k_adj_scatter", [&] {
+                k_adj_scatter<T, D, true><<<c.persistent(8), tpb, 0, c.stream>>>(c.sc, Pin, sb, c.perm, c.keys_sorted,
+                                                                                 c.bstart, c.bend, c.occ, c.counts,
+                                                                                 partials, c.st);
+            });
+        else
+            c.launch("k_adj_scatter", [&] {
+                k_adj_scatter<T, D, false><<<c.persistent(8), tpb, 0, c.stream>>>(c.sc, Pin, sb, c.perm, c.keys_sorted,
+                                                                                  c.bstart, c.bend, c.occ, c.counts,
+                                                                                  partials, c.st);
+            });
+        c.launch("k_adj_grid", [&] {
+            k_adj_grid<T, D><<<c.persistent(4), C::NB, 0, c.stream>>>(c.sc, c.G, gc, partials, c.bstart, c.act,
+                                                                      c.counts + 1, fr_block, c.st);
+        });
+        const bool aff = c.has_aff || c.sc.tpic;
+        if (aff)
+            c.launch("k_adj_p2gT", [&] {
+                k_adj_p2gT<T, D, true><<<gr, 256, sm7, c.stream>>>(c.sc, Pin, gc, c.perm, c.bstart, c.bend, c.occ,
+                                                                   c.counts, cot[bi], c.st);
+            });
+        else
+            c.launch("k_adj_p2gT", [&] {
+                k_adj_p2gT<T, D, false><<<gr, 256, sm7, c.stream>>>(c.sc, Pin, gc, c.perm, c.bstart, c.bend, c.occ,
+                                                                    c.counts, cot[bi], c.st);
+            });
+        int nfr = 0;
+        for (int w = 0; w < 2 * D; ++w)
+            nfr += c.sc.n_fric[w];
+        c.launch("k_pg_reduce", [&] {
+            k_pg_reduce<T><<<1, 1024, 0, c.stream>>>(pg_block, c.bstart, c.sc.nb_total, fr_block, c.nflag,
+                                                     c.sc.nnb_total, nfr, c.sc.material == 0, pg_acc);
+        });
+    }
+
+    template <class Ctx> void pg_reset(Ctx& c, const mpm_param_grads* pg)
+    {
+        double h[PG_SLOTS] = {0};
+        h[0] = pg ? pg->sound_speed : 0.0;
+        h[1] = pg ? pg->viscosity : 0.0;
+        for (int w = 0; w < 2 * D; ++w)
+            if (c.sc.wall_kind[w] == 3 && pg && pg->wall_friction[w])
+                for (int k = 0; k < c.sc.n_fric[w]; ++k)
+                    h[2 + c.sc.fric_off[w] + k] = pg->wall_friction[w][k];
+        c.h2d_raw(pg_acc, h, sizeof(h));
+    }
+
+    template <class Ctx> void pg_download(Ctx& c, mpm_param_grads* pg)
+    {
+        double h[PG_SLOTS];
+        c.d2h_raw(h, pg_acc, sizeof(h));
+        pg->sound_speed = h[0];
+        pg->viscosity = h[1];
+        for (int w = 0; w < 2 * D; ++w)
+            if (c.sc.wall_kind[w] == 3 && pg->wall_friction[w])
+                for (int k = 0; k < c.sc.n_fric[w]; ++k)
+                    pg->wall_friction[w][k] = h[2 + c.sc.fric_off[w] + k];
+    }
+
+    template <class Ctx>
+    void step_vjp_api(Ctx& c, const mpm_state_view* s, const mpm_cot_view* co, mpm_cot_view* ci, mpm_param_grads* pg)
+    {
+        c.upload(s);
+        ensure(c);
+        cot_upload(c, co, 0);
+        pg_reset(c, pg);
+        c.reset_status();
+        vjp_enqueue(c, 0, 1);
+        c.check_status(c.step);
+        cot_download(c, ci, 1);
+        pg_download(c, pg);
+    }
+
+    template <class Ctx>
+    void backprop_api(Ctx& c, const mpm_state_view* s0, int64_t total, int nseg, const mpm_seeder_desc* sd,
+                      mpm_cot_view* c0, mpm_param_grads* pg, mpm_backprop_result* res)
+    {
+        c.backprop_run(*this, s0, total, nseg, sd, c0, pg, res);
     }
 };
 

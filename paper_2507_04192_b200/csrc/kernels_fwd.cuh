@@ -1296,7 +1296,7 @@ __global__ void __launch_bounds__(256) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pin, 
             if (!cell_key<T, D>(sc, xn, key)) {
                 key = 0x7fffffff;
                 atomicMin(&st->ood_pid, pid);
-                st->ood_flag = 1;
+                st->ood_flag = 2;
                 st->abort = 1;
             }
             keys_out[i] = key;
@@ -1354,10 +1354,16 @@ __global__ void k_constitutive(DevScene<T, D> sc, PBuf<T, D> P, int n, DevStatus
     }
 }
 
+// step counter: a step whose only failure is that its OUTPUT left the domain (detected while
+// forming the next step's keys) did complete -- the reference throws in the next step's P2G
 __global__ void k_step_end(DevStatus* st)
 {
-    if (!st->abort)
+    if (!st->abort) {
         st->step += 1;
+    } else if (st->ood_flag == 2 && !st->den_flag && !st->nan_flag && !st->ood_counted) {
+        st->step += 1;
+        st->ood_counted = 1;
+    }
 }
 
 } // namespace mpmgpu
