@@ -25,6 +25,10 @@
 
 using namespace mpmgpu;
 
+#ifndef P2G_WIDE
+#define P2G_WIDE false
+#endif
+
 namespace {
 
 struct ApiError : std::runtime_error {
@@ -342,10 +346,10 @@ template <class T, int D> struct Ctx : CtxBase {
         set(k_g2p<T, D, 0, false, true>);
         set(k_g2p<T, D, 0, true, true>);
         if constexpr (D == 3) {
-            CK(cudaFuncSetAttribute(k_p2g_staged3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(Stage3Cfg<T>::SMEM)));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2g_ctas_per_sm, k_p2g_staged3<T>, Stage3Cfg<T>::THREADS,
-                                                             Stage3Cfg<T>::SMEM));
+            CK(cudaFuncSetAttribute(k_p2g_pipe3<T, P2G_WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(Pipe3Cfg<T, P2G_WIDE>::SMEM)));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2g_ctas_per_sm, k_p2g_pipe3<T, P2G_WIDE>,
+                                                             Pipe3Cfg<T, P2G_WIDE>::THREADS, Pipe3Cfg<T, P2G_WIDE>::SMEM));
         } else {
             CK(cudaFuncSetAttribute(k_p2g_staged<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(StageCfg<T, D>::SMEM)));
@@ -414,9 +418,9 @@ template <class T, int D> struct Ctx : CtxBase {
             });
         } else {
             if constexpr (D == 3) {
-                using S = Stage3Cfg<T>;
+                using S = Pipe3Cfg<T, P2G_WIDE>;
                 launch("k_p2g", [&] {
-                    k_p2g_staged3<T><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
+                    k_p2g_pipe3<T, P2G_WIDE><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
                         sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st);
                 });
             } else {
@@ -499,6 +503,9 @@ template <class T, int D> struct Ctx : CtxBase {
                            "particle " + std::to_string(s.ood_pid) + " outside valid grid interior", s.ood_pid,
                            s.step + 1);
         }
+        if (s.far_flag)
+            throw ApiError(MPM_ERR_NUMERICAL, "P2G: a particle block exceeds the staging capacity (extreme compression)",
+                           -1, s.step + 1);
         throw ApiError(MPM_ERR_NUMERICAL, "device step aborted", -1, s.step);
     }
 

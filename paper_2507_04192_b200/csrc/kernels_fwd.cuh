@@ -839,6 +839,275 @@ __global__ void __launch_bounds__(Stage3Cfg<T>::THREADS, 2)
     }
 }
 
+// 3-D P2G, asynchronous pipeline (PIC / FLIP / blend). Same deterministic march as
+// k_p2g_staged3, but the staging is software-pipelined with cp.async (LDGSTS): work items are
+// (base level, chunk <= CAP particles); item j+2's perm/keys and item j+1's particle fields
+// are in flight while item j is marched, so the dependent gathers through the sort
+// permutation never stall the CTA. Raw fields are staged (x, v, m, V, sigma); fractional
+// offsets, m v and V sigma are formed per visit. One CTA per SM, full register file.
+template <class T, bool WIDE = true> struct Pipe3Cfg {
+    static constexpr int NBC = 64, THREADS = WIDE ? 576 : 192, NSRC = 9, NRAW = 14, MAXIT = 64;
+    static constexpr int CAP = 640;
+    static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
+    static constexpr size_t SMEM_PK = sizeof(int) * 3 * 2 * CAP;
+    static constexpr size_t SMEM_SLOT = sizeof(T) * Cfg<3>::NCOL * NSRC * Cfg<3>::NF;
+    static constexpr size_t SMEM = SMEM_RAW + SMEM_PK + SMEM_SLOT;
+};
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+template <class T> __device__ __forceinline__ void cp_async_t(T* smem, const T* gmem)
+{
+    if constexpr (sizeof(T) == 8)
+        cp_async8(smem, gmem);
+    else
+        cp_async4(smem, gmem);
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <class T, bool WIDE>
+__global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
+    k_p2g_pipe3(DevScene<T, 3> sc, PBuf<T, 3> P, const int* __restrict__ perm, const int* __restrict__ keys,
+                const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ lstart,
+                const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials, DevStatus* st)
+{
+    using C = Cfg<3>;
+    using S = Pipe3Cfg<T, WIDE>;
+    constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW;
+    constexpr int NO1 = WIDE ? 1 : 3; // y-offsets handled per thread
+    // raw field rows: x0..2, v0..2, m, V, sig0..5
+    constexpr int RX = 0, RV = 3, RM = 6, RVOL = 7, RS = 8;
+    extern __shared__ unsigned char smem_raw[];
+    T* raw = reinterpret_cast<T*>(smem_raw);                                   // [2][NRAW][CAP]
+    int* pk = reinterpret_cast<int*>(smem_raw + S::SMEM_RAW);                  // [3][2][CAP] (perm, col)
+    T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_RAW + S::SMEM_PK);      // [NCOL][NSRC][NF]
+    __shared__ int it_start[S::MAXIT], it_len[S::MAXIT], it_lvl[S::MAXIT], it_last[S::MAXIT];
+    __shared__ int nit_s, ccount[NBC], cst[NBC + 1];
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    const int tid = threadIdx.x;
+    const int bc = WIDE ? tid / 9 : tid / 3;
+    const int o0 = WIDE ? (tid % 9) / 3 : tid % 3;
+    const int o1t = WIDE ? tid % 3 : 0; // WIDE: this thread's y-offset
+    const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
+    const T* fld[NRAW] = {P.x[0], P.x[1], P.x[2], P.v[0], P.v[1], P.v[2], P.m, P.V,
+                          P.sig[0], P.sig[1], P.sig[2], P.sig[3], P.sig[4], P.sig[5]};
+
+    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+        const int Q = occ[w];
+        const int s0 = bstart[Q], s1 = bend[Q];
+        int qc[3];
+        block_coords<3>(Q, sc.nb, qc);
+        __syncthreads();
+        if (tid == 0) { // level starts (suffix minimum) -> work items
+            int lv[B + 1];
+            int nxt = s1;
+            lv[B] = s1 - s0;
+            for (int z = B - 1; z >= 0; --z) {
+                const int v = lstart[Q * (B + 1) + z];
+                nxt = (v >= s0 && v < s1) ? v : nxt;
+                lv[z] = nxt - s0;
+            }
+            int k = 0;
+            for (int z = 0; z < B; ++z) {
+                const int nl = lv[z + 1] - lv[z];
+                const int nch = nl > 0 ? (nl + CAP - 1) / CAP : 1;
+                for (int c = 0; c < nch; ++c) {
+                    if (k < S::MAXIT) {
+                        it_start[k] = lv[z] + c * CAP;
+                        it_len[k] = min(CAP, nl - c * CAP);
+                        it_lvl[k] = z;
+                        it_last[k] = c == nch - 1;
+                    }
+                    ++k;
+                }
+            }
+            if (k > S::MAXIT) { // pathological compression: refuse loudly
+                st->far_flag = 1;
+                st->abort = 1;
+                k = 0;
+            }
+            nit_s = k;
+        }
+        __syncthreads();
+        const int nit = nit_s;
+        auto issue_pk = [&](int j) {
+            int* dp = pk + (j % 3) * 2 * CAP;
+            const int b = s0 + it_start[j];
+            for (int r = tid; r < it_len[j]; r += blockDim.x) {
+                cp_async4(dp + r, perm + b + r);
+                cp_async4(dp + CAP + r, keys + b + r);
+            }
+        };
+        auto issue_fields = [&](int j) {
+            const int* pp = pk + (j % 3) * 2 * CAP;
+            T* rb = raw + (j & 1) * NRAW * CAP;
+            const int len = it_len[j];
+            for (int r = tid; r < len; r += blockDim.x) {
+                const int src = pp[r];
+#pragma unroll
+                for (int f = 0; f < NRAW; ++f)
+                    cp_async_t<T>(rb + f * CAP + r, fld[f] + src);
+            }
+        };
+        if (nit > 0)
+            issue_pk(0);
+        if (nit > 1)
+            issue_pk(1);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        if (nit > 0)
+            issue_fields(0);
+        cp_async_commit();
+
+        T* part = partials + (size_t)Q * NF * C::TN;
+        T acc[NO1][3][NF];
+#pragma unroll
+        for (int a = 0; a < NO1; ++a)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    acc[a][k][f] = T(0);
+
+        auto emit_and_reduce = [&](int z) {
+#pragma unroll
+            for (int i1 = 0; i1 < NO1; ++i1) {
+                const int o1 = WIDE ? o1t : i1;
+                const int ncol = (bc0 + o0) * TE + bc1 + o1;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    slots[(ncol * NSRC + o0 * 3 + o1) * NF + f] = acc[i1][0][f];
+                    acc[i1][0][f] = acc[i1][1][f];
+                    acc[i1][1][f] = acc[i1][2][f];
+                    acc[i1][2][f] = T(0);
+                }
+            }
+            __syncthreads();
+            for (int c = tid; c < C::NCOL; c += blockDim.x) {
+                const int n0 = c / TE, n1 = c % TE;
+                T sum[NF];
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    sum[f] = T(0);
+#pragma unroll
+                for (int q = 0; q < NSRC; ++q) {
+                    const int b0 = n0 - q / 3, b1 = n1 - q % 3;
+                    if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
+#pragma unroll
+                        for (int f = 0; f < NF; ++f)
+                            sum[f] += slots[(c * NSRC + q) * NF + f];
+                }
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    part[f * C::TN + z * C::NCOL + c] = sum[f];
+            }
+            __syncthreads();
+        };
+
+        for (int j = 0; j < nit; ++j) {
+            cp_async_wait_all();
+            __syncthreads(); // fields(j) and pk(j+1) have landed for every thread
+            if (j + 1 < nit)
+                issue_fields(j + 1);
+            if (j + 2 < nit)
+                issue_pk(j + 2);
+            cp_async_commit();
+            // column starts of item j (records are column-sorted inside a level)
+            const int len = it_len[j];
+            const int* col = pk + (j % 3) * 2 * CAP + CAP;
+            if (tid < NBC)
+                ccount[tid] = 0;
+            __syncthreads();
+            for (int r = tid; r < len; r += blockDim.x)
+                atomicAdd(&ccount[col[r] & (NBC - 1)], 1);
+            __syncthreads();
+            if (tid < 32) {
+                const int c0 = ccount[2 * tid], c1 = ccount[2 * tid + 1];
+                int v = c0 + c1;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, v, d);
+                    if (tid >= d)
+                        v += t;
+                }
+                const int excl = v - c0 - c1;
+                cst[2 * tid] = excl;
+                cst[2 * tid + 1] = excl + c0;
+                if (tid == 31)
+                    cst[NBC] = v;
+            }
+            __syncthreads();
+            const T* R = raw + (j & 1) * NRAW * CAP;
+            const int kb = cst[bc], ke = cst[bc + 1];
+            for (int k = kb; k < ke; ++k) {
+                T f[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const T u = (R[(RX + a) * CAP + k] - sc.origin[a]) * sc.inv_dh;
+                    f[a] = u - dfloor<T>(u - T(0.5));
+                }
+                T wx, dwx, wy[NO1], dwy[NO1], wz[3], dwz[3];
+                quad_w<T>(f[0], o0, sc.inv_dh, wx, dwx);
+#pragma unroll
+                for (int i1 = 0; i1 < NO1; ++i1)
+                    quad_w<T>(f[1], WIDE ? o1t : i1, sc.inv_dh, wy[i1], dwy[i1]);
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                    quad_w<T>(f[2], q, sc.inv_dh, wz[q], dwz[q]);
+                const T m = R[RM * CAP + k], V = R[RVOL * CAP + k];
+                T mv[3], vs[6];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    mv[a] = m * R[(RV + a) * CAP + k];
+#pragma unroll
+                for (int q = 0; q < 6; ++q)
+                    vs[q] = V * R[(RS + q) * CAP + k];
+#pragma unroll
+                for (int o1 = 0; o1 < NO1; ++o1) {
+                    const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
+                    T u[3], t[3];
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) {
+                        u[r] = vs[sym_idx<3>(r, 0)] * p1 + vs[sym_idx<3>(r, 1)] * p2;
+                        t[r] = vs[sym_idx<3>(r, 2)] * pw;
+                    }
+                    const T mpw = m * pw;
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const T phi = pw * wz[q];
+                        acc[o1][q][0] += mpw * wz[q];
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            acc[o1][q][1 + a] += phi * mv[a];
+                            acc[o1][q][4 + a] -= wz[q] * u[a] + dwz[q] * t[a];
+                        }
+                    }
+                }
+            }
+            if (it_last[j]) {
+                __syncthreads();
+                emit_and_reduce(it_lvl[j]);
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        emit_and_reduce(B);
+        emit_and_reduce(B + 1);
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // grid update: combine partial tiles, momentum update, boundary/contact corrections.
 enum GridMode { G_SUM = 1, G_MOM = 2, G_CORR = 4, G_STORE = 8 };
@@ -1085,7 +1354,7 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
 enum G2PFlags { P_CONSTIT = 1, P_GUARD = 2 };
 
 template <class T, int D, int FLAGS, bool APIC, bool TRACKF>
-__global__ void __launch_bounds__(256) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pin, PBuf<T, D> Pout,
+__global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pin, PBuf<T, D> Pout,
                                              GBuf<T, D> G, const int* __restrict__ perm,
                                              const int* __restrict__ bstart, const int* __restrict__ bend,
                                              const int* __restrict__ occ, const int* __restrict__ n_occ,
@@ -1152,6 +1421,57 @@ __global__ void __launch_bounds__(256) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pin, 
 #pragma unroll
             for (int k = 0; k < D * D; ++k)
                 L[k] = Bm[k] = T(0);
+            if constexpr (!APIC) {
+                // tensor-product factorisation along the last axis: for each outer offset,
+                // A = sum w_z v, Bz = sum dw_z v, Cd = sum w_z (v - v_old); then
+                // v_pic += w_o A, v_inc += w_o Cd, grad v[:, a<d-1] += dw_o A, grad v[:, d-1] += w_o Bz
+#pragma unroll
+                for (int oo = 0; oo < C::NOFF / 3; ++oo) {
+                    int o[D - 1 > 0 ? D - 1 : 1];
+                    int kk = oo, t0 = 0;
+#pragma unroll
+                    for (int a = D - 2; a >= 0; --a) {
+                        o[a] = kk % 3;
+                        kk /= 3;
+                    }
+#pragma unroll
+                    for (int a = 0; a < D - 1; ++a)
+                        t0 = t0 * TE + tb[a] + o[a];
+                    t0 = t0 * TE + tb[D - 1];
+                    T A[D], Bz[D], Cd[D];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        const T* va = tile + a * TN + t0;
+                        const T* voa = tile + (D + a) * TN + t0;
+                        const T v0 = va[0], v1 = va[1], v2 = va[2];
+                        A[a] = w[D - 1][0] * v0 + w[D - 1][1] * v1 + w[D - 1][2] * v2;
+                        Bz[a] = dw[D - 1][0] * v0 + dw[D - 1][1] * v1 + dw[D - 1][2] * v2;
+                        Cd[a] = w[D - 1][0] * (v0 - voa[0]) + w[D - 1][1] * (v1 - voa[1]) + w[D - 1][2] * (v2 - voa[2]);
+                    }
+                    T wo = T(1), po[D - 1 > 0 ? D - 1 : 1];
+#pragma unroll
+                    for (int a = 0; a < D - 1; ++a)
+                        wo *= w[a][o[a]];
+#pragma unroll
+                    for (int a = 0; a < D - 1; ++a) {
+                        T r = dw[a][o[a]];
+#pragma unroll
+                        for (int b = 0; b < D - 1; ++b)
+                            if (b != a)
+                                r *= w[b][o[b]];
+                        po[a] = r;
+                    }
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        vpic[a] += wo * A[a];
+                        vinc[a] += wo * Cd[a];
+#pragma unroll
+                        for (int b = 0; b < D - 1; ++b)
+                            L[a * D + b] += po[b] * A[a];
+                        L[a * D + D - 1] += wo * Bz[a];
+                    }
+                }
+            } else {
 #pragma unroll
             for (int k = 0; k < C::NOFF; ++k) {
                 int o[D];
@@ -1191,17 +1511,16 @@ __global__ void __launch_bounds__(256) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pin, 
 #pragma unroll
                     for (int b = 0; b < D; ++b)
                         L[a * D + b] += nv[a] * gw[b];
-                if constexpr (APIC) {
-                    T r[D];
+                T r[D];
 #pragma unroll
-                    for (int a = 0; a < D; ++a)
-                        r[a] = (sc.origin[a] + T(qc[a] * C::B + tb[a] + o[a]) * sc.dh) - x[a];
+                for (int a = 0; a < D; ++a)
+                    r[a] = (sc.origin[a] + T(qc[a] * C::B + tb[a] + o[a]) * sc.dh) - x[a];
 #pragma unroll
-                    for (int a = 0; a < D; ++a)
+                for (int a = 0; a < D; ++a)
 #pragma unroll
-                        for (int b = 0; b < D; ++b)
-                            Bm[a * D + b] += phi * nv[a] * r[b];
-                }
+                    for (int b = 0; b < D; ++b)
+                        Bm[a * D + b] += phi * nv[a] * r[b];
+            }
             }
             T xn[D], vn[D];
 #pragma unroll
