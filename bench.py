@@ -46,7 +46,7 @@ UNIT = "particle-steps/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
@@ -279,7 +279,7 @@ def bench_b200(a, rank, world, local):
                    "l2_policy": "inputs (state ~1.4 GB f64) larger than the 126 MB L2; no flush",
                    "algorithmic_bytes_per_particle_step": B_fwd, "active_nodes_per_particle": active_nodes_step / n},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic_for(dom, a),
                      "algorithmic_bytes_per_launch": kb[dom], "mean_launch_ms": dom_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
                      "step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak,
@@ -288,6 +288,16 @@ def bench_b200(a, rank, world, local):
         "clocks": ck, "gpu_launches": launches, "e2e": e2e,
     }
     return line
+
+
+def traffic_for(kernel, a):
+    """dram__bytes_read + dram__bytes_write per launch of `kernel` from the committed ncu --set full
+    capture of the same command (profiles/traffic.json); None when absent or another workload."""
+    p = ROOT / "profiles" / "traffic.json"
+    if a.config != "C4" or a.dtype != "f64" or not p.exists():
+        return None
+    t = json.loads(p.read_text()).get(kernel)
+    return t["dram_bytes"] if t else None
 
 
 def bench_e2e(ctx, s, st, steps):

@@ -161,7 +161,11 @@ typedef struct mpm_backprop_result {
 } mpm_backprop_result;
 
 /* advance flags */
-enum { MPM_ADV_NAN_GUARD = 1u /* run(): abort on non-finite state (stepper.hpp:107-109) */ };
+enum {
+    MPM_ADV_NAN_GUARD = 1u, /* run(): abort on non-finite state (stepper.hpp:519-522) */
+    MPM_ADV_STORE_GRID = 2u /* also keep the step's full grid (mass, momentum, force) so that
+                               mpm_grid_download returns Stepper::grid as the reference has it */
+};
 
 typedef struct mpm_ctx mpm_ctx;
 

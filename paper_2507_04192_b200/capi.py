@@ -27,6 +27,7 @@ SCHEME = {"pic": 0, "flip": 1, "blend": 2, "apic": 3, "tpic": 4}
 WALL = {"slip": 0, "no_slip": 1, "fixed": 2, "fixed_wall": 2, "coulomb": 3}
 MAT_FLUID, MAT_DP = 0, 1
 MPM_ADV_NAN_GUARD = 1
+MPM_ADV_STORE_GRID = 2
 MPM_SEEDER_NONE, MPM_SEEDER_LAGRANGIAN_LS = 0, 1
 
 c_double_p = C.POINTER(C.c_double)

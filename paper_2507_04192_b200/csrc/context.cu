@@ -458,11 +458,14 @@ template <class T, int D> struct Ctx : CtxBase {
         keys_valid = true;
     }
 
-    void step_once(bool guard)
+    void step_once(bool guard, bool store = false)
     {
         sort_and_segment();
         p2g_kernel();
-        grid_kernel<G_SUM | G_MOM | G_CORR>();
+        if (store)
+            grid_kernel<G_SUM | G_MOM | G_CORR | G_STORE>();
+        else
+            grid_kernel<G_SUM | G_MOM | G_CORR>();
         if (guard)
             g2p_kernel_fl<P_CONSTIT | P_GUARD>();
         else
@@ -608,10 +611,11 @@ template <class T, int D> struct Ctx : CtxBase {
         if (nsteps <= 0)
             return;
         const bool guard = flags & MPM_ADV_NAN_GUARD;
+        const bool store = flags & MPM_ADV_STORE_GRID;
         reset_status();
-        if (prof) {
+        if (prof || store) {
             for (int64_t k = 0; k < nsteps; ++k)
-                step_once(guard);
+                step_once(guard, store);
         } else {
             // first step runs eagerly (computes keys if needed); the rest replay a captured graph
             step_once(guard);
@@ -725,14 +729,20 @@ template <class T, int D> struct Ctx : CtxBase {
     {
         const int64_t nn = num_nodes();
         std::vector<T> blk((size_t)sc.nnb_total * C::NB);
+        // only node blocks active in the last grid phase hold current values (the rest is stale)
+        std::vector<unsigned char> active(sc.nnb_total);
+        CK(cudaMemcpyAsync(active.data(), nflag, sc.nnb_total, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
         auto pull = [&](T* dptr, void* dst, int comps, int comp) {
             if (!dst)
                 return;
             CK(cudaMemcpyAsync(blk.data(), dptr, blk.size() * sizeof(T), cudaMemcpyDeviceToHost, stream));
             CK(cudaStreamSynchronize(stream));
             T* out = static_cast<T*>(dst);
-            for (int64_t i = 0; i < nn; ++i)
-                out[i * comps + comp] = blk[block_index(i)];
+            for (int64_t i = 0; i < nn; ++i) {
+                const size_t b = block_index(i);
+                out[i * comps + comp] = active[b / C::NB] ? blk[b] : T(0);
+            }
         };
         pull(G.m, g->mass, 1, 0);
         for (int a = 0; a < D; ++a) {

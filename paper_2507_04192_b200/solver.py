@@ -72,8 +72,9 @@ class Context:
         state.sync_from(v, keep)
         return state
 
-    def advance(self, n: int, nan_guard: bool = False):
-        self.check(self.lib.mpm_advance(self.h, int(n), capi.MPM_ADV_NAN_GUARD if nan_guard else 0))
+    def advance(self, n: int, nan_guard: bool = False, store_grid: bool = False):
+        flags = (capi.MPM_ADV_NAN_GUARD if nan_guard else 0) | (capi.MPM_ADV_STORE_GRID if store_grid else 0)
+        self.check(self.lib.mpm_advance(self.h, int(n), flags))
 
     def advance_timed(self, n: int, nan_guard: bool = False) -> float:
         """advance n steps; returns the device time (ms) from CUDA events on the context stream"""
@@ -203,7 +204,7 @@ class Stepper:
         if self._ctx is None or self._ctx.max_particles < n or _scene_changed(self._ctx, self.scene):
             self._ctx = Context(self.scene, n)
         self._ctx.upload(state)
-        self._ctx.advance(1)
+        self._ctx.advance(1, store_grid=True)
         self._ctx.download(state)
 
     def fetch_grid(self) -> Grid:
@@ -244,7 +245,7 @@ def run(scene: Scene, state: SimState, num_steps: int, stride: int, force: bool 
             chunk = min(num_steps - s, stride - (state.step + s) % stride if (state.step + s) % stride else stride)
         else:
             chunk = num_steps - s
-        ctx.advance(chunk, nan_guard=True)
+        ctx.advance(chunk, nan_guard=True, store_grid=observer is not None)
         s += chunk
         cur_step = state.step + s
         if observer is not None:
