@@ -388,14 +388,13 @@ template <class T, int D> struct Ctx : CtxBase {
             launch("k_keys", [&] { k_keys<T, D><<<grid_for(n, 256), 256, 0, stream>>>(sc, buf[cur], int(n), keys, st); });
             keys_valid = true;
         }
+        // radix-sort only the bits a valid key can have (C4: 24 bits -> 3 onesweep passes). An
+        // out-of-domain particle's sentinel key aliases in those bits, but such a step is aborted.
         int end_bit = 1;
-        while ((int64_t(1) << end_bit) <= (int64_t(sc.nb_total) << C::LOGNB))
+        while ((int64_t(1) << end_bit) < (int64_t(sc.nb_total) << C::LOGNB))
             ++end_bit;
-        end_bit = end_bit < 31 ? end_bit + 1 : 31; // room for the out-of-domain sentinel
-        if (end_bit > 31)
-            end_bit = 31;
         size_t bytes = cub_bytes;
-        CK(cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys, keys_sorted, iota, perm, int(n), 0, 32, stream));
+        CK(cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys, keys_sorted, iota, perm, int(n), 0, end_bit, stream));
         CK(cudaMemsetAsync(bstart, 0xff, sizeof(int) * sc.nb_total, stream));
         CK(cudaMemsetAsync(bend, 0xff, sizeof(int) * sc.nb_total, stream));
         CK(cudaMemsetAsync(lstart, 0xff, sizeof(int) * sc.nb_total * (C::B + 1), stream));
@@ -405,7 +404,6 @@ template <class T, int D> struct Ctx : CtxBase {
         launch("k_compact", [&] { k_compact_pos<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, sc.nb_total, occ, counts); });
         launch("k_mark_nodes", [&] { k_mark_nodes<D><<<grid_for(sc.nb_total, 128), 128, 0, stream>>>(occ, counts, d_nb, d_nnb, nflag); });
         launch("k_compact", [&] { k_compact_flag<<<grid_for(sc.nnb_total, 256), 256, 0, stream>>>(nflag, sc.nnb_total, act, counts + 1); });
-        (void)end_bit;
     }
 
     void p2g_kernel()

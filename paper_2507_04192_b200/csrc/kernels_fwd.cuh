@@ -846,7 +846,11 @@ __global__ void __launch_bounds__(Stage3Cfg<T>::THREADS, 2)
 // permutation never stall the CTA. Raw fields are staged (x, v, m, V, sigma); fractional
 // offsets, m v and V sigma are formed per visit. One CTA per SM, full register file.
 template <class T, bool WIDE = true> struct Pipe3Cfg {
-    static constexpr int NBC = 64, THREADS = WIDE ? 576 : 192, NSRC = 9, NRAW = 14, MAXIT = 64;
+    // SPLIT (f64): two warp groups share the staged records, one accumulates mass + momentum,
+    // the other the force -> half the accumulators per thread, twice the warps per SM
+    static constexpr bool SPLIT = false; // measured: 0.597 ms vs 0.583 ms unsplit (C4 f64) -- kept off
+    static constexpr int LANES = WIDE ? 576 : 192;
+    static constexpr int NBC = 64, THREADS = SPLIT ? 2 * LANES : LANES, NSRC = 9, NRAW = 14, MAXIT = 64;
     static constexpr int CAP = 640;
     static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
     static constexpr size_t SMEM_PK = sizeof(int) * 3 * 2 * CAP;
@@ -884,6 +888,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     using S = Pipe3Cfg<T, WIDE>;
     constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW;
     constexpr int NO1 = WIDE ? 1 : 3; // y-offsets handled per thread
+    constexpr bool SPLIT = S::SPLIT;
+    constexpr int NA = SPLIT ? 4 : NF; // accumulated fields per thread
     // raw field rows: x0..2, v0..2, m, V, sig0..5
     constexpr int RX = 0, RV = 3, RM = 6, RVOL = 7, RS = 8;
     extern __shared__ unsigned char smem_raw[];
@@ -896,9 +902,13 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
         return;
     const int nocc = *n_occ;
     const int tid = threadIdx.x;
-    const int bc = WIDE ? tid / 9 : tid / 3;
-    const int o0 = WIDE ? (tid % 9) / 3 : tid % 3;
-    const int o1t = WIDE ? tid % 3 : 0; // WIDE: this thread's y-offset
+    const int grp = SPLIT ? tid / S::LANES : 0;      // 0: mass + momentum (+ force if !SPLIT), 1: force
+    const int lt = SPLIT ? tid % S::LANES : tid;
+    const int bc = WIDE ? lt / 9 : lt / 3;
+    const int o0 = WIDE ? (lt % 9) / 3 : lt % 3;
+    const int o1t = WIDE ? lt % 3 : 0; // WIDE: this thread's y-offset
+    const bool mid = o0 == 1;
+    const T xoff = o0 == 0 ? T(1.5) : (o0 == 1 ? T(1) : T(0.5)); // h = fx - xoff (bspline.hpp:330-335)
     const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
     const T* fld[NRAW] = {P.x[0], P.x[1], P.x[2], P.v[0], P.v[1], P.v[2], P.m, P.V,
                           P.sig[0], P.sig[1], P.sig[2], P.sig[3], P.sig[4], P.sig[5]};
@@ -960,6 +970,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                     cp_async_t<T>(rb + f * CAP + r, fld[f] + src);
             }
         };
+        if (tid < NBC)
+            ccount[tid] = 0;
         if (nit > 0)
             issue_pk(0);
         if (nit > 1)
@@ -972,13 +984,13 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
         cp_async_commit();
 
         T* part = partials + (size_t)Q * NF * C::TN;
-        T acc[NO1][3][NF];
+        T acc[NO1][3][NA];
 #pragma unroll
         for (int a = 0; a < NO1; ++a)
 #pragma unroll
             for (int k = 0; k < 3; ++k)
 #pragma unroll
-                for (int f = 0; f < NF; ++f)
+                for (int f = 0; f < NA; ++f)
                     acc[a][k][f] = T(0);
 
         auto emit_and_reduce = [&](int z) {
@@ -986,9 +998,12 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
             for (int i1 = 0; i1 < NO1; ++i1) {
                 const int o1 = WIDE ? o1t : i1;
                 const int ncol = (bc0 + o0) * TE + bc1 + o1;
+                // group 0 owns fields [0, NA) (m, p), group 1 fields [4, 7) (f)
+                const int nfg = (!SPLIT || grp == 0) ? NA : 3, f0 = grp == 0 ? 0 : 4;
 #pragma unroll
-                for (int f = 0; f < NF; ++f) {
-                    slots[(ncol * NSRC + o0 * 3 + o1) * NF + f] = acc[i1][0][f];
+                for (int f = 0; f < NA; ++f) {
+                    if (f < nfg)
+                        slots[(ncol * NSRC + o0 * 3 + o1) * NF + f0 + f] = acc[i1][0][f];
                     acc[i1][0][f] = acc[i1][1][f];
                     acc[i1][1][f] = acc[i1][2][f];
                     acc[i1][2][f] = T(0);
@@ -1024,14 +1039,28 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
             if (j + 2 < nit)
                 issue_pk(j + 2);
             cp_async_commit();
-            // column starts of item j (records are column-sorted inside a level)
+            // item j: convert each staged particle once (x -> fractional offset, v -> m v,
+            // sigma -> V sigma) and count its column (records are column-sorted inside a level)
             const int len = it_len[j];
             const int* col = pk + (j % 3) * 2 * CAP + CAP;
-            if (tid < NBC)
-                ccount[tid] = 0;
-            __syncthreads();
-            for (int r = tid; r < len; r += blockDim.x)
-                atomicAdd(&ccount[col[r] & (NBC - 1)], 1);
+            {
+                T* Rw = raw + (j & 1) * NRAW * CAP;
+                for (int r = tid; r < len; r += blockDim.x) {
+                    atomicAdd(&ccount[col[r] & (NBC - 1)], 1);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const T u = (Rw[(RX + a) * CAP + r] - sc.origin[a]) * sc.inv_dh;
+                        Rw[(RX + a) * CAP + r] = u - dfloor<T>(u - T(0.5));
+                    }
+                    const T m = Rw[RM * CAP + r], V = Rw[RVOL * CAP + r];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                        Rw[(RV + a) * CAP + r] *= m;
+#pragma unroll
+                    for (int q = 0; q < 6; ++q)
+                        Rw[(RS + q) * CAP + r] *= V;
+                }
+            }
             __syncthreads();
             if (tid < 32) {
                 const int c0 = ccount[2 * tid], c1 = ccount[2 * tid + 1];
@@ -1047,6 +1076,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                 cst[2 * tid + 1] = excl + c0;
                 if (tid == 31)
                     cst[NBC] = v;
+                ccount[2 * tid] = 0; // ready for the next item (counted after the next top barrier)
+                ccount[2 * tid + 1] = 0;
             }
             __syncthreads();
             const T* R = raw + (j & 1) * NRAW * CAP;
@@ -1054,45 +1085,61 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
             for (int k = kb; k < ke; ++k) {
                 T f[3];
 #pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const T u = (R[(RX + a) * CAP + k] - sc.origin[a]) * sc.inv_dh;
-                    f[a] = u - dfloor<T>(u - T(0.5));
-                }
+                for (int a = 0; a < 3; ++a)
+                    f[a] = R[(RX + a) * CAP + k];
                 T wx, dwx, wy[NO1], dwy[NO1], wz[3], dwz[3];
-                quad_w<T>(f[0], o0, sc.inv_dh, wx, dwx);
+                { // this lane's x offset o0 (lanes differ): branch-free quadratic B-spline
+                    const T h = f[0] - xoff;
+                    const T hh = h * h;
+                    wx = mid ? T(0.75) - hh : T(0.5) * hh;
+                    dwx = (mid ? -T(2) * h : h) * sc.inv_dh;
+                }
 #pragma unroll
                 for (int i1 = 0; i1 < NO1; ++i1)
                     quad_w<T>(f[1], WIDE ? o1t : i1, sc.inv_dh, wy[i1], dwy[i1]);
 #pragma unroll
                 for (int q = 0; q < 3; ++q)
                     quad_w<T>(f[2], q, sc.inv_dh, wz[q], dwz[q]);
-                const T m = R[RM * CAP + k], V = R[RVOL * CAP + k];
+                const T m = R[RM * CAP + k];
                 T mv[3], vs[6];
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
-                    mv[a] = m * R[(RV + a) * CAP + k];
+                    mv[a] = R[(RV + a) * CAP + k];
 #pragma unroll
                 for (int q = 0; q < 6; ++q)
-                    vs[q] = V * R[(RS + q) * CAP + k];
+                    vs[q] = R[(RS + q) * CAP + k];
+                if (!SPLIT || grp == 0) {
 #pragma unroll
-                for (int o1 = 0; o1 < NO1; ++o1) {
-                    const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
-                    T u[3], t[3];
+                    for (int o1 = 0; o1 < NO1; ++o1) {
+                        const T pw = wx * wy[o1];
+                        const T mpw = m * pw;
 #pragma unroll
-                    for (int r = 0; r < 3; ++r) {
-                        u[r] = vs[sym_idx<3>(r, 0)] * p1 + vs[sym_idx<3>(r, 1)] * p2;
-                        t[r] = vs[sym_idx<3>(r, 2)] * pw;
-                    }
-                    const T mpw = m * pw;
+                        for (int q = 0; q < 3; ++q) {
+                            const T phi = pw * wz[q];
+                            acc[o1][q][0] += mpw * wz[q];
 #pragma unroll
-                    for (int q = 0; q < 3; ++q) {
-                        const T phi = pw * wz[q];
-                        acc[o1][q][0] += mpw * wz[q];
-#pragma unroll
-                        for (int a = 0; a < 3; ++a) {
-                            acc[o1][q][1 + a] += phi * mv[a];
-                            acc[o1][q][4 + a] -= wz[q] * u[a] + dwz[q] * t[a];
+                            for (int a = 0; a < 3; ++a)
+                                acc[o1][q][1 + a] += phi * mv[a];
                         }
+                    }
+                }
+                if (!SPLIT || grp == 1) {
+                    constexpr int FO = SPLIT ? 0 : 4; // force slots in acc
+#pragma unroll
+                    for (int o1 = 0; o1 < NO1; ++o1) {
+                        // grad phi = (dwx wy wz, wx dwy wz, wx wy dwz): V sigma grad phi = wz u + dwz t
+                        const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
+                        T u[3], t[3];
+#pragma unroll
+                        for (int r = 0; r < 3; ++r) {
+                            u[r] = vs[sym_idx<3>(r, 0)] * p1 + vs[sym_idx<3>(r, 1)] * p2;
+                            t[r] = vs[sym_idx<3>(r, 2)] * pw;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 3; ++q)
+#pragma unroll
+                            for (int a = 0; a < 3; ++a)
+                                acc[o1][q][FO + a] -= wz[q] * u[a] + dwz[q] * t[a];
                     }
                 }
             }
