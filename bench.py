@@ -17,8 +17,11 @@ from init_scene. A "step" is one forward MPM step Phi over all 
   cpu_baseline  the reference compiled unmodified (oracle/_ref, "reference") -- or the oracle
              restatement ("port") if absent -- on a bounded sample of the same workload, one
              process per host core.
-N>1 (torchrun): weak scaling, one C4 replica per rank (replicas only in this revision: the NCCL
-slab decomposition of §8e is not yet on this path), max-over-ranks device time.
+N>1 (torchrun): weak scaling through the slab decomposition of SURVEY.md §8e
+(paper_2507_04192_b200/distributed.py). The C4 domain becomes 256N x 256 x 256 cells with one
+column per rank, and rank r owns the slab x in [256r, 256(r+1)). Every step does a real NCCL halo
+exchange of the 2 shared node planes and migrates particles that cross a slab. The time is
+max-over-ranks device time (CUDA events around K steps). `--mode slab` runs the same path at N=1.
 --impl reference: the reference's own CPU implementation of the step on all host cores (rank 0 only).
 """
 from __future__ import annotations
@@ -52,6 +55,8 @@ def parse():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "plain", "slab"],
+                    help="auto: one context at N=1, slab decomposition for N>1")
     return ap.parse_args()
 
 
@@ -290,6 +295,125 @@ def bench_b200(a, rank, world, local):
     return line
 
 
+def bench_slab(a, rank, world, local):
+    """Slab-decomposed step over NCCL, weak scaling (C4: one column per rank)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2507_04192_b200 import init_scene
+    from paper_2507_04192_b200.distributed import GpuSlabDomain, SlabPlan, SlabStepper, TorchTransport
+    from paper_2507_04192_b200.presets import CONFIGS, c4_column3d
+
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    if a.config == "C4":
+        s = c4_column3d(a.dtype, replicas_x=world)
+        st = init_scene(c4_column3d(a.dtype))  # this rank's column, shifted into its slab
+        n = st.particles.size()
+        st.particles.x[:, 0] += 256 * rank * s.config.dh
+        ids = np.arange(rank * n, (rank + 1) * n, dtype=np.int64)
+        plan = SlabPlan([256 * r for r in range(world + 1)], 8)
+        dom = GpuSlabDomain(s, plan, rank, st, ids, device=local, local=True)
+        n_total = n * world
+        scaling = "weak"
+    else:
+        s = CONFIGS[a.config](a.dtype)
+        full = init_scene(s)
+        plan = SlabPlan.make(s, world, full.particles.x)
+        dom = GpuSlabDomain(s, plan, rank, full, None, device=local)
+        n_total = full.particles.size()
+        scaling = "strong"
+    stp = SlabStepper([dom], TorchTransport())
+    stp.advance(a.warmup)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = dom.ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record()
+    stp.advance(a.steps)
+    torch.cuda.synchronize()  # every library call has synchronised its own stream already
+    ev1.record()
+    ev1.synchronize()
+    dist.barrier()
+    ck = clocks.stop()
+    launches = dom.ctx.launch_count() - l0
+    t = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    mig = torch.tensor([stp.migrated], device="cuda", dtype=torch.int64)
+    dist.all_reduce(mig)
+    # e2e: rank-local upload from pinned host + K decomposed steps + compact download, max over ranks
+    e2e = bench_slab_e2e(dom, stp, a.steps)
+    te = torch.tensor([e2e["seconds"], e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]], device="cuda",
+                      dtype=torch.float64)
+    dist.all_reduce(te[:1], op=dist.ReduceOp.MAX)
+    tb = te[1:].clone()
+    dist.all_reduce(tb)
+    dom.close()
+    dist.barrier()
+    if rank != 0:
+        return None
+    e2e_line = {"value": n_total * a.steps / float(te[0].item()), "unit": UNIT,
+                "h2d_bytes_per_step": float(tb[0].item()), "d2h_bytes_per_step": float(tb[1].item()),
+                "call": e2e["call"], "seconds": float(te[0].item())}
+    return {
+        "metric": METRIC, "value": n_total * a.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": a.dtype, "data": "synthetic (init_scene seeding of the named scene, deterministic)",
+        "config": {"workload": (f"C4 x{world}: 3-D D-P granular column collapse, one 128x64x64-cell column per rank, "
+                                f"domain {s.config.cells}" if a.config == "C4" else a.config),
+                   "particles_total": n_total, "parallelism": f"slab x{world} (NCCL halo + migration)",
+                   "slab_bounds": plan.bounds, "migrated_particles": int(mig.item()),
+                   "l2_policy": "inputs larger than the 126 MB L2; no flush"},
+        "clocks": ck, "gpu_launches": launches, "e2e": e2e_line,
+    }
+
+
+def bench_slab_e2e(dom, stp, steps):
+    """Host state in pinned buffers -> mpm_state_upload_ids -> K decomposed steps ->
+    mpm_state_download_local, wall clock."""
+    import ctypes as C
+
+    import torch
+    from paper_2507_04192_b200.state import SimState
+
+    sub, ids, _ = dom.gather()
+    k = len(ids)
+    st = SimState(sub, 0, 0.0)
+    v, keep = st.to_view()
+    pinned = {}
+    for name, arr in keep.items():
+        if arr is None:
+            continue
+        t = torch.empty(arr.shape, dtype=torch.from_numpy(arr[:0]).dtype, pin_memory=True).numpy()
+        t[...] = arr
+        pinned[name] = t
+        setattr(v, name, t.ctypes.data)
+    ids_p = torch.empty(k, dtype=torch.int64, pin_memory=True).numpy()
+    ids_p[...] = ids
+    lib, h = dom.lib, dom.h
+    out = SimState.zeros(k + dom.capacity // 4, sub.dim, sub.dtype)
+    ov, okeep = out.output_view()
+    oids = np.empty(k + dom.capacity // 4, np.int64)
+    torch.cuda.synchronize()
+    import torch.distributed as dist
+    dist.barrier()
+    t0 = time.perf_counter()
+    dom.ctx.check(lib.mpm_state_upload_ids(h, C.byref(v), ids_p.ctypes.data_as(C.c_void_p)))
+    stp.advance(steps)
+    dom.ctx.check(lib.mpm_state_download_local(h, C.byref(ov), oids.ctypes.data_as(C.c_void_p)))
+    t1 = time.perf_counter()
+    h2d = sum(a.nbytes for a in pinned.values()) + ids_p.nbytes
+    d2h = ov.n * (sum(a.nbytes for a in pinned.values()) + ids_p.nbytes) / max(k, 1)
+    return {"seconds": t1 - t0, "h2d_bytes_per_step": h2d / steps, "d2h_bytes_per_step": d2h / steps,
+            "call": f"mpm_state_upload_ids (pinned host) + {steps} slab steps + mpm_state_download_local, wall clock"}
+
+
 def traffic_for(kernel, a):
     """dram__bytes_read + dram__bytes_write per launch of `kernel` from the committed ncu --set full
     capture of the same command (profiles/traffic.json); None when absent or another workload."""
@@ -385,7 +509,8 @@ def main():
         if line:
             print(json.dumps(line), flush=True)
         return
-    line = bench_b200(a, rank, world, local)
+    slab = a.mode == "slab" or (a.mode == "auto" and world > 1)
+    line = bench_slab(a, rank, world, local) if slab else bench_b200(a, rank, world, local)
     if line is not None:
         if not a.no_cpu_baseline:
             try:

@@ -220,6 +220,38 @@ int mpm_backprop(mpm_ctx* ctx, const mpm_state_view* initial, int64_t total_step
                  const mpm_seeder_desc* seeder, mpm_cot_view* initial_state_cot,
                  mpm_param_grads* pg, mpm_backprop_result* result);
 
+/* ---- slab decomposition across GPUs ------------------------------------ */
+/* One context per GPU, global coordinates; the context owns the particles whose base cell along
+ * x lies in [cell_lo, cell_hi) (multiples of the block edge, 16 in 2-D / 8 in 3-D). A step is
+ *   mpm_step_p2g_local -> halo exchange of the 2 node planes shared with each x-neighbour
+ *   (mpm_halo export/import on caller device buffers) -> mpm_step_finish_local -> migration
+ *   (mpm_migrate_export / mpm_migrate_import) of particles that left the slab.
+ * The transport between GPUs (NCCL over NVLink via torch.distributed, or device copies in the
+ * single-process mode) belongs to the caller (paper_2507_04192_b200/distributed.py). */
+int mpm_slab_set(mpm_ctx* ctx, int cell_lo, int cell_hi, int64_t mig_cap);
+/* enqueue all further work of ctx on `stream` (a cudaStream_t; NULL = the context's own). The
+ * slab entry points below only enqueue (no host synchronisation) except mpm_step_finish_local,
+ * so a transport on the same stream (NCCL via torch) is ordered with them. */
+int mpm_ctx_set_stream(mpm_ctx* ctx, void* stream);
+/* upload a rank-local subset: s holds n particles, ids their global particle ids */
+int mpm_state_upload_ids(mpm_ctx* ctx, const mpm_state_view* s, const int64_t* ids);
+/* compact download of the alive local particles in storage order (s sized >= mpm_local_count)
+ * + their global ids */
+int mpm_state_download_local(mpm_ctx* ctx, mpm_state_view* s, int64_t* ids);
+int64_t mpm_local_count(const mpm_ctx* ctx);
+int mpm_step_p2g_local(mpm_ctx* ctx);
+/* node planes [plane_lo, plane_lo + n_planes) x all other nodes, (1 + 2 dim) scalars each:
+ * mode 0 export into dev_buf; 1 import as received + own; 2 import as own + received */
+int mpm_halo(mpm_ctx* ctx, int plane_lo, int n_planes, void* dev_buf, int mode);
+int mpm_step_finish_local(mpm_ctx* ctx, uint32_t flags);
+/* particles that left the slab during the last step, toward -x (lo) and +x (hi) */
+int mpm_particle_record_size(const mpm_ctx* ctx);
+/* host-side counts of the last mpm_step_finish_local (known after it returns) */
+int mpm_migrate_counts(const mpm_ctx* ctx, int64_t* n_lo, int64_t* n_hi);
+int mpm_migrate_export(mpm_ctx* ctx, void* lo, int* lo_pid, void* hi, int* hi_pid, int64_t cap, int64_t* n_lo,
+                       int64_t* n_hi);
+int mpm_migrate_import(mpm_ctx* ctx, const void* recs, const int* pids, int64_t n);
+
 /* ---- instrumentation (bench / tests) --------------------------------------------------- */
 /* enable per-kernel CUDA-event timing on the context stream */
 int mpm_profile_enable(mpm_ctx* ctx, int enable);

@@ -179,6 +179,19 @@ _PROTOS = {
                                C.POINTER(ParamGradsView)]),
     "mpm_backprop": (C.c_int, [C.c_void_p, C.POINTER(StateView), C.c_int64, C.c_int, C.POINTER(SeederDesc),
                                C.POINTER(CotView), C.POINTER(ParamGradsView), C.POINTER(BackpropResultView)]),
+    "mpm_slab_set": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64]),
+    "mpm_state_upload_ids": (C.c_int, [C.c_void_p, C.POINTER(StateView), C.c_void_p]),
+    "mpm_state_download_local": (C.c_int, [C.c_void_p, C.POINTER(StateView), C.c_void_p]),
+    "mpm_local_count": (C.c_int64, [C.c_void_p]),
+    "mpm_step_p2g_local": (C.c_int, [C.c_void_p]),
+    "mpm_halo": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int]),
+    "mpm_step_finish_local": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "mpm_particle_record_size": (C.c_int, [C.c_void_p]),
+    "mpm_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "mpm_migrate_counts": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "mpm_migrate_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "mpm_migrate_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "mpm_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "mpm_profile_query": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "mpm_profile_reset": (C.c_int, [C.c_void_p]),

@@ -70,6 +70,9 @@ template <class T, int D> struct DevScene {
     int nb[D];    // particle blocks per axis (base cells 0..cells-2)
     int nnb[D];   // node blocks per axis (nodes 0..cells)
     int nb_total, nnb_total;
+    // slab decomposition: this context owns particles whose base cell along x lies in
+    // [slab_lo, slab_hi); the whole domain otherwise. Walls and Coulomb segments stay global.
+    int slab_lo, slab_hi;
 };
 
 // particle buffer: SoA pointers (one array per component)
@@ -110,7 +113,23 @@ struct DevStatus {
     long long step;       // absolute step index of the state currently in the buffers
     long long err_step;   // step during which a den/nan error occurred
     unsigned long long active_nodes;
+    int mig_lo, mig_hi; // particles that left the slab this step, toward -x / +x
+    int mig_over;       // export buffer overflow
+    int pad2;
 };
+
+__global__ inline void k_reset_status(DevStatus* st, long long step)
+{
+    DevStatus s{};
+    s.den_pid = 0x7fffffff;
+    s.ood_pid = 0x7fffffff;
+    s.step = step;
+    s.err_step = -1;
+    *st = s;
+}
+
+constexpr int KEY_OOD = 0x7fffffff;  // out of the domain (error)
+constexpr int KEY_DEAD = 0x7ffffffe; // slot vacated by a migrated particle (sorts last, ignored)
 
 // ---- small math ------------------------------------------------------------------------
 template <class T> __device__ __forceinline__ T dfloor(T x);

@@ -13,6 +13,7 @@
 #include "kernels_util.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -73,6 +74,18 @@ struct CtxBase {
     virtual void backprop(const mpm_state_view* s0, int64_t total, int nseg, const mpm_seeder_desc* sd,
                           mpm_cot_view* c0, mpm_param_grads* pg, mpm_backprop_result* res) = 0;
     virtual void grid_stats(int64_t* an, int64_t* ob, int64_t* anb) = 0;
+    virtual void upload_ids(const mpm_state_view* s, const int64_t* ids) = 0;
+    virtual void download_local(mpm_state_view* s, int64_t* ids) = 0;
+    virtual void slab_set(int lo, int hi, int64_t mig_cap) = 0;
+    virtual void step_p2g_local() = 0;
+    virtual void halo(int plane_lo, int n_planes, void* dev_buf, int mode) = 0;
+    virtual void step_finish_local(uint32_t flags) = 0;
+    virtual void migrate_export(void* lo, int* lo_pid, void* hi, int* hi_pid, int64_t cap, int64_t* n_lo, int64_t* n_hi) = 0;
+    virtual void migrate_import(const void* recs, const int* pids, int64_t k) = 0;
+    virtual int rec_size() const = 0;
+    virtual int64_t local_count() const = 0;
+    virtual void set_stream(void* s) = 0;
+    virtual void migrate_counts(int64_t* lo, int64_t* hi) const = 0;
 
     // profiling
     bool prof = false;
@@ -95,6 +108,7 @@ template <class T, int D> struct Ctx : CtxBase {
     DevScene<T, D> sc{};
     mpm_scene_desc desc{};
     cudaStream_t stream{};
+    cudaStream_t own_stream{}; // stream may be a caller's (mpm_ctx_set_stream)
     int device = 0;
     int64_t cap = 0, n = 0;
     int64_t step = 0;
@@ -123,6 +137,12 @@ template <class T, int D> struct Ctx : CtxBase {
     int nsm = 148;
     int p2g_ctas_per_sm = 1;
     AdjWork<T, D> aw{};
+    // slab decomposition (multi-GPU)
+    bool slab = false;
+    MigBuf<T> mig{};
+    int64_t n_dead = 0;  // vacated slots (pid < 0) left in storage by the last G2P
+    int* d_cells = nullptr;
+    int mig_cnt[2] = {0, 0};
 
     cudaGraphExec_t graphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}}; // [guard][cur]
 
@@ -143,7 +163,8 @@ template <class T, int D> struct Ctx : CtxBase {
         if (prop.major < 10)
             throw ApiError(MPM_ERR_CUDA, "libmpm_b200 requires an sm_100 (Blackwell) device; found " + std::string(prop.name));
         nsm = prop.multiProcessorCount;
-        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+        stream = own_stream;
         build_scene(d);
         cap = max_particles;
         has_aff = d->scheme == MPM_SCHEME_APIC;
@@ -166,6 +187,8 @@ template <class T, int D> struct Ctx : CtxBase {
         nflag = alloc<unsigned char>(sc.nnb_total);
         d_nb = alloc<int>(D);
         d_nnb = alloc<int>(D);
+        d_cells = alloc<int>(D);
+        CK(cudaMemcpyAsync(d_cells, sc.cells, sizeof(int) * D, cudaMemcpyHostToDevice, stream));
         CK(cudaMemcpyAsync(d_nb, sc.nb, sizeof(int) * D, cudaMemcpyHostToDevice, stream));
         CK(cudaMemcpyAsync(d_nnb, sc.nnb, sizeof(int) * D, cudaMemcpyHostToDevice, stream));
         partials = alloc<T>((size_t)sc.nb_total * C::NF * C::TN);
@@ -208,14 +231,16 @@ template <class T, int D> struct Ctx : CtxBase {
             cudaEventDestroy(e.b);
         }
         aw.free_all();
+        if (ids_scratch)
+            cudaFree(ids_scratch);
         for (void* p : allocs)
             cudaFree(p);
         if (st_host)
             cudaFreeHost(st_host);
         if (stage_host)
             cudaFreeHost(stage_host);
-        if (stream)
-            cudaStreamDestroy(stream);
+        if (own_stream)
+            cudaStreamDestroy(own_stream);
     }
 
     void build_scene(const mpm_scene_desc* d)
@@ -235,6 +260,8 @@ template <class T, int D> struct Ctx : CtxBase {
             sc.nb[a] = (d->cells[a] - 1 + C::B - 1) / C::B;
             sc.nnb[a] = (d->cells[a] + 1 + C::B - 1) / C::B;
         }
+        sc.slab_lo = 0;
+        sc.slab_hi = d->cells[0];
         sc.nb_total = 1;
         sc.nnb_total = 1;
         for (int a = 0; a < D; ++a) {
@@ -318,12 +345,8 @@ template <class T, int D> struct Ctx : CtxBase {
 
     void reset_status()
     {
-        DevStatus s{};
-        s.den_pid = 0x7fffffff;
-        s.ood_pid = 0x7fffffff;
-        s.step = step;
-        s.err_step = -1;
-        CK(cudaMemcpyAsync(st, &s, sizeof(s), cudaMemcpyHostToDevice, stream));
+        k_reset_status<<<1, 1, 0, stream>>>(st, (long long)step); // no pageable host copy per step
+        CK(cudaGetLastError());
     }
 
     // ---- kernel launch helpers ------------------------------------------------------------
@@ -378,7 +401,7 @@ template <class T, int D> struct Ctx : CtxBase {
         CK(cudaGetLastError());
     }
 
-    unsigned grid_for(int64_t k, int tpb) const { return unsigned((k + tpb - 1) / tpb); }
+    unsigned grid_for(int64_t k, int tpb) const { return k > 0 ? unsigned((k + tpb - 1) / tpb) : 1u; } // n may be 0 on a slab
     unsigned persistent(int per_sm) const { return unsigned(nsm * per_sm); }
 
     // ---- sort + segment tables ---------------------------------------------------------------
@@ -391,7 +414,8 @@ template <class T, int D> struct Ctx : CtxBase {
         // radix-sort only the bits a valid key can have (C4: 24 bits -> 3 onesweep passes). An
         // out-of-domain particle's sentinel key aliases in those bits, but such a step is aborted.
         int end_bit = 1;
-        while ((int64_t(1) << end_bit) < (int64_t(sc.nb_total) << C::LOGNB))
+        const int64_t need = (int64_t(sc.nb_total) << C::LOGNB) + (slab ? 2 : 0); // dead keys sort last
+        while ((int64_t(1) << end_bit) < need)
             ++end_bit;
         size_t bytes = cub_bytes;
         CK(cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys, keys_sorted, iota, perm, int(n), 0, end_bit, stream));
@@ -445,13 +469,13 @@ template <class T, int D> struct Ctx : CtxBase {
         const size_t sm = g2p_smem();
         const unsigned gr = persistent(D == 2 ? 8 : 4);
         if (has_aff && has_F)
-            launch("k_g2p", [&] { k_g2p<T, D, FL, true, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st); });
+            launch("k_g2p", [&] { k_g2p<T, D, FL, true, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
         else if (has_aff)
-            launch("k_g2p", [&] { k_g2p<T, D, FL, true, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st); });
+            launch("k_g2p", [&] { k_g2p<T, D, FL, true, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
         else if (has_F)
-            launch("k_g2p", [&] { k_g2p<T, D, FL, false, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st); });
+            launch("k_g2p", [&] { k_g2p<T, D, FL, false, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
         else
-            launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st); });
+            launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
         cur ^= 1;
         keys_valid = true;
     }
@@ -511,11 +535,13 @@ template <class T, int D> struct Ctx : CtxBase {
     }
 
     // ---- API ----------------------------------------------------------------------------------
-    void upload(const mpm_state_view* s) override
+    void upload(const mpm_state_view* s) override { upload_ids(s, nullptr); }
+
+    void upload_ids(const mpm_state_view* s, const int64_t* ids) override
     {
-        if (s->n < 1 || s->n > cap)
+        if (s->n < (ids ? 0 : 1) || s->n > cap)
             throw ApiError(MPM_ERR_USAGE, "state size " + std::to_string(s->n) + " outside [1, " + std::to_string(cap) + "]");
-        if (!s->x || !s->v || !s->mass || !s->volume || !s->rho || !s->sigma)
+        if (s->n > 0 && (!s->x || !s->v || !s->mass || !s->volume || !s->rho || !s->sigma))
             throw ApiError(MPM_ERR_USAGE, "state view missing required fields");
         if (has_aff && !s->affine)
             throw ApiError(MPM_ERR_USAGE, "APIC scheme needs the affine field");
@@ -541,10 +567,16 @@ template <class T, int D> struct Ctx : CtxBase {
             else if (f == S_F && has_F)
                 throw ApiError(MPM_ERR_USAGE, "track_def_grad needs the def_grad field");
         }
+        long long* d_ids = nullptr;
+        if (ids) {
+            d_ids = reinterpret_cast<long long*>(aw_ids_scratch(n));
+            CK(cudaMemcpyAsync(d_ids, ids, n * sizeof(long long), cudaMemcpyHostToDevice, stream));
+        }
         launch("k_upload", [&] {
             k_upload<T, D><<<grid_for(n, 256), 256, 0, stream>>>(stage, buf[cur], int(n), D == 2 && s->sigma_zz != nullptr,
-                                                                 has_aff, has_F);
+                                                                 has_aff, has_F, d_ids);
         });
+        n_dead = 0;
         step = s->step;
         time = s->time;
         keys_valid = false;
@@ -554,6 +586,8 @@ template <class T, int D> struct Ctx : CtxBase {
 
     void download(mpm_state_view* s) override
     {
+        if (slab)
+            throw ApiError(MPM_ERR_USAGE, "slab mode: use mpm_state_download_local");
         if (n == 0)
             throw ApiError(MPM_ERR_USAGE, "no state uploaded");
         launch("k_download", [&] { k_download<T, D><<<grid_for(n, 256), 256, 0, stream>>>(stage, buf[cur], int(n), has_aff, has_F); });
@@ -604,6 +638,8 @@ template <class T, int D> struct Ctx : CtxBase {
 
     void advance_enqueue(int64_t nsteps, uint32_t flags)
     {
+        if (slab)
+            throw ApiError(MPM_ERR_USAGE, "slab mode: step with mpm_step_p2g_local / mpm_halo / mpm_step_finish_local");
         if (n == 0)
             throw ApiError(MPM_ERR_USAGE, "no state uploaded");
         if (nsteps <= 0)
@@ -810,6 +846,164 @@ template <class T, int D> struct Ctx : CtxBase {
             *ob = cnt[0];
         if (anb)
             *anb = cnt[1];
+    }
+
+    // ---- slab decomposition (multi-GPU) --------------------------------------------
+    int64_t local_count() const override { return n - n_dead; }
+    void set_stream(void* s) override { stream = s ? static_cast<cudaStream_t>(s) : own_stream; }
+    void migrate_counts(int64_t* lo, int64_t* hi) const override
+    {
+        *lo = mig_cnt[0];
+        *hi = mig_cnt[1];
+    }
+    void* ids_scratch = nullptr;
+    size_t ids_scratch_bytes = 0;
+    void* aw_ids_scratch(int64_t k)
+    {
+        const size_t b = size_t(k) * sizeof(long long);
+        if (b > ids_scratch_bytes) {
+            if (ids_scratch)
+                cudaFree(ids_scratch);
+            CK(cudaMalloc(&ids_scratch, b));
+            ids_scratch_bytes = b;
+        }
+        return ids_scratch;
+    }
+    int rec_size() const override { return 2 * D + 5 + C::NS + D * D + (has_aff ? D * D : 0) + (has_F ? D * D : 0); }
+    void slab_set(int lo, int hi, int64_t mig_cap) override
+    {
+        if (lo < 0 || hi <= lo || lo % C::B || (hi % C::B && hi < sc.cells[0]))
+            throw ApiError(MPM_ERR_USAGE, "slab bounds must be block-aligned (multiples of " + std::to_string(C::B) + ")");
+        sc.slab_lo = lo;
+        sc.slab_hi = hi;
+        slab = true;
+        if (!mig.on || mig.cap < mig_cap) {
+            mig.on = 1;
+            mig.cap = int(mig_cap);
+            mig.rec = rec_size();
+            mig.lo = alloc<T>((size_t)mig_cap * mig.rec);
+            mig.hi = alloc<T>((size_t)mig_cap * mig.rec);
+            mig.lo_pid = alloc<int>(mig_cap);
+            mig.hi_pid = alloc<int>(mig_cap);
+        }
+        for (auto& g : graphs)
+            for (auto& e : g)
+                if (e) {
+                    cudaGraphExecDestroy(e);
+                    e = nullptr;
+                }
+        keys_valid = false;
+    }
+    void step_p2g_local() override
+    {
+        reset_status();
+        sort_and_segment();
+        p2g_kernel();
+        grid_kernel<G_SUM | G_NOGRAV | G_STORE>(); // an abort here is reported by step_finish_local
+    }
+    void halo(int plane_lo, int n_planes, void* dev_buf, int mode) override
+    {
+        int64_t per = n_planes;
+        for (int a = 1; a < D; ++a)
+            per *= sc.cells[a] + 1;
+        launch("k_halo", [&] {
+            k_halo<T, D><<<grid_for(per, 256), 256, 0, stream>>>(G, nflag, d_nnb, d_cells, plane_lo, n_planes,
+                                                                 static_cast<T*>(dev_buf), mode);
+        }); // stream-ordered: the caller's transport runs on the same stream (mpm_ctx_set_stream)
+    }
+    void step_finish_local(uint32_t flags) override
+    {
+        grid_kernel<G_GRAV | G_ZEROV | G_MOM | G_CORR | G_STORE>();
+        if (flags & MPM_ADV_NAN_GUARD)
+            g2p_kernel_fl<P_CONSTIT | P_GUARD>();
+        else
+            g2p_kernel_fl<P_CONSTIT>();
+        launch("k_step_end", [&] { k_step_end<<<1, 1, 0, stream>>>(st); });
+        fetch_status();
+        mig_cnt[0] = st_host->mig_lo;
+        mig_cnt[1] = st_host->mig_hi;
+        const int64_t before = n;
+        n = n - n_dead;          // the previous G2P's vacated slots sorted to the end and are gone
+        n_dead = mig_cnt[0] + mig_cnt[1];
+        (void)before;
+        if (st_host->mig_over)
+            throw ApiError(MPM_ERR_CUDA, "slab migration buffer overflow (raise mig_cap)");
+        check_status(step);
+    }
+    void migrate_export(void* lo, int* lo_pid, void* hi, int* hi_pid, int64_t cap, int64_t* n_lo, int64_t* n_hi) override
+    {
+        if (mig_cnt[0] > cap || mig_cnt[1] > cap)
+            throw ApiError(MPM_ERR_USAGE, "migration export: destination capacity too small");
+        const size_t rb = sizeof(T) * mig.rec;
+        if (mig_cnt[0] && lo) {
+            CK(cudaMemcpyAsync(lo, mig.lo, mig_cnt[0] * rb, cudaMemcpyDeviceToDevice, stream));
+            CK(cudaMemcpyAsync(lo_pid, mig.lo_pid, mig_cnt[0] * sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        }
+        if (mig_cnt[1] && hi) {
+            CK(cudaMemcpyAsync(hi, mig.hi, mig_cnt[1] * rb, cudaMemcpyDeviceToDevice, stream));
+            CK(cudaMemcpyAsync(hi_pid, mig.hi_pid, mig_cnt[1] * sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        }
+        *n_lo = mig_cnt[0];
+        *n_hi = mig_cnt[1];
+    }
+    void migrate_import(const void* recs, const int* pids, int64_t k) override
+    {
+        if (k <= 0)
+            return;
+        if (n + k > cap)
+            throw ApiError(MPM_ERR_USAGE, "migration import exceeds the context capacity");
+        // deterministic append order: by particle id
+        int* keys_in = static_cast<int*>(aw_ids_scratch(4 * k)); // 4k ints: pid copy, sorted, order
+        int* sorted = keys_in + k;
+        int* order = keys_in + 2 * k;
+        CK(cudaMemcpyAsync(keys_in, pids, k * sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        size_t bytes = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, sorted, iota, order, int(k), 0, 31, stream));
+        void* tmp = nullptr;
+        CK(cudaMallocAsync(&tmp, bytes, stream));
+        CK(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_in, sorted, iota, order, int(k), 0, 31, stream));
+        launch("k_mig_unpack", [&] {
+            k_mig_unpack<T, D><<<grid_for(k, 256), 256, 0, stream>>>(buf[cur], int(n), int(k), static_cast<const T*>(recs),
+                                                                     pids, order, mig.rec, has_aff, has_F);
+        });
+        CK(cudaFreeAsync(tmp, stream));
+        n += k;
+        keys_valid = false;
+    }
+    void download_local(mpm_state_view* s, int64_t* ids) override
+    {
+        // compact download of the alive slots in storage order, with their global ids
+        int* idx = static_cast<int*>(aw_ids_scratch(2 * n + 2)); // n slot indices + count (2n ints fit)
+        int* d_num = idx + n;
+        size_t bytes = 0;
+        CK(cub::DeviceSelect::If(nullptr, bytes, iota, idx, d_num, int(n), AliveSlot{buf[cur].pid}, stream));
+        void* tmp = nullptr;
+        CK(cudaMallocAsync(&tmp, bytes > 0 ? bytes : 1, stream));
+        CK(cub::DeviceSelect::If(tmp, bytes, iota, idx, d_num, int(n), AliveSlot{buf[cur].pid}, stream));
+        CK(cudaFreeAsync(tmp, stream));
+        int k = 0;
+        CK(cudaMemcpyAsync(&k, d_num, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (k > cap)
+            throw ApiError(MPM_ERR_CUDA, "download_local: count exceeds capacity");
+        long long* dids = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&dids), sizeof(long long) * (k > 0 ? k : 1), stream));
+        launch("k_download", [&] {
+            k_download_compact<T, D><<<grid_for(k, 256), 256, 0, stream>>>(stage, buf[cur], idx, k, has_aff, has_F, dids);
+        });
+        void* dst[S_NFIELDS] = {s->x, s->v, s->mass, s->volume, s->rho, s->eps_eq, D == 2 ? s->sigma_zz : nullptr,
+                                s->sigma, s->grad_v, has_aff ? s->affine : nullptr, has_F ? s->def_grad : nullptr};
+        for (int f = 0; f < S_NFIELDS; ++f)
+            if (dst[f] && k)
+                CK(cudaMemcpyAsync(dst[f], stage.f[f], (size_t)k * stage_comps<D>(f) * sizeof(T), cudaMemcpyDeviceToHost,
+                                   stream));
+        if (k)
+            CK(cudaMemcpyAsync(ids, dids, sizeof(long long) * k, cudaMemcpyDeviceToHost, stream));
+        CK(cudaFreeAsync(dids, stream));
+        CK(cudaStreamSynchronize(stream));
+        s->n = k;
+        s->step = step;
+        s->time = time;
     }
 
     // ---- small transfer helpers (used by the adjoint workspace) ---------------------------------
@@ -1163,6 +1357,28 @@ int mpm_backprop(mpm_ctx* c, const mpm_state_view* s0, int64_t total, int nseg, 
                  mpm_cot_view* c0, mpm_param_grads* pg, mpm_backprop_result* res)
 {
     MPM_CALL(c, c->impl->backprop(s0, total, nseg, sd, c0, pg, res));
+}
+
+int mpm_state_upload_ids(mpm_ctx* c, const mpm_state_view* s, const int64_t* ids) { MPM_CALL(c, c->impl->upload_ids(s, ids)); }
+int mpm_state_download_local(mpm_ctx* c, mpm_state_view* s, int64_t* ids) { MPM_CALL(c, c->impl->download_local(s, ids)); }
+int mpm_slab_set(mpm_ctx* c, int cell_lo, int cell_hi, int64_t mig_cap) { MPM_CALL(c, c->impl->slab_set(cell_lo, cell_hi, mig_cap)); }
+int mpm_step_p2g_local(mpm_ctx* c) { MPM_CALL(c, c->impl->step_p2g_local()); }
+int mpm_halo(mpm_ctx* c, int plane_lo, int n_planes, void* dev_buf, int mode) { MPM_CALL(c, c->impl->halo(plane_lo, n_planes, dev_buf, mode)); }
+int mpm_step_finish_local(mpm_ctx* c, uint32_t flags) { MPM_CALL(c, c->impl->step_finish_local(flags)); }
+int mpm_migrate_export(mpm_ctx* c, void* lo, int* lo_pid, void* hi, int* hi_pid, int64_t cap, int64_t* n_lo, int64_t* n_hi)
+{
+    MPM_CALL(c, c->impl->migrate_export(lo, lo_pid, hi, hi_pid, cap, n_lo, n_hi));
+}
+int mpm_migrate_import(mpm_ctx* c, const void* recs, const int* pids, int64_t k) { MPM_CALL(c, c->impl->migrate_import(recs, pids, k)); }
+int mpm_particle_record_size(const mpm_ctx* c) { return c ? c->impl->rec_size() : -1; }
+int64_t mpm_local_count(const mpm_ctx* c) { return c ? c->impl->local_count() : -1; }
+int mpm_ctx_set_stream(mpm_ctx* c, void* stream) { MPM_CALL(c, c->impl->set_stream(stream)); }
+int mpm_migrate_counts(const mpm_ctx* c, int64_t* n_lo, int64_t* n_hi)
+{
+    if (!c || !n_lo || !n_hi)
+        return MPM_ERR_USAGE;
+    c->impl->migrate_counts(n_lo, n_hi);
+    return MPM_OK;
 }
 
 int mpm_profile_enable(mpm_ctx* c, int enable) { MPM_CALL(c, c->impl->prof = enable != 0); }

@@ -26,13 +26,17 @@ __global__ void k_keys(DevScene<T, D> sc, PBuf<T, D> P, int n, int* keys, DevSta
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n)
         return;
+    if (P.pid[i] < 0) { // vacated slot (migrated away)
+        keys[i] = KEY_DEAD;
+        return;
+    }
     T x[D];
 #pragma unroll
     for (int a = 0; a < D; ++a)
         x[a] = P.x[a][i];
     int key;
     if (!cell_key<T, D>(sc, x, key)) {
-        key = 0x7fffffff;
+        key = KEY_OOD;
         atomicMin(&st->ood_pid, P.pid[i]);
         st->ood_flag = 1;
         st->abort = 1;
@@ -1157,7 +1161,9 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
 
 // ---------------------------------------------------------------------------------------
 // grid update: combine partial tiles, momentum update, boundary/contact corrections.
-enum GridMode { G_SUM = 1, G_MOM = 2, G_CORR = 4, G_STORE = 8 };
+// G_NOGRAV: sum without the g m_i term (slab halo sums first); G_GRAV: add g m_i to a stored
+// grid; G_ZEROV: massless nodes of a stored grid get v = v_old = 0 (as after a fresh sum)
+enum GridMode { G_SUM = 1, G_MOM = 2, G_CORR = 4, G_STORE = 8, G_NOGRAV = 16, G_GRAV = 32, G_ZEROV = 64 };
 
 // collect_node_corrections + apply_node_correction (contact.hpp:141-224), fixed order
 template <class T, int D>
@@ -1337,9 +1343,11 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
                 }
             }
             // sum_p phi m g = g m_i (transfer.hpp:427, gravity term factored out of the scatter)
+            if (!(MODE & G_NOGRAV)) {
 #pragma unroll
-            for (int a = 0; a < D; ++a)
-                f[a] += sc.gravity[a] * m;
+                for (int a = 0; a < D; ++a)
+                    f[a] += sc.gravity[a] * m;
+            }
         } else {
             m = G.m[gi];
 #pragma unroll
@@ -1348,6 +1356,11 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
                 f[a] = G.f[a][gi];
                 v[a] = G.v[a][gi];
                 vold[a] = G.vold[a][gi];
+            }
+            if (MODE & G_GRAV) {
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    f[a] += sc.gravity[a] * m;
             }
         }
         if (MODE & G_MOM) {
@@ -1359,7 +1372,7 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
                     v[a] = vold[a] + s * f[a];
                 }
                 nact_nodes += inside;
-            } else if (MODE & G_SUM) {
+            } else if (MODE & (G_SUM | G_ZEROV)) {
 #pragma unroll
                 for (int a = 0; a < D; ++a)
                     v[a] = vold[a] = T(0);
@@ -1400,12 +1413,21 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
 // G2P (+ constitutive): CTA per occupied particle block, node tile (v, v_old) in smem.
 enum G2PFlags { P_CONSTIT = 1, P_GUARD = 2 };
 
+// migration export buffers (slab mode): one record of `rec` scalars + the pid per mover
+template <class T> struct MigBuf {
+    int on, cap, rec;
+    T* lo;
+    T* hi;
+    int* lo_pid;
+    int* hi_pid;
+};
+
 template <class T, int D, int FLAGS, bool APIC, bool TRACKF>
 __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pin, PBuf<T, D> Pout,
                                              GBuf<T, D> G, const int* __restrict__ perm,
                                              const int* __restrict__ bstart, const int* __restrict__ bend,
                                              const int* __restrict__ occ, const int* __restrict__ n_occ,
-                                             int* __restrict__ keys_out, DevStatus* st)
+                                             int* __restrict__ keys_out, DevStatus* st, MigBuf<T> MG)
 {
     using C = Cfg<D>;
     constexpr int TE = C::TE, TN = C::TN;
@@ -1660,10 +1682,53 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
             }
             int key;
             if (!cell_key<T, D>(sc, xn, key)) {
-                key = 0x7fffffff;
+                key = KEY_OOD;
                 atomicMin(&st->ood_pid, pid);
                 st->ood_flag = 2;
                 st->abort = 1;
+            } else if (MG.on) {
+                const int bx = int(dfloor<T>((xn[0] - sc.origin[0]) * sc.inv_dh - T(0.5)));
+                if (bx < sc.slab_lo || bx >= sc.slab_hi) { // leaves the slab: export, vacate the slot
+                    const int side = bx < sc.slab_lo ? 0 : 1;
+                    const int k = atomicAdd(side ? &st->mig_hi : &st->mig_lo, 1);
+                    if (k < MG.cap) {
+                        T* rec = (side ? MG.hi : MG.lo) + (size_t)k * MG.rec;
+                        int q = 0;
+#pragma unroll
+                        for (int a = 0; a < D; ++a)
+                            rec[q++] = xn[a];
+#pragma unroll
+                        for (int a = 0; a < D; ++a)
+                            rec[q++] = vn[a];
+                        rec[q++] = m;
+                        rec[q++] = V;
+                        rec[q++] = rho;
+                        rec[q++] = eps;
+                        rec[q++] = szz;
+#pragma unroll
+                        for (int s2 = 0; s2 < C::NS; ++s2)
+                            rec[q++] = sig[s2];
+#pragma unroll
+                        for (int k2 = 0; k2 < D * D; ++k2)
+                            rec[q++] = L[k2];
+                        if constexpr (APIC) {
+#pragma unroll
+                            for (int k2 = 0; k2 < D * D; ++k2)
+                                rec[q++] = Bm[k2];
+                        }
+                        if constexpr (TRACKF) {
+#pragma unroll
+                            for (int k2 = 0; k2 < D * D; ++k2)
+                                rec[q++] = Fm[k2];
+                        }
+                        (side ? MG.hi_pid : MG.lo_pid)[k] = pid;
+                    } else {
+                        st->mig_over = 1;
+                        st->abort = 1;
+                    }
+                    Pout.pid[i] = -1;
+                    key = KEY_DEAD;
+                }
             }
             keys_out[i] = key;
         }

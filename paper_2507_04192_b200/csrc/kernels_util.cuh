@@ -22,7 +22,8 @@ template <class T, int D> struct Stage {
 };
 
 template <class T, int D>
-__global__ void k_upload(Stage<T, D> S, PBuf<T, D> P, int n, int has_szz, int has_aff, int has_F)
+__global__ void k_upload(Stage<T, D> S, PBuf<T, D> P, int n, int has_szz, int has_aff, int has_F,
+                         const long long* __restrict__ ids)
 {
     using C = Cfg<D>;
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -55,8 +56,96 @@ __global__ void k_upload(Stage<T, D> S, PBuf<T, D> P, int n, int has_szz, int ha
             if (has_F)
                 P.F[r * D + c][i] = S.f[S_F][i * D * D + c * D + r];
         }
-    P.pid[i] = i;
+    P.pid[i] = ids ? int(ids[i]) : i;
     (void)C::NS;
+}
+
+// append migrated particles (records sorted by pid beforehand) at storage [base, base + n)
+template <class T, int D>
+__global__ void k_mig_unpack(PBuf<T, D> P, int base, int n, const T* __restrict__ recs, const int* __restrict__ pids,
+                             const int* __restrict__ order, int rec, int has_aff, int has_F)
+{
+    using C = Cfg<D>;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n)
+        return;
+    const int r = order[j];
+    const T* in = recs + (size_t)r * rec;
+    const int i = base + j;
+    int q = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        P.x[a][i] = in[q++];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        P.v[a][i] = in[q++];
+    P.m[i] = in[q++];
+    P.V[i] = in[q++];
+    P.rho[i] = in[q++];
+    P.eps[i] = in[q++];
+    const T szz = in[q++];
+    if (D == 2)
+        P.szz[i] = szz;
+#pragma unroll
+    for (int s = 0; s < C::NS; ++s)
+        P.sig[s][i] = in[q++];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k)
+        P.gv[k][i] = in[q++];
+    if (has_aff)
+        for (int k = 0; k < D * D; ++k)
+            P.aff[k][i] = in[q++];
+    if (has_F)
+        for (int k = 0; k < D * D; ++k)
+            P.F[k][i] = in[q++];
+    P.pid[i] = pids[r];
+}
+
+// halo planes of the stored grid: node x-planes [p0, p0 + np) x all (y[, z]) nodes, NF fields
+// (m, p, f); export writes zeros for inactive node blocks; import adds into active blocks only,
+// in a fixed order (received + own, or own + received) so both owners of a band agree bitwise.
+template <class T, int D>
+__global__ void k_halo(GBuf<T, D> G, const unsigned char* __restrict__ nflag, const int* __restrict__ nnb,
+                       const int* __restrict__ cells, int p0, int np, T* __restrict__ buf, int mode)
+{
+    using C = Cfg<D>;
+    constexpr int NF = 1 + 2 * D;
+    long long per = 1;
+    for (int a = 1; a < D; ++a)
+        per *= cells[a] + 1;
+    const long long total = per * np;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= total)
+        return;
+    int n[D];
+    n[0] = p0 + int(t / per);
+    long long rem = t % per;
+    for (int a = D - 1; a >= 1; --a) {
+        n[a] = int(rem % (cells[a] + 1));
+        rem /= cells[a] + 1;
+    }
+    int q = 0, loc = 0;
+    bool ok = n[0] >= 0 && n[0] <= cells[0];
+    for (int a = 0; a < D; ++a) {
+        q = q * nnb[a] + (n[a] >> C::LOGB);
+        loc = (loc << C::LOGB) | (n[a] & (C::B - 1));
+    }
+    ok = ok && nflag[q];
+    const size_t gi = (size_t)q * C::NB + loc;
+    T* b = buf + (size_t)t * NF;
+    T* fld[NF];
+    fld[0] = G.m;
+    for (int a = 0; a < D; ++a) {
+        fld[1 + a] = G.p[a];
+        fld[1 + D + a] = G.f[a];
+    }
+    if (mode == 0) {
+        for (int f = 0; f < NF; ++f)
+            b[f] = ok ? fld[f][gi] : T(0);
+    } else if (ok) {
+        for (int f = 0; f < NF; ++f)
+            fld[f][gi] = mode == 1 ? b[f] + fld[f][gi] : fld[f][gi] + b[f];
+    }
 }
 
 template <class T, int D>
@@ -66,6 +155,8 @@ __global__ void k_download(Stage<T, D> S, PBuf<T, D> P, int n, int has_aff, int 
     if (i >= n)
         return;
     const int p = P.pid[i];
+    if (p < 0)
+        return; // vacated slot
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         S.f[S_X][p * D + a] = P.x[a][i];
@@ -89,6 +180,45 @@ __global__ void k_download(Stage<T, D> S, PBuf<T, D> P, int n, int has_aff, int 
                 S.f[S_F][p * D * D + c * D + r] = P.F[r * D + c][i];
         }
 }
+
+// compact download for a slab: slot list idx[0..k) (storage order), ids alongside
+template <class T, int D>
+__global__ void k_download_compact(Stage<T, D> S, PBuf<T, D> P, const int* __restrict__ idx, int k, int has_aff,
+                                   int has_F, long long* __restrict__ ids)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k)
+        return;
+    const int i = idx[j];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        S.f[S_X][j * D + a] = P.x[a][i];
+        S.f[S_V][j * D + a] = P.v[a][i];
+    }
+    S.f[S_M][j] = P.m[i];
+    S.f[S_VOL][j] = P.V[i];
+    S.f[S_RHO][j] = P.rho[i];
+    S.f[S_EPS][j] = P.eps[i];
+    if (D == 2)
+        S.f[S_SZZ][j] = P.szz[i];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            S.f[S_SIG][j * D * D + c * D + r] = P.sig[sym_idx<D>(r, c)][i];
+            S.f[S_GV][j * D * D + c * D + r] = P.gv[r * D + c][i];
+            if (has_aff)
+                S.f[S_AFF][j * D * D + c * D + r] = P.aff[r * D + c][i];
+            if (has_F)
+                S.f[S_F][j * D * D + c * D + r] = P.F[r * D + c][i];
+        }
+    ids[j] = P.pid[i];
+}
+
+struct AliveSlot {
+    const int* pid;
+    __device__ __forceinline__ bool operator()(int i) const { return pid[i] >= 0; }
+};
 
 // unordered compaction of a dense predicate (list order does not affect results: every
 // listed block is processed independently)
@@ -145,7 +275,7 @@ __global__ void k_digest(PBuf<T, D> P, int n, int has_aff, unsigned long long* o
     using C = Cfg<D>;
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long h = 0;
-    if (i < n) {
+    if (i < n && P.pid[i] >= 0) {
         h = mix64((unsigned long long)P.pid[i]);
 #pragma unroll
         for (int a = 0; a < D; ++a) {
@@ -179,7 +309,7 @@ __global__ void k_max_speed(PBuf<T, D> P, int n, unsigned long long* out)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     double s = 0;
-    if (i < n) {
+    if (i < n && P.pid[i] >= 0) {
         T q = T(0);
 #pragma unroll
         for (int a = 0; a < D; ++a)

@@ -1,0 +1,454 @@
+"""Slab decomposition of the MPM step across GPUs.
+
+The reference is single-process (stepper.hpp:462-483 has no decomposition). This module shards
+the same step along x across one process per GPU. Every rank owns the particles whose base cell
+along x lies in its slab `[lo, hi)`. Slab bounds are multiples of the particle-block edge: 16
+cells in 2-D, 8 in 3-D. One step runs in four phases:
+
+  1. P2G. Each rank calls `mpm_step_p2g_local`: it scatters its own particles into its grid,
+     without the `g m_i` term.
+  2. Halo sum. Neighbouring slabs share the 2 node planes `[hi, hi + 2)` that both scatter into.
+     Each rank exports its partial (m, p, f) on those planes and adds the neighbour's. The sum
+     runs in a fixed order, lower rank's partial first, so both owners hold bit-identical nodes.
+  3. Finish. Each rank calls `mpm_step_finish_local`: add `g m_i`, momentum update, boundary
+     corrections, then G2P and the constitutive update on its own particles.
+  4. Migration. A particle whose new base cell left the slab is exported from G2P and vacated
+     from its slot. It is then appended by the receiving neighbour, in particle-id order.
+
+There is no all-reduce on the data path. Each step does one small MAX all-reduce of an error
+flag, so that a NaN/OOD abort on one rank stops every rank at the same step (stepper.hpp:519-522).
+
+Transports:
+  * TorchTransport runs torch.distributed point-to-point (NCCL over NVLink on device tensors;
+    gloo on CPU tensors for the CPU tests). It carries one rank per process.
+  * LocalTransport hands tensors between domains that live in the same process. It serves the
+    single-GPU tests: R contexts on one device, stepped in lock-step, never waiting on each other.
+
+Domains implement the per-rank protocol of `SlabDomain`. The product domain is GpuSlabDomain,
+which calls the C ABI. tests/slab_oracle.py holds an oracle-backed domain used by the CPU tests.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import MPMError, NumericalError
+from .scene import Scene
+from .state import ParticleSoA, SimState
+
+
+def block_edge(dim: int) -> int:
+    """particle/node block edge in cells (csrc/common.cuh Cfg<D>::B)"""
+    return 16 if dim == 2 else 8
+
+
+def base_cell_x(scene: Scene, x: np.ndarray) -> np.ndarray:
+    """base node index along x of the quadratic stencil (bspline.hpp:315-327): floor(u - 1/2)"""
+    c = scene.config
+    u = (x[:, 0] - c.origin[0]) / c.dh
+    return np.floor(u - 0.5).astype(np.int64)
+
+
+@dataclass
+class SlabPlan:
+    """Cell bounds along x for each rank. There are R+1 bounds, all multiples of `block`, with
+    bounds[0] = 0 and bounds[R] = cells_x."""
+
+    bounds: list
+    block: int
+    halo_planes: int = 2
+
+    @property
+    def n_ranks(self) -> int:
+        return len(self.bounds) - 1
+
+    def lo(self, r: int) -> int:
+        return self.bounds[r]
+
+    def hi(self, r: int) -> int:
+        return self.bounds[r + 1]
+
+    @staticmethod
+    def make(scene: Scene, n_ranks: int, x: np.ndarray | None = None) -> "SlabPlan":
+        """Split the x-blocks into n_ranks contiguous slabs. With particle positions `x`, balance
+        the particle counts; otherwise split the blocks evenly. Every slab is at least one block
+        wide and at least 3 cells wide, so that a particle's stencil never spans three slabs."""
+        B = block_edge(scene.dim)
+        cx = scene.config.cells[0]
+        nbx = -(-cx // B)
+        if n_ranks < 1 or n_ranks > nbx:
+            raise ValueError(f"cannot split {nbx} x-blocks into {n_ranks} slabs")
+        if x is None or len(x) == 0:
+            cuts = [round(k * nbx / n_ranks) for k in range(n_ranks + 1)]
+        else:
+            bx = np.clip(base_cell_x(scene, x) // B, 0, nbx - 1)
+            cum = np.concatenate([[0], np.cumsum(np.bincount(bx, minlength=nbx))])
+            total = cum[-1]
+            cuts = [0]
+            for k in range(1, n_ranks):
+                # block boundary whose cumulative count is closest to k/R of the total; keep at
+                # least one block for each remaining rank
+                lo_c, hi_c = cuts[-1] + 1, nbx - (n_ranks - k)
+                c = lo_c + int(np.argmin(np.abs(cum[lo_c:hi_c + 1] - total * k / n_ranks)))
+                cuts.append(c)
+            cuts.append(nbx)
+        bounds = [min(c * B, cx) for c in cuts]
+        bounds[-1] = cx
+        return SlabPlan(bounds, B)
+
+    def owner(self, base_x: np.ndarray) -> np.ndarray:
+        """rank owning each base cell; out-of-range bases clamp to the edge slabs"""
+        return np.clip(np.searchsorted(np.asarray(self.bounds[1:-1]), base_x, side="right"), 0, self.n_ranks - 1)
+
+    def partition(self, scene: Scene, state: SimState) -> list:
+        """global particle ids of each rank, ascending"""
+        own = self.owner(base_cell_x(scene, state.particles.x))
+        return [np.nonzero(own == r)[0].astype(np.int64) for r in range(self.n_ranks)]
+
+    def nodes_per_plane(self, scene: Scene) -> int:
+        c = scene.config.cells
+        return int(np.prod([c[a] + 1 for a in range(1, scene.dim)]))
+
+
+# ---------------------------------------------------------------------------------------------
+class SlabDomain:
+    """Per-rank protocol driven by SlabStepper.
+
+    Buffers are torch tensors: device tensors for the GPU domain, CPU tensors for the oracle
+    domain. halo_export must return a tensor that stays valid until the next call.
+    """
+
+    rank: int
+    plan: SlabPlan
+
+    def p2g(self) -> None: ...
+    def halo_export(self, plane_lo: int, n_planes: int, side: int): ...
+    def halo_import(self, plane_lo: int, n_planes: int, buf, mode: int) -> None: ...
+    def finish(self, nan_guard: bool): ...   # -> (n_lo, n_hi) particles leaving toward -x / +x
+    def migrate_export(self): ...            # -> (lo_recs, lo_pids, hi_recs, hi_pids)
+    def migrate_import(self, recs, pids) -> None: ...
+    def local_count(self) -> int: ...
+    def gather(self): ...                    # -> (ParticleSoA subset, ids int64)
+    def empty_records(self, k: int): ...     # -> (recs, pids) receive buffers
+    def empty_halo(self, n_planes: int): ...
+
+
+class PeerFailure(NumericalError):
+    """Another rank aborted this step."""
+
+
+class LocalTransport:
+    """In-process neighbour exchange. Every domain lives in this process and is stepped in
+    lock-step, so no rank ever waits on another rank's kernels."""
+
+    def exchange(self, sends: dict, domains: dict, kind: str, report: dict | None = None) -> dict:
+        """sends[r] = (to_lo, to_hi) -> recv[r] = (from_lo, from_hi)"""
+        out = {}
+        for r in domains:
+            from_lo = sends[r - 1][1] if r - 1 in sends else None
+            from_hi = sends[r + 1][0] if r + 1 in sends else None
+            out[r] = (from_lo, from_hi)
+        return out
+
+    def report(self, local: dict, n_ranks: int) -> dict:
+        """local[r] = (failed, n_lo, n_hi) -> the same for every rank"""
+        return dict(local)
+
+
+class TorchTransport:
+    """torch.distributed point-to-point between x-neighbours (one rank per process)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def exchange(self, sends: dict, domains: dict, kind: str, report: dict | None = None) -> dict:
+        """One rank per process: sends[r] = (to_lo, to_hi); migration sizes come from `report`."""
+        dist = self.dist
+        r = self.rank
+        d = domains[r]
+        to_lo, to_hi = sends[r]
+        lo_peer = r - 1 if r > 0 else None
+        hi_peer = r + 1 if r + 1 < self.size else None
+        ops, recv = [], {}
+        for peer, out in ((lo_peer, to_lo), (hi_peer, to_hi)):
+            if peer is None:
+                continue
+            if kind == "halo":
+                inc = d.empty_halo(2)
+                ops += [dist.P2POp(dist.isend, out, peer, self.group), dist.P2POp(dist.irecv, inc, peer, self.group)]
+                recv[peer] = inc
+                continue
+            if out is not None and out[1].numel():
+                ops += [dist.P2POp(dist.isend, out[0], peer, self.group), dist.P2POp(dist.isend, out[1], peer, self.group)]
+            # what the peer sends us: its count toward this rank
+            k = report[peer][2] if peer == lo_peer else report[peer][1]
+            if k:
+                recs, pids = d.empty_records(k)
+                recv[peer] = (recs, pids)
+                ops += [dist.P2POp(dist.irecv, recs, peer, self.group), dist.P2POp(dist.irecv, pids, peer, self.group)]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()  # NCCL: orders the current stream (the library's); gloo: blocks the host
+        return {r: (recv.get(lo_peer), recv.get(hi_peer))}
+
+    def report(self, local: dict, n_ranks: int) -> dict:
+        import torch
+
+        (r, (failed, n_lo, n_hi)), = local.items()
+        mine = torch.tensor([int(failed), int(n_lo), int(n_hi)], dtype=torch.int64, device=self._dev)
+        allr = torch.empty(self.size * 3, dtype=torch.int64, device=self._dev)
+        self.dist.all_gather_into_tensor(allr, mine, group=self.group)
+        rows = allr.view(self.size, 3).cpu().tolist()  # the one host synchronisation of the exchange
+        return {q: (bool(rows[q][0]), rows[q][1], rows[q][2]) for q in range(self.size)}
+
+    _dev = "cpu"
+
+
+class SlabStepper:
+    """Drives one step of the decomposition over the domains this process owns.
+
+    Mirrors Stepper::advance (stepper.hpp:462-483). Every rank advances by one step, and an
+    error on any rank raises on all of them at the same step.
+    """
+
+    def __init__(self, domains: list, transport):
+        self.domains = {d.rank: d for d in domains}
+        self.transport = transport
+        if isinstance(transport, TorchTransport):
+            import torch
+
+            d0 = next(iter(self.domains.values()))
+            transport._dev = d0.device
+            # NCCL: the first operation on the group involves every rank before any P2P batch
+            t = torch.zeros(1, device=transport._dev)
+            transport.dist.all_reduce(t, group=transport.group)
+            if getattr(d0, "stream", None) is not None:
+                d0.stream.wait_stream(torch.cuda.current_stream(d0.device))
+        self.migrated = 0
+        self.steps_done = 0  # steps every rank completed (an aborted step is not counted)
+
+    def step(self, nan_guard: bool = False):
+        stream = getattr(next(iter(self.domains.values())), "stream", None)
+        if stream is not None:
+            import torch
+
+            with torch.cuda.stream(stream):
+                return self._step(nan_guard)
+        return self._step(nan_guard)
+
+    def _step(self, nan_guard: bool):
+        doms = self.domains
+        n_ranks = next(iter(doms.values())).plan.n_ranks
+        errs: dict = {}
+        counts: dict = {}
+        for r, d in doms.items():
+            try:
+                d.p2g()
+            except MPMError as e:
+                errs[r] = e
+        # halo: the 2 node planes shared with each neighbour
+        sends = {}
+        for r, d in doms.items():
+            p = d.plan
+            to_lo = d.halo_export(p.lo(r), 2, 0) if r > 0 else None
+            to_hi = d.halo_export(p.hi(r), 2, 1) if r + 1 < n_ranks else None
+            sends[r] = (to_lo, to_hi)
+        recv = self.transport.exchange(sends, doms, "halo")
+        for r, d in doms.items():
+            from_lo, from_hi = recv[r]
+            p = d.plan
+            if from_lo is not None:
+                d.halo_import(p.lo(r), 2, from_lo, 1)  # lower rank's partial first
+            if from_hi is not None:
+                d.halo_import(p.hi(r), 2, from_hi, 2)  # own partial first
+            if r in errs:
+                counts[r] = (0, 0)
+                continue
+            try:
+                counts[r] = d.finish(nan_guard)
+            except MPMError as e:
+                errs[r] = e
+                counts[r] = (0, 0)
+        # one gather of (failed, n_lo, n_hi) from every rank
+        rep = self.transport.report({r: (r in errs, *counts[r]) for r in doms}, n_ranks)
+        if any(v[0] for v in rep.values()):
+            for r in doms:
+                if r in errs:
+                    raise errs[r]
+            raise PeerFailure("step aborted on another rank")
+        if rep.get(0, (0, 0, 0))[1] or rep.get(n_ranks - 1, (0, 0, 0))[2]:
+            raise NumericalError("a particle left the outermost slab")  # OOD catches this first
+        # migration of particles that left their slab
+        sends = {}
+        for r, d in doms.items():
+            lo_r, lo_p, hi_r, hi_p = d.migrate_export()
+            sends[r] = ((lo_r, lo_p) if r > 0 else None, (hi_r, hi_p) if r + 1 < n_ranks else None)
+        recv = self.transport.exchange(sends, doms, "mig", rep)
+        for r, d in doms.items():
+            parts = [x for x in recv[r] if x is not None and x[1].numel()]
+            if parts:
+                import torch
+
+                recs = parts[0][0] if len(parts) == 1 else torch.cat([x[0] for x in parts])
+                pids = parts[0][1] if len(parts) == 1 else torch.cat([x[1] for x in parts])
+                d.migrate_import(recs, pids)
+                self.migrated += int(pids.shape[0])
+        self.steps_done += 1
+
+    def advance(self, n: int, nan_guard: bool = False):
+        for _ in range(int(n)):
+            self.step(nan_guard)
+
+    def gather_local(self, template: SimState) -> SimState:
+        """Assemble the global state from domains in this process (every rank local)"""
+        out = template.copy()
+        step = None
+        for d in self.domains.values():
+            sub, ids, st = d.gather()
+            out.particles.put(ids, sub)
+            step = st
+        if step is not None:
+            out.step, out.time = step
+        return out
+
+
+# ---------------------------------------------------------------------------------------------
+class GpuSlabDomain(SlabDomain):
+    """One rank's slab on one GPU, through the C ABI (include/mpm_capi.h, slab section)."""
+
+    def __init__(self, scene: Scene, plan: SlabPlan, rank: int, state: SimState, ids: np.ndarray | None = None,
+                 device: int = 0, capacity: int | None = None, mig_cap: int | None = None, local: bool = False):
+        """state: the global state (this rank takes rows `ids`, default its slab's particles), or
+        with local=True this rank's particles already, `ids` their global ids."""
+        import torch
+
+        from . import capi
+        from .solver import Context
+
+        self.scene, self.plan, self.rank = scene, plan, rank
+        self.device = torch.device("cuda", device)
+        if local:
+            sub = state
+            n_total = state.particles.size() * plan.n_ranks
+        else:
+            if ids is None:
+                ids = plan.partition(scene, state)[rank]
+            sub = SimState(state.particles.take(ids), state.step, state.time)
+            n_total = state.particles.size()
+        # room for particles arriving from the neighbours (a quarter of an average slab by default)
+        self.capacity = int(capacity or max(1024, int(1.25 * len(ids)) + n_total // (4 * plan.n_ranks) + 1024))
+        self.mig_cap = int(mig_cap or max(1024, self.capacity // 8))
+        self.ctx = Context(scene, self.capacity, device)
+        self.lib, self.h = self.ctx.lib, self.ctx.h
+        # the library, the halo/migration buffers and the transport share one stream per device
+        self.stream = _slab_stream(device)
+        self.ctx.check(self.lib.mpm_ctx_set_stream(self.h, C.c_void_p(self.stream.cuda_stream)))
+        self.ctx.check(self.lib.mpm_slab_set(self.h, plan.lo(rank), plan.hi(rank), self.mig_cap))
+        v, keep = sub.to_view()
+        ids64 = np.ascontiguousarray(ids, dtype=np.int64)
+        self.ctx.check(self.lib.mpm_state_upload_ids(self.h, C.byref(v), ids64.ctypes.data_as(C.c_void_p)))
+        self.rec = int(self.lib.mpm_particle_record_size(self.h))
+        self.tdtype = torch.float64 if scene.np_dtype == np.float64 else torch.float32
+        self.nf = 1 + 2 * scene.dim
+        self.per = plan.nodes_per_plane(scene)
+        with torch.cuda.stream(self.stream):
+            self._halo = [self.empty_halo(2), self.empty_halo(2)]
+            self._mig = [(torch.empty((self.mig_cap, self.rec), dtype=self.tdtype, device=self.device),
+                          torch.empty(self.mig_cap, dtype=torch.int32, device=self.device)) for _ in range(2)]
+        self._counts = (0, 0)
+        self._template = sub
+        self._flags = capi
+
+    def empty_halo(self, n_planes: int):
+        import torch
+
+        return torch.empty((n_planes * self.per, self.nf), dtype=self.tdtype, device=self.device)
+
+    def empty_records(self, k: int):
+        import torch
+
+        return (torch.empty((k, self.rec), dtype=self.tdtype, device=self.device),
+                torch.empty(k, dtype=torch.int32, device=self.device))
+
+    def p2g(self):
+        self.ctx.check(self.lib.mpm_step_p2g_local(self.h))
+
+    def halo_export(self, plane_lo, n_planes, side):
+        buf = self._halo[side]
+        self.ctx.check(self.lib.mpm_halo(self.h, int(plane_lo), int(n_planes), C.c_void_p(buf.data_ptr()), 0))
+        return buf
+
+    def halo_import(self, plane_lo, n_planes, buf, mode):
+        buf = buf.contiguous()
+        self.ctx.check(self.lib.mpm_halo(self.h, int(plane_lo), int(n_planes), C.c_void_p(buf.data_ptr()), int(mode)))
+
+    def finish(self, nan_guard):
+        self.ctx.check(self.lib.mpm_step_finish_local(self.h, self._flags.MPM_ADV_NAN_GUARD if nan_guard else 0))
+        nlo, nhi = C.c_int64(), C.c_int64()
+        self.ctx.check(self.lib.mpm_migrate_counts(self.h, C.byref(nlo), C.byref(nhi)))
+        self._counts = (nlo.value, nhi.value)
+        return self._counts
+
+    def migrate_export(self):
+        (lr, lp), (hr, hp) = self._mig
+        nlo, nhi = C.c_int64(), C.c_int64()
+        self.ctx.check(self.lib.mpm_migrate_export(self.h, C.c_void_p(lr.data_ptr()), C.c_void_p(lp.data_ptr()),
+                                                   C.c_void_p(hr.data_ptr()), C.c_void_p(hp.data_ptr()),
+                                                   self.mig_cap, C.byref(nlo), C.byref(nhi)))
+        return lr[: nlo.value], lp[: nlo.value], hr[: nhi.value], hp[: nhi.value]  # stream-ordered copies
+
+    def migrate_import(self, recs, pids):
+        recs, pids = recs.contiguous(), pids.contiguous()
+        self.ctx.check(self.lib.mpm_migrate_import(self.h, C.c_void_p(recs.data_ptr()), C.c_void_p(pids.data_ptr()),
+                                                   int(pids.numel())))
+
+    def local_count(self) -> int:
+        return int(self.lib.mpm_local_count(self.h))
+
+    def gather(self):
+        k = self.local_count()
+        p = self._template.particles
+        sub = SimState(ParticleSoA(k, p.dim, p.dtype, p.affine is not None, p.def_grad is not None))
+        v, keep = sub.output_view()
+        ids = np.empty(max(k, 1), np.int64)
+        self.ctx.check(self.lib.mpm_state_download_local(self.h, C.byref(v), ids.ctypes.data_as(C.c_void_p)))
+        sub.sync_from(v, keep)
+        return sub.particles, ids[:k], (sub.step, sub.time)
+
+    def close(self):
+        self.ctx.close()
+
+
+_STREAMS: dict = {}
+
+
+def _slab_stream(device: int):
+    import torch
+
+    if device not in _STREAMS:
+        _STREAMS[device] = torch.cuda.Stream(device=device)
+    return _STREAMS[device]
+
+
+def local_slab_run(scene: Scene, state: SimState, n_ranks: int, steps: int, nan_guard: bool = False,
+                   device: int = 0, balance: bool = True):
+    """Single-process decomposition on one GPU (R contexts stepped in lock-step): the testable
+    form of the multi-GPU path. Returns (final global state, stepper)."""
+    plan = SlabPlan.make(scene, n_ranks, state.particles.x if balance else None)
+    ids = plan.partition(scene, state)
+    doms = [GpuSlabDomain(scene, plan, r, state, ids[r], device) for r in range(n_ranks)]
+    stp = SlabStepper(doms, LocalTransport())
+    stp.advance(steps, nan_guard)
+    out = stp.gather_local(state)
+    return out, stp, plan
+
+
+__all__ = ["SlabPlan", "SlabDomain", "SlabStepper", "LocalTransport", "TorchTransport", "GpuSlabDomain",
+           "PeerFailure", "local_slab_run", "block_edge", "base_cell_x"]

@@ -63,6 +63,23 @@ class ParticleSoA:
         return c
 
 
+    def take(self, idx) -> "ParticleSoA":
+        """rows idx (a rank's subset under a slab decomposition)"""
+        c = ParticleSoA.__new__(ParticleSoA)
+        c.dim = self.dim
+        for f in self.FIELDS:
+            a = getattr(self, f)
+            setattr(c, f, None if a is None else (a[idx] if a.shape[0] else a.copy()))
+        return c
+
+    def put(self, idx, other: "ParticleSoA"):
+        """rows idx <- other (inverse of take)"""
+        for f in self.FIELDS:
+            a, b = getattr(self, f), getattr(other, f)
+            if a is not None and a.shape[0]:
+                a[idx] = b
+
+
 class SimState:
     """state.hpp:146-168"""
 
