@@ -75,8 +75,18 @@ template <class T, int D> struct DevScene {
     int slab_lo, slab_hi;
 };
 
-// particle buffer: SoA pointers (one array per component)
+// particle buffer field order inside one strided allocation (field k at base + k * S)
+template <int D> struct PLay {
+    static constexpr int X = 0, V = D, M = 2 * D, VOL = 2 * D + 1, RHO = 2 * D + 2, EPS = 2 * D + 3,
+                         SZZ = 2 * D + 4, SIG = 2 * D + 4 + (D == 2 ? 1 : 0), GV = SIG + Cfg<D>::NS,
+                         AFF = GV + D * D, F = AFF + D * D, END = F + D * D;
+};
+
+// particle buffer: SoA pointers (one array per component). The hot kernels address field k as
+// base + k * S (PLay order) so that they need two kernel parameters instead of ~40 pointers.
 template <class T, int D> struct PBuf {
+    T* base;
+    long long S;
     T* x[D];
     T* v[D];
     T* m;
@@ -124,6 +134,17 @@ __global__ inline void k_reset_status(DevStatus* st, long long step)
     s.den_pid = 0x7fffffff;
     s.ood_pid = 0x7fffffff;
     s.step = step;
+    s.err_step = -1;
+    *st = s;
+}
+
+// per-step reset that keeps the device-maintained step counter (capturable in a graph)
+__global__ inline void k_reset_flags(DevStatus* st)
+{
+    DevStatus s{};
+    s.den_pid = 0x7fffffff;
+    s.ood_pid = 0x7fffffff;
+    s.step = st->step;
     s.err_step = -1;
     *st = s;
 }

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -109,6 +110,7 @@ template <class T, int D> struct Ctx : CtxBase {
     mpm_scene_desc desc{};
     cudaStream_t stream{};
     cudaStream_t own_stream{}; // stream may be a caller's (mpm_ctx_set_stream)
+    int p2g_impl = 1, p2g_lanes_per_sm = 1; // 3-D P2G: 1 pipe3 (default), 0 lanes3 (experimental)
     int device = 0;
     int64_t cap = 0, n = 0;
     int64_t step = 0;
@@ -145,6 +147,45 @@ template <class T, int D> struct Ctx : CtxBase {
     int mig_cnt[2] = {0, 0};
 
     cudaGraphExec_t graphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}}; // [guard][cur]
+    // slab phases: P2G phase [cur] (valid for slab_g1_n[cur] particles), finish phase [guard][cur]
+    cudaGraphExec_t slab_g1[2] = {nullptr, nullptr};
+    int64_t slab_g1_n[2] = {-1, -1};
+    int64_t slab_g1_launches = 0, slab_g2_launches = 0;
+    cudaGraphExec_t slab_g2[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    bool status_dirty = true; // host step changed (upload): push it to the device counter
+    void drop_slab_graphs()
+    {
+        for (auto& e : slab_g1)
+            if (e) {
+                cudaGraphExecDestroy(e);
+                e = nullptr;
+            }
+        for (auto& g : slab_g2)
+            for (auto& e : g)
+                if (e) {
+                    cudaGraphExecDestroy(e);
+                    e = nullptr;
+                }
+        slab_g1_n[0] = slab_g1_n[1] = -1;
+    }
+    // capture f() on the stream into `out` (launch counter, buffer parity and key state restored)
+    template <class F> int64_t capture(cudaGraphExec_t& out, F&& f)
+    {
+        const int cur0 = cur;
+        const bool kv0 = keys_valid;
+        const int64_t l0 = launches;
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        f();
+        CK(cudaStreamEndCapture(stream, &g));
+        CK(cudaGraphInstantiate(&out, g, 0));
+        CK(cudaGraphDestroy(g));
+        const int64_t k = launches - l0;
+        launches = l0;
+        cur = cur0;
+        keys_valid = kv0;
+        return k;
+    }
 
     template <class X> X* alloc(size_t k)
     {
@@ -226,6 +267,7 @@ template <class T, int D> struct Ctx : CtxBase {
             for (auto& e : g)
                 if (e)
                     cudaGraphExecDestroy(e);
+        drop_slab_graphs();
         for (auto& e : events) {
             cudaEventDestroy(e.a);
             cudaEventDestroy(e.b);
@@ -312,21 +354,27 @@ template <class T, int D> struct Ctx : CtxBase {
 
     void alloc_pbuf(PBuf<T, D>& P)
     {
+        using L = PLay<D>;
+        const long long S = (cap + 63) / 64 * 64; // 512-byte aligned field stride
+        const int nf = has_F ? L::END : (has_aff ? L::F : L::AFF);
+        P.base = alloc<T>((size_t)S * nf);
+        P.S = S;
+        auto f = [&](int k) { return P.base + (size_t)k * S; };
         for (int a = 0; a < D; ++a) {
-            P.x[a] = alloc<T>(cap);
-            P.v[a] = alloc<T>(cap);
+            P.x[a] = f(L::X + a);
+            P.v[a] = f(L::V + a);
         }
-        P.m = alloc<T>(cap);
-        P.V = alloc<T>(cap);
-        P.rho = alloc<T>(cap);
-        P.eps = alloc<T>(cap);
-        P.szz = D == 2 ? alloc<T>(cap) : nullptr;
+        P.m = f(L::M);
+        P.V = f(L::VOL);
+        P.rho = f(L::RHO);
+        P.eps = f(L::EPS);
+        P.szz = D == 2 ? f(L::SZZ) : nullptr;
         for (int s = 0; s < C::NS; ++s)
-            P.sig[s] = alloc<T>(cap);
+            P.sig[s] = f(L::SIG + s);
         for (int k = 0; k < D * D; ++k) {
-            P.gv[k] = alloc<T>(cap);
-            P.aff[k] = has_aff ? alloc<T>(cap) : nullptr;
-            P.F[k] = has_F ? alloc<T>(cap) : nullptr;
+            P.gv[k] = f(L::GV + k);
+            P.aff[k] = has_aff ? f(L::AFF + k) : nullptr;
+            P.F[k] = has_F ? f(L::F + k) : nullptr;
         }
         P.pid = alloc<int>(cap);
     }
@@ -350,11 +398,14 @@ template <class T, int D> struct Ctx : CtxBase {
     }
 
     // ---- kernel launch helpers ------------------------------------------------------------
-    size_t g2p_smem() const { return sizeof(T) * 2 * D * C::TN; }
+    size_t g2p_smem(bool trackf) const
+    {
+        return trackf ? G2PStage<T, D, true>::SMEM : G2PStage<T, D, false>::SMEM;
+    }
 
     void set_smem_attrs()
     {
-        size_t sm = g2p_smem();
+        size_t sm = g2p_smem(true);
         auto set = [&](auto kern) { CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))); };
         set(k_g2p<T, D, P_CONSTIT, false, false>);
         set(k_g2p<T, D, P_CONSTIT | P_GUARD, false, false>);
@@ -373,6 +424,14 @@ template <class T, int D> struct Ctx : CtxBase {
                                     int(Pipe3Cfg<T, P2G_WIDE>::SMEM)));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2g_ctas_per_sm, k_p2g_pipe3<T, P2G_WIDE>,
                                                              Pipe3Cfg<T, P2G_WIDE>::THREADS, Pipe3Cfg<T, P2G_WIDE>::SMEM));
+            CK(cudaFuncSetAttribute(k_p2g_lanes3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(Lane3Cfg<T>::SMEM)));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2g_lanes_per_sm, k_p2g_lanes3<T>, Lane3Cfg<T>::THREADS,
+                                                             Lane3Cfg<T>::SMEM));
+            if (p2g_lanes_per_sm < 1)
+                p2g_lanes_per_sm = 1;
+            if (const char* e = std::getenv("MPM_P2G_IMPL")) // A/B measurement only
+                p2g_impl = std::string(e) == "lanes3" ? 0 : 1;
         } else {
             CK(cudaFuncSetAttribute(k_p2g_staged<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(StageCfg<T, D>::SMEM)));
@@ -440,11 +499,19 @@ template <class T, int D> struct Ctx : CtxBase {
             });
         } else {
             if constexpr (D == 3) {
-                using S = Pipe3Cfg<T, P2G_WIDE>;
-                launch("k_p2g", [&] {
-                    k_p2g_pipe3<T, P2G_WIDE><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
-                        sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st);
-                });
+                if (p2g_impl == 1) {
+                    using S = Pipe3Cfg<T, P2G_WIDE>;
+                    launch("k_p2g", [&] {
+                        k_p2g_pipe3<T, P2G_WIDE><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
+                            sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st);
+                    });
+                } else {
+                    using S = Lane3Cfg<T>;
+                    launch("k_p2g", [&] {
+                        k_p2g_lanes3<T><<<unsigned(nsm * p2g_lanes_per_sm), S::THREADS, S::SMEM, stream>>>(
+                            sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st);
+                    });
+                }
             } else {
                 using S = StageCfg<T, D>;
                 launch("k_p2g", [&] {
@@ -466,7 +533,7 @@ template <class T, int D> struct Ctx : CtxBase {
     {
         auto& Pin = buf[cur];
         auto& Pout = buf[cur ^ 1];
-        const size_t sm = g2p_smem();
+        const size_t sm = g2p_smem(has_F);
         const unsigned gr = persistent(D == 2 ? 8 : 4);
         if (has_aff && has_F)
             launch("k_g2p", [&] { k_g2p<T, D, FL, true, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
@@ -577,6 +644,7 @@ template <class T, int D> struct Ctx : CtxBase {
                                                                  has_aff, has_F, d_ids);
         });
         n_dead = 0;
+        status_dirty = true;
         step = s->step;
         time = s->time;
         keys_valid = false;
@@ -892,14 +960,36 @@ template <class T, int D> struct Ctx : CtxBase {
                     cudaGraphExecDestroy(e);
                     e = nullptr;
                 }
+        drop_slab_graphs();
         keys_valid = false;
     }
-    void step_p2g_local() override
+    void p2g_phase()
     {
-        reset_status();
+        launch("k_reset", [&] { k_reset_flags<<<1, 1, 0, stream>>>(st); });
         sort_and_segment();
         p2g_kernel();
         grid_kernel<G_SUM | G_NOGRAV | G_STORE>(); // an abort here is reported by step_finish_local
+    }
+    void step_p2g_local() override
+    {
+        if (status_dirty) {
+            reset_status();
+            status_dirty = false;
+        }
+        if (!keys_valid || prof) { // keys need computing (after upload / import): eager
+            p2g_phase();
+            return;
+        }
+        // replay a graph of the phase; recapture when the particle count changed (migration)
+        if (!slab_g1[cur] || slab_g1_n[cur] != n) {
+            if (slab_g1[cur])
+                cudaGraphExecDestroy(slab_g1[cur]);
+            slab_g1[cur] = nullptr;
+            slab_g1_launches = capture(slab_g1[cur], [&] { p2g_phase(); });
+            slab_g1_n[cur] = n;
+        }
+        CK(cudaGraphLaunch(slab_g1[cur], stream));
+        launches += slab_g1_launches;
     }
     void halo(int plane_lo, int n_planes, void* dev_buf, int mode) override
     {
@@ -911,14 +1001,29 @@ template <class T, int D> struct Ctx : CtxBase {
                                                                  static_cast<T*>(dev_buf), mode);
         }); // stream-ordered: the caller's transport runs on the same stream (mpm_ctx_set_stream)
     }
-    void step_finish_local(uint32_t flags) override
+    void finish_phase(bool guard)
     {
         grid_kernel<G_GRAV | G_ZEROV | G_MOM | G_CORR | G_STORE>();
-        if (flags & MPM_ADV_NAN_GUARD)
+        if (guard)
             g2p_kernel_fl<P_CONSTIT | P_GUARD>();
         else
             g2p_kernel_fl<P_CONSTIT>();
         launch("k_step_end", [&] { k_step_end<<<1, 1, 0, stream>>>(st); });
+    }
+    void step_finish_local(uint32_t flags) override
+    {
+        const bool guard = flags & MPM_ADV_NAN_GUARD;
+        if (prof) {
+            finish_phase(guard);
+        } else {
+            cudaGraphExec_t& ge = slab_g2[guard][cur];
+            if (!ge)
+                slab_g2_launches = capture(ge, [&] { finish_phase(guard); });
+            CK(cudaGraphLaunch(ge, stream));
+            launches += slab_g2_launches;
+            cur ^= 1;
+            keys_valid = true;
+        }
         fetch_status();
         mig_cnt[0] = st_host->mig_lo;
         mig_cnt[1] = st_host->mig_hi;

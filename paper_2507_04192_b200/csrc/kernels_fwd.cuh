@@ -1159,6 +1159,254 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     }
 }
 
+// 3-D P2G, lane-per-stencil-offset (PIC / FLIP / blend). A warp owns 4 particle columns of
+// the block; lane (i, j, k) < 27 owns the stencil offset (i, j, k) and accumulates the column's
+// contributions to node (x + i, y + j, z + k) for the current base level z in 7 registers per
+// column. After a level, lanes k = 0 hold the column's finished node-plane z; the window rolls by
+// one lane (__shfl_down). Each staged particle is converted once per level into its weights,
+// m v and V sigma (shared memory, read by broadcast LDS.128), so a lane-particle costs ~20 FP64
+// instructions. 16 warps per SM with 7 x 4 accumulators each (vs 6 warps holding 63 in
+// k_p2g_pipe3) hide the FP64 latency. Same partial tiles and fixed combine order as pipe3.
+// MEASURED (C4 f64, ncu): 0.88-0.91 ms vs pipe3's 0.58 ms -- shared-memory bound: 16 broadcast
+// LDS.64 per lane-particle cost ~2 wavefronts each (154M wavefronts, L1 74% busy). Kept for A/B
+// (MPM_P2G_IMPL=lanes3); a node per lane is too little reuse of each particle read.
+template <class T> struct Lane3Cfg {
+    static constexpr int THREADS = 512, WARPS = THREADS / 32, NBC = 64, CPW = NBC / WARPS;
+    static constexpr int CAP = 384, NRAW = 14, ND = 28, NSRC = 9, MAXIT = 64;
+    static constexpr size_t SMEM_RAW = sizeof(T) * NRAW * CAP;
+    static constexpr size_t SMEM_DER = sizeof(T) * ND * CAP;
+    static constexpr size_t SMEM_PK = sizeof(int) * 3 * 2 * CAP;
+    static constexpr size_t SMEM_SLOT = sizeof(T) * Cfg<3>::NCOL * NSRC * Cfg<3>::NF;
+    static constexpr size_t SMEM = SMEM_RAW + SMEM_DER + SMEM_PK + SMEM_SLOT;
+};
+
+template <class T>
+__global__ void __launch_bounds__(Lane3Cfg<T>::THREADS, 1)
+    k_p2g_lanes3(DevScene<T, 3> sc, PBuf<T, 3> P, const int* __restrict__ perm, const int* __restrict__ keys,
+                 const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ lstart,
+                 const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials, DevStatus* st)
+{
+    using C = Cfg<3>;
+    using S = Lane3Cfg<T>;
+    using PL = PLay<3>;
+    constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW,
+                  ND = S::ND, CPW = S::CPW, NT = S::THREADS;
+    // derived record per particle (ND doubles): (w, dw) pairs x0..2 | y0..2 | z0..2, m, m v, V sigma
+    constexpr int DX = 0, DY = 6, DZ = 12, DM = 18, DS = 22;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* raw = reinterpret_cast<T*>(smem_raw);                                           // [NRAW][CAP]
+    T* der = reinterpret_cast<T*>(smem_raw + S::SMEM_RAW);                             // [CAP][ND]
+    int* pk = reinterpret_cast<int*>(smem_raw + S::SMEM_RAW + S::SMEM_DER);            // [3][2][CAP]
+    T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_RAW + S::SMEM_DER + S::SMEM_PK); // [NCOL][NSRC][NF]
+    __shared__ int it_start[S::MAXIT], it_len[S::MAXIT], it_lvl[S::MAXIT], it_last[S::MAXIT];
+    __shared__ int nit_s, ccount[NBC], cst[NBC + 1];
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool act = lane < 27;
+    const int li = lane / 9, lj = (lane / 3) % 3, lk = lane % 3; // this lane's stencil offset
+    const long long SI = P.S;
+
+    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+        const int Q = occ[w];
+        const int s0 = bstart[Q], s1 = bend[Q];
+        __syncthreads();
+        if (tid == 0) { // level starts (suffix minimum) -> work items of <= CAP particles
+            int lv[B + 1];
+            int nxt = s1;
+            lv[B] = s1 - s0;
+            for (int z = B - 1; z >= 0; --z) {
+                const int v = lstart[Q * (B + 1) + z];
+                nxt = (v >= s0 && v < s1) ? v : nxt;
+                lv[z] = nxt - s0;
+            }
+            int k = 0;
+            for (int z = 0; z < B; ++z) {
+                const int nl = lv[z + 1] - lv[z];
+                const int nch = nl > 0 ? (nl + CAP - 1) / CAP : 1;
+                for (int c = 0; c < nch; ++c) {
+                    if (k < S::MAXIT) {
+                        it_start[k] = lv[z] + c * CAP;
+                        it_len[k] = min(CAP, nl - c * CAP);
+                        it_lvl[k] = z;
+                        it_last[k] = c == nch - 1;
+                    }
+                    ++k;
+                }
+            }
+            if (k > S::MAXIT) { // pathological compression: refuse loudly
+                st->far_flag = 1;
+                st->abort = 1;
+                k = 0;
+            }
+            nit_s = k;
+        }
+        if (tid < NBC)
+            ccount[tid] = 0;
+        __syncthreads();
+        const int nit = nit_s;
+        auto issue_pk = [&](int j) {
+            int* dp = pk + (j % 3) * 2 * CAP;
+            const int b = s0 + it_start[j];
+            for (int r = tid; r < it_len[j]; r += NT) {
+                cp_async4(dp + r, perm + b + r);
+                cp_async4(dp + CAP + r, keys + b + r);
+            }
+        };
+        // raw rows: x0..2 v0..2 m V sigma0..5 (PLay fields 0..7 and SIG..SIG+5; rho, eps skipped)
+        constexpr int RX = 0, RV = 3, RM = 6, RVOL = 7, RS = 8;
+        static_assert(PL::M == RM && PL::VOL == RVOL && PL::SIG == RS + 2 && RS + 6 == NRAW, "raw row map");
+        auto issue_raw = [&](int j) {
+            const int* pp = pk + (j % 3) * 2 * CAP;
+            for (int r = tid; r < it_len[j]; r += NT) {
+                const T* q = P.base + pp[r];
+#pragma unroll
+                for (int f = 0; f < NRAW; ++f)
+                    cp_async_t<T>(raw + f * CAP + r, q + (f < RS ? f : f + 2) * SI);
+            }
+        };
+        if (nit > 0)
+            issue_pk(0);
+        if (nit > 1)
+            issue_pk(1);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        if (nit > 0)
+            issue_raw(0);
+        cp_async_commit();
+
+        T* part = partials + (size_t)Q * NF * C::TN;
+        T acc[CPW][NF];
+#pragma unroll
+        for (int c = 0; c < CPW; ++c)
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+                acc[c][f] = T(0);
+
+        // lanes k = 0 publish node plane z of their columns, the window rolls, columns are combined
+        auto emit = [&](int z) {
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                const int bc = warp + c * S::WARPS;
+                const int ncol = ((bc >> 3) + li) * TE + (bc & 7) + lj;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    if (act && lk == 0)
+                        slots[(ncol * NSRC + li * 3 + lj) * NF + f] = acc[c][f];
+                    const T nx = __shfl_down_sync(0xffffffffu, acc[c][f], 1);
+                    acc[c][f] = (lk < 2 && act) ? nx : T(0);
+                }
+            }
+            __syncthreads();
+            for (int t = tid; t < C::NCOL * NF; t += NT) {
+                const int cidx = t / NF, f = t - cidx * NF;
+                const int n0 = cidx / TE, n1 = cidx - n0 * TE;
+                T sum = T(0);
+#pragma unroll
+                for (int q = 0; q < NSRC; ++q) {
+                    const int b0 = n0 - q / 3, b1 = n1 - q % 3;
+                    if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
+                        sum += slots[(cidx * NSRC + q) * NF + f];
+                }
+                part[f * C::TN + z * C::NCOL + cidx] = sum;
+            }
+            __syncthreads();
+        };
+
+        for (int j = 0; j < nit; ++j) {
+            cp_async_wait_all();
+            __syncthreads(); // raw(j), pk(j + 1) landed for every thread
+            const int len = it_len[j];
+            const int* col = pk + (j % 3) * 2 * CAP + CAP;
+            // convert each staged particle once: weights (bspline.hpp:330-344), m v, V sigma
+            for (int r = tid; r < len; r += NT) {
+                atomicAdd(&ccount[col[r] & (NBC - 1)], 1);
+                T* d = der + r * ND;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const T u = (raw[(RX + a) * CAP + r] - sc.origin[a]) * sc.inv_dh;
+                    const T fx = u - dfloor<T>(u - T(0.5));
+                    const T h0 = T(1.5) - fx, h1 = fx - T(1), h2 = fx - T(0.5);
+                    d[a * 6 + 0] = T(0.5) * h0 * h0;
+                    d[a * 6 + 1] = -h0 * sc.inv_dh;
+                    d[a * 6 + 2] = T(0.75) - h1 * h1;
+                    d[a * 6 + 3] = -T(2) * h1 * sc.inv_dh;
+                    d[a * 6 + 4] = T(0.5) * h2 * h2;
+                    d[a * 6 + 5] = h2 * sc.inv_dh;
+                }
+                const T m = raw[RM * CAP + r], V = raw[RVOL * CAP + r];
+                d[DM] = m;
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    d[DM + 1 + a] = m * raw[(RV + a) * CAP + r];
+#pragma unroll
+                for (int q = 0; q < 6; ++q)
+                    d[DS + q] = V * raw[(RS + q) * CAP + r];
+            }
+            __syncthreads(); // derived ready, raw free, counts complete
+            if (j + 1 < nit)
+                issue_raw(j + 1);
+            if (j + 2 < nit)
+                issue_pk(j + 2);
+            cp_async_commit();
+            if (tid < 32) {
+                const int c0 = ccount[2 * tid], c1 = ccount[2 * tid + 1];
+                int v = c0 + c1;
+#pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, v, dd);
+                    if (tid >= dd)
+                        v += t;
+                }
+                const int excl = v - c0 - c1;
+                cst[2 * tid] = excl;
+                cst[2 * tid + 1] = excl + c0;
+                if (tid == 31)
+                    cst[NBC] = v;
+                ccount[2 * tid] = 0;
+                ccount[2 * tid + 1] = 0;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                const int bc = warp + c * S::WARPS;
+                const int kb = cst[bc], ke = cst[bc + 1];
+                for (int k = kb; k < ke; ++k) {
+                    const T* d = der + k * ND;
+                    // broadcast reads: (w, dw) of this lane's x, y, z offsets; m, m v; V sigma
+                    const T wx = d[DX + 2 * li], dwx = d[DX + 2 * li + 1];
+                    const T wy = d[DY + 2 * lj], dwy = d[DY + 2 * lj + 1];
+                    const T wz = d[DZ + 2 * lk], dwz = d[DZ + 2 * lk + 1];
+                    const T m = d[DM], mv0 = d[DM + 1], mv1 = d[DM + 2], mv2 = d[DM + 3];
+                    const T s00 = d[DS + 0], s11 = d[DS + 1], s22 = d[DS + 2], s01 = d[DS + 3], s02 = d[DS + 4],
+                            s12 = d[DS + 5];
+                    const T wxy = wx * wy;
+                    const T wgt = wxy * wz;
+                    const T g0 = (dwx * wy) * wz, g1 = (wx * dwy) * wz, g2 = wxy * dwz; // grad phi
+                    acc[c][0] += m * wgt;
+                    acc[c][1] += mv0 * wgt;
+                    acc[c][2] += mv1 * wgt;
+                    acc[c][3] += mv2 * wgt;
+                    // f -= V sigma grad phi (transfer.hpp:420-427); gravity is added per node in k_grid
+                    acc[c][4] -= s00 * g0 + s01 * g1 + s02 * g2;
+                    acc[c][5] -= s01 * g0 + s11 * g1 + s12 * g2;
+                    acc[c][6] -= s02 * g0 + s12 * g1 + s22 * g2;
+                }
+            }
+            if (it_last[j]) {
+                __syncthreads();
+                emit(it_lvl[j]);
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        emit(B);
+        emit(B + 1);
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // grid update: combine partial tiles, momentum update, boundary/contact corrections.
 // G_NOGRAV: sum without the g m_i term (slab halo sums first); G_GRAV: add g m_i to a stored
@@ -1422,6 +1670,14 @@ template <class T> struct MigBuf {
     int* hi_pid;
 };
 
+// per-thread staging of a particle's G2P inputs (x, v, m, V, rho, eps, [szz], sigma, [F])
+template <class T, int D, bool TRACKF> struct G2PStage {
+    static constexpr int NSF = 2 * D + 4 + (D == 2 ? 1 : 0) + Cfg<D>::NS + (TRACKF ? D * D : 0);
+    static constexpr int THREADS = 256;
+    static constexpr size_t TILE = sizeof(T) * 2 * D * Cfg<D>::TN;
+    static constexpr size_t SMEM = TILE + sizeof(T) * 2 * NSF * THREADS; // tile + 2 slots
+};
+
 template <class T, int D, int FLAGS, bool APIC, bool TRACKF>
 __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pin, PBuf<T, D> Pout,
                                              GBuf<T, D> G, const int* __restrict__ perm,
@@ -1430,19 +1686,46 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                                              int* __restrict__ keys_out, DevStatus* st, MigBuf<T> MG)
 {
     using C = Cfg<D>;
-    constexpr int TE = C::TE, TN = C::TN;
+    using SG = G2PStage<T, D, TRACKF>;
+    constexpr int TE = C::TE, TN = C::TN, NSF = SG::NSF, NT = SG::THREADS;
     extern __shared__ unsigned char smem_raw[];
     T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]: v[0..D), vold[0..D)
+    T* stg = tile + 2 * D * TN;               // [2][NSF][NT]: this thread's column only
     if (st->abort)
         return;
     const int nocc = *n_occ;
     const T alpha = sc.alpha;
+    const int tid = threadIdx.x;
+    // cp.async of particle `src`'s inputs into slot `slot` (each thread its own column: no barrier)
+    using PL = PLay<D>;
+    const long long SI = Pin.S, SO = Pout.S;
+    auto issue = [&](int slot, int src) {
+        T* b = stg + slot * NSF * NT + tid;
+        const T* q = Pin.base + src; // field k at q + k * SI (PLay order: x v m V rho eps [szz] sigma)
+#pragma unroll
+        for (int f = 0; f < PL::SIG + C::NS; ++f)
+            cp_async_t<T>(b + f * NT, q + f * SI);
+        if constexpr (TRACKF) {
+#pragma unroll
+            for (int k = 0; k < D * D; ++k)
+                cp_async_t<T>(b + (PL::SIG + C::NS + k) * NT, q + (PL::F + k) * SI);
+        }
+    };
+    static_assert(PL::SIG + C::NS + (TRACKF ? D * D : 0) == NSF, "staging mirrors the PLay field order");
     for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
         int qc[D];
         block_coords<D>(Q, sc.nb, qc);
+        cp_async_wait_all();
         __syncthreads();
+        // first particle of this thread in flight while the node tile loads
+        int i0 = s0 + tid;
+        int src_a = i0 < s1 ? perm[i0] : -1;                    // particle i0
+        int src_b = i0 + NT < s1 ? perm[i0 + NT] : -1;          // particle i0 + NT (prefetched index)
+        if (src_a >= 0)
+            issue(0, src_a);
+        cp_async_commit();
         for (int t = threadIdx.x; t < TN; t += blockDim.x) {
             int tl[D], rem = t, nid = 0, loc = 0;
             bool ok = true;
@@ -1467,13 +1750,23 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
             }
         }
         __syncthreads();
-        for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
-            const int src = perm[i];
+        int slot = 0;
+        for (int i = i0; i < s1; i += NT) {
+            const int src = src_a;
+            // keep the next particle's fields and the one after's index in flight
+            src_a = src_b;
+            src_b = i + 2 * NT < s1 ? perm[i + 2 * NT] : -1;
+            if (src_a >= 0)
+                issue(slot ^ 1, src_a);
+            cp_async_commit();
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory"); // this thread's slot `slot` landed
+            const T* sb = stg + slot * NSF * NT + tid;
+            slot ^= 1;
             T x[D], v[D];
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-                x[a] = __ldg(Pin.x[a] + src);
-                v[a] = __ldg(Pin.v[a] + src);
+                x[a] = sb[a * NT];
+                v[a] = sb[(D + a) * NT];
             }
             T w[D][3], dw[D][3];
             int tb[D];
@@ -1597,17 +1890,18 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                 vn[a] = alpha * (v[a] + vinc[a]) + (T(1) - alpha) * vpic[a];
                 xn[a] = x[a] + sc.dt * vpic[a];
             }
-            T m = __ldg(Pin.m + src), V = __ldg(Pin.V + src), rho = __ldg(Pin.rho + src), eps = __ldg(Pin.eps + src);
-            T szz = D == 2 ? __ldg(Pin.szz + src) : T(0);
+            constexpr int FM = 2 * D, FS = 2 * D + 4 + (D == 2 ? 1 : 0);
+            T m = sb[FM * NT], V = sb[(FM + 1) * NT], rho = sb[(FM + 2) * NT], eps = sb[(FM + 3) * NT];
+            T szz = D == 2 ? sb[(FM + 4) * NT] : T(0);
             T sig[C::NS];
 #pragma unroll
             for (int s = 0; s < C::NS; ++s)
-                sig[s] = __ldg(Pin.sig[s] + src);
+                sig[s] = sb[(FS + s) * NT];
             T Fm[D * D];
             if constexpr (TRACKF) {
 #pragma unroll
                 for (int k = 0; k < D * D; ++k)
-                    Fm[k] = __ldg(Pin.F[k] + src);
+                    Fm[k] = sb[(FS + C::NS + k) * NT];
             }
             bool ok_den = true;
             if (FLAGS & P_CONSTIT) {
@@ -1630,33 +1924,34 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                 }
             }
             const int pid = Pin.pid[src];
-            // write the new state at sorted slot i
+            // write the new state at sorted slot i (field k at o + k * SO)
+            T* o = Pout.base + i;
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-                Pout.x[a][i] = xn[a];
-                Pout.v[a][i] = vn[a];
+                o[(PL::X + a) * SO] = xn[a];
+                o[(PL::V + a) * SO] = vn[a];
             }
-            Pout.m[i] = m;
-            Pout.V[i] = V;
-            Pout.rho[i] = rho;
-            Pout.eps[i] = eps;
+            o[PL::M * SO] = m;
+            o[PL::VOL * SO] = V;
+            o[PL::RHO * SO] = rho;
+            o[PL::EPS * SO] = eps;
             if (D == 2)
-                Pout.szz[i] = szz;
+                o[PL::SZZ * SO] = szz;
 #pragma unroll
             for (int s = 0; s < C::NS; ++s)
-                Pout.sig[s][i] = sig[s];
+                o[(PL::SIG + s) * SO] = sig[s];
 #pragma unroll
             for (int k = 0; k < D * D; ++k)
-                Pout.gv[k][i] = L[k];
+                o[(PL::GV + k) * SO] = L[k];
             if constexpr (APIC) {
 #pragma unroll
                 for (int k = 0; k < D * D; ++k)
-                    Pout.aff[k][i] = Bm[k];
+                    o[(PL::AFF + k) * SO] = Bm[k];
             }
             if constexpr (TRACKF) {
 #pragma unroll
                 for (int k = 0; k < D * D; ++k)
-                    Pout.F[k][i] = Fm[k];
+                    o[(PL::F + k) * SO] = Fm[k];
             }
             Pout.pid[i] = pid;
             if (!ok_den) {
