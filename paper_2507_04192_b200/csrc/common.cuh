@@ -73,6 +73,14 @@ template <class T, int D> struct DevScene {
     // slab decomposition: this context owns particles whose base cell along x lies in
     // [slab_lo, slab_hi); the whole domain otherwise. Walls and Coulomb segments stay global.
     int slab_lo, slab_hi;
+    // scene constants of the constitutive updates, evaluated once on the device with the exact
+    // expressions of constitutive.hpp (k_scene_consts) so results are bit-identical
+    T dp_lam;      // K - 2G/3
+    T dp_dlam_den; // G + K q_phi q_psi
+    T dp_deps_fac; // sqrt(1/3 + 2/9 q_psi^2)
+    T dp_apex;     // k_phi / q_phi
+    T dp_deps_t;   // sqrt(2) / 3
+    T fl_k;        // visc / dt (rate form) or visc
 };
 
 // particle buffer field order inside one strided allocation (field k at base + k * S)

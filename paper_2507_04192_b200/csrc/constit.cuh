@@ -9,6 +9,16 @@
 
 namespace mpmgpu {
 
+template <class T, int D> __global__ void k_scene_consts(DevScene<T, D>* s)
+{
+    s->dp_lam = s->K - T(2) * s->G / T(3);
+    s->dp_dlam_den = s->G + s->K * s->q_phi * s->q_psi;
+    s->dp_deps_fac = dsqrt<T>(T(1) / T(3) + T(2) / T(9) * s->q_psi * s->q_psi);
+    s->dp_apex = s->q_phi > T(0) ? s->k_phi / s->q_phi : T(0);
+    s->dp_deps_t = dsqrt<T>(T(2)) / T(3);
+    s->fl_k = s->rate_form ? s->visc / s->dt : s->visc;
+}
+
 template <class T> struct M3 {
     T a[3][3];
 };
@@ -39,20 +49,26 @@ __device__ __forceinline__ void dp_trial(const DevScene<T, D>& sc, const T (&S)[
             t.dw[i][j] = T(0.5) * (Lf[i][j] - Lf[j][i]) * sc.dt;
         }
     // sR = S + S dw^T + dw S^T  (constitutive.hpp:117)
+    // X = S dw^T, so that (dw S^T)_ij = X_ji: each product sum is formed once (same operands and
+    // order as the two sums it replaces, so bit-identical)
+    T X[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-            T a = T(0), b = T(0);
+            T a = T(0);
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
+            for (int k = 0; k < 3; ++k)
                 a += S[i][k] * t.dw[j][k];
-                b += t.dw[i][k] * S[j][k];
-            }
-            t.sR[i][j] = S[i][j] + a + b;
+            X[i][j] = a;
         }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            t.sR[i][j] = S[i][j] + X[i][j] + X[j][i];
     t.trd = t.dd[0][0] + t.dd[1][1] + t.dd[2][2];
-    T lam = sc.K - T(2) * sc.G / T(3);
+    const T lam = sc.dp_lam;
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -92,12 +108,12 @@ __device__ __forceinline__ T dp_update(const DevScene<T, D>& sc, const T (&S)[3]
             out[i][j] = t.trial[i][j];
     deps = T(0);
     if (t.zone == 2) {
-        T dlam = t.fs / (sc.G + sc.K * sc.q_phi * sc.q_psi);
-        deps = dlam * dsqrt<T>(T(1) / T(3) + T(2) / T(9) * sc.q_psi * sc.q_psi);
+        T dlam = t.fs / sc.dp_dlam_den;
+        deps = dlam * sc.dp_deps_fac;
         T sm_new = t.sm - sc.K * sc.q_psi * dlam;
         T tau_new = sc.k_phi - sc.q_phi * sm_new;
         if (t.tau <= T(0) || tau_new < T(0)) {
-            sm_new = sc.q_phi > T(0) ? sc.k_phi / sc.q_phi : sm_new;
+            sm_new = sc.q_phi > T(0) ? sc.dp_apex : sm_new;
 #pragma unroll
             for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -118,7 +134,7 @@ __device__ __forceinline__ T dp_update(const DevScene<T, D>& sc, const T (&S)[3]
         }
     } else if (t.zone == 3) {
         T dlam_t = t.ft / sc.K;
-        deps = dsqrt<T>(T(2)) / T(3) * dlam_t;
+        deps = sc.dp_deps_t * dlam_t;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
             out[i][i] = t.trial[i][i] + (sc.sigma_t - t.sm);
@@ -157,7 +173,7 @@ __device__ __forceinline__ bool constitutive_particle(const DevScene<T, D>& sc, 
             return false;
         T rho_new = rho / den;
         T pres = sc.c * sc.c * (rho_new - sc.rho0);
-        T k = sc.rate_form ? sc.visc / sc.dt : sc.visc;
+        T k = sc.fl_k;
         T vis = (T(2) / T(3)) * k * trd, k2 = T(2) * k;
 #pragma unroll
         for (int i = 0; i < D; ++i)

@@ -350,6 +350,15 @@ template <class T, int D> struct Ctx : CtxBase {
             for (int k = 0; k < 2 * D; ++k)
                 sc.obst[o][k] = T(d->obstacles[o * 2 * D + k]);
         sc.mass_eps = T(d->mass_epsilon);
+        // constitutive scene constants, evaluated by the device with the expressions they replace
+        DevScene<T, D>* ds = nullptr;
+        CK(cudaMalloc(&ds, sizeof(sc)));
+        CK(cudaMemcpyAsync(ds, &sc, sizeof(sc), cudaMemcpyHostToDevice, stream));
+        k_scene_consts<T, D><<<1, 1, 0, stream>>>(ds);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&sc, ds, sizeof(sc), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        CK(cudaFree(ds));
     }
 
     void alloc_pbuf(PBuf<T, D>& P)

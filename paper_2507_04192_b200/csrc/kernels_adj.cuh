@@ -77,7 +77,7 @@ __device__ __forceinline__ void fluid_vjp_dev(const DevScene<T, D>& sc, T rho, T
     const T den = T(1) + trd;
     const T rho_new = rho / den;
     const T c = sc.c;
-    const T k = sc.rate_form ? sc.visc / sc.dt : sc.visc;
+    const T k = sc.fl_k;
     T trs = T(0);
 #pragma unroll
     for (int i = 0; i < D; ++i)
@@ -169,7 +169,7 @@ __device__ __forceinline__ void dp_vjp_dev(const DevScene<T, D>& sc, const T (&S
             for (int j = 0; j < 3; ++j)
                 tc[i][j] = oc[i][j];
     } else if (t.zone == 2) {
-        const T denom = sc.G + sc.K * sc.q_phi * sc.q_psi;
+        const T denom = sc.dp_dlam_den;
         const T dlam = t.fs / denom;
         const T sm_new = t.sm - sc.K * sc.q_psi * dlam;
         const T tau_new = sc.k_phi - sc.q_phi * sm_new;
@@ -231,7 +231,7 @@ __device__ __forceinline__ void dp_vjp_dev(const DevScene<T, D>& sc, const T (&S
         }
     }
     // trial = sR + 2G dd + (K - 2G/3) tr(dd) I
-    const T lam = sc.K - T(2) * sc.G / T(3);
+    const T lam = sc.dp_lam;
     const T ttr = tc[0][0] + tc[1][1] + tc[2][2];
     T dd_c[3][3];
 #pragma unroll

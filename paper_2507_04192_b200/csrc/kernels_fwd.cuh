@@ -1689,7 +1689,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
     using SG = G2PStage<T, D, TRACKF>;
     constexpr int TE = C::TE, TN = C::TN, NSF = SG::NSF, NT = SG::THREADS;
     extern __shared__ unsigned char smem_raw[];
-    T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]: v[0..D), vold[0..D)
+    T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]: v[0..D), v - vold[0..D) (formed once per node)
     T* stg = tile + 2 * D * TN;               // [2][NSF][NT]: this thread's column only
     if (st->abort)
         return;
@@ -1745,8 +1745,9 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
             const size_t gi = (size_t)nid * C::NB + loc;
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-                tile[a * TN + t] = ok ? G.v[a][gi] : T(0);
-                tile[(D + a) * TN + t] = ok ? G.vold[a][gi] : T(0);
+                const T vn = ok ? G.v[a][gi] : T(0), vo = ok ? G.vold[a][gi] : T(0);
+                tile[a * TN + t] = vn;
+                tile[(D + a) * TN + t] = vn - vo;
             }
         }
         __syncthreads();
@@ -1808,7 +1809,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                         const T v0 = va[0], v1 = va[1], v2 = va[2];
                         A[a] = w[D - 1][0] * v0 + w[D - 1][1] * v1 + w[D - 1][2] * v2;
                         Bz[a] = dw[D - 1][0] * v0 + dw[D - 1][1] * v1 + dw[D - 1][2] * v2;
-                        Cd[a] = w[D - 1][0] * (v0 - voa[0]) + w[D - 1][1] * (v1 - voa[1]) + w[D - 1][2] * (v2 - voa[2]);
+                        Cd[a] = w[D - 1][0] * voa[0] + w[D - 1][1] * voa[1] + w[D - 1][2] * voa[2]; // voa: v - vold
                     }
                     T wo = T(1), po[D - 1 > 0 ? D - 1 : 1];
 #pragma unroll
@@ -1864,9 +1865,9 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
                     nv[a] = tile[a * TN + ti];
-                    const T nvo = tile[(D + a) * TN + ti];
+                    const T ndv = tile[(D + a) * TN + ti]; // v - vold
                     vpic[a] += phi * nv[a];
-                    vinc[a] += phi * (nv[a] - nvo);
+                    vinc[a] += phi * ndv;
                 }
 #pragma unroll
                 for (int a = 0; a < D; ++a)
