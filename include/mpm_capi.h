@@ -223,9 +223,11 @@ int mpm_backprop(mpm_ctx* ctx, const mpm_state_view* initial, int64_t total_step
 /* ---- slab decomposition across GPUs ------------------------------------ */
 /* One context per GPU, global coordinates; the context owns the particles whose base cell along
  * x lies in [cell_lo, cell_hi) (multiples of the block edge, 16 in 2-D / 8 in 3-D). A step is
- *   mpm_step_p2g_local -> halo exchange of the 2 node planes shared with each x-neighbour
- *   (mpm_halo export/import on caller device buffers) -> mpm_step_finish_local -> migration
- *   (mpm_migrate_export / mpm_migrate_import) of particles that left the slab.
+ *   mpm_step_p2g_local (P2G + partial sums of the 2 node planes shared with each x-neighbour)
+ *   -> mpm_halo export, start the neighbour send/recv -> mpm_step_grid_interior (all other
+ *   nodes, overlapping the transfer) -> wait, mpm_halo import -> mpm_step_finish_local (band
+ *   nodes, G2P) -> migration (mpm_migrate_export / mpm_migrate_import) of particles that left
+ *   the slab.
  * The transport between GPUs (NCCL over NVLink via torch.distributed, or device copies in the
  * single-process mode) belongs to the caller (paper_2507_04192_b200/distributed.py). */
 int mpm_slab_set(mpm_ctx* ctx, int cell_lo, int cell_hi, int64_t mig_cap);
@@ -240,10 +242,16 @@ int mpm_state_upload_ids(mpm_ctx* ctx, const mpm_state_view* s, const int64_t* i
 int mpm_state_download_local(mpm_ctx* ctx, mpm_state_view* s, int64_t* ids);
 int64_t mpm_local_count(const mpm_ctx* ctx);
 int mpm_step_p2g_local(mpm_ctx* ctx);
+int mpm_step_grid_interior(mpm_ctx* ctx);
 /* node planes [plane_lo, plane_lo + n_planes) x all other nodes, (1 + 2 dim) scalars each:
  * mode 0 export into dev_buf; 1 import as received + own; 2 import as own + received */
 int mpm_halo(mpm_ctx* ctx, int plane_lo, int n_planes, void* dev_buf, int mode);
 int mpm_step_finish_local(mpm_ctx* ctx, uint32_t flags);
+/* the same without a host synchronisation: enqueues the finish and writes (failed, n_lo, n_hi) as
+ * int64 into device memory `dev_report` on the context stream, for the caller's collective; then
+ * mpm_step_commit with the counts and whether any rank failed (raises this rank's own error) */
+int mpm_step_finish_async(mpm_ctx* ctx, uint32_t flags, int64_t* dev_report);
+int mpm_step_commit(mpm_ctx* ctx, int64_t n_lo, int64_t n_hi, int any_failed);
 /* particles that left the slab during the last step, toward -x (lo) and +x (hi) */
 int mpm_particle_record_size(const mpm_ctx* ctx);
 /* host-side counts of the last mpm_step_finish_local (known after it returns) */

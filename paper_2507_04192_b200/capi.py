@@ -184,8 +184,11 @@ _PROTOS = {
     "mpm_state_download_local": (C.c_int, [C.c_void_p, C.POINTER(StateView), C.c_void_p]),
     "mpm_local_count": (C.c_int64, [C.c_void_p]),
     "mpm_step_p2g_local": (C.c_int, [C.c_void_p]),
+    "mpm_step_grid_interior": (C.c_int, [C.c_void_p]),
     "mpm_halo": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int]),
     "mpm_step_finish_local": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "mpm_step_finish_async": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "mpm_step_commit": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int]),
     "mpm_particle_record_size": (C.c_int, [C.c_void_p]),
     "mpm_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "mpm_migrate_counts": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -73,6 +73,9 @@ template <class T, int D> struct DevScene {
     // slab decomposition: this context owns particles whose base cell along x lies in
     // [slab_lo, slab_hi); the whole domain otherwise. Walls and Coulomb segments stay global.
     int slab_lo, slab_hi;
+    // halo bands: node x-planes [band_lo, band_lo + 2) and [band_hi, band_hi + 2) are shared with
+    // the x-neighbours (far outside the grid when there is no neighbour)
+    int band_lo, band_hi;
     // scene constants of the constitutive updates, evaluated once on the device with the exact
     // expressions of constitutive.hpp (k_scene_consts) so results are bit-identical
     T dp_lam;      // K - 2G/3

@@ -79,8 +79,11 @@ struct CtxBase {
     virtual void download_local(mpm_state_view* s, int64_t* ids) = 0;
     virtual void slab_set(int lo, int hi, int64_t mig_cap) = 0;
     virtual void step_p2g_local() = 0;
+    virtual void step_grid_interior() = 0;
     virtual void halo(int plane_lo, int n_planes, void* dev_buf, int mode) = 0;
     virtual void step_finish_local(uint32_t flags) = 0;
+    virtual void step_finish_async(uint32_t flags, long long* dev_report) = 0;
+    virtual void step_commit(int64_t n_lo, int64_t n_hi, int any_failed) = 0;
     virtual void migrate_export(void* lo, int* lo_pid, void* hi, int* hi_pid, int64_t cap, int64_t* n_lo, int64_t* n_hi) = 0;
     virtual void migrate_import(const void* recs, const int* pids, int64_t k) = 0;
     virtual int rec_size() const = 0;
@@ -304,6 +307,7 @@ template <class T, int D> struct Ctx : CtxBase {
         }
         sc.slab_lo = 0;
         sc.slab_hi = d->cells[0];
+        sc.band_lo = sc.band_hi = -(1 << 28); // no neighbours
         sc.nb_total = 1;
         sc.nnb_total = 1;
         for (int a = 0; a < D; ++a) {
@@ -953,6 +957,8 @@ template <class T, int D> struct Ctx : CtxBase {
             throw ApiError(MPM_ERR_USAGE, "slab bounds must be block-aligned (multiples of " + std::to_string(C::B) + ")");
         sc.slab_lo = lo;
         sc.slab_hi = hi;
+        sc.band_lo = lo > 0 ? lo : -(1 << 28);
+        sc.band_hi = hi < sc.cells[0] ? hi : -(1 << 28);
         slab = true;
         if (!mig.on || mig.cap < mig_cap) {
             mig.on = 1;
@@ -977,8 +983,13 @@ template <class T, int D> struct Ctx : CtxBase {
         launch("k_reset", [&] { k_reset_flags<<<1, 1, 0, stream>>>(st); });
         sort_and_segment();
         p2g_kernel();
-        grid_kernel<G_SUM | G_NOGRAV | G_STORE>(); // an abort here is reported by step_finish_local
+        // halo-band nodes only: their partial sums (without g m) go to the neighbours; an abort
+        // here is reported by step_finish_local
+        grid_kernel<G_BANDONLY | G_SUM | G_NOGRAV | G_STORE>();
     }
+    // every node off the halo bands: the fused sum + g m + momentum + corrections, enqueued while
+    // the bands travel (the transport overlaps it)
+    void step_grid_interior() override { grid_kernel<G_INTERIOR | G_SUM | G_MOM | G_CORR>(); }
     void step_p2g_local() override
     {
         if (status_dirty) {
@@ -1012,7 +1023,7 @@ template <class T, int D> struct Ctx : CtxBase {
     }
     void finish_phase(bool guard)
     {
-        grid_kernel<G_GRAV | G_ZEROV | G_MOM | G_CORR | G_STORE>();
+        grid_kernel<G_BANDONLY | G_GRAV | G_ZEROV | G_MOM | G_CORR | G_STORE>();
         if (guard)
             g2p_kernel_fl<P_CONSTIT | P_GUARD>();
         else
@@ -1043,6 +1054,41 @@ template <class T, int D> struct Ctx : CtxBase {
         if (st_host->mig_over)
             throw ApiError(MPM_ERR_CUDA, "slab migration buffer overflow (raise mig_cap)");
         check_status(step);
+    }
+    // finish without a host synchronisation: the (failed, n_lo, n_hi) report lands in device memory
+    // behind G2P so the caller's collective can gather it on the same stream; step_commit does the
+    // host bookkeeping once the caller has the gathered reports
+    void step_finish_async(uint32_t flags, long long* dev_report) override
+    {
+        const bool guard = flags & MPM_ADV_NAN_GUARD;
+        if (prof) {
+            finish_phase(guard);
+        } else {
+            cudaGraphExec_t& ge = slab_g2[guard][cur];
+            if (!ge)
+                slab_g2_launches = capture(ge, [&] { finish_phase(guard); });
+            CK(cudaGraphLaunch(ge, stream));
+            launches += slab_g2_launches;
+            cur ^= 1;
+            keys_valid = true;
+        }
+        launch("k_report", [&] { k_report<<<1, 1, 0, stream>>>(st, dev_report); });
+    }
+    void step_commit(int64_t n_lo, int64_t n_hi, int any_failed) override
+    {
+        mig_cnt[0] = int(n_lo);
+        mig_cnt[1] = int(n_hi);
+        n = n - n_dead;
+        n_dead = n_lo + n_hi;
+        if (any_failed) { // raise this rank's own error, if it has one
+            fetch_status();
+            if (st_host->mig_over)
+                throw ApiError(MPM_ERR_CUDA, "slab migration buffer overflow (raise mig_cap)");
+            check_status(step);
+            return;
+        }
+        step += 1; // k_step_end advanced the device counter
+        time = double(T(step) * sc.dt);
     }
     void migrate_export(void* lo, int* lo_pid, void* hi, int* hi_pid, int64_t cap, int64_t* n_lo, int64_t* n_hi) override
     {
@@ -1477,8 +1523,17 @@ int mpm_state_upload_ids(mpm_ctx* c, const mpm_state_view* s, const int64_t* ids
 int mpm_state_download_local(mpm_ctx* c, mpm_state_view* s, int64_t* ids) { MPM_CALL(c, c->impl->download_local(s, ids)); }
 int mpm_slab_set(mpm_ctx* c, int cell_lo, int cell_hi, int64_t mig_cap) { MPM_CALL(c, c->impl->slab_set(cell_lo, cell_hi, mig_cap)); }
 int mpm_step_p2g_local(mpm_ctx* c) { MPM_CALL(c, c->impl->step_p2g_local()); }
+int mpm_step_grid_interior(mpm_ctx* c) { MPM_CALL(c, c->impl->step_grid_interior()); }
 int mpm_halo(mpm_ctx* c, int plane_lo, int n_planes, void* dev_buf, int mode) { MPM_CALL(c, c->impl->halo(plane_lo, n_planes, dev_buf, mode)); }
 int mpm_step_finish_local(mpm_ctx* c, uint32_t flags) { MPM_CALL(c, c->impl->step_finish_local(flags)); }
+int mpm_step_finish_async(mpm_ctx* c, uint32_t flags, int64_t* dev_report)
+{
+    MPM_CALL(c, c->impl->step_finish_async(flags, reinterpret_cast<long long*>(dev_report)));
+}
+int mpm_step_commit(mpm_ctx* c, int64_t n_lo, int64_t n_hi, int any_failed)
+{
+    MPM_CALL(c, c->impl->step_commit(n_lo, n_hi, any_failed));
+}
 int mpm_migrate_export(mpm_ctx* c, void* lo, int* lo_pid, void* hi, int* hi_pid, int64_t cap, int64_t* n_lo, int64_t* n_hi)
 {
     MPM_CALL(c, c->impl->migrate_export(lo, lo_pid, hi, hi_pid, cap, n_lo, n_hi));

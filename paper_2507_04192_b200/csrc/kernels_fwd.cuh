@@ -1411,7 +1411,15 @@ __global__ void __launch_bounds__(Lane3Cfg<T>::THREADS, 1)
 // grid update: combine partial tiles, momentum update, boundary/contact corrections.
 // G_NOGRAV: sum without the g m_i term (slab halo sums first); G_GRAV: add g m_i to a stored
 // grid; G_ZEROV: massless nodes of a stored grid get v = v_old = 0 (as after a fresh sum)
-enum GridMode { G_SUM = 1, G_MOM = 2, G_CORR = 4, G_STORE = 8, G_NOGRAV = 16, G_GRAV = 32, G_ZEROV = 64 };
+// G_BANDONLY / G_INTERIOR: only the halo-band nodes / only the others (slab decomposition)
+enum GridMode {
+    G_SUM = 1, G_MOM = 2, G_CORR = 4, G_STORE = 8, G_NOGRAV = 16, G_GRAV = 32, G_ZEROV = 64, G_BANDONLY = 128,
+    G_INTERIOR = 256
+};
+template <class T, int D> __device__ __forceinline__ bool in_band(const DevScene<T, D>& sc, int x)
+{
+    return (unsigned)(x - sc.band_lo) < 2u || (unsigned)(x - sc.band_hi) < 2u;
+}
 
 // collect_node_corrections + apply_node_correction (contact.hpp:141-224), fixed order
 template <class T, int D>
@@ -1542,11 +1550,24 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
         const int q = act[w];
         int qc[D], n[D];
         block_coords<D>(q, sc.nnb, qc);
+        if constexpr ((MODE & G_BANDONLY) != 0) { // whole node blocks off the bands: nothing to do
+            const int x0 = qc[0] * C::B;
+            if (!((sc.band_lo + 1 >= x0 && sc.band_lo < x0 + C::B) || (sc.band_hi + 1 >= x0 && sc.band_hi < x0 + C::B)))
+                continue;
+        }
         bool inside = true;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
             n[a] = qc[a] * C::B + lc[a];
             inside &= n[a] <= sc.cells[a];
+        }
+        if constexpr ((MODE & G_BANDONLY) != 0) {
+            if (!in_band<T, D>(sc, n[0]))
+                continue;
+        }
+        if constexpr ((MODE & G_INTERIOR) != 0) {
+            if (in_band<T, D>(sc, n[0]))
+                continue;
         }
         const size_t gi = (size_t)q * C::NB + tid;
         T m = T(0), p[D], f[D], v[D], vold[D];

@@ -181,6 +181,14 @@ __global__ void k_download(Stage<T, D> S, PBuf<T, D> P, int n, int has_aff, int 
         }
 }
 
+// slab step report for the caller's collective: (failed, left toward -x, left toward +x)
+__global__ inline void k_report(const DevStatus* st, long long* out)
+{
+    out[0] = st->abort ? 1 : 0;
+    out[1] = st->mig_lo;
+    out[2] = st->mig_hi;
+}
+
 // compact download for a slab: slot list idx[0..k) (storage order), ids alongside
 template <class T, int D>
 __global__ void k_download_compact(Stage<T, D> S, PBuf<T, D> P, const int* __restrict__ idx, int k, int has_aff,

@@ -5,13 +5,14 @@ the same step along x across one process per GPU. Every rank owns the particles 
 along x lies in its slab `[lo, hi)`. Slab bounds are multiples of the particle-block edge: 16
 cells in 2-D, 8 in 3-D. One step runs in four phases:
 
-  1. P2G. Each rank calls `mpm_step_p2g_local`: it scatters its own particles into its grid,
-     without the `g m_i` term.
-  2. Halo sum. Neighbouring slabs share the 2 node planes `[hi, hi + 2)` that both scatter into.
-     Each rank exports its partial (m, p, f) on those planes and adds the neighbour's. The sum
-     runs in a fixed order, lower rank's partial first, so both owners hold bit-identical nodes.
-  3. Finish. Each rank calls `mpm_step_finish_local`: add `g m_i`, momentum update, boundary
-     corrections, then G2P and the constitutive update on its own particles.
+  1. P2G. Each rank calls `mpm_step_p2g_local`: it scatters its own particles and sums the
+     nodes of the 2 node planes `[hi, hi + 2)` it shares with each neighbour, without `g m_i`.
+  2. Halo sum. Each rank exports its partial (m, p, f) on those planes and posts the neighbour
+     send/recv. While the bands travel, `mpm_step_grid_interior` updates every other node (sum,
+     `g m_i`, momentum, corrections). Then each rank adds the neighbour's partial in a fixed
+     order, lower rank's partial first, so both owners hold bit-identical nodes.
+  3. Finish. Each rank calls `mpm_step_finish_local`: the band nodes get `g m_i`, the momentum
+     update and the boundary corrections; then G2P and the constitutive update.
   4. Migration. A particle whose new base cell left the slab is exported from G2P and vacated
      from its slot. It is then appended by the receiving neighbour, in particle-id order.
 
@@ -124,9 +125,11 @@ class SlabDomain:
     plan: SlabPlan
 
     def p2g(self) -> None: ...
+    def grid_interior(self) -> None: ...    # grid update of the nodes off the halo bands
     def halo_export(self, plane_lo: int, n_planes: int, side: int): ...
     def halo_import(self, plane_lo: int, n_planes: int, buf, mode: int) -> None: ...
-    def finish(self, nan_guard: bool): ...   # -> (n_lo, n_hi) particles leaving toward -x / +x
+    def finish_async(self, nan_guard: bool): ...  # -> int64[3] (failed, n_lo, n_hi), may be on device
+    def commit(self, n_lo: int, n_hi: int, any_failed: bool) -> None: ...  # raises this rank's error
     def migrate_export(self): ...            # -> (lo_recs, lo_pids, hi_recs, hi_pids)
     def migrate_import(self, recs, pids) -> None: ...
     def local_count(self) -> int: ...
@@ -152,9 +155,19 @@ class LocalTransport:
             out[r] = (from_lo, from_hi)
         return out
 
+    def start(self, sends: dict, domains: dict, kind: str, report: dict | None = None):
+        return self.exchange(sends, domains, kind, report)
+
+    def wait(self, handle) -> dict:
+        return handle
+
     def report(self, local: dict, n_ranks: int) -> dict:
-        """local[r] = (failed, n_lo, n_hi) -> the same for every rank"""
-        return dict(local)
+        """local[r] = int64 tensor (failed, n_lo, n_hi) or None (failed) -> tuples for every rank"""
+        out = {}
+        for r, t in local.items():
+            f, lo, hi = (1, 0, 0) if t is None else [int(v) for v in t.tolist()]
+            out[r] = (bool(f), lo, hi)
+        return out
 
 
 class TorchTransport:
@@ -168,7 +181,7 @@ class TorchTransport:
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
 
-    def exchange(self, sends: dict, domains: dict, kind: str, report: dict | None = None) -> dict:
+    def _post(self, sends: dict, domains: dict, kind: str, report: dict | None = None):
         """One rank per process: sends[r] = (to_lo, to_hi); migration sizes come from `report`."""
         dist = self.dist
         r = self.rank
@@ -193,16 +206,28 @@ class TorchTransport:
                 recs, pids = d.empty_records(k)
                 recv[peer] = (recs, pids)
                 ops += [dist.P2POp(dist.irecv, recs, peer, self.group), dist.P2POp(dist.irecv, pids, peer, self.group)]
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()  # NCCL: orders the current stream (the library's); gloo: blocks the host
-        return {r: (recv.get(lo_peer), recv.get(hi_peer))}
+        works = dist.batch_isend_irecv(ops) if ops else []
+        return works, {r: (recv.get(lo_peer), recv.get(hi_peer))}
+
+    def start(self, sends: dict, domains: dict, kind: str, report: dict | None = None):
+        """post the neighbour sends/receives; the caller may enqueue independent work before wait()"""
+        return self._post(sends, domains, kind, report)
+
+    def wait(self, handle) -> dict:
+        works, recv = handle
+        for w in works:
+            w.wait()  # NCCL: orders the current stream (the library's); gloo: blocks the host
+        return recv
+
+    def exchange(self, sends: dict, domains: dict, kind: str, report: dict | None = None) -> dict:
+        return self.wait(self.start(sends, domains, kind, report))
 
     def report(self, local: dict, n_ranks: int) -> dict:
         import torch
 
-        (r, (failed, n_lo, n_hi)), = local.items()
-        mine = torch.tensor([int(failed), int(n_lo), int(n_hi)], dtype=torch.int64, device=self._dev)
+        (r, mine), = local.items()
+        if mine is None:
+            mine = torch.tensor([1, 0, 0], dtype=torch.int64, device=self._dev)
         allr = torch.empty(self.size * 3, dtype=torch.int64, device=self._dev)
         self.dist.all_gather_into_tensor(allr, mine, group=self.group)
         rows = allr.view(self.size, 3).cpu().tolist()  # the one host synchronisation of the exchange
@@ -247,7 +272,7 @@ class SlabStepper:
         doms = self.domains
         n_ranks = next(iter(doms.values())).plan.n_ranks
         errs: dict = {}
-        counts: dict = {}
+        reps: dict = {}
         for r, d in doms.items():
             try:
                 d.p2g()
@@ -260,7 +285,11 @@ class SlabStepper:
             to_lo = d.halo_export(p.lo(r), 2, 0) if r > 0 else None
             to_hi = d.halo_export(p.hi(r), 2, 1) if r + 1 < n_ranks else None
             sends[r] = (to_lo, to_hi)
-        recv = self.transport.exchange(sends, doms, "halo")
+        pending = self.transport.start(sends, doms, "halo")
+        for r, d in doms.items():  # nodes off the bands, while the bands travel
+            if r not in errs:
+                d.grid_interior()
+        recv = self.transport.wait(pending)
         for r, d in doms.items():
             from_lo, from_hi = recv[r]
             p = d.plan
@@ -269,16 +298,24 @@ class SlabStepper:
             if from_hi is not None:
                 d.halo_import(p.hi(r), 2, from_hi, 2)  # own partial first
             if r in errs:
-                counts[r] = (0, 0)
+                reps[r] = None
                 continue
             try:
-                counts[r] = d.finish(nan_guard)
+                reps[r] = d.finish_async(nan_guard)  # (failed, n_lo, n_hi), written behind G2P
             except MPMError as e:
                 errs[r] = e
-                counts[r] = (0, 0)
-        # one gather of (failed, n_lo, n_hi) from every rank
-        rep = self.transport.report({r: (r in errs, *counts[r]) for r in doms}, n_ranks)
-        if any(v[0] for v in rep.values()):
+                reps[r] = None
+        # one gather of (failed, n_lo, n_hi) from every rank: the step's only host synchronisation
+        rep = self.transport.report(reps, n_ranks)
+        any_failed = any(v[0] for v in rep.values())
+        for r, d in doms.items():
+            if r in errs:
+                continue
+            try:
+                d.commit(rep[r][1], rep[r][2], any_failed)  # raises this rank's own error
+            except MPMError as e:
+                errs[r] = e
+        if any_failed:
             for r in doms:
                 if r in errs:
                     raise errs[r]
@@ -363,6 +400,8 @@ class GpuSlabDomain(SlabDomain):
             self._mig = [(torch.empty((self.mig_cap, self.rec), dtype=self.tdtype, device=self.device),
                           torch.empty(self.mig_cap, dtype=torch.int32, device=self.device)) for _ in range(2)]
         self._counts = (0, 0)
+        with torch.cuda.stream(self.stream):
+            self._rep = torch.zeros(3, dtype=torch.int64, device=self.device)
         self._template = sub
         self._flags = capi
 
@@ -380,6 +419,9 @@ class GpuSlabDomain(SlabDomain):
     def p2g(self):
         self.ctx.check(self.lib.mpm_step_p2g_local(self.h))
 
+    def grid_interior(self):
+        self.ctx.check(self.lib.mpm_step_grid_interior(self.h))
+
     def halo_export(self, plane_lo, n_planes, side):
         buf = self._halo[side]
         self.ctx.check(self.lib.mpm_halo(self.h, int(plane_lo), int(n_planes), C.c_void_p(buf.data_ptr()), 0))
@@ -390,11 +432,21 @@ class GpuSlabDomain(SlabDomain):
         self.ctx.check(self.lib.mpm_halo(self.h, int(plane_lo), int(n_planes), C.c_void_p(buf.data_ptr()), int(mode)))
 
     def finish(self, nan_guard):
+        """synchronous form (status read here); the stepper uses finish_async + commit"""
         self.ctx.check(self.lib.mpm_step_finish_local(self.h, self._flags.MPM_ADV_NAN_GUARD if nan_guard else 0))
         nlo, nhi = C.c_int64(), C.c_int64()
         self.ctx.check(self.lib.mpm_migrate_counts(self.h, C.byref(nlo), C.byref(nhi)))
         self._counts = (nlo.value, nhi.value)
         return self._counts
+
+    def finish_async(self, nan_guard):
+        self.ctx.check(self.lib.mpm_step_finish_async(self.h, self._flags.MPM_ADV_NAN_GUARD if nan_guard else 0,
+                                                      C.c_void_p(self._rep.data_ptr())))
+        return self._rep
+
+    def commit(self, n_lo, n_hi, any_failed):
+        self.ctx.check(self.lib.mpm_step_commit(self.h, int(n_lo), int(n_hi), int(bool(any_failed))))
+        self._counts = (int(n_lo), int(n_hi))
 
     def migrate_export(self):
         (lr, lp), (hr, hp) = self._mig

@@ -38,6 +38,9 @@ class OracleSlabDomain(SlabDomain):
         else:
             self.grid = self.orc.new_grid(self.scene)
 
+    def grid_interior(self):
+        pass  # the oracle's p2g already formed the whole grid; nothing to overlap
+
     def _band(self, plane_lo, n_planes):
         return slice(plane_lo * self.per, (plane_lo + n_planes) * self.per)
 
@@ -77,6 +80,19 @@ class OracleSlabDomain(SlabDomain):
         self._lo_idx = np.nonzero(bx < self.plan.lo(self.rank))[0]
         self._hi_idx = np.nonzero(bx >= self.plan.hi(self.rank))[0]
         return len(self._lo_idx), len(self._hi_idx)
+
+    def finish_async(self, nan_guard):
+        self._err = None
+        try:
+            lo, hi = self.finish(nan_guard)
+            return torch.tensor([0, lo, hi], dtype=torch.int64)
+        except Exception as e:  # reported through the gather, raised by commit
+            self._err = e
+            return torch.tensor([1, 0, 0], dtype=torch.int64)
+
+    def commit(self, n_lo, n_hi, any_failed):
+        if any_failed and self._err is not None:
+            raise self._err
 
     # ---- migration ---------------------------------------------------------------------------
     def _pack(self, idx):

@@ -23,7 +23,7 @@ for tr in (TorchTransport(), LocalTransport()):
     stp = SlabStepper([dom], tr)
     stp.advance(5)
     T = {}
-    orig = {k: getattr(dom, k) for k in ("p2g", "finish", "migrate_export", "migrate_import")}
+    orig = {k: getattr(dom, k) for k in ("p2g", "grid_interior", "finish_async", "commit", "migrate_export", "migrate_import")}
     def wrap(k):
         f = orig[k]
         def g(*a, **kw):
