@@ -252,6 +252,19 @@ int mpm_step_finish_local(mpm_ctx* ctx, uint32_t flags);
  * mpm_step_commit with the counts and whether any rank failed (raises this rank's own error) */
 int mpm_step_finish_async(mpm_ctx* ctx, uint32_t flags, int64_t* dev_report);
 int mpm_step_commit(mpm_ctx* ctx, int64_t n_lo, int64_t n_hi, int any_failed);
+/* step_vjp over a slab (adjoint.hpp:328-525 decomposed). The state (this rank's particles at step t,
+ * uploaded with mpm_state_upload in the same order as cot_out) and per step:
+ *   mpm_slab_vjp_begin (forward replay: P2G + band sums) -> mpm_halo export/exchange/import ->
+ *   mpm_slab_vjp_interior -> mpm_slab_vjp_scatter (band finish, G2P transpose and its scatter,
+ *   band sums of the node v / v_old cotangents) -> mpm_halo_cot export/exchange/import (2 dim
+ *   values per node) -> mpm_slab_vjp_finish (grid VJP, P2G transpose; cot_in overwritten, pg =
+ *   this rank's partial ParamGrads, which the caller sums over the ranks). */
+int mpm_slab_vjp_begin(mpm_ctx* ctx, const mpm_cot_view* cot_out);
+int mpm_slab_vjp_interior(mpm_ctx* ctx);
+int mpm_slab_vjp_scatter(mpm_ctx* ctx);
+int mpm_halo_cot(mpm_ctx* ctx, int plane_lo, int n_planes, void* dev_buf, int mode);
+int mpm_slab_vjp_finish(mpm_ctx* ctx, mpm_cot_view* cot_in, mpm_param_grads* pg);
+
 /* particles that left the slab during the last step, toward -x (lo) and +x (hi) */
 int mpm_particle_record_size(const mpm_ctx* ctx);
 /* host-side counts of the last mpm_step_finish_local (known after it returns) */

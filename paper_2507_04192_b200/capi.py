@@ -185,6 +185,11 @@ _PROTOS = {
     "mpm_local_count": (C.c_int64, [C.c_void_p]),
     "mpm_step_p2g_local": (C.c_int, [C.c_void_p]),
     "mpm_step_grid_interior": (C.c_int, [C.c_void_p]),
+    "mpm_slab_vjp_begin": (C.c_int, [C.c_void_p, C.POINTER(CotView)]),
+    "mpm_slab_vjp_interior": (C.c_int, [C.c_void_p]),
+    "mpm_slab_vjp_scatter": (C.c_int, [C.c_void_p]),
+    "mpm_halo_cot": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int]),
+    "mpm_slab_vjp_finish": (C.c_int, [C.c_void_p, C.POINTER(CotView), C.POINTER(ParamGradsView)]),
     "mpm_halo": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int]),
     "mpm_step_finish_local": (C.c_int, [C.c_void_p, C.c_uint32]),
     "mpm_step_finish_async": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),

@@ -80,6 +80,11 @@ struct CtxBase {
     virtual void slab_set(int lo, int hi, int64_t mig_cap) = 0;
     virtual void step_p2g_local() = 0;
     virtual void step_grid_interior() = 0;
+    virtual void slab_vjp_begin(const mpm_cot_view* co) = 0;
+    virtual void slab_vjp_interior() = 0;
+    virtual void slab_vjp_scatter() = 0;
+    virtual void halo_cot(int plane_lo, int n_planes, void* dev_buf, int mode) = 0;
+    virtual void slab_vjp_finish(mpm_cot_view* ci, mpm_param_grads* pg) = 0;
     virtual void halo(int plane_lo, int n_planes, void* dev_buf, int mode) = 0;
     virtual void step_finish_local(uint32_t flags) = 0;
     virtual void step_finish_async(uint32_t flags, long long* dev_report) = 0;
@@ -619,7 +624,7 @@ template <class T, int D> struct Ctx : CtxBase {
 
     void upload_ids(const mpm_state_view* s, const int64_t* ids) override
     {
-        if (s->n < (ids ? 0 : 1) || s->n > cap)
+        if (s->n < ((ids || slab) ? 0 : 1) || s->n > cap) // a slab may hold no particles
             throw ApiError(MPM_ERR_USAGE, "state size " + std::to_string(s->n) + " outside [1, " + std::to_string(cap) + "]");
         if (s->n > 0 && (!s->x || !s->v || !s->mass || !s->volume || !s->rho || !s->sigma))
             throw ApiError(MPM_ERR_USAGE, "state view missing required fields");
@@ -990,6 +995,20 @@ template <class T, int D> struct Ctx : CtxBase {
     // every node off the halo bands: the fused sum + g m + momentum + corrections, enqueued while
     // the bands travel (the transport overlaps it)
     void step_grid_interior() override { grid_kernel<G_INTERIOR | G_SUM | G_MOM | G_CORR>(); }
+    // step_vjp over a slab (same exchange points as the forward step, plus the node cotangents)
+    void slab_vjp_begin(const mpm_cot_view* co) override
+    {
+        if (!slab)
+            throw ApiError(MPM_ERR_USAGE, "mpm_slab_vjp_begin needs mpm_slab_set first");
+        aw.slab_vjp_begin(*this, co);
+    }
+    void slab_vjp_interior() override { aw.slab_vjp_interior(*this); }
+    void slab_vjp_scatter() override { aw.slab_vjp_scatter(*this); }
+    void halo_cot(int plane_lo, int n_planes, void* dev_buf, int mode) override
+    {
+        halo_fields(aw.cot_halo_fields(), plane_lo, n_planes, dev_buf, mode);
+    }
+    void slab_vjp_finish(mpm_cot_view* ci, mpm_param_grads* pg) override { aw.slab_vjp_finish(*this, ci, pg); }
     void step_p2g_local() override
     {
         if (status_dirty) {
@@ -1013,11 +1032,22 @@ template <class T, int D> struct Ctx : CtxBase {
     }
     void halo(int plane_lo, int n_planes, void* dev_buf, int mode) override
     {
+        HaloFields<T> H{};
+        H.nf = 1 + 2 * D;
+        H.f[0] = G.m;
+        for (int a = 0; a < D; ++a) {
+            H.f[1 + a] = G.p[a];
+            H.f[1 + D + a] = G.f[a];
+        }
+        halo_fields(H, plane_lo, n_planes, dev_buf, mode);
+    }
+    void halo_fields(const HaloFields<T>& H, int plane_lo, int n_planes, void* dev_buf, int mode)
+    {
         int64_t per = n_planes;
         for (int a = 1; a < D; ++a)
             per *= sc.cells[a] + 1;
         launch("k_halo", [&] {
-            k_halo<T, D><<<grid_for(per, 256), 256, 0, stream>>>(G, nflag, d_nnb, d_cells, plane_lo, n_planes,
+            k_halo<T, D><<<grid_for(per, 256), 256, 0, stream>>>(H, nflag, d_nnb, d_cells, plane_lo, n_planes,
                                                                  static_cast<T*>(dev_buf), mode);
         }); // stream-ordered: the caller's transport runs on the same stream (mpm_ctx_set_stream)
     }
@@ -1524,6 +1554,17 @@ int mpm_state_download_local(mpm_ctx* c, mpm_state_view* s, int64_t* ids) { MPM_
 int mpm_slab_set(mpm_ctx* c, int cell_lo, int cell_hi, int64_t mig_cap) { MPM_CALL(c, c->impl->slab_set(cell_lo, cell_hi, mig_cap)); }
 int mpm_step_p2g_local(mpm_ctx* c) { MPM_CALL(c, c->impl->step_p2g_local()); }
 int mpm_step_grid_interior(mpm_ctx* c) { MPM_CALL(c, c->impl->step_grid_interior()); }
+int mpm_slab_vjp_begin(mpm_ctx* c, const mpm_cot_view* cot_out) { MPM_CALL(c, c->impl->slab_vjp_begin(cot_out)); }
+int mpm_slab_vjp_interior(mpm_ctx* c) { MPM_CALL(c, c->impl->slab_vjp_interior()); }
+int mpm_slab_vjp_scatter(mpm_ctx* c) { MPM_CALL(c, c->impl->slab_vjp_scatter()); }
+int mpm_halo_cot(mpm_ctx* c, int plane_lo, int n_planes, void* dev_buf, int mode)
+{
+    MPM_CALL(c, c->impl->halo_cot(plane_lo, n_planes, dev_buf, mode));
+}
+int mpm_slab_vjp_finish(mpm_ctx* c, mpm_cot_view* cot_in, mpm_param_grads* pg)
+{
+    MPM_CALL(c, c->impl->slab_vjp_finish(cot_in, pg));
+}
 int mpm_halo(mpm_ctx* c, int plane_lo, int n_planes, void* dev_buf, int mode) { MPM_CALL(c, c->impl->halo(plane_lo, n_planes, dev_buf, mode)); }
 int mpm_step_finish_local(mpm_ctx* c, uint32_t flags) { MPM_CALL(c, c->impl->step_finish_local(flags)); }
 int mpm_step_finish_async(mpm_ctx* c, uint32_t flags, int64_t* dev_report)

@@ -960,7 +960,13 @@ __device__ __forceinline__ void corr_vjp_chain(const DevScene<T, D>& sc, const i
     }
 }
 
-template <class T, int D>
+// MODE (slab decomposition): ADJ_FULL every node; ADJ_BAND_SUM halo-band nodes only, partial
+// sums of the v / v_old cotangents parked in GC.gmom / GC.gf for the exchange; ADJ_INTERIOR the
+// other nodes; ADJ_BAND_LOAD band nodes from the exchanged sums. Friction gradients count only
+// nodes this rank owns (x in [slab_lo, slab_hi)), so a band node is not counted twice.
+enum AdjGridMode { ADJ_FULL = 0, ADJ_BAND_SUM = 1, ADJ_INTERIOR = 2, ADJ_BAND_LOAD = 3 };
+
+template <class T, int D, int MODE = ADJ_FULL>
 __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf<T, D> G, GCBuf<T, D> GC,
                                                          const T* __restrict__ partials, const int* __restrict__ bstart,
                                                          const int* __restrict__ act, const int* __restrict__ n_act,
@@ -989,19 +995,42 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf
         const int q = act[wq];
         int qc[D], n[D];
         block_coords<D>(q, sc.nnb, qc);
+        if constexpr (MODE == ADJ_BAND_SUM || MODE == ADJ_BAND_LOAD) { // block-uniform skip
+            const int x0 = qc[0] * C::B;
+            if (!((sc.band_lo + 1 >= x0 && sc.band_lo < x0 + C::B) || (sc.band_hi + 1 >= x0 && sc.band_hi < x0 + C::B)))
+                continue;
+        }
         bool inside = true;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
             n[a] = qc[a] * C::B + lc[a];
             inside &= n[a] <= sc.cells[a];
         }
+        const bool band = in_band<T, D>(sc, n[0]);
+        const bool mine = MODE == ADJ_FULL || ((MODE == ADJ_INTERIOR) ? !band : band);
+        const bool owned = n[0] >= sc.slab_lo && (n[0] < sc.slab_hi || sc.slab_hi >= sc.cells[0]);
+        if constexpr (MODE == ADJ_BAND_SUM) { // no block reductions in this mode: per-thread skip
+            if (!mine)
+                continue;
+        }
         const size_t gi = (size_t)q * C::NB + tid;
         T gv[D], gvo[D];
 #pragma unroll
         for (int a = 0; a < D; ++a)
             gv[a] = gvo[a] = T(0);
+        if constexpr (MODE == ADJ_BAND_LOAD) {
+            if (mine) {
 #pragma unroll
-        for (int s = 0; s < (1 << D); ++s) {
+                for (int a = 0; a < D; ++a) {
+                    gv[a] = GC.gmom[a][gi];
+                    gvo[a] = GC.gf[a][gi];
+                }
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < (MODE == ADJ_BAND_LOAD ? 0 : (1 << D)); ++s) {
+            if (!mine)
+                break;
             int Qid = 0, colx = 0, z = 0;
             bool ok = true;
 #pragma unroll
@@ -1025,6 +1054,14 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf
                 gvo[a] += part[(D + a) * C::TN];
             }
         }
+        if constexpr (MODE == ADJ_BAND_SUM) { // park the partial sums for the halo exchange
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                GC.gmom[a][gi] = gv[a];
+                GC.gf[a][gi] = gvo[a];
+            }
+            continue;
+        }
         const T m = G.m[gi];
         T fr_acc[MAX_FRIC];
         for (int k = 0; k < nfr; ++k)
@@ -1033,7 +1070,7 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf
 #pragma unroll
         for (int a = 0; a < D; ++a)
             gmom[a] = gf[a] = T(0);
-        if (inside && m > sc.mass_eps) {
+        if (mine && inside && m > sc.mass_eps) {
             T p[D], f[D], vt[D];
 #pragma unroll
             for (int a = 0; a < D; ++a) {
@@ -1061,17 +1098,27 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf
             }
             gm = -(pu) / (m * m) - sc.dt * (fv) / (m * m);
         }
-        GC.gm[gi] = gm;
+        if (mine) {
+            GC.gm[gi] = gm;
 #pragma unroll
-        for (int a = 0; a < D; ++a) {
-            GC.gmom[a][gi] = gmom[a];
-            GC.gf[a][gi] = gf[a];
+            for (int a = 0; a < D; ++a) {
+                GC.gmom[a][gi] = gmom[a];
+                GC.gf[a][gi] = gf[a];
+            }
         }
-        // friction gradient partials per node block (fixed-order tree)
+        if (!owned)
+            for (int k = 0; k < nfr; ++k)
+                fr_acc[k] = T(0);
+        // friction gradient partials per node block (fixed-order tree); the band pass adds to the
+        // interior pass's value of the same block
         for (int k = 0; k < nfr; ++k) {
             const T s = block_sum_fixed<T, C::NB>(fr_acc[k], red);
-            if (tid == 0)
-                fr_block[(size_t)q * MAX_FRIC + k] = s;
+            if (tid == 0) {
+                if constexpr (MODE == ADJ_BAND_LOAD)
+                    fr_block[(size_t)q * MAX_FRIC + k] += s;
+                else
+                    fr_block[(size_t)q * MAX_FRIC + k] = s;
+            }
         }
     }
 }
@@ -1661,9 +1708,71 @@ template <class T, int D> struct AdjWork {
         c.sort_and_segment();
         c.p2g_kernel();
         c.template grid_kernel<G_SUM | G_MOM | G_CORR | G_STORE>();
+        k5(c, bo, bi);
+        c.launch("k_adj_grid", [&] {
+            k_adj_grid<T, D><<<c.persistent(4), C::NB, 0, c.stream>>>(c.sc, c.G, gc, partials, c.bstart, c.act,
+                                                                      c.counts + 1, fr_block, c.st);
+        });
+        k7(c, bi);
+    }
+
+    // ---- slab decomposition of step_vjp (SURVEY §8e adjoint row): the forward replay and the
+    // node-cotangent sum each exchange the 2 halo planes with the x-neighbours
+    template <class Ctx> void slab_vjp_begin(Ctx& c, const mpm_cot_view* co)
+    {
+        ensure(c);
+        cot_upload(c, co, 0);
+        pg_reset(c, nullptr); // this rank's partial; the caller sums the ranks
+        c.reset_status();
+        c.sort_and_segment();
+        c.p2g_kernel();
+        c.template grid_kernel<G_BANDONLY | G_SUM | G_NOGRAV | G_STORE>();
+    }
+    template <class Ctx> void slab_vjp_interior(Ctx& c)
+    {
+        c.template grid_kernel<G_INTERIOR | G_SUM | G_MOM | G_CORR | G_STORE>();
+    }
+    template <class Ctx> void slab_vjp_scatter(Ctx& c)
+    {
+        c.template grid_kernel<G_BANDONLY | G_GRAV | G_ZEROV | G_MOM | G_CORR | G_STORE>();
+        k5(c, 0, 1);
+        c.launch("k_adj_grid", [&] {
+            k_adj_grid<T, D, ADJ_BAND_SUM><<<c.persistent(4), C::NB, 0, c.stream>>>(
+                c.sc, c.G, gc, partials, c.bstart, c.act, c.counts + 1, fr_block, c.st);
+        });
+    }
+    HaloFields<T> cot_halo_fields() const
+    {
+        HaloFields<T> H{};
+        H.nf = 2 * D;
+        for (int a = 0; a < D; ++a) {
+            H.f[a] = gc.gmom[a]; // v cotangent partial sums (parked)
+            H.f[D + a] = gc.gf[a]; // v_old cotangent partial sums (parked)
+        }
+        return H;
+    }
+    template <class Ctx> void slab_vjp_finish(Ctx& c, mpm_cot_view* ci, mpm_param_grads* pg)
+    {
+        c.launch("k_adj_grid", [&] {
+            k_adj_grid<T, D, ADJ_INTERIOR><<<c.persistent(4), C::NB, 0, c.stream>>>(
+                c.sc, c.G, gc, partials, c.bstart, c.act, c.counts + 1, fr_block, c.st);
+        });
+        c.launch("k_adj_grid", [&] {
+            k_adj_grid<T, D, ADJ_BAND_LOAD><<<c.persistent(4), C::NB, 0, c.stream>>>(
+                c.sc, c.G, gc, partials, c.bstart, c.act, c.counts + 1, fr_block, c.st);
+        });
+        k7(c, 1);
+        c.check_status(c.step);
+        cot_download(c, ci, 1);
+        pg_download(c, pg);
+    }
+
+    // K5a gather + constitutive VJP, K5b scatter of the v / v_old cotangents into partial tiles
+    template <class Ctx> void k5(Ctx& c, int bo, int bi)
+    {
         auto& Pin = c.buf[c.cur];
         const unsigned gr = c.persistent(4);
-        const size_t sm5 = sizeof(T) * 2 * D * C::TN, sm7 = sizeof(T) * (1 + 2 * D) * C::TN;
+        const size_t sm5 = sizeof(T) * 2 * D * C::TN;
         if (c.has_aff)
             c.launch("k_adj_g2pT_gather", [&] {
                 k_adj_g2pT_gather<T, D, true><<<gr, 256, sm5, c.stream>>>(c.sc, Pin, c.G, c.perm, c.bstart, c.bend,
@@ -1689,10 +1798,14 @@ template <class T, int D> struct AdjWork {
                                                                                   c.bstart, c.bend, c.occ, c.counts,
                                                                                   partials, c.st);
             });
-        c.launch("k_adj_grid", [&] {
-            k_adj_grid<T, D><<<c.persistent(4), C::NB, 0, c.stream>>>(c.sc, c.G, gc, partials, c.bstart, c.act,
-                                                                      c.counts + 1, fr_block, c.st);
-        });
+    }
+
+    // K7 P2G-transpose gather into the particle cotangents, then the fixed-order ParamGrads reduce
+    template <class Ctx> void k7(Ctx& c, int bi)
+    {
+        auto& Pin = c.buf[c.cur];
+        const unsigned gr = c.persistent(4);
+        const size_t sm7 = sizeof(T) * (1 + 2 * D) * C::TN;
         const bool aff = c.has_aff || c.sc.tpic;
         if (aff)
             c.launch("k_adj_p2gT", [&] {

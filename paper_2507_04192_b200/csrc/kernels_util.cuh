@@ -101,15 +101,20 @@ __global__ void k_mig_unpack(PBuf<T, D> P, int base, int n, const T* __restrict_
     P.pid[i] = pids[r];
 }
 
-// halo planes of the stored grid: node x-planes [p0, p0 + np) x all (y[, z]) nodes, NF fields
-// (m, p, f); export writes zeros for inactive node blocks; import adds into active blocks only,
-// in a fixed order (received + own, or own + received) so both owners of a band agree bitwise.
+// halo planes of a set of node fields: node x-planes [p0, p0 + np) x all (y[, z]) nodes, nf values
+// per node (forward: m, p, f; adjoint: the v and v_old cotangents). Export writes zeros for
+// inactive node blocks; import adds into active blocks only, in a fixed order (received + own, or
+// own + received) so both owners of a band agree bitwise.
+template <class T> struct HaloFields {
+    T* f[7];
+    int nf;
+};
+
 template <class T, int D>
-__global__ void k_halo(GBuf<T, D> G, const unsigned char* __restrict__ nflag, const int* __restrict__ nnb,
+__global__ void k_halo(HaloFields<T> H, const unsigned char* __restrict__ nflag, const int* __restrict__ nnb,
                        const int* __restrict__ cells, int p0, int np, T* __restrict__ buf, int mode)
 {
     using C = Cfg<D>;
-    constexpr int NF = 1 + 2 * D;
     long long per = 1;
     for (int a = 1; a < D; ++a)
         per *= cells[a] + 1;
@@ -132,19 +137,13 @@ __global__ void k_halo(GBuf<T, D> G, const unsigned char* __restrict__ nflag, co
     }
     ok = ok && nflag[q];
     const size_t gi = (size_t)q * C::NB + loc;
-    T* b = buf + (size_t)t * NF;
-    T* fld[NF];
-    fld[0] = G.m;
-    for (int a = 0; a < D; ++a) {
-        fld[1 + a] = G.p[a];
-        fld[1 + D + a] = G.f[a];
-    }
+    T* b = buf + (size_t)t * H.nf;
     if (mode == 0) {
-        for (int f = 0; f < NF; ++f)
-            b[f] = ok ? fld[f][gi] : T(0);
+        for (int f = 0; f < H.nf; ++f)
+            b[f] = ok ? H.f[f][gi] : T(0);
     } else if (ok) {
-        for (int f = 0; f < NF; ++f)
-            fld[f][gi] = mode == 1 ? b[f] + fld[f][gi] : fld[f][gi] + b[f];
+        for (int f = 0; f < H.nf; ++f)
+            H.f[f][gi] = mode == 1 ? b[f] + H.f[f][gi] : H.f[f][gi] + b[f];
     }
 }
 

@@ -161,6 +161,13 @@ class LocalTransport:
     def wait(self, handle) -> dict:
         return handle
 
+    def sum_ordered(self, local: dict) -> np.ndarray:
+        """sum of per-rank f64 vectors in rank order (deterministic ParamGrads reduction)"""
+        tot = None
+        for r in sorted(local):
+            tot = local[r].copy() if tot is None else tot + local[r]
+        return tot
+
     def report(self, local: dict, n_ranks: int) -> dict:
         """local[r] = int64 tensor (failed, n_lo, n_hi) or None (failed) -> tuples for every rank"""
         out = {}
@@ -193,8 +200,8 @@ class TorchTransport:
         for peer, out in ((lo_peer, to_lo), (hi_peer, to_hi)):
             if peer is None:
                 continue
-            if kind == "halo":
-                inc = d.empty_halo(2)
+            if kind in ("halo", "halo_cot"):
+                inc = d.empty_halo(2) if kind == "halo" else d.empty_halo_cot(2)
                 ops += [dist.P2POp(dist.isend, out, peer, self.group), dist.P2POp(dist.irecv, inc, peer, self.group)]
                 recv[peer] = inc
                 continue
@@ -232,6 +239,21 @@ class TorchTransport:
         self.dist.all_gather_into_tensor(allr, mine, group=self.group)
         rows = allr.view(self.size, 3).cpu().tolist()  # the one host synchronisation of the exchange
         return {q: (bool(rows[q][0]), rows[q][1], rows[q][2]) for q in range(self.size)}
+
+    def sum_ordered(self, local: dict) -> np.ndarray:
+        """all-gather of the per-rank f64 vectors, summed in rank order on every rank (a NCCL/gloo
+        all-reduce does not fix the summation order)"""
+        import torch
+
+        (r, vec), = local.items()
+        t = torch.as_tensor(np.ascontiguousarray(vec), dtype=torch.float64).to(self._dev)
+        allv = torch.empty(self.size * t.numel(), dtype=torch.float64, device=self._dev)
+        self.dist.all_gather_into_tensor(allv, t, group=self.group)
+        rows = allv.view(self.size, -1).cpu().numpy()
+        tot = rows[0].copy()
+        for q in range(1, self.size):
+            tot = tot + rows[q]
+        return tot
 
     _dev = "cpu"
 
@@ -464,6 +486,54 @@ class GpuSlabDomain(SlabDomain):
     def local_count(self) -> int:
         return int(self.lib.mpm_local_count(self.h))
 
+    # ---- step_vjp over the slab (adjoint.hpp:328-525 decomposed; include/mpm_capi.h) ----------
+    def empty_halo_cot(self, n_planes: int):
+        import torch
+
+        return torch.empty((n_planes * self.per, 2 * self.scene.dim), dtype=self.tdtype, device=self.device)
+
+    def vjp_begin(self, state: SimState, cot_out):
+        """state: this rank's particles at step t (replaces the context's state), cot_out the
+        cotangents of the same particles at t + 1, same order"""
+        v, keep = state.to_view()
+        self.ctx.check(self.lib.mpm_state_upload(self.h, C.byref(v)))
+        co, kco = cot_out.to_view()
+        self.ctx.check(self.lib.mpm_slab_vjp_begin(self.h, C.byref(co)))
+        self._vjp_state = state
+        if not hasattr(self, "_hcot"):
+            import torch
+
+            with torch.cuda.stream(self.stream):
+                self._hcot = [self.empty_halo_cot(2), self.empty_halo_cot(2)]
+
+    def vjp_interior(self):
+        self.ctx.check(self.lib.mpm_slab_vjp_interior(self.h))
+
+    def vjp_scatter(self):
+        self.ctx.check(self.lib.mpm_slab_vjp_scatter(self.h))
+
+    def halo_cot_export(self, plane_lo, n_planes, side):
+        buf = self._hcot[side]
+        self.ctx.check(self.lib.mpm_halo_cot(self.h, int(plane_lo), int(n_planes), C.c_void_p(buf.data_ptr()), 0))
+        return buf
+
+    def halo_cot_import(self, plane_lo, n_planes, buf, mode):
+        buf = buf.contiguous()
+        self.ctx.check(self.lib.mpm_halo_cot(self.h, int(plane_lo), int(n_planes), C.c_void_p(buf.data_ptr()),
+                                             int(mode)))
+
+    def vjp_finish(self):
+        from .state import ParamGrads, StateCotangent
+
+        cin = StateCotangent.zeros_like(self._vjp_state.particles)
+        ci, kci = cin.to_view()
+        pg = ParamGrads(self.scene.boundary)
+        pv = pg.to_view()
+        self.ctx.check(self.lib.mpm_slab_vjp_finish(self.h, C.byref(ci), C.byref(pv)))
+        cin.sync_from(kci)
+        pg.sync_from(pv)
+        return cin, pg
+
     def gather(self):
         k = self.local_count()
         p = self._template.particles
@@ -476,6 +546,58 @@ class GpuSlabDomain(SlabDomain):
 
     def close(self):
         self.ctx.close()
+
+
+def slab_step_vjp(domains: list, transport, states: dict, cot_outs: dict, pg) -> dict:
+    """step_vjp (adjoint.hpp:328-331) over the slab decomposition: states[r] / cot_outs[r] are rank
+    r's particles at step t and their cotangents at t + 1 (same order). Returns cot_in per rank
+    (overwritten semantics) and accumulates the ParamGrads of all ranks into pg, summed in rank
+    order. Two halo exchanges: the forward replay's (m, p, f) and the node (v, v_old) cotangents;
+    the interior grid replay overlaps the first."""
+    doms = {d.rank: d for d in domains}
+    stream = getattr(next(iter(doms.values())), "stream", None)
+    if stream is not None:
+        import torch
+
+        with torch.cuda.stream(stream):
+            return _slab_step_vjp(doms, transport, states, cot_outs, pg)
+    return _slab_step_vjp(doms, transport, states, cot_outs, pg)
+
+
+def _slab_step_vjp(doms, transport, states, cot_outs, pg):
+    n_ranks = next(iter(doms.values())).plan.n_ranks
+    for r, d in doms.items():
+        d.vjp_begin(states[r], cot_outs[r])
+
+    def exchange(export, imp, kind, overlap=None):
+        sends = {}
+        for r, d in doms.items():
+            p = d.plan
+            sends[r] = (export(d, p.lo(r), 0) if r > 0 else None, export(d, p.hi(r), 1) if r + 1 < n_ranks else None)
+        pending = transport.start(sends, doms, kind)
+        if overlap is not None:
+            for d in doms.values():
+                overlap(d)
+        recv = transport.wait(pending)
+        for r, d in doms.items():
+            from_lo, from_hi = recv[r]
+            if from_lo is not None:
+                imp(d, d.plan.lo(r), from_lo, 1)  # lower rank's partial first
+            if from_hi is not None:
+                imp(d, d.plan.hi(r), from_hi, 2)
+
+    exchange(lambda d, lo, side: d.halo_export(lo, 2, side), lambda d, lo, b, m: d.halo_import(lo, 2, b, m), "halo",
+             overlap=lambda d: d.vjp_interior())
+    for d in doms.values():
+        d.vjp_scatter()
+    exchange(lambda d, lo, side: d.halo_cot_export(lo, 2, side), lambda d, lo, b, m: d.halo_cot_import(lo, 2, b, m),
+             "halo_cot")
+    out, parts = {}, {}
+    for r, d in doms.items():
+        out[r], pr = d.vjp_finish()
+        parts[r] = pr.flat()
+    pg.add_flat(transport.sum_ordered(parts))
+    return out
 
 
 _STREAMS: dict = {}
@@ -503,4 +625,4 @@ def local_slab_run(scene: Scene, state: SimState, n_ranks: int, steps: int, nan_
 
 
 __all__ = ["SlabPlan", "SlabDomain", "SlabStepper", "LocalTransport", "TorchTransport", "GpuSlabDomain",
-           "PeerFailure", "local_slab_run", "block_edge", "base_cell_x"]
+           "PeerFailure", "local_slab_run", "slab_step_vjp", "block_edge", "base_cell_x"]

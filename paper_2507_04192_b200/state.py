@@ -187,6 +187,21 @@ class StateCotangent:
             setattr(c, f, None if a is None else a.copy())
         return c
 
+    def take(self, idx) -> "StateCotangent":
+        """rows idx (a rank's particles under the slab decomposition)"""
+        c = StateCotangent.__new__(StateCotangent)
+        c.dim = self.dim
+        for f in self.FIELDS:
+            a = getattr(self, f)
+            setattr(c, f, None if a is None else (a[idx] if a.shape[0] else a.copy()))
+        return c
+
+    def put(self, idx, other: "StateCotangent"):
+        for f in self.FIELDS:
+            a, b = getattr(self, f), getattr(other, f)
+            if a is not None and a.shape[0]:
+                a[idx] = b
+
     def axpy(self, a, o: "StateCotangent"):
         for f in self.FIELDS:
             x = getattr(self, f)
@@ -254,6 +269,18 @@ class ParamGrads:
     def sync_from(self, v):
         self.sound_speed = float(v.sound_speed)
         self.viscosity = float(v.viscosity)
+
+    def flat(self) -> np.ndarray:
+        """(c, mu, friction of every wall) as one f64 vector"""
+        return np.concatenate([[self.sound_speed, self.viscosity], *self.wall_friction]).astype(np.float64)
+
+    def add_flat(self, vec: np.ndarray):
+        self.sound_speed += float(vec[0])
+        self.viscosity += float(vec[1])
+        k = 2
+        for a in self.wall_friction:
+            a += vec[k:k + len(a)]
+            k += len(a)
 
 
 class Grid:

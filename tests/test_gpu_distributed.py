@@ -18,6 +18,7 @@ from paper_2507_04192_b200 import init_scene
 from paper_2507_04192_b200.distributed import (GpuSlabDomain, LocalTransport, SlabPlan, SlabStepper, local_slab_run)
 from paper_2507_04192_b200.errors import NumericalError
 from paper_2507_04192_b200.solver import Context
+from paper_2507_04192_b200.state import SimState
 
 from helpers import assert_state_close
 from test_distributed import moving_fluid_scene
@@ -118,3 +119,51 @@ def test_abort_stops_all_ranks_like_plain():
     assert type(slab_err.value) is type(plain_err.value) and str(slab_err.value) == str(plain_err.value)
     got = (stp.steps_done, doms[0].ctx.last_error_step(), doms[1].ctx.last_error_step())
     assert got[:2] == (plain_done, err_step), (got, plain_done, err_step)
+
+
+# ---- adjoint over slabs (SURVEY §8e adjoint row) -------------------------------------------------
+def coulomb_slide_scene(dim=2):
+    """the moving fluid on a segmented Coulomb floor: friction gradients on both sides of the slabs"""
+    from paper_2507_04192_b200.scene import Wall
+
+    s = moving_fluid_scene(dim)
+    s.boundary.walls[2] = Wall("coulomb", [0.2, 0.35, 0.5, 0.3])
+    g = s.geometry[0]
+    g.lo[1], g.hi[1] = 0.02, 0.02 + (g.hi[1] - g.lo[1])  # on the floor: nodes in the 2-layer friction band
+    return s
+
+
+@pytest.mark.parametrize("dim,R,coulomb", [(2, 2, False), (2, 3, True), (2, 4, True), (3, 2, True), (3, 4, False)])
+def test_slab_step_vjp_matches_single_context(dim, R, coulomb):
+    from paper_2507_04192_b200.distributed import slab_step_vjp
+    from paper_2507_04192_b200.state import ParamGrads
+
+    from test_gpu_adjoint import cot_errs, random_cot
+
+    s = coulomb_slide_scene(dim) if coulomb else moving_fluid_scene(dim)
+    st = plain_gpu(s, init_scene(s), 8 if dim == 2 else 4)  # a state with stress and a flow
+    cot = random_cot(st, 7)
+    ctx = Context(s, st.particles.size())
+    pg_ref = ParamGrads(s.boundary)
+    want = ctx.step_vjp(st, cot, pg_ref)
+    ctx.close()
+
+    plan = SlabPlan.make(s, R, st.particles.x)
+    ids = plan.partition(s, st)
+    doms = [GpuSlabDomain(s, plan, r, st, ids[r]) for r in range(R)]
+    pg = ParamGrads(s.boundary)
+    got_r = slab_step_vjp(doms, LocalTransport(), {r: SimState(st.particles.take(ids[r]), st.step, st.time)
+                                                   for r in range(R)},
+                          {r: cot.take(ids[r]) for r in range(R)}, pg)
+    got = want.copy()
+    for r in range(R):
+        got.put(ids[r], got_r[r])
+    # halo-node sums run in a different order than on one context: rounding-level differences,
+    # amplified in the x cotangent by the stencil Hessian terms (measured up to 1.1e-9)
+    errs = cot_errs(got, want)
+    assert all(v < 1e-8 for v in errs.values()), errs
+    assert abs(pg.sound_speed - pg_ref.sound_speed) <= 1e-8 * abs(pg_ref.sound_speed) + 1e-300
+    if coulomb:
+        a, b = pg.wall_friction[2], pg_ref.wall_friction[2]
+        assert np.abs(b).max() > 0
+        assert np.abs(a - b).max() <= 1e-8 * np.abs(b).max(), (a, b)
