@@ -161,6 +161,9 @@ class LocalTransport:
     def wait(self, handle) -> dict:
         return handle
 
+    def allgather_obj(self, local: dict) -> dict:
+        return dict(local)
+
     def sum_ordered(self, local: dict) -> np.ndarray:
         """sum of per-rank f64 vectors in rank order (deterministic ParamGrads reduction)"""
         tot = None
@@ -239,6 +242,12 @@ class TorchTransport:
         self.dist.all_gather_into_tensor(allr, mine, group=self.group)
         rows = allr.view(self.size, 3).cpu().tolist()  # the one host synchronisation of the exchange
         return {q: (bool(rows[q][0]), rows[q][1], rows[q][2]) for q in range(self.size)}
+
+    def allgather_obj(self, local: dict) -> dict:
+        (r, obj), = local.items()
+        out = [None] * self.size
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return {q: out[q] for q in range(self.size)}
 
     def sum_ordered(self, local: dict) -> np.ndarray:
         """all-gather of the per-rank f64 vectors, summed in rank order on every rank (a NCCL/gloo
@@ -486,6 +495,12 @@ class GpuSlabDomain(SlabDomain):
     def local_count(self) -> int:
         return int(self.lib.mpm_local_count(self.h))
 
+    def restore(self, particles: ParticleSoA, ids, step: int, time: float):
+        """load a checkpoint of this rank (its particles, their global ids, step, time)"""
+        v, keep = SimState(particles, step, time).to_view()
+        ids64 = np.ascontiguousarray(ids, dtype=np.int64)
+        self.ctx.check(self.lib.mpm_state_upload_ids(self.h, C.byref(v), ids64.ctypes.data_as(C.c_void_p)))
+
     # ---- step_vjp over the slab (adjoint.hpp:328-525 decomposed; include/mpm_capi.h) ----------
     def empty_halo_cot(self, n_planes: int):
         import torch
@@ -600,6 +615,109 @@ def _slab_step_vjp(doms, transport, states, cot_outs, pg):
     return out
 
 
+def _digest(particles: ParticleSoA, ids) -> int:
+    """order-independent content digest of a rank's particles (id-sorted bytes)"""
+    import hashlib
+
+    o = np.argsort(np.asarray(ids), kind="stable")
+    h = hashlib.sha256(np.asarray(ids)[o].tobytes())
+    for f in ("x", "v", "volume", "rho", "eps_eq", "sigma_zz", "sigma", "grad_v", "affine"):
+        a = getattr(particles, f)
+        if a is not None and a.size:
+            h.update(np.ascontiguousarray(a[o]).tobytes())
+    return int.from_bytes(h.digest()[:8], "little")
+
+
+def slab_backprop_trajectory(scene: Scene, plan, seeder, domains: list, transport, n_total: int):
+    """backprop_trajectory (checkpoint.hpp:72-143) over the slab decomposition.
+
+    The domains hold the initial state. Per rank, checkpoints are the rank's (particles, ids) at
+    segment starts. The replay of a segment is checked against the forward sweep's boundary
+    digest (checkpoint.hpp:124-126), and the reverse sweep runs slab_step_vjp. A rank's
+    cotangent rows at step t are those of its particles at t. Particles that migrated during the
+    step get their cotangent from an id-indexed assembly through the transport, which costs O(N)
+    host traffic per step; a neighbour-only exchange of the migrants' rows is the scalable form.
+    The seeder is evaluated per rank on global ids (LagrangianLeastSquares.loss_local / seed_local),
+    with loss terms summed in rank order. Returns a solver.BackpropResult with the global
+    initial-state cotangent.
+    """
+    from .errors import NumericalError as _NE
+    from .solver import BackpropResult
+    from .state import ParamGrads, StateCotangent
+
+    doms = {d.rank: d for d in domains}
+    stp = SlabStepper(domains, transport)
+
+    def gather():
+        return {r: d.gather() for r, d in doms.items()}
+
+    def loss_of(step, snap):
+        if not seeder.observes(step):
+            return 0.0
+        part = {r: np.array([seeder.loss_local(step, sub, ids)]) for r, (sub, ids, _) in snap.items()}
+        return float(transport.sum_ordered(part)[0])
+
+    # forward sweep: checkpoints at segment starts, digests at every boundary
+    nseg = plan.n_segments
+    snap = gather()
+    loss = loss_of(0, snap)
+    ckpt, bdig = [], []
+    for k in range(nseg):
+        ckpt.append(snap)
+        bdig.append({r: _digest(sub, ids) for r, (sub, ids, _) in snap.items()})
+        for t in range(plan.boundaries[k], plan.boundaries[k + 1]):
+            stp.step()
+            if seeder.observes(t + 1):
+                snap = gather()
+                loss += loss_of(t + 1, snap)
+        snap = gather()
+    bdig.append({r: _digest(sub, ids) for r, (sub, ids, _) in snap.items()})
+
+    # backward sweep (host-global cotangent rows by id)
+    template = next(iter(snap.values()))[0]
+    cot = StateCotangent(n_total, template.dim, template.dtype, template.affine is not None)
+    pg = ParamGrads(scene.boundary)
+    peak = 0
+
+    def seed(step, snap_t):
+        if not seeder.observes(step):
+            return
+        local = {}
+        for r, (sub, ids, _) in snap_t.items():
+            rows, dz = seeder.seed_local(step, sub, ids)
+            local[r] = (np.asarray(ids)[rows], dz)
+        for r in sorted(allg := transport.allgather_obj(local)):
+            gid, dz = allg[r]
+            tgt = cot.x if seeder.field == "x" else cot.v
+            tgt[gid] += dz
+
+    for k in range(nseg - 1, -1, -1):
+        b0, b1 = plan.boundaries[k], plan.boundaries[k + 1]
+        for r, d in doms.items():
+            sub, ids, (st, tm) = ckpt[k][r]
+            d.restore(sub, ids, st, tm)
+        replay = [ckpt[k]]
+        for _ in range(b0, b1):
+            stp.step()
+            replay.append(gather())
+        if {r: _digest(sub, ids) for r, (sub, ids, _) in replay[-1].items()} != bdig[k + 1]:
+            raise _NE(f"checkpoint mismatch: recomputed segment end differs from the recorded state at step {b1}")
+        peak = max(peak, len(replay))
+        for t in range(b1, b0, -1):
+            seed(t, replay[t - b0])
+            prev = replay[t - b0 - 1]
+            states = {r: SimState(sub, st, tm) for r, (sub, ids, (st, tm)) in prev.items()}
+            outs = {r: cot.take(np.asarray(ids)) for r, (sub, ids, _) in prev.items()}
+            cin = slab_step_vjp(domains, transport, states, outs, pg)
+            allg = transport.allgather_obj({r: (np.asarray(prev[r][1]), cin[r]) for r in cin})
+            cot = StateCotangent(n_total, template.dim, template.dtype, template.affine is not None)
+            for r in sorted(allg):
+                gid, c = allg[r]
+                cot.put(gid, c)
+    seed(0, ckpt[0])
+    return BackpropResult(cot, pg, loss, nseg, peak)
+
+
 _STREAMS: dict = {}
 
 
@@ -625,4 +743,4 @@ def local_slab_run(scene: Scene, state: SimState, n_ranks: int, steps: int, nan_
 
 
 __all__ = ["SlabPlan", "SlabDomain", "SlabStepper", "LocalTransport", "TorchTransport", "GpuSlabDomain",
-           "PeerFailure", "local_slab_run", "slab_step_vjp", "block_edge", "base_cell_x"]
+           "PeerFailure", "local_slab_run", "slab_step_vjp", "slab_backprop_trajectory", "block_edge", "base_cell_x"]

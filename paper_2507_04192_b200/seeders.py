@@ -23,6 +23,36 @@ class LagrangianLeastSquares:
     def desc(self) -> dict:
         return {"field": self.field, "obs_steps": self.obs_steps, "sel": self.sel, "target": self.target}
 
+    # ---- the same seeder on one rank's particles (slab decomposition; global ids) --------------
+    def observes(self, step: int) -> bool:
+        return int(step) in self.obs_steps
+
+    def _local(self, step, particles, ids):
+        k = self.obs_steps.index(int(step))
+        ids = np.asarray(ids, np.int64)
+        if self.sel is None:
+            rows, l = np.arange(len(ids)), ids
+        else:
+            if not hasattr(self, "_inv") or len(self._inv) <= (ids.max() if len(ids) else 0):
+                n = int(max(self.sel.max() + 1, (ids.max() + 1) if len(ids) else 0))
+                self._inv = np.full(n, -1, np.int64)
+                self._inv[self.sel] = np.arange(len(self.sel))
+            l = self._inv[ids] if len(ids) else ids
+            rows = np.nonzero(l >= 0)[0]
+            l = l[rows]
+        z = (particles.x if self.field == "x" else particles.v)[rows]
+        return rows, z - self.target[k][l]
+
+    def loss_local(self, step, particles, ids) -> float:
+        """this rank's share of loss_at (checkpoint.hpp:63-66)"""
+        _, r = self._local(step, particles, ids)
+        return float((r.astype(np.float64) ** 2).sum())
+
+    def seed_local(self, step, particles, ids):
+        """(rows, d z) of this rank's share of seed: cot.z[rows] += 2 (z - target)"""
+        rows, r = self._local(step, particles, ids)
+        return rows, 2 * r
+
 
 def make_seeder_desc(seeder: dict | None, T):
     sd = capi.SeederDesc()

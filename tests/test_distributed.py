@@ -174,3 +174,52 @@ def test_gloo_world2_matches_local_bitwise(orc, dim):
         ref = st.copy()
         orc.advance(s, ref, steps)
         assert_state_close(loc, ref, 1e-10)
+
+
+class _FakeDom:
+    def __init__(self, rank, per=5, dim=2):
+        self.rank, self.per, self.dim, self.device = rank, per, dim, torch.device("cpu")
+
+    def empty_halo(self, n):
+        return torch.empty((n * self.per, 1 + 2 * self.dim), dtype=torch.float64)
+
+    def empty_halo_cot(self, n):
+        return torch.empty((n * self.per, 2 * self.dim), dtype=torch.float64)
+
+
+def _gloo_adjoint_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tr = TorchTransport()
+        d = _FakeDom(rank)
+        mk = lambda v: torch.full((2 * d.per, 2 * d.dim), float(v), dtype=torch.float64)  # noqa: E731
+        sends = {rank: (mk(10 * rank + 1) if rank > 0 else None, mk(10 * rank + 2) if rank + 1 < world else None)}
+        recv = tr.exchange(sends, {rank: d}, "halo_cot")[rank]
+        tot = tr.sum_ordered({rank: np.array([0.1 * (rank + 1), 1e-17 * rank])})
+        objs = tr.allgather_obj({rank: ("ids", rank)})
+        res = {"from_lo": None if recv[0] is None else float(recv[0][0, 0]),
+               "from_hi": None if recv[1] is None else float(recv[1][0, 0]), "tot": tot.tolist(),
+               "objs": [objs[q][1] for q in range(world)]}
+        np.save(out_path + f".{rank}.npy", np.array([res], dtype=object), allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_adjoint_transport_primitives():
+    """the cotangent halo band, the rank-ordered ParamGrads sum and the object gather over gloo"""
+    world = 3
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "adj")
+        mp.start_processes(_gloo_adjoint_worker, args=(world, _free_port(), path), nprocs=world, join=True,
+                           start_method="spawn")
+        res = [np.load(path + f".{r}.npy", allow_pickle=True)[0] for r in range(world)]
+    for r in range(world):
+        assert res[r]["from_lo"] == (None if r == 0 else 10 * (r - 1) + 2)  # lower neighbour's upper band
+        assert res[r]["from_hi"] == (None if r == world - 1 else 10 * (r + 1) + 1)
+        assert res[r]["objs"] == list(range(world))
+        assert res[r]["tot"] == res[0]["tot"]  # identical bits on every rank
+    want = 0.1 * 1
+    for r in range(1, world):
+        want = want + 0.1 * (r + 1)  # rank order
+    assert res[0]["tot"][0] == want

@@ -167,3 +167,39 @@ def test_slab_step_vjp_matches_single_context(dim, R, coulomb):
         a, b = pg.wall_friction[2], pg_ref.wall_friction[2]
         assert np.abs(b).max() > 0
         assert np.abs(a - b).max() <= 1e-8 * np.abs(b).max(), (a, b)
+
+
+@pytest.mark.parametrize("dim,R,nseg", [(2, 2, 3), (2, 3, 1), (3, 2, 2)])
+def test_slab_backprop_matches_single_context(dim, R, nseg):
+    """backprop_trajectory over slabs vs the single-context device backprop: the initial-state
+    cotangent, the ParamGrads (incl. Coulomb friction) and the loss"""
+    from paper_2507_04192_b200.distributed import slab_backprop_trajectory
+    from paper_2507_04192_b200.seeders import LagrangianLeastSquares
+    from paper_2507_04192_b200.solver import CheckpointPlan
+
+    from test_gpu_adjoint import cot_errs
+
+    s = coulomb_slide_scene(dim)
+    st = init_scene(s)
+    N = 12 if dim == 2 else 6
+    n = st.particles.size()
+    mid, fin = plain_gpu(s, st, N // 2), plain_gpu(s, st, N)
+    rng = np.random.default_rng(3)
+    tgt = np.stack([mid.particles.x + 0.002 * rng.standard_normal(mid.particles.x.shape),
+                    fin.particles.x + 0.002 * rng.standard_normal(fin.particles.x.shape)])
+    seeder = LagrangianLeastSquares([N // 2, N], tgt, "x")
+    ctx = Context(s, n)
+    c0, pg_ref, res = ctx.backprop(st, N, nseg, seeder.desc())
+    ctx.close()
+
+    plan_s = SlabPlan.make(s, R, st.particles.x)
+    ids = plan_s.partition(s, st)
+    doms = [GpuSlabDomain(s, plan_s, r, st, ids[r]) for r in range(R)]
+    out = slab_backprop_trajectory(s, CheckpointPlan.make(N, nseg), seeder, doms, LocalTransport(), n)
+    assert out.loss == pytest.approx(res.loss, rel=1e-10)
+    errs = cot_errs(out.initial_state_cot, c0)
+    assert all(v < 1e-8 for v in errs.values()), errs
+    a, b = out.param_grads.wall_friction[2], pg_ref.wall_friction[2]
+    assert np.abs(b).max() > 0 and np.abs(a - b).max() <= 1e-8 * np.abs(b).max(), (a, b)
+    assert abs(out.param_grads.sound_speed - pg_ref.sound_speed) <= 1e-8 * abs(pg_ref.sound_speed)
+    assert out.checkpoints_stored == nseg
