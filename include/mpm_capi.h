@@ -141,8 +141,14 @@ typedef struct mpm_grid_view {
 /* Built-in loss seeders for backprop_trajectory (checkpoint.hpp:63-66 Seeder protocol):
  * masked Lagrangian least squares (SPEC.md observe_lagrangian + loss):
  *   L = sum_{k<n_obs} sum_{l<n_sel} || z_{sel[l]}(obs_steps[k]) - target[k][l] ||^2,
- * z = x (field 0) or v (field 1); sel = NULL means all particles in id order. */
-enum { MPM_SEEDER_NONE = 0, MPM_SEEDER_LAGRANGIAN_LS = 1 };
+ * z = x (field 0) or v (field 1); sel = NULL means all particles in id order.
+ * masked Eulerian least squares (SPEC.md observe_eulerian, PAPER §3.2 "average over all particles
+ * within this region"): monitor regions are closed boxes |x - center| <= half per axis,
+ *   Q_l(t) = mean of z over the particles inside region l at step t,
+ *   L = sum_k sum_l m[k][l] || Q_l(obs_steps[k]) - target[k][l] ||^2,
+ * an empty region has m = 0 (no term, no gradient); mask = NULL means all 1. The membership is
+ * piecewise constant in x, so only the z cotangent is seeded: 2 m (Q_l - target) / |P_l| per member. */
+enum { MPM_SEEDER_NONE = 0, MPM_SEEDER_LAGRANGIAN_LS = 1, MPM_SEEDER_EULERIAN_LS = 2 };
 typedef struct mpm_seeder_desc {
     int kind;
     int field;               /* 0 = x, 1 = v */
@@ -150,7 +156,12 @@ typedef struct mpm_seeder_desc {
     const int64_t* obs_steps;
     int64_t n_sel;
     const int64_t* sel;      /* particle ids, or NULL = all */
-    const void* target;      /* T[n_obs][n_sel][dim] */
+    const void* target;      /* T[n_obs][n_sel][dim] (Lagrangian) or T[n_obs][n_regions][dim] (Eulerian) */
+    /* Eulerian only */
+    int64_t n_regions;
+    const void* centers;     /* T[n_regions][dim] */
+    const void* half;        /* T[n_regions][dim] */
+    const unsigned char* mask; /* [n_obs][n_regions] or NULL */
 } mpm_seeder_desc;
 
 /* BackpropResult (checkpoint.hpp:53-61) counters */

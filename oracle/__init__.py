@@ -222,20 +222,8 @@ class CpuOracle:
 
 
 def make_seeder(seeder: dict | None, T):
-    """Builds an mpm_seeder_desc (Lagrangian least squares) plus its keep-alive arrays."""
-    sd = capi.SeederDesc()
-    if not seeder:
-        sd.kind = capi.MPM_SEEDER_NONE
-        return sd, {}
-    obs = np.ascontiguousarray(np.asarray(seeder["obs_steps"], np.int64))
-    sel = seeder.get("sel")
-    sel = None if sel is None else np.ascontiguousarray(np.asarray(sel, np.int64))
-    tgt = np.ascontiguousarray(np.asarray(seeder["target"], T))
-    sd.kind = capi.MPM_SEEDER_LAGRANGIAN_LS
-    sd.field = 0 if seeder.get("field", "x") == "x" else 1
-    sd.n_obs = len(obs)
-    sd.obs_steps = obs.ctypes.data_as(C.POINTER(C.c_int64))
-    sd.n_sel = 0 if sel is None else len(sel)
-    sd.sel = None if sel is None else sel.ctypes.data_as(C.POINTER(C.c_int64))
-    sd.target = tgt.ctypes.data
-    return sd, {"obs": obs, "sel": sel, "tgt": tgt}
+    """Builds an mpm_seeder_desc (Lagrangian or Eulerian least squares) plus its keep-alive arrays;
+    the descriptor layout is the product ABI's (include/mpm_capi.h), so the package builds it."""
+    from paper_2507_04192_b200.seeders import make_seeder_desc
+
+    return make_seeder_desc(seeder, T)

@@ -1779,21 +1779,56 @@ template <class T, int D> struct OpBackprop {
             Scene<T, D> sc = decode<T, D>(d);
             State<T, D> s0 = load_state<T, D>(v);
             int64_t n = s0.n;
-            // built-in Lagrangian least-squares seeder (checkpoint.hpp:63-66 protocol)
+            // built-in least-squares seeders (checkpoint.hpp:63-66 protocol): Lagrangian, and the
+            // Eulerian monitor regions of SPEC.md observe_eulerian / PAPER §3.2 (the reference
+            // specifies but does not implement the inverse module; restated from the SPEC formula)
+            const bool eul = sd && sd->kind == MPM_SEEDER_EULERIAN_LS;
             auto find = [&](int64_t step) {
-                if (!sd || sd->kind != MPM_SEEDER_LAGRANGIAN_LS)
+                if (!sd || (sd->kind != MPM_SEEDER_LAGRANGIAN_LS && !eul))
                     return -1;
                 for (int k = 0; k < sd->n_obs; ++k)
                     if (sd->obs_steps[k] == step)
                         return k;
                 return -1;
             };
-            int64_t nsel = sd && sd->sel ? sd->n_sel : n;
+            int64_t nsel = eul ? sd->n_regions : (sd && sd->sel ? sd->n_sel : n);
             auto pid = [&](int64_t l) { return sd && sd->sel ? sd->sel[l] : l; };
             auto tgt = [&](int k, int64_t l) { return static_cast<const T*>(sd->target) + (int64_t(k) * nsel + l) * D; };
+            // Eulerian: Q_l = mean z over particles p with |x_p - c_l| <= h_l (every axis), in index order
+            auto inside = [&](const State<T, D>& s, int64_t p, int64_t l) {
+                const T* c = static_cast<const T*>(sd->centers) + l * D;
+                const T* h = static_cast<const T*>(sd->half) + l * D;
+                for (int a = 0; a < D; ++a)
+                    if (!(std::fabs(s.x[p].a[a] - c[a]) <= h[a]))
+                        return false;
+                return true;
+            };
+            auto region = [&](int k, const State<T, D>& s, int64_t l, T* r) { // r = m (Q - target); count
+                const auto& z = sd->field == 0 ? s.x : s.v;
+                T sum[D] = {}, cnt = T(0);
+                for (int64_t p = 0; p < s.n; ++p)
+                    if (inside(s, p, l)) {
+                        for (int a = 0; a < D; ++a)
+                            sum[a] += z[p].a[a];
+                        cnt += T(1);
+                    }
+                const bool on = cnt > T(0) && (!sd->mask || sd->mask[int64_t(k) * nsel + l]);
+                for (int a = 0; a < D; ++a)
+                    r[a] = on ? sum[a] / cnt - tgt(k, l)[a] : T(0);
+                return on ? cnt : T(0);
+            };
             auto loss_at = [&](int64_t step, const State<T, D>& s) {
                 int k = find(step);
                 T L = T(0);
+                if (eul) {
+                    for (int64_t l = 0; l < nsel; ++l) {
+                        T r[D];
+                        region(k, s, l, r);
+                        for (int a = 0; a < D; ++a)
+                            L += r[a] * r[a];
+                    }
+                    return L;
+                }
                 const auto& z = sd->field == 0 ? s.x : s.v;
                 for (int64_t l = 0; l < nsel; ++l)
                     for (int a = 0; a < D; ++a) {
@@ -1806,6 +1841,18 @@ template <class T, int D> struct OpBackprop {
                 int k = find(step);
                 const auto& z = sd->field == 0 ? s.x : s.v;
                 auto& zc = sd->field == 0 ? c.x : c.v;
+                if (eul) { // d/dz_p of m ||Q - target||^2 = 2 m (Q - target) / |P| for every member p
+                    for (int64_t l = 0; l < nsel; ++l) {
+                        T r[D];
+                        const T cnt = region(k, s, l, r);
+                        if (cnt > T(0))
+                            for (int64_t p = 0; p < s.n; ++p)
+                                if (inside(s, p, l))
+                                    for (int a = 0; a < D; ++a)
+                                        zc[p].a[a] += T(2) * r[a] / cnt;
+                    }
+                    return;
+                }
                 for (int64_t l = 0; l < nsel; ++l)
                     for (int a = 0; a < D; ++a)
                         zc[pid(l)].a[a] += T(2) * (z[pid(l)].a[a] - tgt(k, l)[a]);

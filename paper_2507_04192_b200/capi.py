@@ -28,7 +28,7 @@ WALL = {"slip": 0, "no_slip": 1, "fixed": 2, "fixed_wall": 2, "coulomb": 3}
 MAT_FLUID, MAT_DP = 0, 1
 MPM_ADV_NAN_GUARD = 1
 MPM_ADV_STORE_GRID = 2
-MPM_SEEDER_NONE, MPM_SEEDER_LAGRANGIAN_LS = 0, 1
+MPM_SEEDER_NONE, MPM_SEEDER_LAGRANGIAN_LS, MPM_SEEDER_EULERIAN_LS = 0, 1, 2
 
 c_double_p = C.POINTER(C.c_double)
 
@@ -134,6 +134,10 @@ class SeederDesc(C.Structure):
         ("n_sel", C.c_int64),
         ("sel", C.POINTER(C.c_int64)),
         ("target", C.c_void_p),
+        ("n_regions", C.c_int64),
+        ("centers", C.c_void_p),
+        ("half", C.c_void_p),
+        ("mask", C.POINTER(C.c_ubyte)),
     ]
 
 

@@ -1284,13 +1284,34 @@ template <class T, int D> struct Ctx : CtxBase {
         const PBuf<T, D> own0 = buf[0], own1 = buf[1];
         const int cur0 = cur;
         // seeder tables on the device
-        const bool seeding = sd && sd->kind == MPM_SEEDER_LAGRANGIAN_LS && sd->n_obs > 0;
-        const int64_t nsel = seeding ? (sd->sel ? sd->n_sel : n) : 0;
+        const bool eul = sd && sd->kind == MPM_SEEDER_EULERIAN_LS && sd->n_obs > 0;
+        const bool seeding = (sd && sd->kind == MPM_SEEDER_LAGRANGIAN_LS && sd->n_obs > 0) || eul;
+        const int64_t nsel = seeding ? (eul ? sd->n_regions : (sd->sel ? sd->n_sel : n)) : 0;
         std::vector<void*> owned;
         long long* d_sel = nullptr;
         T* d_tgt = nullptr;
+        T *d_cen = nullptr, *d_half = nullptr, *d_epart = nullptr, *d_g = nullptr;
+        unsigned char* d_mask = nullptr;
+        const int eblocks = int(grid_for(n, 256));
+        if (eul) {
+            if (sd->n_regions < 1 || sd->n_regions > EUL_MAXREG || !sd->centers || !sd->half)
+                throw ApiError(MPM_ERR_VALIDATION, "seeder: Eulerian needs 1.." + std::to_string(EUL_MAXREG) +
+                                                       " regions with centers and half sizes");
+            auto dev = [&](auto*& p, size_t bytes, const void* src) {
+                CK(cudaMalloc(reinterpret_cast<void**>(&p), bytes));
+                owned.push_back(p);
+                if (src)
+                    h2d_raw(p, src, bytes);
+            };
+            dev(d_cen, (size_t)nsel * D * sizeof(T), sd->centers);
+            dev(d_half, (size_t)nsel * D * sizeof(T), sd->half);
+            if (sd->mask)
+                dev(d_mask, (size_t)sd->n_obs * nsel, sd->mask);
+            dev(d_epart, (size_t)eblocks * nsel * (D + 1) * sizeof(T), nullptr);
+            dev(d_g, (size_t)nsel * D * sizeof(T), nullptr);
+        }
         if (seeding) {
-            if (sd->sel) {
+            if (sd->sel && !eul) {
                 CK(cudaMalloc(&d_sel, nsel * sizeof(long long)));
                 owned.push_back(d_sel);
                 std::vector<long long> hs(sd->sel, sd->sel + nsel);
@@ -1312,6 +1333,24 @@ template <class T, int D> struct Ctx : CtxBase {
             return -1;
         };
         auto seed = [&](const PBuf<T, D>& P, int k, int cb, int do_cot) {
+            if (eul) {
+                launch("k_seed", [&] {
+                    k_eul_partial<T, D><<<eblocks, 256, 0, stream>>>(P, int(n), d_cen, d_half, int(nsel), sd->field,
+                                                                     d_epart);
+                });
+                launch("k_seed", [&] {
+                    k_eul_final<T, D><<<1, EUL_MAXREG, 0, stream>>>(d_epart, eblocks, int(nsel),
+                                                                    d_tgt + (size_t)k * nsel * D,
+                                                                    d_mask ? d_mask + (size_t)k * nsel : nullptr,
+                                                                    d_g, aw.loss_acc);
+                });
+                if (do_cot)
+                    launch("k_seed", [&] {
+                        k_eul_seed<T, D><<<eblocks, 256, 0, stream>>>(P, int(n), d_cen, d_half, int(nsel), d_g,
+                                                                      sd->field, aw.cot[cb]);
+                    });
+                return;
+            }
             launch("k_slot_of_pid", [&] { k_slot_of_pid<T, D><<<grid_for(n, 256), 256, 0, stream>>>(P, int(n), aw.slot_of_pid); });
             launch("k_seed", [&] {
                 k_seed_lagrangian<T, D><<<1, 1024, 0, stream>>>(P, int(n), aw.slot_of_pid, d_sel, nsel,

@@ -1484,6 +1484,115 @@ __global__ void __launch_bounds__(1024) k_seed_lagrangian(PBuf<T, D> P, int n, c
         *loss_acc += double(tot);
 }
 
+// ---- Eulerian monitor regions (SPEC observe_eulerian): per-block sums of (z, 1) over the
+// particles inside each region, in storage order (warp shuffles, then warps in order)
+constexpr int EUL_MAXREG = 64;
+template <class T, int D>
+__global__ void __launch_bounds__(256) k_eul_partial(PBuf<T, D> P, int n, const T* __restrict__ centers,
+                                                     const T* __restrict__ half, int nreg, int field,
+                                                     T* __restrict__ partials)
+{
+    __shared__ T wsum[8][D + 1];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool live = i < n && P.pid[i] >= 0;
+    T x[D], z[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        x[a] = live ? P.x[a][i] : T(0);
+        z[a] = live ? (field == 0 ? P.x[a][i] : P.v[a][i]) : T(0);
+    }
+    for (int l = 0; l < nreg; ++l) {
+        bool in = live;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            in = in && fabs(x[a] - centers[l * D + a]) <= half[l * D + a];
+        T v[D + 1];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            v[a] = in ? z[a] : T(0);
+        v[D] = in ? T(1) : T(0);
+#pragma unroll
+        for (int c = 0; c <= D; ++c)
+            for (int o = 16; o > 0; o >>= 1)
+                v[c] += __shfl_down_sync(0xffffffffu, v[c], o);
+        __syncthreads();
+        if (lane == 0)
+#pragma unroll
+            for (int c = 0; c <= D; ++c)
+                wsum[wid][c] = v[c];
+        __syncthreads();
+        if (threadIdx.x <= D) {
+            T s = T(0);
+            for (int w = 0; w < int(blockDim.x / 32); ++w)
+                s += wsum[w][threadIdx.x];
+            partials[((size_t)blockIdx.x * nreg + l) * (D + 1) + threadIdx.x] = s;
+        }
+    }
+}
+
+// block sums in block order -> Q_l; loss += sum_l m ||Q_l - target||^2; g_l = 2 m (Q_l - target)/|P_l|
+template <class T, int D>
+__global__ void k_eul_final(const T* __restrict__ partials, int nblocks, int nreg, const T* __restrict__ target,
+                            const unsigned char* __restrict__ mask, T* __restrict__ g, double* loss_acc)
+{
+    __shared__ T term[EUL_MAXREG];
+    const int l = threadIdx.x;
+    if (l < nreg) {
+        T s[D + 1];
+#pragma unroll
+        for (int c = 0; c <= D; ++c)
+            s[c] = T(0);
+        for (int b = 0; b < nblocks; ++b)
+#pragma unroll
+            for (int c = 0; c <= D; ++c)
+                s[c] += partials[((size_t)b * nreg + l) * (D + 1) + c];
+        const bool on = s[D] > T(0) && (!mask || mask[l]);
+        T t = T(0);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const T r = on ? s[a] / s[D] - target[l * D + a] : T(0);
+            t += r * r;
+            g[l * D + a] = on ? T(2) * r / s[D] : T(0);
+        }
+        term[l] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T L = T(0);
+        for (int k = 0; k < nreg; ++k)
+            L += term[k];
+        *loss_acc += double(L);
+    }
+}
+
+// cot.z[pid] += g_l for every region containing the particle (region order)
+template <class T, int D>
+__global__ void k_eul_seed(PBuf<T, D> P, int n, const T* __restrict__ centers, const T* __restrict__ half, int nreg,
+                           const T* __restrict__ g, int field, CBuf<T, D> cot)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || P.pid[i] < 0)
+        return;
+    const int pid = P.pid[i];
+    T x[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        x[a] = P.x[a][i];
+    for (int l = 0; l < nreg; ++l) {
+        bool in = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            in = in && fabs(x[a] - centers[l * D + a]) <= half[l * D + a];
+        if (in)
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                T* zc = field == 0 ? cot.x[a] : cot.v[a];
+                zc[pid] += g[l * D + a];
+            }
+    }
+}
+
 template <class T, int D> __global__ void k_slot_of_pid(PBuf<T, D> P, int n, int* slot_of_pid)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;

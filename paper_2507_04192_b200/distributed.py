@@ -651,9 +651,16 @@ def slab_backprop_trajectory(scene: Scene, plan, seeder, domains: list, transpor
     def gather():
         return {r: d.gather() for r, d in doms.items()}
 
+    glob = getattr(seeder, "global_stats", False)  # Eulerian: region sums span the ranks
+
+    def stats(step, snap):
+        return transport.sum_ordered({r: seeder.stats_local(step, sub, ids) for r, (sub, ids, _) in snap.items()})
+
     def loss_of(step, snap):
         if not seeder.observes(step):
             return 0.0
+        if glob:
+            return seeder.loss_from_stats(step, stats(step, snap))
         part = {r: np.array([seeder.loss_local(step, sub, ids)]) for r, (sub, ids, _) in snap.items()}
         return float(transport.sum_ordered(part)[0])
 
@@ -683,8 +690,9 @@ def slab_backprop_trajectory(scene: Scene, plan, seeder, domains: list, transpor
         if not seeder.observes(step):
             return
         local = {}
+        st = stats(step, snap_t) if glob else None
         for r, (sub, ids, _) in snap_t.items():
-            rows, dz = seeder.seed_local(step, sub, ids)
+            rows, dz = seeder.seed_local(step, sub, ids, st) if glob else seeder.seed_local(step, sub, ids)
             local[r] = (np.asarray(ids)[rows], dz)
         for r in sorted(allg := transport.allgather_obj(local)):
             gid, dz = allg[r]

@@ -54,11 +54,90 @@ class LagrangianLeastSquares:
         return rows, 2 * r
 
 
+class EulerianLeastSquares:
+    """Velocity-monitor supervision (SPEC.md observe_eulerian, PAPER §3.2 and §5.1 "sparse
+    velocity-monitor supervision"): region l is the closed box |x - centers[l]| <= half[l];
+    Q_l(t) = mean of z over the particles inside; L = sum_t sum_l m[t][l] ||Q_l(t) - target[t][l]||^2,
+    an empty region carries no term (mask 0). `half` may be a scalar, per region or per region and
+    axis; `mask` = [n_obs, n_regions] of {0, 1} or None."""
+
+    def __init__(self, obs_steps, centers, half, target, field: str = "v", mask=None):
+        self.obs_steps = list(int(s) for s in obs_steps)
+        self.centers = np.atleast_2d(np.asarray(centers, np.float64))
+        nreg, dim = self.centers.shape
+        h = np.asarray(half, np.float64)
+        self.half = np.broadcast_to(h.reshape(-1, 1) if h.ndim == 1 else h, (nreg, dim)).copy()
+        self.target = np.asarray(target)
+        self.field = field
+        self.mask = None if mask is None else np.asarray(mask, np.uint8)
+
+    def desc(self) -> dict:
+        return {"kind": "eulerian", "field": self.field, "obs_steps": self.obs_steps, "centers": self.centers,
+                "half": self.half, "target": self.target, "mask": self.mask}
+
+    # ---- slab decomposition: region statistics are summed over the ranks before Q is formed ----
+    global_stats = True
+
+    def observes(self, step: int) -> bool:
+        return int(step) in self.obs_steps
+
+    def _members(self, particles):
+        x = particles.x
+        return np.all(np.abs(x[:, None, :] - self.centers[None]) <= self.half[None], axis=2)  # [n, nreg]
+
+    def stats_local(self, step, particles, ids) -> np.ndarray:
+        """per region (sum z, count) of this rank's particles, flattened"""
+        inm = self._members(particles)
+        z = particles.x if self.field == "x" else particles.v
+        s = np.concatenate([inm.T.astype(np.float64) @ z.astype(np.float64), inm.sum(0)[:, None]], axis=1)
+        return s.reshape(-1)
+
+    def _coef(self, step, stats):
+        k = self.obs_steps.index(int(step))
+        nreg, dim = self.centers.shape
+        st = stats.reshape(nreg, dim + 1)
+        cnt = st[:, dim]
+        on = cnt > 0
+        if self.mask is not None:
+            on &= self.mask[k].astype(bool)
+        q = np.where(on[:, None], st[:, :dim] / np.where(on, cnt, 1)[:, None], 0.0)
+        r = np.where(on[:, None], q - self.target[k], 0.0)
+        return r, cnt, on
+
+    def loss_from_stats(self, step, stats) -> float:
+        r, _, _ = self._coef(step, stats)
+        return float((r ** 2).sum())
+
+    def seed_local(self, step, particles, ids, stats):
+        r, cnt, on = self._coef(step, stats)
+        g = np.where(on[:, None], 2 * r / np.where(on, cnt, 1)[:, None], 0.0)
+        dz = self._members(particles).astype(np.float64) @ g
+        return np.arange(len(ids)), dz.astype(particles.x.dtype)
+
+
 def make_seeder_desc(seeder: dict | None, T):
     sd = capi.SeederDesc()
     if not seeder:
         sd.kind = capi.MPM_SEEDER_NONE
         return sd, {}
+    if seeder.get("kind") == "eulerian":
+        obs = np.ascontiguousarray(np.asarray(seeder["obs_steps"], np.int64))
+        cen = np.ascontiguousarray(np.asarray(seeder["centers"], T))
+        half = np.ascontiguousarray(np.asarray(seeder["half"], T))
+        tgt = np.ascontiguousarray(np.asarray(seeder["target"], T))
+        mask = seeder.get("mask")
+        mask = None if mask is None else np.ascontiguousarray(np.asarray(mask, np.uint8))
+        sd.kind = capi.MPM_SEEDER_EULERIAN_LS
+        sd.field = 0 if seeder.get("field", "v") == "x" else 1
+        sd.n_obs = len(obs)
+        sd.obs_steps = obs.ctypes.data_as(C.POINTER(C.c_int64))
+        sd.n_sel = 0
+        sd.target = tgt.ctypes.data
+        sd.n_regions = len(cen)
+        sd.centers = cen.ctypes.data
+        sd.half = half.ctypes.data
+        sd.mask = None if mask is None else mask.ctypes.data_as(C.POINTER(C.c_ubyte))
+        return sd, {"obs": obs, "cen": cen, "half": half, "tgt": tgt, "mask": mask}
     obs = np.ascontiguousarray(np.asarray(seeder["obs_steps"], np.int64))
     sel = seeder.get("sel")
     sel = None if sel is None else np.ascontiguousarray(np.asarray(sel, np.int64))
