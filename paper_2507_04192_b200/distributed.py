@@ -83,20 +83,33 @@ class SlabPlan:
             raise ValueError(f"cannot split {nbx} x-blocks into {n_ranks} slabs")
         if x is None or len(x) == 0:
             cuts = [round(k * nbx / n_ranks) for k in range(n_ranks + 1)]
-        else:
-            bx = np.clip(base_cell_x(scene, x) // B, 0, nbx - 1)
-            cum = np.concatenate([[0], np.cumsum(np.bincount(bx, minlength=nbx))])
-            total = cum[-1]
-            cuts = [0]
-            for k in range(1, n_ranks):
-                # block boundary whose cumulative count is closest to k/R of the total; keep at
-                # least one block for each remaining rank
-                lo_c, hi_c = cuts[-1] + 1, nbx - (n_ranks - k)
-                c = lo_c + int(np.argmin(np.abs(cum[lo_c:hi_c + 1] - total * k / n_ranks)))
-                cuts.append(c)
-            cuts.append(nbx)
-        bounds = [min(c * B, cx) for c in cuts]
-        bounds[-1] = cx
+            bounds = [min(c * B, cx) for c in cuts]
+            bounds[-1] = cx
+            return SlabPlan(bounds, B)
+        return SlabPlan.from_histogram(SlabPlan.block_histogram(scene, x), B, cx, n_ranks)
+
+    @staticmethod
+    def block_histogram(scene: Scene, x: np.ndarray) -> np.ndarray:
+        """particle count per x-block column of base cells"""
+        B = block_edge(scene.dim)
+        nbx = -(-scene.config.cells[0] // B)
+        return np.bincount(np.clip(base_cell_x(scene, x) // B, 0, nbx - 1), minlength=nbx).astype(np.float64)
+
+    @staticmethod
+    def from_histogram(hist: np.ndarray, B: int, cells_x: int, n_ranks: int) -> "SlabPlan":
+        """balanced cuts: each block boundary whose cumulative count is closest to k/R of the total,
+        at least one block per rank"""
+        nbx = len(hist)
+        cum = np.concatenate([[0.0], np.cumsum(hist)])
+        total = cum[-1]
+        cuts = [0]
+        for k in range(1, n_ranks):
+            lo_c, hi_c = cuts[-1] + 1, nbx - (n_ranks - k)
+            c = lo_c + int(np.argmin(np.abs(cum[lo_c:hi_c + 1] - total * k / n_ranks)))
+            cuts.append(c)
+        cuts.append(nbx)
+        bounds = [min(c * B, cells_x) for c in cuts]
+        bounds[-1] = cells_x
         return SlabPlan(bounds, B)
 
     def owner(self, base_x: np.ndarray) -> np.ndarray:
@@ -274,9 +287,14 @@ class SlabStepper:
     error on any rank raises on all of them at the same step.
     """
 
-    def __init__(self, domains: list, transport):
+    def __init__(self, domains: list, transport, rebalance_every: int = 0, imbalance: float = 1.2):
+        """rebalance_every > 0: every that many steps, re-plan the slabs when the largest rank holds
+        more than `imbalance` times the mean particle count (granular flows spread)"""
         self.domains = {d.rank: d for d in domains}
         self.transport = transport
+        self.rebalance_every = int(rebalance_every)
+        self.imbalance = float(imbalance)
+        self.rebalances = 0
         if isinstance(transport, TorchTransport):
             import torch
 
@@ -373,6 +391,51 @@ class SlabStepper:
     def advance(self, n: int, nan_guard: bool = False):
         for _ in range(int(n)):
             self.step(nan_guard)
+            if self.rebalance_every and self.steps_done % self.rebalance_every == 0:
+                self.maybe_rebalance()
+
+    def counts(self) -> dict:
+        return {r: int(c) for r, c in self.transport.allgather_obj({r: d.local_count()
+                                                                   for r, d in self.domains.items()}).items()}
+
+    def maybe_rebalance(self) -> bool:
+        c = self.counts()
+        mean = sum(c.values()) / len(c)
+        if mean <= 0 or max(c.values()) <= self.imbalance * mean:
+            return False
+        self.rebalance()
+        return True
+
+    def rebalance(self):
+        """New slab bounds from the global x-block histogram (summed over the ranks in rank order),
+        then every particle moves to its new owner: host-orchestrated (rebalancing is rare), the
+        received particles appended in id order so the storage order stays deterministic."""
+        doms = self.domains
+        d0 = next(iter(doms.values()))
+        scene, old = d0.scene, d0.plan
+        snaps = {r: d.gather() for r, d in doms.items()}
+        hist = self.transport.sum_ordered({r: SlabPlan.block_histogram(scene, sub.x)
+                                           for r, (sub, ids, _) in snaps.items()})
+        plan = SlabPlan.from_histogram(hist, old.block, scene.config.cells[0], old.n_ranks)
+        out = {}
+        for r, (sub, ids, _) in snaps.items():
+            own = plan.owner(base_cell_x(scene, sub.x))
+            out[r] = {q: (sub.take(np.nonzero(own == q)[0]), np.asarray(ids)[own == q]) for q in range(plan.n_ranks)}
+        allg = self.transport.allgather_obj(out)
+        for r, d in doms.items():
+            parts = [allg[src][r] for src in sorted(allg)]
+            ids = np.concatenate([p[1] for p in parts]).astype(np.int64)
+            order = np.argsort(ids, kind="stable")
+            tmpl = snaps[r][0]
+            sub = ParticleSoA(len(ids), tmpl.dim, tmpl.dtype, tmpl.affine is not None, tmpl.def_grad is not None)
+            at = 0
+            for p in parts:
+                k = len(p[1])
+                sub.put(np.arange(at, at + k), p[0])
+                at += k
+            step, time = snaps[r][2]
+            d.retarget(plan, sub.take(order), ids[order], step, time)
+        self.rebalances += 1
 
     def gather_local(self, template: SimState) -> SimState:
         """Assemble the global state from domains in this process (every rank local)"""
@@ -494,6 +557,20 @@ class GpuSlabDomain(SlabDomain):
 
     def local_count(self) -> int:
         return int(self.lib.mpm_local_count(self.h))
+
+    def retarget(self, plan: SlabPlan, particles: ParticleSoA, ids, step: int, time: float):
+        """move to new slab bounds and load this rank's new particle set (rebalancing)"""
+        self.plan = plan
+        if len(ids) > self.capacity:  # grow: a fresh context on the same stream
+            from .solver import Context
+
+            self.ctx.close()
+            self.capacity = int(1.25 * len(ids)) + 1024
+            self.ctx = Context(self.scene, self.capacity, self.device.index or 0)
+            self.lib, self.h = self.ctx.lib, self.ctx.h
+            self.ctx.check(self.lib.mpm_ctx_set_stream(self.h, C.c_void_p(self.stream.cuda_stream)))
+        self.ctx.check(self.lib.mpm_slab_set(self.h, plan.lo(self.rank), plan.hi(self.rank), self.mig_cap))
+        self.restore(particles, ids, step, time)
 
     def restore(self, particles: ParticleSoA, ids, step: int, time: float):
         """load a checkpoint of this rank (its particles, their global ids, step, time)"""

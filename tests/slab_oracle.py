@@ -169,5 +169,10 @@ class OracleSlabDomain(SlabDomain):
     def local_count(self):
         return self.sub.particles.size()
 
+    def retarget(self, plan, particles, ids, step, time):
+        self.plan = plan
+        self.sub = SimState(particles, step, time)
+        self.ids = np.asarray(ids, np.int64)
+
     def gather(self):
         return self.sub.particles, self.ids, (self.sub.step, self.sub.time)

@@ -203,3 +203,23 @@ def test_slab_backprop_matches_single_context(dim, R, nseg):
     assert np.abs(b).max() > 0 and np.abs(a - b).max() <= 1e-8 * np.abs(b).max(), (a, b)
     assert abs(out.param_grads.sound_speed - pg_ref.sound_speed) <= 1e-8 * abs(pg_ref.sound_speed)
     assert out.checkpoints_stored == nseg
+
+
+def test_gpu_rebalancing_matches_single_context():
+    """dynamic slab rebalancing on the device path: even split -> re-planned"""
+    s = moving_fluid_scene(2)
+    st = init_scene(s)
+    plan = SlabPlan.make(s, 3, None)
+    ids = plan.partition(s, st)
+    doms = [GpuSlabDomain(s, plan, r, st, ids[r]) for r in range(3)]
+    stp = SlabStepper(doms, LocalTransport(), rebalance_every=5, imbalance=1.05)
+    stp.advance(20)
+    assert stp.rebalances >= 1
+    c = stp.counts()
+    got = stp.gather_local(st)
+    from paper_2507_04192_b200.distributed import base_cell_x, block_edge
+
+    col = np.bincount(base_cell_x(s, got.particles.x) // block_edge(2)).max()  # balance is per x-block
+    assert max(c.values()) - min(c.values()) <= 2 * col and sum(c.values()) == st.particles.size()
+    ref = plain_gpu(s, st, 20)
+    assert_state_close(got, ref, 1e-10, what="rebalanced device slabs")
