@@ -231,6 +231,25 @@ int mpm_backprop(mpm_ctx* ctx, const mpm_state_view* initial, int64_t total_step
                  const mpm_seeder_desc* seeder, mpm_cot_view* initial_state_cot,
                  mpm_param_grads* pg, mpm_backprop_result* result);
 
+/* ---- device scene seeding ------------------------------------------- */
+/* GeometryRegion + VelocityExpr (config.hpp:99-184) */
+typedef struct mpm_region {
+    int shape;                               /* 0 box, 1 cylinder */
+    double lo[3], hi[3];                     /* box: lo <= x < hi */
+    double center[3], radius, zmin, zmax;    /* cylinder: |xy - center| < radius, zmin <= z < zmax */
+    int vel_kind;                            /* 0 constant, 1 linear_in_y, 2 parabolic_sine */
+    double value[3], alpha, h0, amplitude, perturbation, frequency;
+    double min_y;                            /* the region's lowest y (velocity profile origin) */
+} mpm_region;
+/* init_scene (scene.hpp:55-116) on the device, into the context's state: 2^d sub-cell lattice at
+ * +-dh/4 in every cell of the regions' bounding box (cells row-major, axis 0 slowest, corners in
+ * bit order), the first containing region owns a point; mass / volume / rho0 as init_scene sets
+ * them (passed in so the host formula stays the single source). Same particles, order and bits as
+ * the host seeding, except parabolic_sine (device sin). *n_out = particles seeded; fails with
+ * MPM_ERR_USAGE and *n_out = the count when it exceeds the context capacity. */
+int mpm_init_scene(mpm_ctx* ctx, const mpm_region* regions, int n_regions, double mass, double volume, double rho0,
+                   int64_t* n_out);
+
 /* ---- slab decomposition across GPUs ------------------------------------ */
 /* One context per GPU, global coordinates; the context owns the particles whose base cell along
  * x lies in [cell_lo, cell_hi) (multiples of the block edge, 16 in 2-D / 8 in 3-D). A step is

@@ -141,6 +141,19 @@ class SeederDesc(C.Structure):
     ]
 
 
+class Region(C.Structure):
+    """mpm_region: GeometryRegion + VelocityExpr (config.hpp:99-184)"""
+    _fields_ = [
+        ("shape", C.c_int),
+        ("lo", C.c_double * 3), ("hi", C.c_double * 3),
+        ("center", C.c_double * 3), ("radius", C.c_double), ("zmin", C.c_double), ("zmax", C.c_double),
+        ("vel_kind", C.c_int),
+        ("value", C.c_double * 3), ("alpha", C.c_double), ("h0", C.c_double), ("amplitude", C.c_double),
+        ("perturbation", C.c_double), ("frequency", C.c_double),
+        ("min_y", C.c_double),
+    ]
+
+
 class BackpropResultView(C.Structure):
     _fields_ = [
         ("loss", C.c_double),
@@ -189,6 +202,8 @@ _PROTOS = {
     "mpm_local_count": (C.c_int64, [C.c_void_p]),
     "mpm_step_p2g_local": (C.c_int, [C.c_void_p]),
     "mpm_step_grid_interior": (C.c_int, [C.c_void_p]),
+    "mpm_init_scene": (C.c_int, [C.c_void_p, C.POINTER(Region), C.c_int, C.c_double, C.c_double, C.c_double,
+                                 C.POINTER(C.c_int64)]),
     "mpm_slab_vjp_begin": (C.c_int, [C.c_void_p, C.POINTER(CotView)]),
     "mpm_slab_vjp_interior": (C.c_int, [C.c_void_p]),
     "mpm_slab_vjp_scatter": (C.c_int, [C.c_void_p]),

@@ -13,6 +13,7 @@
 #include "kernels_util.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
@@ -80,6 +81,8 @@ struct CtxBase {
     virtual void slab_set(int lo, int hi, int64_t mig_cap) = 0;
     virtual void step_p2g_local() = 0;
     virtual void step_grid_interior() = 0;
+    virtual void init_scene_dev(const mpm_region* rg, int nreg, double mass, double volume, double rho0,
+                                int64_t* n_out) = 0;
     virtual void slab_vjp_begin(const mpm_cot_view* co) = 0;
     virtual void slab_vjp_interior() = 0;
     virtual void slab_vjp_scatter() = 0;
@@ -995,6 +998,78 @@ template <class T, int D> struct Ctx : CtxBase {
     // every node off the halo bands: the fused sum + g m + momentum + corrections, enqueued while
     // the bands travel (the transport overlaps it)
     void step_grid_interior() override { grid_kernel<G_INTERIOR | G_SUM | G_MOM | G_CORR>(); }
+    // init_scene (scene.hpp:55-116) on the device: count per cell, exclusive scan, write in order
+    void init_scene_dev(const mpm_region* rg, int nreg, double mass, double volume, double rho0,
+                        int64_t* n_out) override
+    {
+        if (nreg < 1 || !rg)
+            throw ApiError(MPM_ERR_VALIDATION, "scene: no geometry regions");
+        SeedBox bx{};
+        bx.ncell = 1;
+        for (int a = 0; a < D; ++a) { // union bounding box, as the host seeding restricts its visit
+            double lo = 1e300, hi = -1e300;
+            for (int r = 0; r < nreg; ++r) {
+                const mpm_region& g = rg[r];
+                const double l = g.shape == 0 ? g.lo[a] : (a < 2 ? g.center[a] - g.radius : g.zmin);
+                const double h = g.shape == 0 ? g.hi[a] : (a < 2 ? g.center[a] + g.radius : g.zmax);
+                lo = std::min(lo, l);
+                hi = std::max(hi, h);
+            }
+            const double o = desc.origin[a], dh = desc.dh;
+            bx.lo[a] = std::max(0, int(std::floor((lo - o) / dh)) - 1);
+            const int hc = std::min(desc.cells[a], int(std::ceil((hi - o) / dh)) + 1);
+            bx.ext[a] = std::max(0, hc - bx.lo[a]);
+            bx.ncell *= bx.ext[a];
+        }
+        if (bx.ncell <= 0)
+            throw ApiError(MPM_ERR_VALIDATION, "scene: geometry produced no particles");
+        mpm_region* d_rg = nullptr;
+        int *counts_d = nullptr, *offs = nullptr;
+        void* tmp = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&d_rg), sizeof(mpm_region) * nreg, stream));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&counts_d), sizeof(int) * bx.ncell, stream));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&offs), sizeof(int) * bx.ncell, stream));
+        CK(cudaMemcpyAsync(d_rg, rg, sizeof(mpm_region) * nreg, cudaMemcpyHostToDevice, stream));
+        launch("k_seed", [&] {
+            k_seed_count<T, D><<<grid_for(bx.ncell, 256), 256, 0, stream>>>(sc, bx, d_rg, nreg, counts_d);
+        });
+        size_t bytes = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts_d, offs, int(bx.ncell), stream));
+        CK(cudaMallocAsync(&tmp, bytes, stream));
+        CK(cub::DeviceScan::ExclusiveSum(tmp, bytes, counts_d, offs, int(bx.ncell), stream));
+        int last[2] = {0, 0};
+        CK(cudaMemcpyAsync(&last[0], offs + bx.ncell - 1, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(&last[1], counts_d + bx.ncell - 1, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        const int64_t total = int64_t(last[0]) + last[1];
+        *n_out = total;
+        auto release = [&] {
+            cudaFreeAsync(tmp, stream);
+            cudaFreeAsync(offs, stream);
+            cudaFreeAsync(counts_d, stream);
+            cudaFreeAsync(d_rg, stream);
+        };
+        if (total < 1 || total > cap) {
+            release();
+            throw ApiError(total < 1 ? MPM_ERR_VALIDATION : MPM_ERR_USAGE,
+                           total < 1 ? "scene: geometry produced no particles"
+                                     : "init_scene: " + std::to_string(total) + " particles exceed the context capacity " +
+                                           std::to_string(cap));
+        }
+        launch("k_seed", [&] {
+            k_seed_write<T, D><<<grid_for(bx.ncell, 256), 256, 0, stream>>>(sc, bx, d_rg, nreg, offs, buf[cur], T(mass),
+                                                                           T(volume), T(rho0), has_aff, has_F);
+        });
+        release();
+        CK(cudaStreamSynchronize(stream));
+        n = total;
+        n_dead = 0;
+        keys_valid = false;
+        status_dirty = true;
+        step = 0;
+        time = 0.0;
+    }
+
     // step_vjp over a slab (same exchange points as the forward step, plus the node cotangents)
     void slab_vjp_begin(const mpm_cot_view* co) override
     {
@@ -1593,6 +1668,11 @@ int mpm_state_download_local(mpm_ctx* c, mpm_state_view* s, int64_t* ids) { MPM_
 int mpm_slab_set(mpm_ctx* c, int cell_lo, int cell_hi, int64_t mig_cap) { MPM_CALL(c, c->impl->slab_set(cell_lo, cell_hi, mig_cap)); }
 int mpm_step_p2g_local(mpm_ctx* c) { MPM_CALL(c, c->impl->step_p2g_local()); }
 int mpm_step_grid_interior(mpm_ctx* c) { MPM_CALL(c, c->impl->step_grid_interior()); }
+int mpm_init_scene(mpm_ctx* c, const mpm_region* regions, int n_regions, double mass, double volume, double rho0,
+                   int64_t* n_out)
+{
+    MPM_CALL(c, c->impl->init_scene_dev(regions, n_regions, mass, volume, rho0, n_out));
+}
 int mpm_slab_vjp_begin(mpm_ctx* c, const mpm_cot_view* cot_out) { MPM_CALL(c, c->impl->slab_vjp_begin(cot_out)); }
 int mpm_slab_vjp_interior(mpm_ctx* c) { MPM_CALL(c, c->impl->slab_vjp_interior()); }
 int mpm_slab_vjp_scatter(mpm_ctx* c) { MPM_CALL(c, c->impl->slab_vjp_scatter()); }

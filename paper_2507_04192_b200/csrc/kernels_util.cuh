@@ -180,6 +180,132 @@ __global__ void k_download(Stage<T, D> S, PBuf<T, D> P, int n, int has_aff, int 
         }
 }
 
+// ---- device scene seeding (init_scene, scene.hpp:55-116) ------------------------------------
+// exact IEEE ops (no FMA contraction) so the lattice matches the host seeding bit for bit
+template <class T> __device__ __forceinline__ T radd(T a, T b);
+template <class T> __device__ __forceinline__ T rmul(T a, T b);
+template <> __device__ __forceinline__ double radd<double>(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float radd<float>(float a, float b) { return __fadd_rn(a, b); }
+template <> __device__ __forceinline__ double rmul<double>(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ float rmul<float>(float a, float b) { return __fmul_rn(a, b); }
+
+struct SeedBox {
+    int lo[3], ext[3];
+    long long ncell;
+};
+
+template <class T, int D>
+__device__ __forceinline__ void seed_points(const DevScene<T, D>& sc, const SeedBox& bx, long long c, T (*p)[D])
+{
+    int ci[D];
+    long long r = c;
+    for (int a = D - 1; a >= 0; --a) {
+        ci[a] = bx.lo[a] + int(r % bx.ext[a]);
+        r /= bx.ext[a];
+    }
+    const T quarter = sc.dh / T(4); // exact
+#pragma unroll
+    for (int k = 0; k < (1 << D); ++k)
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const T center = radd<T>(sc.origin[a], rmul<T>(radd<T>(T(ci[a]), T(0.5)), sc.dh));
+            p[k][a] = ((k >> a) & 1) ? radd<T>(center, quarter) : radd<T>(center, -quarter);
+        }
+}
+
+template <class T, int D> __device__ __forceinline__ int seed_owner(const mpm_region* rg, int nreg, const T* p)
+{
+    for (int r = 0; r < nreg; ++r) {
+        const mpm_region& g = rg[r];
+        bool ok = true;
+        if (g.shape == 0) {
+            for (int a = 0; a < D; ++a)
+                ok = ok && p[a] >= T(g.lo[a]) && p[a] < T(g.hi[a]);
+        } else {
+            if (D == 3)
+                ok = p[2] >= T(g.zmin) && p[2] < T(g.zmax);
+            const T dx = radd<T>(p[0], -T(g.center[0])), dy = radd<T>(p[1], -T(g.center[1]));
+            const T rr = rmul<T>(T(g.radius), T(g.radius));
+            ok = ok && radd<T>(rmul<T>(dx, dx), rmul<T>(dy, dy)) < rr;
+        }
+        if (ok)
+            return r;
+    }
+    return -1;
+}
+
+template <class T, int D>
+__global__ void k_seed_count(DevScene<T, D> sc, SeedBox bx, const mpm_region* __restrict__ rg, int nreg,
+                             int* __restrict__ counts)
+{
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= bx.ncell)
+        return;
+    T p[1 << D][D];
+    seed_points<T, D>(sc, bx, c, p);
+    int k = 0;
+#pragma unroll
+    for (int q = 0; q < (1 << D); ++q)
+        k += seed_owner<T, D>(rg, nreg, p[q]) >= 0;
+    counts[c] = k;
+}
+
+template <class T, int D>
+__global__ void k_seed_write(DevScene<T, D> sc, SeedBox bx, const mpm_region* __restrict__ rg, int nreg,
+                             const int* __restrict__ offs, PBuf<T, D> P, T mass, T volume, T rho0, int has_aff,
+                             int has_F)
+{
+    using C = Cfg<D>;
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= bx.ncell)
+        return;
+    T p[1 << D][D];
+    seed_points<T, D>(sc, bx, c, p);
+    int i = offs[c];
+    for (int q = 0; q < (1 << D); ++q) {
+        const int r = seed_owner<T, D>(rg, nreg, p[q]);
+        if (r < 0)
+            continue;
+        const mpm_region& g = rg[r];
+        T v[D];
+        for (int a = 0; a < D; ++a)
+            v[a] = T(0);
+        const T yr = radd<T>(p[q][1], -T(g.min_y));
+        if (g.vel_kind == 0) { // VelocityExpr::evaluate (config.hpp:109-129)
+            for (int a = 0; a < D; ++a)
+                v[a] = T(g.value[a]);
+        } else if (g.vel_kind == 1) {
+            v[0] = rmul<T>(T(g.alpha), radd<T>(T(g.h0), -yr));
+        } else {
+            const T yn = yr / T(g.h0);
+            const T arg = rmul<T>(rmul<T>(T(g.frequency), T(3.14159265358979323846)), yn);
+            v[0] = radd<T>(rmul<T>(T(g.amplitude), radd<T>(T(1), -rmul<T>(yn, yn))),
+                           rmul<T>(T(g.perturbation), T(sin(double(arg)))));
+        }
+        for (int a = 0; a < D; ++a) {
+            P.x[a][i] = p[q][a];
+            P.v[a][i] = v[a];
+        }
+        P.m[i] = mass;
+        P.V[i] = volume;
+        P.rho[i] = rho0;
+        P.eps[i] = T(0);
+        if (D == 2)
+            P.szz[i] = T(0);
+        for (int s2 = 0; s2 < C::NS; ++s2)
+            P.sig[s2][i] = T(0);
+        for (int k = 0; k < D * D; ++k) {
+            P.gv[k][i] = T(0);
+            if (has_aff)
+                P.aff[k][i] = T(0);
+            if (has_F)
+                P.F[k][i] = (k % (D + 1) == 0) ? T(1) : T(0);
+        }
+        P.pid[i] = i;
+        ++i;
+    }
+}
+
 // slab step report for the caller's collective: (failed, left toward -x, left toward +x)
 __global__ inline void k_report(const DevStatus* st, long long* out)
 {

@@ -372,6 +372,56 @@ def _velocity(g: GeometryRegion, y_rel: np.ndarray, dim: int, T) -> np.ndarray:
     return out
 
 
+def seeding_constants(scene: Scene):
+    """(mpm_region list, mass, volume, rho0) of init_scene for the device seeding; validates the
+    scene and sets scene.mass_epsilon exactly as init_scene does"""
+    from . import capi
+
+    scene.validate()
+    dim, T = scene.dim, scene.np_dtype
+    dh = T(scene.config.dh)
+    rho0 = T(scene.material.rho0)
+    mp = T(rho0 * T(T(dh) ** dim) / T(1 << dim))
+    kinds = {"constant": 0, "linear_in_y": 1, "parabolic_sine": 2}
+    regs = []
+    for g in scene.geometry:
+        r = capi.Region()
+        r.shape = 0 if g.shape == "box" else 1
+        for a in range(dim):
+            if g.shape == "box":
+                r.lo[a], r.hi[a] = g.lo[a], g.hi[a]
+        if g.shape != "box":
+            for a in range(2):
+                r.center[a] = g.center[a]
+            r.radius, r.zmin, r.zmax = g.radius, g.zmin, g.zmax
+        ve = g.velocity
+        if ve.kind not in kinds:
+            raise ValidationError(f"velocity expression {ve.kind!r} is not supported")
+        r.vel_kind = kinds[ve.kind]
+        val = ve.value if ve.value is not None else [0.0] * dim
+        for a in range(dim):
+            r.value[a] = val[a]
+        r.alpha, r.h0, r.amplitude, r.perturbation, r.frequency = ve.alpha, ve.h0, ve.amplitude, ve.perturbation, \
+            ve.frequency
+        r.min_y = float(T(g.min_y()))
+        regs.append(r)
+    scene.mass_epsilon = float(T(T(1e-12) * mp))
+    return regs, float(mp), float(T(mp / rho0)), float(rho0)
+
+
+def seeding_capacity(scene: Scene) -> int:
+    """upper bound on init_scene's particle count: 2^d per cell of the regions' bounding box"""
+    cfg, dim = scene.config, scene.dim
+    n = 1 << dim
+    for a in range(dim):
+        lo = min(g.bound_lo(dim)[a] for g in scene.geometry)
+        hi = max(g.bound_hi(dim)[a] for g in scene.geometry)
+        lc = max(0, int(math.floor((lo - cfg.origin[a]) / cfg.dh)) - 1)
+        hc = min(cfg.cells[a], int(math.ceil((hi - cfg.origin[a]) / cfg.dh)) + 1)
+        n *= max(0, hc - lc)
+    return n
+
+
 def init_scene(scene: Scene):
     """init_scene (scene.hpp:55-116): 2^d sub-cell lattice at +-dh/4 in every covered cell, cells
     visited row-major (axis 0 slowest), corners in bit order; first containing region owns the

@@ -66,6 +66,18 @@ class Context:
         v, keep = state.to_view()
         self.check(self.lib.mpm_state_upload(self.h, C.byref(v)))
 
+    def init_scene(self, scene: Scene) -> int:
+        """init_scene (scene.hpp:55-116) seeded on the device into this context:
+        the same particles, order and bits as scene.init_scene (except parabolic_sine's sin).
+        Returns the particle count; sets scene.mass_epsilon like init_scene."""
+        from .scene import seeding_constants
+
+        regs, mass, volume, rho0 = seeding_constants(scene)
+        arr = (capi.Region * len(regs))(*regs)
+        n = C.c_int64()
+        self.check(self.lib.mpm_init_scene(self.h, arr, len(regs), mass, volume, rho0, C.byref(n)))
+        return n.value
+
     def download(self, state: SimState) -> SimState:
         v, keep = state.output_view()
         self.check(self.lib.mpm_state_download(self.h, C.byref(v)))
@@ -171,6 +183,22 @@ class Context:
 
 # -------------------------------------------------------------------------------------------
 _CTX_CACHE: dict = {}
+
+
+def init_scene_device(scene: Scene, device: int = 0, capacity: int | None = None) -> Context:
+    """init_scene (scene.hpp:55-116) seeded directly on the device: returns a
+    Context holding the seeded state, with the same CFL refusal as init_scene for fluids."""
+    from .scene import FluidParams, seeding_capacity, seeding_constants
+
+    seeding_constants(scene)  # validates and sets mass_epsilon before the context copies the scene
+    ctx = Context(scene, capacity or seeding_capacity(scene), device)
+    ctx.n = ctx.init_scene(scene)
+    if isinstance(scene.material, FluidParams):
+        courant = cfl_report(scene.config, scene.material, ctx.max_speed())
+        if courant > 1:
+            ctx.close()
+            raise ValidationError(f"scene: CFL violation, Courant number {courant} > 1 (reduce dt or coarsen the grid)")
+    return ctx
 
 
 def _context_for(scene: Scene, n: int) -> Context:
