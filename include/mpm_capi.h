@@ -250,6 +250,13 @@ typedef struct mpm_region {
 int mpm_init_scene(mpm_ctx* ctx, const mpm_region* regions, int n_regions, double mass, double volume, double rho0,
                    int64_t* n_out);
 
+/* Asynchronous snapshots (run's snapshot policy, stepper.hpp:112-117): mpm_snapshot_begin gathers
+ * the current state in id order on the context stream and copies it to library-owned pinned host
+ * memory on a second stream, overlapping the steps that follow; mpm_snapshot_fetch (slot 0 or 1)
+ * waits for that copy and fills `s` (reference layout). A slot holds one snapshot at a time. */
+int mpm_snapshot_begin(mpm_ctx* ctx, int slot);
+int mpm_snapshot_fetch(mpm_ctx* ctx, int slot, mpm_state_view* s);
+
 /* ---- slab decomposition across GPUs ------------------------------------ */
 /* One context per GPU, global coordinates; the context owns the particles whose base cell along
  * x lies in [cell_lo, cell_hi) (multiples of the block edge, 16 in 2-D / 8 in 3-D). A step is

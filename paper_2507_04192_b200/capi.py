@@ -202,6 +202,8 @@ _PROTOS = {
     "mpm_local_count": (C.c_int64, [C.c_void_p]),
     "mpm_step_p2g_local": (C.c_int, [C.c_void_p]),
     "mpm_step_grid_interior": (C.c_int, [C.c_void_p]),
+    "mpm_snapshot_begin": (C.c_int, [C.c_void_p, C.c_int]),
+    "mpm_snapshot_fetch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(StateView)]),
     "mpm_init_scene": (C.c_int, [C.c_void_p, C.POINTER(Region), C.c_int, C.c_double, C.c_double, C.c_double,
                                  C.POINTER(C.c_int64)]),
     "mpm_slab_vjp_begin": (C.c_int, [C.c_void_p, C.POINTER(CotView)]),

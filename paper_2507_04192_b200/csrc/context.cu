@@ -81,6 +81,8 @@ struct CtxBase {
     virtual void slab_set(int lo, int hi, int64_t mig_cap) = 0;
     virtual void step_p2g_local() = 0;
     virtual void step_grid_interior() = 0;
+    virtual void snapshot_begin(int slot) = 0;
+    virtual void snapshot_fetch(int slot, mpm_state_view* s) = 0;
     virtual void init_scene_dev(const mpm_region* rg, int nreg, double mass, double volume, double rho0,
                                 int64_t* n_out) = 0;
     virtual void slab_vjp_begin(const mpm_cot_view* co) = 0;
@@ -292,6 +294,16 @@ template <class T, int D> struct Ctx : CtxBase {
             cudaFreeHost(st_host);
         if (stage_host)
             cudaFreeHost(stage_host);
+        for (auto& q : snaps) {
+            if (q.host)
+                cudaFreeHost(q.host);
+            if (q.gathered)
+                cudaEventDestroy(q.gathered);
+            if (q.ready)
+                cudaEventDestroy(q.ready);
+        }
+        if (copy_stream)
+            cudaStreamDestroy(copy_stream);
         if (own_stream)
             cudaStreamDestroy(own_stream);
     }
@@ -690,6 +702,78 @@ template <class T, int D> struct Ctx : CtxBase {
         s->n = n;
         s->step = step;
         s->time = time;
+    }
+
+    // ---- asynchronous snapshots (run's snapshot policy, stepper.hpp:112-117) -----
+    struct Snap {
+        Stage<T, D> dev{};
+        T* dbase = nullptr;
+        T* host = nullptr;
+        cudaEvent_t gathered{}, ready{};
+        int64_t n = 0, step = 0;
+        double time = 0;
+        bool pending = false;
+    };
+    Snap snaps[2];
+    cudaStream_t copy_stream{};
+    void snapshot_begin(int slot) override
+    {
+        if (slot < 0 || slot > 1)
+            throw ApiError(MPM_ERR_USAGE, "snapshot slot must be 0 or 1");
+        if (slab || n == 0)
+            throw ApiError(MPM_ERR_USAGE, "snapshot: no single-context state");
+        Snap& q = snaps[slot];
+        if (!q.dbase) {
+            q.dbase = alloc<T>(stage_elems);
+            size_t off = 0;
+            for (int f = 0; f < S_NFIELDS; ++f) {
+                q.dev.f[f] = q.dbase + off;
+                off += (size_t)cap * stage_comps<D>(f);
+            }
+            CK(cudaMallocHost(&q.host, stage_elems * sizeof(T)));
+            CK(cudaEventCreateWithFlags(&q.gathered, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&q.ready, cudaEventDisableTiming));
+            if (!copy_stream)
+                CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+        }
+        if (q.pending) // the previous snapshot in this slot must have left the staging buffer
+            CK(cudaEventSynchronize(q.ready));
+        // id-order gather on the compute stream (reads the current buffer before a later step
+        // overwrites it), the D2H copy on the copy stream, overlapping the following steps
+        launch("k_download", [&] { k_download<T, D><<<grid_for(n, 256), 256, 0, stream>>>(q.dev, buf[cur], int(n), has_aff, has_F); });
+        CK(cudaEventRecord(q.gathered, stream));
+        CK(cudaStreamWaitEvent(copy_stream, q.gathered, 0));
+        size_t off = 0;
+        for (int f = 0; f < S_NFIELDS; ++f) {
+            const size_t len = (size_t)n * stage_comps<D>(f);
+            CK(cudaMemcpyAsync(q.host + off, q.dev.f[f], len * sizeof(T), cudaMemcpyDeviceToHost, copy_stream));
+            off += (size_t)cap * stage_comps<D>(f);
+        }
+        CK(cudaEventRecord(q.ready, copy_stream));
+        q.n = n;
+        q.step = step;
+        q.time = time;
+        q.pending = true;
+    }
+    void snapshot_fetch(int slot, mpm_state_view* s) override
+    {
+        if (slot < 0 || slot > 1 || !snaps[slot].pending)
+            throw ApiError(MPM_ERR_USAGE, "snapshot_fetch: no snapshot in that slot");
+        Snap& q = snaps[slot];
+        CK(cudaEventSynchronize(q.ready));
+        void* dst[S_NFIELDS] = {s->x, s->v, s->mass, s->volume, s->rho, s->eps_eq, D == 2 ? s->sigma_zz : nullptr,
+                                s->sigma, s->grad_v, has_aff ? s->affine : nullptr, has_F ? s->def_grad : nullptr};
+        size_t off = 0;
+        for (int f = 0; f < S_NFIELDS; ++f) {
+            const size_t len = (size_t)q.n * stage_comps<D>(f);
+            if (dst[f])
+                std::memcpy(dst[f], q.host + off, len * sizeof(T));
+            off += (size_t)cap * stage_comps<D>(f);
+        }
+        s->n = q.n;
+        s->step = q.step;
+        s->time = q.time;
+        q.pending = false;
     }
 
     uint64_t digest() override
@@ -1668,6 +1752,8 @@ int mpm_state_download_local(mpm_ctx* c, mpm_state_view* s, int64_t* ids) { MPM_
 int mpm_slab_set(mpm_ctx* c, int cell_lo, int cell_hi, int64_t mig_cap) { MPM_CALL(c, c->impl->slab_set(cell_lo, cell_hi, mig_cap)); }
 int mpm_step_p2g_local(mpm_ctx* c) { MPM_CALL(c, c->impl->step_p2g_local()); }
 int mpm_step_grid_interior(mpm_ctx* c) { MPM_CALL(c, c->impl->step_grid_interior()); }
+int mpm_snapshot_begin(mpm_ctx* c, int slot) { MPM_CALL(c, c->impl->snapshot_begin(slot)); }
+int mpm_snapshot_fetch(mpm_ctx* c, int slot, mpm_state_view* s) { MPM_CALL(c, c->impl->snapshot_fetch(slot, s)); }
 int mpm_init_scene(mpm_ctx* c, const mpm_region* regions, int n_regions, double mass, double volume, double rho0,
                    int64_t* n_out)
 {

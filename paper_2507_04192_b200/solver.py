@@ -78,6 +78,16 @@ class Context:
         self.check(self.lib.mpm_init_scene(self.h, arr, len(regs), mass, volume, rho0, C.byref(n)))
         return n.value
 
+    def snapshot_begin(self, slot: int):
+        self.check(self.lib.mpm_snapshot_begin(self.h, int(slot)))
+
+    def snapshot_fetch(self, slot: int, template: SimState) -> SimState:
+        out = template.copy()
+        v, keep = out.output_view()
+        self.check(self.lib.mpm_snapshot_fetch(self.h, int(slot), C.byref(v)))
+        out.sync_from(v, keep)
+        return out
+
     def download(self, state: SimState) -> SimState:
         v, keep = state.output_view()
         self.check(self.lib.mpm_state_download(self.h, C.byref(v)))
@@ -266,6 +276,11 @@ def run(scene: Scene, state: SimState, num_steps: int, stride: int, force: bool 
     ctx.upload(state)
     t0 = _time.perf_counter()
     s = 0
+    pending = []  # snapshot slots in flight (their D2H copies overlap the following steps)
+
+    def take():
+        res.snapshots.append(ctx.snapshot_fetch(pending.pop(0), state))
+
     while s < num_steps:
         if observer is not None:
             chunk = 1
@@ -280,8 +295,16 @@ def run(scene: Scene, state: SimState, num_steps: int, stride: int, force: bool 
             st = ctx.download(state.copy())
             observer(st, ctx.grid_download())
         if stride > 0 and cur_step % stride == 0 and cur_step != num_steps:
-            res.snapshots.append(ctx.download(state.copy()))
+            free = ({0, 1} - set(pending))
+            if not free:
+                take()
+                free = ({0, 1} - set(pending))
+            slot = min(free)
+            ctx.snapshot_begin(slot)
+            pending.append(slot)
     t1 = _time.perf_counter()
+    while pending:
+        take()
     if num_steps > 0:
         res.snapshots.append(ctx.download(state.copy()))
         res.seconds_per_1000_steps = (t1 - t0) / num_steps * 1000.0

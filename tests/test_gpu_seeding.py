@@ -106,3 +106,22 @@ def test_device_seeding_capacity_and_cfl():
     s.geometry[0].velocity = VelocityExpr("constant", value=[5000.0, 0.0])
     with pytest.raises(ValidationError):
         init_scene_device(s)  # init_scene's CFL refusal
+
+
+def test_run_async_snapshots_equal_synchronous_downloads():
+    """run's snapshots (two asynchronous slots, reused) equal plain downloads at the same steps"""
+    from paper_2507_04192_b200.solver import Context, run
+
+    s = c1_column()
+    st = init_scene(s)
+    res = run(s, st, 40, 5)
+    assert [x.step for x in res.snapshots] == list(range(0, 41, 5))
+    ctx = Context(s, st.particles.size())
+    ctx.upload(st)
+    for snap in res.snapshots[1:]:
+        ctx.advance(5, nan_guard=True)
+        want = ctx.download(st.copy())
+        assert want.step == snap.step and want.time == snap.time
+        for f in ("x", "v", "sigma", "rho", "volume", "grad_v", "eps_eq", "sigma_zz"):
+            assert np.array_equal(getattr(snap.particles, f), getattr(want.particles, f)), (snap.step, f)
+    ctx.close()
