@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     int* pk = reinterpret_cast<int*>(smem_raw + S::SMEM_RAW);                  // [3][2][CAP] (perm, col)
     T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_RAW + S::SMEM_PK);      // [NCOL][NSRC][NF]
     __shared__ int it_start[S::MAXIT], it_len[S::MAXIT], it_lvl[S::MAXIT], it_last[S::MAXIT];
-    __shared__ int nit_s, ccount[NBC], cst[NBC + 1];
+    __shared__ int nit_s, ccount[2][NBC]; // per-item column counts, double-buffered
     if (st->abort)
         return;
     const int nocc = *n_occ;
@@ -914,8 +914,11 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     const bool mid = o0 == 1;
     const T xoff = o0 == 0 ? T(1.5) : (o0 == 1 ? T(1) : T(0.5)); // h = fx - xoff (bspline.hpp:330-335)
     const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
-    const T* fld[NRAW] = {P.x[0], P.x[1], P.x[2], P.v[0], P.v[1], P.v[2], P.m, P.V,
-                          P.sig[0], P.sig[1], P.sig[2], P.sig[3], P.sig[4], P.sig[5]};
+    // raw rows x0..2 v0..2 m V sigma0..5 = PLay fields 0..7 and SIG..SIG+5 of the strided buffer
+    // (one base pointer and a stride instead of 14 pointers reloaded from the parameter bank)
+    using PL = PLay<3>;
+    static_assert(PL::M == RM && PL::VOL == RVOL && PL::SIG == RS + 2 && RS + 6 == NRAW, "raw row map");
+    const long long SI = P.S;
 
     for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
         const int Q = occ[w];
@@ -968,14 +971,16 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
             T* rb = raw + (j & 1) * NRAW * CAP;
             const int len = it_len[j];
             for (int r = tid; r < len; r += blockDim.x) {
-                const int src = pp[r];
+                const T* q = P.base + pp[r];
 #pragma unroll
                 for (int f = 0; f < NRAW; ++f)
-                    cp_async_t<T>(rb + f * CAP + r, fld[f] + src);
+                    cp_async_t<T>(rb + f * CAP + r, q + (f < RS ? f : f + 2) * SI);
             }
         };
-        if (tid < NBC)
-            ccount[tid] = 0;
+        if (tid < NBC) {
+            ccount[0][tid] = 0;
+            ccount[1][tid] = 0;
+        }
         if (nit > 0)
             issue_pk(0);
         if (nit > 1)
@@ -1013,26 +1018,22 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                     acc[i1][2][f] = T(0);
                 }
             }
-            __syncthreads();
-            for (int c = tid; c < C::NCOL; c += blockDim.x) {
-                const int n0 = c / TE, n1 = c % TE;
-                T sum[NF];
-#pragma unroll
-                for (int f = 0; f < NF; ++f)
-                    sum[f] = T(0);
+            __syncthreads(); // slots complete
+            // one (node column, field) per task: 700 short fixed-order sums over all threads
+            for (int t = tid; t < C::NCOL * NF; t += blockDim.x) {
+                const int c = t / NF, f = t - c * NF;
+                const int n0 = c / TE, n1 = c - n0 * TE;
+                T sum = T(0);
 #pragma unroll
                 for (int q = 0; q < NSRC; ++q) {
                     const int b0 = n0 - q / 3, b1 = n1 - q % 3;
                     if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
-#pragma unroll
-                        for (int f = 0; f < NF; ++f)
-                            sum[f] += slots[(c * NSRC + q) * NF + f];
+                        sum += slots[(c * NSRC + q) * NF + f];
                 }
-#pragma unroll
-                for (int f = 0; f < NF; ++f)
-                    part[f * C::TN + z * C::NCOL + c] = sum[f];
+                part[f * C::TN + z * C::NCOL + c] = sum;
             }
-            __syncthreads();
+            // no closing barrier: the next emit's slot writes follow the next item's top barrier
+            // (or the explicit one between the two final emits)
         };
 
         for (int j = 0; j < nit; ++j) {
@@ -1047,10 +1048,13 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
             // sigma -> V sigma) and count its column (records are column-sorted inside a level)
             const int len = it_len[j];
             const int* col = pk + (j % 3) * 2 * CAP + CAP;
+            int* cnt = ccount[j & 1];
+            if (tid < NBC) // the other buffer was last read before this item's top barrier
+                ccount[(j + 1) & 1][tid] = 0;
             {
                 T* Rw = raw + (j & 1) * NRAW * CAP;
                 for (int r = tid; r < len; r += blockDim.x) {
-                    atomicAdd(&ccount[col[r] & (NBC - 1)], 1);
+                    atomicAdd(&cnt[col[r] & (NBC - 1)], 1);
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         const T u = (Rw[(RX + a) * CAP + r] - sc.origin[a]) * sc.inv_dh;
@@ -1065,27 +1069,29 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                         Rw[(RS + q) * CAP + r] *= V;
                 }
             }
-            __syncthreads();
-            if (tid < 32) {
-                const int c0 = ccount[2 * tid], c1 = ccount[2 * tid + 1];
+            __syncthreads(); // converted records and the counts are complete
+            // every warp scans the 64 column counts itself (no extra barrier): lane l holds the
+            // exclusive prefix of columns 2l and 2l+1
+            int kb, ke;
+            {
+                const int lane = tid & 31;
+                const int c0 = cnt[2 * lane], c1 = cnt[2 * lane + 1];
                 int v = c0 + c1;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
                     const int t = __shfl_up_sync(0xffffffffu, v, d);
-                    if (tid >= d)
+                    if (lane >= d)
                         v += t;
                 }
                 const int excl = v - c0 - c1;
-                cst[2 * tid] = excl;
-                cst[2 * tid + 1] = excl + c0;
-                if (tid == 31)
-                    cst[NBC] = v;
-                ccount[2 * tid] = 0; // ready for the next item (counted after the next top barrier)
-                ccount[2 * tid + 1] = 0;
+                const int src = bc >> 1;
+                const int e = __shfl_sync(0xffffffffu, excl, src);
+                const int a0 = __shfl_sync(0xffffffffu, c0, src);
+                const int a1 = __shfl_sync(0xffffffffu, c1, src);
+                kb = (bc & 1) ? e + a0 : e;
+                ke = kb + ((bc & 1) ? a1 : a0);
             }
-            __syncthreads();
             const T* R = raw + (j & 1) * NRAW * CAP;
-            const int kb = cst[bc], ke = cst[bc + 1];
             for (int k = kb; k < ke; ++k) {
                 T f[3];
 #pragma unroll
@@ -1147,14 +1153,13 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                     }
                 }
             }
-            if (it_last[j]) {
-                __syncthreads();
+            if (it_last[j]) // slots were last read before the previous emit's closing barrier
                 emit_and_reduce(it_lvl[j]);
-            }
         }
         cp_async_wait_all();
         __syncthreads();
         emit_and_reduce(B);
+        __syncthreads(); // slots reused by the next emit right away
         emit_and_reduce(B + 1);
     }
 }
