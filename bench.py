@@ -152,7 +152,7 @@ def _cpu_worker(args):
     sys.path.insert(0, str(ROOT))
     from oracle import CpuOracle  # test infrastructure: the CPU baseline, never the product path
     from paper_2507_04192_b200.presets import CONFIGS
-    s = CONFIGS[cfg](dtype)
+    s = CONFIGS[cfg](dtype=dtype)
     o = CpuOracle(kind)
     st = o.init_scene(s)
     secs = o.run_seconds_per_1000(s, st, steps) / 1000.0 * steps
@@ -209,7 +209,7 @@ def bench_b200(a, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    s = CONFIGS[a.config](a.dtype)
+    s = CONFIGS[a.config](dtype=a.dtype)
     st = init_scene(s)
     n = st.particles.size()
     ctx = Context(s, n, device=local)
@@ -319,7 +319,7 @@ def bench_slab(a, rank, world, local):
         n_total = n * world
         scaling = "weak"
     else:
-        s = CONFIGS[a.config](a.dtype)
+        s = CONFIGS[a.config](dtype=a.dtype)
         full = init_scene(s)
         plan = SlabPlan.make(s, world, full.particles.x)
         dom = GpuSlabDomain(s, plan, rank, full, None, device=local)

@@ -57,3 +57,17 @@ def test_f32_seeding_matches_reference_layout():
     s = c1_column("f32")
     st = init_scene(s)
     assert st.particles.x.dtype == np.float32 and st.particles.size() == 20000
+
+
+def test_presets_build_with_dtype_keyword():
+    """bench.py builds every config as CONFIGS[name](dtype=...); C1-C3 seed on the host here"""
+    from paper_2507_04192_b200 import init_scene
+    from paper_2507_04192_b200.presets import CONFIGS
+
+    for name, make in CONFIGS.items():
+        for dt in ("f64", "f32"):
+            s = make(dtype=dt)
+            assert s.np_dtype == (np.float64 if dt == "f64" else np.float32), name
+            if name in ("C1", "C3"):
+                n = init_scene(s).particles.size()
+                assert n == {"C1": 20000, "C3": 102400}[name]
