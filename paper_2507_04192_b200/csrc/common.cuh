@@ -139,7 +139,7 @@ struct DevStatus {
     int pad2;
 };
 
-__global__ inline void k_reset_status(DevStatus* st, long long step)
+__global__ void k_reset_status(DevStatus* st, long long step)
 {
     DevStatus s{};
     s.den_pid = 0x7fffffff;
@@ -150,7 +150,7 @@ __global__ inline void k_reset_status(DevStatus* st, long long step)
 }
 
 // per-step reset that keeps the device-maintained step counter (capturable in a graph)
-__global__ inline void k_reset_flags(DevStatus* st)
+__global__ void k_reset_flags(DevStatus* st)
 {
     DevStatus s{};
     s.den_pid = 0x7fffffff;

@@ -1131,7 +1131,7 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
                                                   const int* __restrict__ n_occ, CBuf<T, D> ci, const DevStatus* st)
 {
     using C = Cfg<D>;
-    constexpr int TE = C::TE, TN = C::TN, NF = 1 + 2 * D;
+    constexpr int TE = C::TE, TN = C::TN; // tile fields: 1 + 2 D
     extern __shared__ unsigned char smem_raw[];
     T* tile = reinterpret_cast<T*>(smem_raw); // [NF][TN]: gm, gmom[D], gf[D]
     if (st->abort)

@@ -1701,7 +1701,7 @@ template <class T, int D, bool TRACKF> struct G2PStage {
     static constexpr int NSF = 2 * D + 4 + (D == 2 ? 1 : 0) + Cfg<D>::NS + (TRACKF ? D * D : 0);
     static constexpr int THREADS = 256;
     static constexpr size_t TILE = sizeof(T) * 2 * D * Cfg<D>::TN;
-    static constexpr size_t SMEM = TILE + sizeof(T) * 2 * NSF * THREADS; // tile + 2 slots
+    static constexpr size_t SMEM = TILE + sizeof(T) * 2 * NSF * THREADS + sizeof(int) * 2 * THREADS; // tile + 2 slots (+ pid)
 };
 
 template <class T, int D, int FLAGS, bool APIC, bool TRACKF>
@@ -1717,6 +1717,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
     extern __shared__ unsigned char smem_raw[];
     T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]: v[0..D), v - vold[0..D) (formed once per node)
     T* stg = tile + 2 * D * TN;               // [2][NSF][NT]: this thread's column only
+    int* stg_pid = reinterpret_cast<int*>(stg + 2 * NSF * NT); // [2][NT]
     if (st->abort)
         return;
     const int nocc = *n_occ;
@@ -1736,6 +1737,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
             for (int k = 0; k < D * D; ++k)
                 cp_async_t<T>(b + (PL::SIG + C::NS + k) * NT, q + (PL::F + k) * SI);
         }
+        cp_async4(stg_pid + slot * NT + tid, Pin.pid + src); // its id too: no exposed load before the stores
     };
     static_assert(PL::SIG + C::NS + (TRACKF ? D * D : 0) == NSF, "staging mirrors the PLay field order");
     for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
@@ -1779,7 +1781,6 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
         __syncthreads();
         int slot = 0;
         for (int i = i0; i < s1; i += NT) {
-            const int src = src_a;
             // keep the next particle's fields and the one after's index in flight
             src_a = src_b;
             src_b = i + 2 * NT < s1 ? perm[i + 2 * NT] : -1;
@@ -1788,6 +1789,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
             cp_async_commit();
             asm volatile("cp.async.wait_group 1;\n" ::: "memory"); // this thread's slot `slot` landed
             const T* sb = stg + slot * NSF * NT + tid;
+            const int pid = stg_pid[slot * NT + tid];
             slot ^= 1;
             T x[D], v[D];
 #pragma unroll
@@ -1950,7 +1952,6 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                         Fm[k] = Fn[k];
                 }
             }
-            const int pid = Pin.pid[src];
             // write the new state at sorted slot i (field k at o + k * SO)
             T* o = Pout.base + i;
 #pragma unroll

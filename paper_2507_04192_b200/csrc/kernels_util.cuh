@@ -307,7 +307,7 @@ __global__ void k_seed_write(DevScene<T, D> sc, SeedBox bx, const mpm_region* __
 }
 
 // slab step report for the caller's collective: (failed, left toward -x, left toward +x)
-__global__ inline void k_report(const DevStatus* st, long long* out)
+__global__ void k_report(const DevStatus* st, long long* out)
 {
     out[0] = st->abort ? 1 : 0;
     out[1] = st->mig_lo;
