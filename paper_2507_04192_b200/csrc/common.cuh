@@ -33,6 +33,10 @@ template <int D> struct Cfg {
     static constexpr int SEGS = D == 2 ? 8 : 2;            // march segments (B % SEGS == 0, >= 2 levels each)
 };
 
+// index of node (tile level z, node column col) inside a P2G partial tile: z fastest, so that
+// k_grid's threads (node-block-local index, z fastest) read consecutive addresses
+template <int D> __host__ __device__ __forceinline__ int ptile(int z, int col) { return col * Cfg<D>::TE + z; }
+
 // packed symmetric index (i,j) -> slot; 2-D: 00 11 01, 3-D: 00 11 22 01 02 12
 template <int D> __host__ __device__ constexpr int sym_idx(int i, int j)
 {

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, co
                     }
                 }
                 // node z of this column is final for this segment
-                const int idx = z * C::NCOL + col;
+                const int idx = ptile<D>(z, col);
 #pragma unroll
                 for (int f = 0; f < NF; ++f) {
                     part[f * C::TN + idx] = acc[0][f];
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, co
                 for (int k = 0; k < 2; ++k)
 #pragma unroll
                     for (int f = 0; f < NF; ++f)
-                        part[f * C::TN + (ze + k) * C::NCOL + col] = acc[k][f];
+                        part[f * C::TN + ptile<D>(ze + k, col)] = acc[k][f];
             } else {
 #pragma unroll
                 for (int k = 0; k < 2; ++k)
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, co
             for (int k = 0; k < 2; ++k)
 #pragma unroll
                 for (int f = 0; f < NF; ++f) {
-                    T* p = part + f * C::TN + (ze + k) * C::NCOL + col;
+                    T* p = part + f * C::TN + ptile<D>(ze + k, col);
                     *p = *p + ov[k][f];
                 }
         }
@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(StageCfg<T, D>::THREADS, 1)
                 }
 #pragma unroll
                 for (int f = 0; f < NF; ++f)
-                    part[f * C::TN + z * C::NCOL + c] = sum[f];
+                    part[f * C::TN + ptile<D>(z, c)] = sum[f];
             }
         };
 
@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(Stage3Cfg<T>::THREADS, 2)
                 }
 #pragma unroll
                 for (int f = 0; f < NF; ++f)
-                    part[f * C::TN + z * C::NCOL + c] = sum[f];
+                    part[f * C::TN + ptile<3>(z, c)] = sum[f];
             }
         };
 
@@ -1030,7 +1030,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                     if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
                         sum += slots[(c * NSRC + q) * NF + f];
                 }
-                part[f * C::TN + z * C::NCOL + c] = sum;
+                part[f * C::TN + ptile<3>(z, c)] = sum;
             }
             // no closing barrier: the next emit's slot writes follow the next item's top barrier
             // (or the explicit one between the two final emits)
@@ -1315,7 +1315,7 @@ __global__ void __launch_bounds__(Lane3Cfg<T>::THREADS, 1)
                     if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
                         sum += slots[(cidx * NSRC + q) * NF + f];
                 }
-                part[f * C::TN + z * C::NCOL + cidx] = sum;
+                part[f * C::TN + ptile<3>(z, cidx)] = sum;
             }
             __syncthreads();
         };
@@ -1607,7 +1607,7 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
                     else
                         colx = colx * C::TE + t;
                 }
-                tl = z * C::NCOL + colx;
+                tl = ptile<D>(z, colx);
                 const T* part = partials + (size_t)Qid * C::NF * C::TN + tl;
                 m += part[0];
 #pragma unroll
