@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, co
                                 for (int b = 0; b < D; ++b)
                                     sg += sig[sym_idx<D>(a, b)] * gw[b];
                                 acc[o2][1 + a] += mphi * vel[a];
-                                acc[o2][1 + D + a] += -(V * sg); // gravity: + g m_i per node (k_grid)
+                                acc[o2][1 + D + a] = acc[o2][1 + D + a] - V * sg; // gravity: + g m_i per node (k_grid)
                             }
                         }
                     }
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(StageCfg<T, D>::THREADS, 1)
 #pragma unroll
                         for (int a = 0; a < D; ++a) {
                             acc[q][1 + a] += phi * mv[a];
-                            acc[q][1 + D + a] -= wz[q] * u[a] + dwz[q] * t[a];
+                            acc[q][1 + D + a] = acc[q][1 + D + a] - wz[q] * u[a] - dwz[q] * t[a]; // two FMAs
                         }
                     }
                 }
@@ -827,7 +827,7 @@ __global__ void __launch_bounds__(Stage3Cfg<T>::THREADS, 2)
 #pragma unroll
                             for (int a = 0; a < 3; ++a) {
                                 acc[o1][q][1 + a] += phi * mv[a];
-                                acc[o1][q][4 + a] -= wz[q] * u[a] + dwz[q] * t[a];
+                                acc[o1][q][4 + a] = acc[o1][q][4 + a] - wz[q] * u[a] - dwz[q] * t[a];
                             }
                         }
                     }
@@ -1149,7 +1149,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                         for (int q = 0; q < 3; ++q)
 #pragma unroll
                             for (int a = 0; a < 3; ++a)
-                                acc[o1][q][FO + a] -= wz[q] * u[a] + dwz[q] * t[a];
+                                acc[o1][q][FO + a] = acc[o1][q][FO + a] - wz[q] * u[a] - dwz[q] * t[a]; // two FMAs
                     }
                 }
             }
@@ -1395,9 +1395,9 @@ __global__ void __launch_bounds__(Lane3Cfg<T>::THREADS, 1)
                     acc[c][2] += mv1 * wgt;
                     acc[c][3] += mv2 * wgt;
                     // f -= V sigma grad phi (transfer.hpp:420-427); gravity is added per node in k_grid
-                    acc[c][4] -= s00 * g0 + s01 * g1 + s02 * g2;
-                    acc[c][5] -= s01 * g0 + s11 * g1 + s12 * g2;
-                    acc[c][6] -= s02 * g0 + s12 * g1 + s22 * g2;
+                    acc[c][4] = acc[c][4] - s00 * g0 - s01 * g1 - s02 * g2;
+                    acc[c][5] = acc[c][5] - s01 * g0 - s11 * g1 - s12 * g2;
+                    acc[c][6] = acc[c][6] - s02 * g0 - s12 * g1 - s22 * g2;
                 }
             }
             if (it_last[j]) {
