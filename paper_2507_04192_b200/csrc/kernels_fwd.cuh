@@ -638,19 +638,7 @@ __global__ void __launch_bounds__(StageCfg<T, D>::THREADS, 1)
     }
 }
 
-// 3-D P2G (PIC / FLIP / blend): thread = (base column, x-offset o0), looping the 3 y-offsets
-// (63 accumulators: 3 node columns x rolling 3-node window). 3 adjacent lanes share a base
-// column -> broadcast record reads; 192 threads and ~110 KB smem -> 2 CTAs per SM overlap each
-// other's barrier phases. Records hold the fractional offsets; weights are formed per visit.
-template <class T> struct Stage3Cfg {
-    static constexpr int NBC = 64, THREADS = 192, NSRC = 9;
-    static constexpr int NREC = 3 + 1 + 3 + 6; // fx[3], m, m v[3], V sigma[6]
-    static constexpr int CAP = sizeof(T) == 8 ? 512 : 1024;
-    static constexpr size_t SMEM_REC = sizeof(T) * NREC * CAP;
-    static constexpr size_t SMEM_SLOT = sizeof(T) * Cfg<3>::NCOL * NSRC * Cfg<3>::NF;
-    static constexpr size_t SMEM = SMEM_REC + SMEM_SLOT;
-};
-
+// quadratic B-spline weight and derivative of stencil offset o (bspline.hpp:330-344)
 template <class T> __device__ __forceinline__ void quad_w(T fx, int o, T inv_dh, T& w, T& dw)
 {
     if (o == 0) {
@@ -668,193 +656,17 @@ template <class T> __device__ __forceinline__ void quad_w(T fx, int o, T inv_dh,
     }
 }
 
-template <class T>
-__global__ void __launch_bounds__(Stage3Cfg<T>::THREADS, 2)
-    k_p2g_staged3(DevScene<T, 3> sc, PBuf<T, 3> P, const int* __restrict__ perm, const int* __restrict__ keys,
-                  const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ lstart,
-                  const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials,
-                  const DevStatus* st)
-{
-    using C = Cfg<3>;
-    using S = Stage3Cfg<T>;
-    constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC;
-    constexpr int RFX = 0, RM = 3, RMV = 4, RVS = 7;
-    extern __shared__ unsigned char smem_raw[];
-    T* rec = reinterpret_cast<T*>(smem_raw);                 // [NREC][CAP]
-    T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_REC); // [NCOL][NSRC][NF]
-    __shared__ int lvl[B + 1];
-    __shared__ int ccount[NBC], cst[NBC + 1];
-    if (st->abort)
-        return;
-    const int nocc = *n_occ;
-    const int tid = threadIdx.x;
-    const int bc = tid / 3, o0 = tid % 3;
-    const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
-
-    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
-        const int Q = occ[w];
-        const int s0 = bstart[Q], s1 = bend[Q];
-        __syncthreads();
-        if (tid == 0) { // level starts: suffix minimum over the recorded non-empty levels
-            int nxt = s1;
-            lvl[B] = s1 - s0;
-            for (int z = B - 1; z >= 0; --z) {
-                const int v = lstart[Q * (B + 1) + z];
-                nxt = (v >= s0 && v < s1) ? v : nxt;
-                lvl[z] = nxt - s0;
-            }
-        }
-        T* part = partials + (size_t)Q * NF * C::TN;
-        T acc[3][3][NF]; // [o1][window][field]
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-#pragma unroll
-                for (int f = 0; f < NF; ++f)
-                    acc[a][k][f] = T(0);
-
-        auto emit_and_reduce = [&](int z) {
-#pragma unroll
-            for (int o1 = 0; o1 < 3; ++o1) {
-                const int ncol = (bc0 + o0) * TE + bc1 + o1;
-#pragma unroll
-                for (int f = 0; f < NF; ++f) {
-                    slots[(ncol * NSRC + o0 * 3 + o1) * NF + f] = acc[o1][0][f];
-                    acc[o1][0][f] = acc[o1][1][f];
-                    acc[o1][1][f] = acc[o1][2][f];
-                    acc[o1][2][f] = T(0);
-                }
-            }
-            __syncthreads();
-            for (int c = tid; c < C::NCOL; c += blockDim.x) {
-                const int n0 = c / TE, n1 = c % TE;
-                T sum[NF];
-#pragma unroll
-                for (int f = 0; f < NF; ++f)
-                    sum[f] = T(0);
-#pragma unroll
-                for (int q = 0; q < NSRC; ++q) {
-                    const int b0 = n0 - q / 3, b1 = n1 - q % 3;
-                    if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
-#pragma unroll
-                        for (int f = 0; f < NF; ++f)
-                            sum[f] += slots[(c * NSRC + q) * NF + f];
-                }
-#pragma unroll
-                for (int f = 0; f < NF; ++f)
-                    part[f * C::TN + ptile<3>(z, c)] = sum[f];
-            }
-        };
-
-        for (int z = 0; z < B; ++z) {
-            __syncthreads(); // lvl ready, previous level's slots reduced
-            const int l0 = lvl[z], nl = lvl[z + 1] - l0;
-            for (int ch = 0; ch * CAP < nl || ch == 0; ++ch) {
-                const int b0 = l0 + ch * CAP, cl = max(0, min(CAP, nl - ch * CAP));
-                if (ch > 0)
-                    __syncthreads();
-                if (tid < NBC)
-                    ccount[tid] = 0;
-                __syncthreads();
-                for (int r = tid; r < cl; r += blockDim.x) {
-                    const int src = __ldg(perm + s0 + b0 + r);
-                    const int lc = __ldg(keys + s0 + b0 + r) & (NBC - 1);
-                    atomicAdd(&ccount[lc], 1);
-                    const T m = __ldg(P.m + src), V = __ldg(P.V + src);
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        const T u = (__ldg(P.x[a] + src) - sc.origin[a]) * sc.inv_dh;
-                        rec[(RFX + a) * CAP + r] = u - dfloor<T>(u - T(0.5));
-                        rec[(RMV + a) * CAP + r] = m * __ldg(P.v[a] + src);
-                    }
-                    rec[RM * CAP + r] = m;
-#pragma unroll
-                    for (int q = 0; q < 6; ++q)
-                        rec[(RVS + q) * CAP + r] = V * __ldg(P.sig[q] + src);
-                }
-                __syncthreads();
-                if (tid < 32) { // exclusive scan of the 64 column counts (records are column-sorted)
-                    const int c0 = ccount[2 * tid], c1 = ccount[2 * tid + 1];
-                    int v = c0 + c1;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const int t = __shfl_up_sync(0xffffffffu, v, d);
-                        if (tid >= d)
-                            v += t;
-                    }
-                    const int excl = v - c0 - c1;
-                    cst[2 * tid] = excl;
-                    cst[2 * tid + 1] = excl + c0;
-                    if (tid == 31)
-                        cst[NBC] = v;
-                }
-                __syncthreads();
-                const int kb = cst[bc], ke = cst[bc + 1];
-                for (int k = kb; k < ke; ++k) {
-                    T wx, dwx;
-                    quad_w<T>(rec[(RFX + 0) * CAP + k], o0, sc.inv_dh, wx, dwx);
-                    const T fy = rec[(RFX + 1) * CAP + k], fz = rec[(RFX + 2) * CAP + k];
-                    T wy[3], dwy[3], wz[3], dwz[3];
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) {
-                        quad_w<T>(fy, q, sc.inv_dh, wy[q], dwy[q]);
-                        quad_w<T>(fz, q, sc.inv_dh, wz[q], dwz[q]);
-                    }
-                    const T m = rec[RM * CAP + k];
-                    T mv[3], vs[6];
-#pragma unroll
-                    for (int a = 0; a < 3; ++a)
-                        mv[a] = rec[(RMV + a) * CAP + k];
-#pragma unroll
-                    for (int q = 0; q < 6; ++q)
-                        vs[q] = rec[(RVS + q) * CAP + k];
-#pragma unroll
-                    for (int o1 = 0; o1 < 3; ++o1) {
-                        // grad phi = (dwx wy wz, wx dwy wz, wx wy dwz): V sigma grad phi = wz u + dwz t
-                        const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
-                        T u[3], t[3];
-#pragma unroll
-                        for (int r = 0; r < 3; ++r) {
-                            u[r] = vs[sym_idx<3>(r, 0)] * p1 + vs[sym_idx<3>(r, 1)] * p2;
-                            t[r] = vs[sym_idx<3>(r, 2)] * pw;
-                        }
-                        const T mpw = m * pw;
-#pragma unroll
-                        for (int q = 0; q < 3; ++q) {
-                            const T phi = pw * wz[q];
-                            acc[o1][q][0] += mpw * wz[q];
-#pragma unroll
-                            for (int a = 0; a < 3; ++a) {
-                                acc[o1][q][1 + a] += phi * mv[a];
-                                acc[o1][q][4 + a] = acc[o1][q][4 + a] - wz[q] * u[a] - dwz[q] * t[a];
-                            }
-                        }
-                    }
-                }
-            }
-            __syncthreads(); // records of this level consumed, slots free
-            emit_and_reduce(z);
-        }
-        __syncthreads();
-        emit_and_reduce(B);
-        __syncthreads();
-        emit_and_reduce(B + 1);
-    }
-}
-
-// 3-D P2G, asynchronous pipeline (PIC / FLIP / blend). Same deterministic march as
-// k_p2g_staged3, but the staging is software-pipelined with cp.async (LDGSTS): work items are
+// 3-D P2G, asynchronous pipeline (PIC / FLIP / blend). Thread = (base column, x-offset o0),
+// looping the 3 y-offsets: 63 accumulators (3 node columns x a rolling 3-node window along z);
+// the 3 lanes of a column read its particle records as shared-memory broadcasts. The staging
+// is software-pipelined with cp.async (LDGSTS): work items are
 // (base level, chunk <= CAP particles); item j+2's perm/keys and item j+1's particle fields
 // are in flight while item j is marched, so the dependent gathers through the sort
 // permutation never stall the CTA. Raw fields are staged (x, v, m, V, sigma); fractional
 // offsets, m v and V sigma are formed per visit. One CTA per SM, full register file.
 template <class T, bool WIDE = true> struct Pipe3Cfg {
-    // SPLIT (f64): two warp groups share the staged records, one accumulates mass + momentum,
-    // the other the force -> half the accumulators per thread, twice the warps per SM
-    static constexpr bool SPLIT = false; // measured: 0.597 ms vs 0.583 ms unsplit (C4 f64) -- kept off
     static constexpr int LANES = WIDE ? 576 : 192;
-    static constexpr int NBC = 64, THREADS = SPLIT ? 2 * LANES : LANES, NSRC = 9, NRAW = 14, MAXIT = 64;
+    static constexpr int NBC = 64, THREADS = LANES, NSRC = 9, NRAW = 14, MAXIT = 64;
     static constexpr int CAP = 640;
     static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
     static constexpr size_t SMEM_PK = sizeof(int) * 3 * 2 * CAP;
@@ -892,8 +704,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     using S = Pipe3Cfg<T, WIDE>;
     constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW;
     constexpr int NO1 = WIDE ? 1 : 3; // y-offsets handled per thread
-    constexpr bool SPLIT = S::SPLIT;
-    constexpr int NA = SPLIT ? 4 : NF; // accumulated fields per thread
+    constexpr int NA = NF; // accumulated fields per thread
     // raw field rows: x0..2, v0..2, m, V, sig0..5
     constexpr int RX = 0, RV = 3, RM = 6, RVOL = 7, RS = 8;
     extern __shared__ unsigned char smem_raw[];
@@ -906,8 +717,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
         return;
     const int nocc = *n_occ;
     const int tid = threadIdx.x;
-    const int grp = SPLIT ? tid / S::LANES : 0;      // 0: mass + momentum (+ force if !SPLIT), 1: force
-    const int lt = SPLIT ? tid % S::LANES : tid;
+    const int lt = tid;
     const int bc = WIDE ? lt / 9 : lt / 3;
     const int o0 = WIDE ? (lt % 9) / 3 : lt % 3;
     const int o1t = WIDE ? lt % 3 : 0; // WIDE: this thread's y-offset
@@ -1007,12 +817,9 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
             for (int i1 = 0; i1 < NO1; ++i1) {
                 const int o1 = WIDE ? o1t : i1;
                 const int ncol = (bc0 + o0) * TE + bc1 + o1;
-                // group 0 owns fields [0, NA) (m, p), group 1 fields [4, 7) (f)
-                const int nfg = (!SPLIT || grp == 0) ? NA : 3, f0 = grp == 0 ? 0 : 4;
 #pragma unroll
                 for (int f = 0; f < NA; ++f) {
-                    if (f < nfg)
-                        slots[(ncol * NSRC + o0 * 3 + o1) * NF + f0 + f] = acc[i1][0][f];
+                    slots[(ncol * NSRC + o0 * 3 + o1) * NF + f] = acc[i1][0][f];
                     acc[i1][0][f] = acc[i1][1][f];
                     acc[i1][1][f] = acc[i1][2][f];
                     acc[i1][2][f] = T(0);
@@ -1118,7 +925,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
 #pragma unroll
                 for (int q = 0; q < 6; ++q)
                     vs[q] = R[(RS + q) * CAP + k];
-                if (!SPLIT || grp == 0) {
+                {
 #pragma unroll
                     for (int o1 = 0; o1 < NO1; ++o1) {
                         const T pw = wx * wy[o1];
@@ -1133,8 +940,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                         }
                     }
                 }
-                if (!SPLIT || grp == 1) {
-                    constexpr int FO = SPLIT ? 0 : 4; // force slots in acc
+                {
+                    constexpr int FO = 4; // force slots in acc
 #pragma unroll
                     for (int o1 = 0; o1 < NO1; ++o1) {
                         // grad phi = (dwx wy wz, wx dwy wz, wx wy dwz): V sigma grad phi = wz u + dwz t
