@@ -645,17 +645,8 @@ template <class T, int D> struct Ctx : CtxBase {
             throw ApiError(MPM_ERR_USAGE, "state view missing required fields");
         if (has_aff && !s->affine)
             throw ApiError(MPM_ERR_USAGE, "APIC scheme needs the affine field");
+        const int64_t n_prev = n;
         n = s->n;
-        // symmetric stress contract (packed storage): reject genuinely non-symmetric input
-        const T* sg = static_cast<const T*>(s->sigma);
-        for (int64_t i = 0; i < n; ++i)
-            for (int r = 0; r < D; ++r)
-                for (int c = r + 1; c < D; ++c) {
-                    T a = sg[i * D * D + c * D + r], b = sg[i * D * D + r * D + c];
-                    T scale = std::max(std::abs(a), std::abs(b));
-                    if (std::abs(a - b) > T(1e-5) * scale + T(0))
-                        throw ApiError(MPM_ERR_VALIDATION, "stress of particle " + std::to_string(i) + " is not symmetric", i);
-                }
         const void* src[S_NFIELDS] = {s->x, s->v, s->mass, s->volume, s->rho, s->eps_eq, D == 2 ? s->sigma_zz : nullptr,
                                       s->sigma, s->grad_v, s->affine, s->def_grad};
         for (int f = 0; f < S_NFIELDS; ++f) {
@@ -671,6 +662,23 @@ template <class T, int D> struct Ctx : CtxBase {
         if (ids) {
             d_ids = reinterpret_cast<long long*>(aw_ids_scratch(n));
             CK(cudaMemcpyAsync(d_ids, ids, n * sizeof(long long), cudaMemcpyHostToDevice, stream));
+        }
+        // symmetric stress contract (packed storage): reject genuinely non-symmetric input before
+        // the particle buffers change, checked on the device copy (no host pass over the state)
+        if (n > 0) {
+            int* d_bad = reinterpret_cast<int*>(d_red); // scratch; the digest / max-speed reductions reset it
+            const int big = 0x7fffffff;
+            CK(cudaMemcpyAsync(d_bad, &big, sizeof(int), cudaMemcpyHostToDevice, stream));
+            launch("k_check_sym", [&] {
+                k_check_sym<T, D><<<grid_for(n, 256), 256, 0, stream>>>(stage.f[S_SIG], int(n), d_bad);
+            });
+            int bad = big;
+            CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            if (bad != big) {
+                n = n_prev;
+                throw ApiError(MPM_ERR_VALIDATION, "stress of particle " + std::to_string(bad) + " is not symmetric", bad);
+            }
         }
         launch("k_upload", [&] {
             k_upload<T, D><<<grid_for(n, 256), 256, 0, stream>>>(stage, buf[cur], int(n), D == 2 && s->sigma_zz != nullptr,

@@ -60,6 +60,26 @@ __global__ void k_upload(Stage<T, D> S, PBuf<T, D> P, int n, int has_szz, int ha
     (void)C::NS;
 }
 
+// the packed-symmetric stress contract, checked on the staged upload (lowest offending index)
+template <class T, int D>
+__global__ void k_check_sym(const T* __restrict__ sig, int n, int* __restrict__ bad)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    bool ok = true;
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = r + 1; c < D; ++c) {
+            const T a = sig[i * D * D + c * D + r], b = sig[i * D * D + r * D + c];
+            const T scale = fmax(fabs(a), fabs(b));
+            ok = ok && !(fabs(a - b) > T(1e-5) * scale); // NaN passes here, as on the host
+        }
+    if (!ok)
+        atomicMin(bad, i);
+}
+
 // append migrated particles (records sorted by pid beforehand) at storage [base, base + n)
 template <class T, int D>
 __global__ void k_mig_unpack(PBuf<T, D> P, int base, int n, const T* __restrict__ recs, const int* __restrict__ pids,

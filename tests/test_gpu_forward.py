@@ -283,9 +283,18 @@ def test_catastrophic_compression_raises():
 
 
 def test_unsymmetric_stress_rejected():
+    """the packed-symmetric contract is checked on the device copy: the lowest offending particle
+    is reported and the context keeps its previous state"""
     s = small_fluid_scene("pic")
     st = init_scene(s)
-    st.particles.sigma[0] = [[1.0, 2.0], [3.0, 4.0]]
     ctx = Context(s, st.particles.size())
-    with pytest.raises(ValidationError):
-        ctx.upload(st)
+    ctx.upload(st)
+    d0 = ctx.digest()
+    bad = st.copy()
+    bad.particles.sigma[7] = [[1.0, 2.0], [3.0, 4.0]]
+    bad.particles.sigma[3] = [[1.0, 2.0], [2.5, 4.0]]
+    with pytest.raises(ValidationError, match="particle 3 "):
+        ctx.upload(bad)
+    assert ctx.digest() == d0
+    ctx.advance(2)  # still usable
+    ctx.close()
