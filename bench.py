@@ -289,6 +289,7 @@ def bench_b200(a, rank, world, local):
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
                      "step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak,
                               "bytes_per_particle_step": B_fwd}},
+        "fp64": fp64_for(prof, a),
         "kernels": prof, "profiled_step_ms": total_ms / 3,
         "clocks": ck, "gpu_launches": launches, "e2e": e2e,
     }
@@ -412,6 +413,23 @@ def bench_slab_e2e(dom, stp, steps):
     d2h = ov.n * (sum(a.nbytes for a in pinned.values()) + ids_p.nbytes) / max(k, 1)
     return {"seconds": t1 - t0, "h2d_bytes_per_step": h2d / steps, "d2h_bytes_per_step": d2h / steps,
             "call": f"mpm_state_upload_ids (pinned host) + {steps} slab steps + mpm_state_download_local, wall clock"}
+
+
+def fp64_for(prof, a):
+    """The f64 kernels are co-limited by FP64 issue, not HBM: FP64 flops per launch
+    (ncu SASS op counts, profiles/fp64.json: 2 x DFMA + DMUL + DADD) over the live mean launch time,
+    against the datasheet FP64 vector peak (not measured on this pool; MEASURED_PEAKS has no FP64)."""
+    p = ROOT / "profiles" / "fp64.json"
+    if a.config != "C4" or a.dtype != "f64" or not p.exists():
+        return None
+    ref = json.loads(p.read_text())
+    out = {"peak_tflops": 37.0, "peak_source": "HGX B200 datasheet FP64 (not measured)", "unit": "TFLOP/s"}
+    for k in ("k_p2g", "k_g2p"):
+        if k in ref and k in prof:
+            tf = ref[k]["fp64_flops"] / (prof[k]["ms_per_launch"] * 1e-3) / 1e12
+            out[k] = {"achieved": tf, "frac": tf / out["peak_tflops"], "flops_per_launch": ref[k]["fp64_flops"],
+                      "fp64_pipe_active_pct_ncu": ref[k]["fp64_pipe_active_pct"]}
+    return out
 
 
 def traffic_for(kernel, a):
