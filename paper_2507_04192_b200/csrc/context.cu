@@ -281,6 +281,8 @@ template <class T, int D> struct Ctx : CtxBase {
                 if (e)
                     cudaGraphExecDestroy(e);
         drop_slab_graphs();
+        for (void* p : bp_pool_mem)
+            cudaFree(p);
         for (auto& e : events) {
             cudaEventDestroy(e.a);
             cudaEventDestroy(e.b);
@@ -1364,6 +1366,11 @@ template <class T, int D> struct Ctx : CtxBase {
     }
 
     // ---- small transfer helpers (used by the adjoint workspace) ---------------------------------
+    void copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind)
+    {
+        CK(cudaMemcpyAsync(dst, src, bytes, kind, stream));
+    }
+    void sync() { CK(cudaStreamSynchronize(stream)); }
     void h2d(T* dst, const T* src, int64_t k) { CK(cudaMemcpyAsync(dst, src, k * sizeof(T), cudaMemcpyHostToDevice, stream)); CK(cudaStreamSynchronize(stream)); }
     void d2h(T* dst, const T* src, int64_t k) { CK(cudaMemcpyAsync(dst, src, k * sizeof(T), cudaMemcpyDeviceToHost, stream)); CK(cudaStreamSynchronize(stream)); }
     void zero(T* dst, int64_t k) { if (dst) CK(cudaMemsetAsync(dst, 0, k * sizeof(T), stream)); }
@@ -1401,6 +1408,16 @@ template <class T, int D> struct Ctx : CtxBase {
         auto d = pbuf_arrays(dst), s = pbuf_arrays(src);
         for (size_t i = 0; i < d.size(); ++i)
             CK(cudaMemcpyAsync(d[i].first, s[i].first, n * s[i].second, cudaMemcpyDeviceToDevice, stream));
+    }
+    // backprop's checkpoint / replay particle buffers, kept across calls (allocation of several
+    // GB per call dominated a short backprop); released with the context
+    std::vector<PBuf<T, D>> bp_pool;
+    std::vector<void*> bp_pool_mem;
+    PBuf<T, D> pool_buf(size_t k)
+    {
+        while (bp_pool.size() <= k)
+            bp_pool.push_back(pbuf_alloc(bp_pool_mem));
+        return bp_pool[k];
     }
     PBuf<T, D> pbuf_alloc(std::vector<void*>& owned)
     {
@@ -1477,6 +1494,11 @@ template <class T, int D> struct Ctx : CtxBase {
             dev(d_epart, (size_t)eblocks * nsel * (D + 1) * sizeof(T), nullptr);
             dev(d_g, (size_t)nsel * D * sizeof(T), nullptr);
         }
+        T* d_lblk = nullptr; // per-block loss partials of the Lagrangian seeder
+        if (seeding && !eul) {
+            CK(cudaMalloc(&d_lblk, sizeof(T) * std::max<int64_t>(1, grid_for(nsel, 256))));
+            owned.push_back(d_lblk);
+        }
         if (seeding) {
             if (sd->sel && !eul) {
                 CK(cudaMalloc(&d_sel, nsel * sizeof(long long)));
@@ -1519,18 +1541,20 @@ template <class T, int D> struct Ctx : CtxBase {
                 return;
             }
             launch("k_slot_of_pid", [&] { k_slot_of_pid<T, D><<<grid_for(n, 256), 256, 0, stream>>>(P, int(n), aw.slot_of_pid); });
+            const int sb = int(grid_for(nsel, 256));
             launch("k_seed", [&] {
-                k_seed_lagrangian<T, D><<<1, 1024, 0, stream>>>(P, int(n), aw.slot_of_pid, d_sel, nsel,
+                k_seed_lagrangian<T, D><<<sb, 256, 0, stream>>>(P, int(n), aw.slot_of_pid, d_sel, nsel,
                                                                 d_tgt + (size_t)k * nsel * D, sd->field, aw.cot[cb],
-                                                                do_cot, aw.loss_acc);
+                                                                do_cot, d_lblk);
             });
+            launch("k_seed", [&] { k_seed_sum<T><<<1, 1024, 0, stream>>>(d_lblk, sb, aw.loss_acc); });
         };
         try {
             std::vector<PBuf<T, D>> ckpt(nseg), replay(Lmax + 1);
-            for (auto& P : ckpt)
-                P = pbuf_alloc(owned);
-            for (auto& P : replay)
-                P = pbuf_alloc(owned);
+            for (int k = 0; k < nseg; ++k) // checkpoint and replay slots persist across calls
+                ckpt[k] = pool_buf(size_t(k));
+            for (int64_t j = 0; j <= Lmax; ++j)
+                replay[j] = pool_buf(size_t(nseg + j));
             std::vector<uint64_t> bhash(nseg + 1);
             CK(cudaMemsetAsync(aw.loss_acc, 0, sizeof(double), stream));
             // forward sweep

@@ -1452,20 +1452,18 @@ __global__ void __launch_bounds__(1024) k_pg_reduce(const T* __restrict__ pg_blo
 }
 
 // ---- Lagrangian least-squares seeder (SPEC observe_lagrangian + loss) -------------------------
-// loss += sum ||z - target||^2 (fixed-order), cot.z[pid] += 2 (z - target), z = x or v.
+// loss += sum ||z - target||^2, cot.z[pid] += 2 (z - target), z = x or v. Grid-wide: one
+// selection entry per thread, per-block sums (fixed tree), then k_seed_sum adds the blocks in order.
 template <class T, int D>
-__global__ void __launch_bounds__(1024) k_seed_lagrangian(PBuf<T, D> P, int n, const int* __restrict__ slot_of_pid,
-                                                          const long long* __restrict__ sel, long long nsel,
-                                                          const T* __restrict__ target, int field, CBuf<T, D> cot,
-                                                          int do_cot, double* loss_acc)
+__global__ void __launch_bounds__(256) k_seed_lagrangian(PBuf<T, D> P, int n, const int* __restrict__ slot_of_pid,
+                                                         const long long* __restrict__ sel, long long nsel,
+                                                         const T* __restrict__ target, int field, CBuf<T, D> cot,
+                                                         int do_cot, T* __restrict__ block_loss)
 {
-    __shared__ T red[1024];
+    __shared__ T red[256];
     T acc = T(0);
-    const long long per = (nsel + 1023) / 1024;
-    for (long long j = 0; j < per; ++j) {
-        const long long l = threadIdx.x * per + j;
-        if (l >= nsel)
-            break;
+    const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < nsel) {
         const int pid = sel ? int(sel[l]) : int(l);
         const int s = slot_of_pid[pid];
 #pragma unroll
@@ -1478,6 +1476,21 @@ __global__ void __launch_bounds__(1024) k_seed_lagrangian(PBuf<T, D> P, int n, c
                 zc[pid] += T(2) * r;
             }
         }
+    }
+    const T tot = block_sum_fixed<T, 256>(acc, red);
+    if (threadIdx.x == 0)
+        block_loss[blockIdx.x] = tot;
+}
+template <class T>
+__global__ void __launch_bounds__(1024) k_seed_sum(const T* __restrict__ block_loss, int nb, double* loss_acc)
+{
+    __shared__ T red[1024];
+    T acc = T(0);
+    const int per = (nb + 1023) / 1024;
+    for (int j = 0; j < per; ++j) { // contiguous ranges per thread, then a fixed tree
+        const int b = threadIdx.x * per + j;
+        if (b < nb)
+            acc += block_loss[b];
     }
     const T tot = block_sum_fixed<T, 1024>(acc, red);
     if (threadIdx.x == 0)
@@ -1593,6 +1606,66 @@ __global__ void k_eul_seed(PBuf<T, D> P, int n, const T* __restrict__ centers, c
     }
 }
 
+// cotangent views (reference layout, id order: vectors [n][d], matrices [n][d*d] column-major)
+// <-> id-indexed SoA cotangents, through the context's device staging buffer
+enum CotField { CF_X = 1, CF_V = 2, CF_RHO = 4, CF_VOL = 8, CF_EPS = 16, CF_SZZ = 32, CF_SIG = 64, CF_GV = 128,
+                CF_AFF = 256 };
+template <class T, int D>
+__global__ void k_cot_in(Stage<T, D> S, CBuf<T, D> k, int n, int mask, int has_aff)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    auto get = [&](int f, int bit, size_t idx) { return (mask & bit) ? S.f[f][idx] : T(0); };
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        k.x[a][i] = get(S_X, CF_X, (size_t)i * D + a);
+        k.v[a][i] = get(S_V, CF_V, (size_t)i * D + a);
+    }
+    k.rho[i] = get(S_RHO, CF_RHO, i);
+    k.V[i] = get(S_VOL, CF_VOL, i);
+    k.eps[i] = T(0); // the eps cotangent is discarded (adjoint.hpp:399-400)
+    if (D == 2)
+        k.szz[i] = get(S_SZZ, CF_SZZ, i);
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            const size_t m = (size_t)i * D * D + q * D + r; // column-major (r, q)
+            k.sig[r * D + q][i] = get(S_SIG, CF_SIG, m);
+            k.gv[r * D + q][i] = get(S_GV, CF_GV, m);
+            if (has_aff)
+                k.aff[r * D + q][i] = get(S_AFF, CF_AFF, m);
+        }
+}
+template <class T, int D>
+__global__ void k_cot_out(Stage<T, D> S, CBuf<T, D> k, int n, int has_aff)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        S.f[S_X][(size_t)i * D + a] = k.x[a][i];
+        S.f[S_V][(size_t)i * D + a] = k.v[a][i];
+    }
+    S.f[S_RHO][i] = k.rho[i];
+    S.f[S_VOL][i] = k.V[i];
+    S.f[S_EPS][i] = k.eps[i];
+    if (D == 2)
+        S.f[S_SZZ][i] = k.szz[i];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            const size_t m = (size_t)i * D * D + q * D + r;
+            S.f[S_SIG][m] = k.sig[r * D + q][i];
+            S.f[S_GV][m] = k.gv[r * D + q][i];
+            if (has_aff)
+                S.f[S_AFF][m] = k.aff[r * D + q][i];
+        }
+}
+
 template <class T, int D> __global__ void k_slot_of_pid(PBuf<T, D> P, int n, int* slot_of_pid)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1696,55 +1769,24 @@ template <class T, int D> struct AdjWork {
     // upload / download a host cotangent view (reference layout, id order) <-> cot[b]
     template <class Ctx> void cot_upload(Ctx& c, const mpm_cot_view* v, int b)
     {
-        auto& k = cot[b];
         const int64_t n = c.n;
-        std::vector<T> h((size_t)n);
-        auto put_vec = [&](T* const* dst, const void* srcp) {
-            for (int a = 0; a < D; ++a) {
-                if (srcp) {
-                    const T* s = static_cast<const T*>(srcp);
-                    for (int64_t i = 0; i < n; ++i)
-                        h[i] = s[i * D + a];
-                } else
-                    std::fill(h.begin(), h.end(), T(0));
-                c.h2d(dst[a], h.data(), n);
+        if (n == 0)
+            return;
+        const void* src[S_NFIELDS] = {v->x, v->v, nullptr, v->volume, v->rho, nullptr, D == 2 ? v->sigma_zz : nullptr,
+                                      v->sigma, v->grad_v, c.has_aff ? v->affine : nullptr, nullptr};
+        const int bit[S_NFIELDS] = {CF_X, CF_V, 0, CF_VOL, CF_RHO, 0, CF_SZZ, CF_SIG, CF_GV, CF_AFF, 0};
+        int mask = 0;
+        for (int f = 0; f < S_NFIELDS; ++f)
+            if (src[f]) {
+                c.copy_async(c.stage.f[f], src[f], (size_t)n * stage_comps<D>(f) * sizeof(T),
+                             cudaMemcpyHostToDevice);
+                mask |= bit[f];
             }
-        };
-        auto put_sc = [&](T* dst, const void* srcp) {
-            if (!dst)
-                return;
-            if (srcp)
-                c.h2d(dst, static_cast<const T*>(srcp), n);
-            else
-                c.zero(dst, n);
-        };
-        auto put_mat = [&](T* const* dst, const void* srcp) {
-            if (!dst[0])
-                return;
-            for (int r = 0; r < D; ++r)
-                for (int q = 0; q < D; ++q) {
-                    if (srcp) {
-                        const T* s = static_cast<const T*>(srcp);
-                        for (int64_t i = 0; i < n; ++i)
-                            h[i] = s[i * D * D + q * D + r]; // column-major (r, q)
-                    } else
-                        std::fill(h.begin(), h.end(), T(0));
-                    c.h2d(dst[r * D + q], h.data(), n);
-                }
-        };
-        put_vec(k.x, v->x);
-        put_vec(k.v, v->v);
-        put_sc(k.rho, v->rho);
-        put_sc(k.V, v->volume);
-        put_sc(k.eps, nullptr);
-        if (D == 2)
-            put_sc(k.szz, v->sigma_zz);
-        put_mat(k.sig, v->sigma);
-        put_mat(k.gv, v->grad_v);
-        if (c.has_aff)
-            put_mat(k.aff, v->affine);
+        c.launch("k_cot_in", [&] {
+            k_cot_in<T, D><<<c.grid_for(n, 256), 256, 0, c.stream>>>(c.stage, cot[b], int(n), mask, c.has_aff);
+        });
+        c.sync(); // the staging buffer is reused by the next transfer
     }
-
     template <class Ctx> void cot_zero(Ctx& c, int b)
     {
         auto& k = cot[b];
@@ -1768,45 +1810,19 @@ template <class T, int D> struct AdjWork {
 
     template <class Ctx> void cot_download(Ctx& c, mpm_cot_view* v, int b)
     {
-        auto& k = cot[b];
         const int64_t n = c.n;
-        std::vector<T> h((size_t)n);
-        auto get_vec = [&](T* const* srcd, void* dstp) {
-            if (!dstp)
-                return;
-            T* d = static_cast<T*>(dstp);
-            for (int a = 0; a < D; ++a) {
-                c.d2h(h.data(), srcd[a], n);
-                for (int64_t i = 0; i < n; ++i)
-                    d[i * D + a] = h[i];
-            }
-        };
-        auto get_sc = [&](T* srcd, void* dstp) {
-            if (dstp && srcd)
-                c.d2h(static_cast<T*>(dstp), srcd, n);
-        };
-        auto get_mat = [&](T* const* srcd, void* dstp) {
-            if (!dstp || !srcd[0])
-                return;
-            T* d = static_cast<T*>(dstp);
-            for (int r = 0; r < D; ++r)
-                for (int q = 0; q < D; ++q) {
-                    c.d2h(h.data(), srcd[r * D + q], n);
-                    for (int64_t i = 0; i < n; ++i)
-                        d[i * D * D + q * D + r] = h[i];
-                }
-        };
-        get_vec(k.x, v->x);
-        get_vec(k.v, v->v);
-        get_sc(k.rho, v->rho);
-        get_sc(k.V, v->volume);
-        get_sc(k.eps, v->eps_eq);
-        if (D == 2)
-            get_sc(k.szz, v->sigma_zz);
-        get_mat(k.sig, v->sigma);
-        get_mat(k.gv, v->grad_v);
-        if (c.has_aff)
-            get_mat(k.aff, v->affine);
+        if (n == 0)
+            return;
+        c.launch("k_cot_out", [&] {
+            k_cot_out<T, D><<<c.grid_for(n, 256), 256, 0, c.stream>>>(c.stage, cot[b], int(n), c.has_aff);
+        });
+        void* dst[S_NFIELDS] = {v->x, v->v, nullptr, v->volume, v->rho, v->eps_eq, D == 2 ? v->sigma_zz : nullptr,
+                                v->sigma, v->grad_v, c.has_aff ? v->affine : nullptr, nullptr};
+        for (int f = 0; f < S_NFIELDS; ++f)
+            if (dst[f])
+                c.copy_async(dst[f], c.stage.f[f], (size_t)n * stage_comps<D>(f) * sizeof(T),
+                             cudaMemcpyDeviceToHost);
+        c.sync();
     }
 
     // one reverse step on the state currently in c.buf[c.cur]: cot[bo] (out) -> cot[bi] (in)
