@@ -166,6 +166,7 @@ template <class T, int D> struct Ctx : CtxBase {
     int64_t slab_g1_launches = 0, slab_g2_launches = 0;
     cudaGraphExec_t slab_g2[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     bool status_dirty = true; // host step changed (upload): push it to the device counter
+    bool has_state = false;   // a state was uploaded or seeded (it may hold no particles)
     void drop_slab_graphs()
     {
         for (auto& e : slab_g1)
@@ -220,7 +221,7 @@ template <class T, int D> struct Ctx : CtxBase {
         CK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
         stream = own_stream;
         build_scene(d);
-        cap = max_particles;
+        cap = std::max<int64_t>(max_particles, 1); // an empty state still gets valid (1-slot) buffers
         has_aff = d->scheme == MPM_SCHEME_APIC;
         has_F = d->track_def_grad != 0;
         for (int b = 0; b < 2; ++b)
@@ -641,7 +642,7 @@ template <class T, int D> struct Ctx : CtxBase {
 
     void upload_ids(const mpm_state_view* s, const int64_t* ids) override
     {
-        if (s->n < ((ids || slab) ? 0 : 1) || s->n > cap) // a slab may hold no particles
+        if (s->n < 0 || s->n > cap) // an empty state is valid (the reference steps it; a slab may be empty)
             throw ApiError(MPM_ERR_USAGE, "state size " + std::to_string(s->n) + " outside [1, " + std::to_string(cap) + "]");
         if (s->n > 0 && (!s->x || !s->v || !s->mass || !s->volume || !s->rho || !s->sigma))
             throw ApiError(MPM_ERR_USAGE, "state view missing required fields");
@@ -688,6 +689,7 @@ template <class T, int D> struct Ctx : CtxBase {
         });
         n_dead = 0;
         status_dirty = true;
+        has_state = true;
         step = s->step;
         time = s->time;
         keys_valid = false;
@@ -699,7 +701,7 @@ template <class T, int D> struct Ctx : CtxBase {
     {
         if (slab)
             throw ApiError(MPM_ERR_USAGE, "slab mode: use mpm_state_download_local");
-        if (n == 0)
+        if (!has_state)
             throw ApiError(MPM_ERR_USAGE, "no state uploaded");
         launch("k_download", [&] { k_download<T, D><<<grid_for(n, 256), 256, 0, stream>>>(stage, buf[cur], int(n), has_aff, has_F); });
         void* dst[S_NFIELDS] = {s->x, s->v, s->mass, s->volume, s->rho, s->eps_eq, D == 2 ? s->sigma_zz : nullptr,
@@ -730,7 +732,7 @@ template <class T, int D> struct Ctx : CtxBase {
     {
         if (slot < 0 || slot > 1)
             throw ApiError(MPM_ERR_USAGE, "snapshot slot must be 0 or 1");
-        if (slab || n == 0)
+        if (slab || !has_state)
             throw ApiError(MPM_ERR_USAGE, "snapshot: no single-context state");
         Snap& q = snaps[slot];
         if (!q.dbase) {
@@ -810,7 +812,7 @@ template <class T, int D> struct Ctx : CtxBase {
 
     void advance(int64_t nsteps, uint32_t flags) override
     {
-        if (n == 0)
+        if (!has_state)
             throw ApiError(MPM_ERR_USAGE, "no state uploaded");
         if (nsteps <= 0)
             return;
@@ -823,7 +825,7 @@ template <class T, int D> struct Ctx : CtxBase {
     {
         if (slab)
             throw ApiError(MPM_ERR_USAGE, "slab mode: step with mpm_step_p2g_local / mpm_halo / mpm_step_finish_local");
-        if (n == 0)
+        if (!has_state)
             throw ApiError(MPM_ERR_USAGE, "no state uploaded");
         if (nsteps <= 0)
             return;
@@ -1160,6 +1162,7 @@ template <class T, int D> struct Ctx : CtxBase {
         n_dead = 0;
         keys_valid = false;
         status_dirty = true;
+        has_state = true;
         step = 0;
         time = 0.0;
     }
@@ -1703,7 +1706,7 @@ int mpm_device_name(char* buf, size_t len)
 
 int mpm_ctx_create(const mpm_scene_desc* d, int64_t max_particles, int device, mpm_ctx** out)
 {
-    if (!d || !out || max_particles < 1)
+    if (!d || !out || max_particles < 0)
         return MPM_ERR_USAGE;
     *out = nullptr;
     static thread_local mpm_ctx scratch;

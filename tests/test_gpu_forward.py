@@ -298,3 +298,29 @@ def test_unsymmetric_stress_rejected():
     assert ctx.digest() == d0
     ctx.advance(2)  # still usable
     ctx.close()
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_empty_state_steps_like_the_reference(orc, ref, dim):
+    """an empty particle set is a valid state: the reference steps it (step and time advance, no
+    particles); so do the device path, run() and step_vjp"""
+    from paper_2507_04192_b200.solver import run, step_vjp
+    from paper_2507_04192_b200.state import ParamGrads, SimState, StateCotangent
+
+    from test_distributed import moving_fluid_scene
+
+    s = moving_fluid_scene(dim) if dim == 3 else small_fluid_scene("flip")
+    init_scene(s)  # sets mass_epsilon
+    st = SimState.zeros(0, dim, s.np_dtype)
+    want = st.copy()
+    ref.advance(s, want, 3)
+    ctx = Context(s, 0)
+    ctx.upload(st)
+    ctx.advance(3, nan_guard=True)
+    got = ctx.download(st.copy())
+    ctx.close()
+    assert got.step == want.step == 3 and got.time == want.time and got.particles.size() == 0
+    res = run(s, st, 4, 2)
+    assert [x.step for x in res.snapshots] == [0, 2, 4]
+    cin = step_vjp(s, st, StateCotangent.zeros_like(st.particles), None, ParamGrads(s.boundary))
+    assert cin.x.shape == (0, dim)
