@@ -772,6 +772,256 @@ __global__ void __launch_bounds__(256) k_adj_scatter(DevScene<T, D> sc, PBuf<T, 
     }
 }
 
+// ---- K5b, 3-D PIC / FLIP / blend: the same pipelined column march as the forward P2G ----------
+// (k_p2g_pipe3). Staged per particle: fx (through the sort permutation), the scatter record
+// a = pic_cot + inc_cot, inc_cot and L = grad-v cotangent (sorted slot order). Thread = (base
+// column, x-offset), 3 y-offsets x a rolling 3-node z window x 6 fields. Per node
+// (adjoint.hpp:427-436): gv_cot += phi a + L grad(phi) = wz u + dwz t with u = pw a + L[:,0] p1 +
+// L[:,1] p2, t = L[:,2] pw; gvold_cot -= phi inc. Fixed-order slot reduction into the partial tiles.
+template <class T> struct AdjScatterCfg {
+    static constexpr int THREADS = 192, NBC = 64, NSRC = 9, NRAW = 18, MAXIT = 64, CAP = 512, NF = 6;
+    static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
+    static constexpr size_t SMEM_PK = sizeof(int) * 3 * 2 * CAP;
+    static constexpr size_t SMEM_SLOT = sizeof(T) * Cfg<3>::NCOL * NSRC * NF;
+    static constexpr size_t SMEM = SMEM_RAW + SMEM_PK + SMEM_SLOT;
+};
+
+template <class T>
+__global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
+    k_adj_scatter_pipe3(DevScene<T, 3> sc, PBuf<T, 3> P, SBuf<T, 3> Sb, const int* __restrict__ perm,
+                        const int* __restrict__ keys, const int* __restrict__ bstart, const int* __restrict__ bend,
+                        const int* __restrict__ lstart, const int* __restrict__ occ, const int* __restrict__ n_occ,
+                        T* __restrict__ partials, const DevStatus* st)
+{
+    using C = Cfg<3>;
+    using S = AdjScatterCfg<T>;
+    constexpr int B = C::B, TE = C::TE, NF = S::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW;
+    constexpr int RX = 0, RA = 3, RI = 6, RL = 9; // raw rows: fx, a, inc, L (row-major a*3+b)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* raw = reinterpret_cast<T*>(smem_raw);                              // [2][NRAW][CAP]
+    int* pk = reinterpret_cast<int*>(smem_raw + S::SMEM_RAW);             // [3][2][CAP] (perm, key)
+    T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_RAW + S::SMEM_PK); // [NCOL][NSRC][NF]
+    __shared__ int it_start[S::MAXIT], it_len[S::MAXIT], it_lvl[S::MAXIT], it_last[S::MAXIT];
+    __shared__ int nit_s, ccount[2][NBC];
+    if (st->abort)
+        return;
+    const int nocc = *n_occ;
+    const int tid = threadIdx.x;
+    const int bc = tid / 3, o0 = tid % 3;
+    const bool mid = o0 == 1;
+    const T xoff = o0 == 0 ? T(1.5) : (o0 == 1 ? T(1) : T(0.5));
+    const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
+    const long long SI = P.S;
+
+    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+        const int Q = occ[w];
+        const int s0 = bstart[Q], s1 = bend[Q];
+        __syncthreads();
+        if (tid == 0) { // level starts -> work items (as k_p2g_pipe3)
+            int lv[B + 1];
+            int nxt = s1;
+            lv[B] = s1 - s0;
+            for (int z = B - 1; z >= 0; --z) {
+                const int v = lstart[Q * (B + 1) + z];
+                nxt = (v >= s0 && v < s1) ? v : nxt;
+                lv[z] = nxt - s0;
+            }
+            int k = 0;
+            for (int z = 0; z < B; ++z) {
+                const int nl = lv[z + 1] - lv[z];
+                const int nch = nl > 0 ? (nl + CAP - 1) / CAP : 1;
+                for (int c = 0; c < nch; ++c) {
+                    if (k < S::MAXIT) {
+                        it_start[k] = lv[z] + c * CAP;
+                        it_len[k] = min(CAP, nl - c * CAP);
+                        it_lvl[k] = z;
+                        it_last[k] = c == nch - 1;
+                    }
+                    ++k;
+                }
+            }
+            nit_s = k > S::MAXIT ? -1 : k;
+        }
+        __syncthreads();
+        int nit = nit_s;
+        if (nit < 0) // the forward refused this block already (far_flag); nothing consistent to do
+            nit = 0;
+        auto issue_pk = [&](int j) {
+            int* dp = pk + (j % 3) * 2 * CAP;
+            const int b = s0 + it_start[j];
+            for (int r = tid; r < it_len[j]; r += blockDim.x) {
+                cp_async4(dp + r, perm + b + r);
+                cp_async4(dp + CAP + r, keys + b + r);
+            }
+        };
+        auto issue_fields = [&](int j) {
+            const int* pp = pk + (j % 3) * 2 * CAP;
+            T* rb = raw + (j & 1) * NRAW * CAP;
+            const int b = s0 + it_start[j];
+            for (int r = tid; r < it_len[j]; r += blockDim.x) {
+                const T* q = P.base + pp[r];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    cp_async_t<T>(rb + (RX + a) * CAP + r, q + a * SI); // x (PLay field 0..2)
+                    cp_async_t<T>(rb + (RA + a) * CAP + r, Sb.a[a] + b + r);
+                    cp_async_t<T>(rb + (RI + a) * CAP + r, Sb.inc[a] + b + r);
+                }
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+                    cp_async_t<T>(rb + (RL + k) * CAP + r, Sb.L[k] + b + r);
+            }
+        };
+        if (tid < NBC) {
+            ccount[0][tid] = 0;
+            ccount[1][tid] = 0;
+        }
+        if (nit > 0)
+            issue_pk(0);
+        if (nit > 1)
+            issue_pk(1);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        if (nit > 0)
+            issue_fields(0);
+        cp_async_commit();
+
+        T* part = partials + (size_t)Q * NF * C::TN;
+        T acc[3][3][NF];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    acc[a][k][f] = T(0);
+
+        auto emit_and_reduce = [&](int z) {
+#pragma unroll
+            for (int o1 = 0; o1 < 3; ++o1) {
+                const int ncol = (bc0 + o0) * TE + bc1 + o1;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    slots[(ncol * NSRC + o0 * 3 + o1) * NF + f] = acc[o1][0][f];
+                    acc[o1][0][f] = acc[o1][1][f];
+                    acc[o1][1][f] = acc[o1][2][f];
+                    acc[o1][2][f] = T(0);
+                }
+            }
+            __syncthreads(); // slots complete
+            for (int t = tid; t < C::NCOL * NF; t += blockDim.x) {
+                const int c = t / NF, f = t - c * NF;
+                const int n0 = c / TE, n1 = c - n0 * TE;
+                T sum = T(0);
+#pragma unroll
+                for (int q = 0; q < NSRC; ++q) {
+                    const int b0 = n0 - q / 3, b1 = n1 - q % 3;
+                    if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
+                        sum += slots[(c * NSRC + q) * NF + f];
+                }
+                part[f * C::TN + z * C::NCOL + c] = sum; // the adjoint partial-tile layout (k_adj_grid)
+            }
+        };
+
+        for (int j = 0; j < nit; ++j) {
+            cp_async_wait_all();
+            __syncthreads();
+            if (j + 1 < nit)
+                issue_fields(j + 1);
+            if (j + 2 < nit)
+                issue_pk(j + 2);
+            cp_async_commit();
+            const int len = it_len[j];
+            const int* col = pk + (j % 3) * 2 * CAP + CAP;
+            int* cnt = ccount[j & 1];
+            if (tid < NBC)
+                ccount[(j + 1) & 1][tid] = 0;
+            {
+                T* Rw = raw + (j & 1) * NRAW * CAP;
+                for (int r = tid; r < len; r += blockDim.x) {
+                    atomicAdd(&cnt[col[r] & (NBC - 1)], 1);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const T u = (Rw[(RX + a) * CAP + r] - sc.origin[a]) * sc.inv_dh;
+                        Rw[(RX + a) * CAP + r] = u - dfloor<T>(u - T(0.5));
+                    }
+                }
+            }
+            __syncthreads();
+            int kb, ke;
+            {
+                const int lane = tid & 31;
+                const int c0 = cnt[2 * lane], c1 = cnt[2 * lane + 1];
+                int v = c0 + c1;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, v, d);
+                    if (lane >= d)
+                        v += t;
+                }
+                const int excl = v - c0 - c1;
+                const int src = bc >> 1;
+                const int e = __shfl_sync(0xffffffffu, excl, src);
+                const int a0 = __shfl_sync(0xffffffffu, c0, src);
+                const int a1 = __shfl_sync(0xffffffffu, c1, src);
+                kb = (bc & 1) ? e + a0 : e;
+                ke = kb + ((bc & 1) ? a1 : a0);
+            }
+            const T* R = raw + (j & 1) * NRAW * CAP;
+            for (int k = kb; k < ke; ++k) {
+                const T fx = R[(RX + 0) * CAP + k], fy = R[(RX + 1) * CAP + k], fz = R[(RX + 2) * CAP + k];
+                T wx, dwx, wy[3], dwy[3], wz[3], dwz[3];
+                {
+                    const T h = fx - xoff;
+                    const T hh = h * h;
+                    wx = mid ? T(0.75) - hh : T(0.5) * hh;
+                    dwx = (mid ? -T(2) * h : h) * sc.inv_dh;
+                }
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    quad_w<T>(fy, q, sc.inv_dh, wy[q], dwy[q]);
+                    quad_w<T>(fz, q, sc.inv_dh, wz[q], dwz[q]);
+                }
+                T av[3], iv[3], L[9];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    av[a] = R[(RA + a) * CAP + k];
+                    iv[a] = R[(RI + a) * CAP + k];
+                }
+#pragma unroll
+                for (int q = 0; q < 9; ++q)
+                    L[q] = R[(RL + q) * CAP + k];
+#pragma unroll
+                for (int o1 = 0; o1 < 3; ++o1) {
+                    // grad phi = (p1 wz, p2 wz, pw dwz) with pw = wx wy, p1 = dwx wy, p2 = wx dwy
+                    const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
+                    T u[3], t[3], ui[3];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        u[a] = pw * av[a] + L[a * 3 + 0] * p1 + L[a * 3 + 1] * p2;
+                        t[a] = L[a * 3 + 2] * pw;
+                        ui[a] = pw * iv[a];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 3; ++q)
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            acc[o1][q][a] = acc[o1][q][a] + wz[q] * u[a] + dwz[q] * t[a];
+                            acc[o1][q][3 + a] = acc[o1][q][3 + a] - wz[q] * ui[a];
+                        }
+                }
+            }
+            if (it_last[j])
+                emit_and_reduce(it_lvl[j]);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        emit_and_reduce(B);
+        __syncthreads();
+        emit_and_reduce(B + 1);
+    }
+}
+
 // ---- K6: per node: sum partials, correction-chain VJP, momentum-update transpose ------------
 template <class T, int D>
 __device__ __forceinline__ void corr_vjp_chain(const DevScene<T, D>& sc, const int* n, const T* vtilde, T* cot,
@@ -1763,6 +2013,9 @@ template <class T, int D> struct AdjWork {
         cudaFuncSetAttribute(k_adj_g2pT_gather<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm5);
         cudaFuncSetAttribute(k_adj_p2gT<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm7);
         cudaFuncSetAttribute(k_adj_p2gT<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm7);
+        if constexpr (D == 3)
+            cudaFuncSetAttribute(k_adj_scatter_pipe3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(AdjScatterCfg<T>::SMEM));
         (void)c;
     }
 
@@ -1911,6 +2164,17 @@ template <class T, int D> struct AdjWork {
                                                                             pg_block, c.st);
             });
         const int tpb = D == 2 ? 160 : 256;
+        if constexpr (D == 3) {
+            if (!c.has_aff) { // pipelined column march (as the forward P2G)
+                using SC = AdjScatterCfg<T>;
+                c.launch("k_adj_scatter", [&] {
+                    k_adj_scatter_pipe3<T><<<c.persistent(1), SC::THREADS, SC::SMEM, c.stream>>>(
+                        c.sc, Pin, sb, c.perm, c.keys_sorted, c.bstart, c.bend, c.lstart, c.occ, c.counts, partials,
+                        c.st);
+                });
+                return;
+            }
+        }
         if (c.has_aff)
             c.launch("k_adj_scatter", [&] {
                 k_adj_scatter<T, D, true><<<c.persistent(8), tpb, 0, c.stream>>>(c.sc, Pin, sb, c.perm, c.keys_sorted,
