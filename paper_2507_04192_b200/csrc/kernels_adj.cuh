@@ -291,18 +291,121 @@ __device__ __forceinline__ T block_sum_fixed(T v, T* scratch)
     return r;
 }
 
+// ---- tensor-product stencil moments ----------------------------------------------------------
+// For one node field f of a tile (last axis fastest, t0 = the particle's stencil corner):
+//   phi  = sum_o  w0 w1 (w2) f                        (PHI)
+//   g[a] = sum_o  d(phi)/dx_a f                       (grad of the shape function)
+//   h    = sum_o  d2(phi)/dx_a dx_b f                 (HES; stencil_hessian, adjoint.hpp:95-110)
+// evaluated axis by axis (last-axis sums, then the middle axis, then the first). All 1 + D +
+// D(D+1)/2 moments of a field cost ~150 FP64 ops in 3-D instead of 27 x (weight products +
+// contraction); the per-node weight products are never formed. The second-derivative weights are
+// (1, -2, 1) / dh^2 on every axis (bspline.hpp:43-108), applied as adds and one scale at the end.
+template <class T, int D> struct Mom {
+    T phi;
+    T g[D];
+    T h[D][D];
+};
+template <class T, int D, bool PHI, bool HES>
+__device__ __forceinline__ void stencil_moments(const T* __restrict__ f, int t0, const T (&w)[D][3],
+                                                const T (&dw)[D][3], T idh2, Mom<T, D>& m)
+{
+    constexpr int TE = Cfg<D>::TE;
+    if constexpr (D == 3) {
+        T phi = T(0), g0 = T(0), g1 = T(0), g2 = T(0);
+        T h00 = T(0), h11 = T(0), h22 = T(0), h01 = T(0), h02 = T(0), h12 = T(0);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            T ww = T(0), dww = T(0), wdw = T(0), ddw = T(0), wdd = T(0), dwdw = T(0);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const T* p = f + t0 + (i * TE + j) * TE;
+                const T f0 = p[0], f1 = p[1], f2 = p[2];
+                const T zw = w[2][0] * f0 + w[2][1] * f1 + w[2][2] * f2;
+                const T zdw = dw[2][0] * f0 + dw[2][1] * f1 + dw[2][2] * f2;
+                ww += w[1][j] * zw;
+                dww += dw[1][j] * zw;
+                wdw += w[1][j] * zdw;
+                if constexpr (HES) {
+                    const T zdd = (f0 + f2) - T(2) * f1;
+                    ddw += (j == 1 ? T(-2) : T(1)) * zw;
+                    wdd += w[1][j] * zdd;
+                    dwdw += dw[1][j] * zdw;
+                }
+            }
+            if constexpr (PHI)
+                phi += w[0][i] * ww;
+            g0 += dw[0][i] * ww;
+            g1 += w[0][i] * dww;
+            g2 += w[0][i] * wdw;
+            if constexpr (HES) {
+                h00 += (i == 1 ? T(-2) : T(1)) * ww;
+                h11 += w[0][i] * ddw;
+                h22 += w[0][i] * wdd;
+                h01 += dw[0][i] * dww;
+                h02 += dw[0][i] * wdw;
+                h12 += w[0][i] * dwdw;
+            }
+        }
+        m.phi = phi;
+        m.g[0] = g0;
+        m.g[1] = g1;
+        m.g[2] = g2;
+        if constexpr (HES) {
+            m.h[0][0] = h00 * idh2;
+            m.h[1][1] = h11 * idh2;
+            m.h[2][2] = h22 * idh2;
+            m.h[0][1] = m.h[1][0] = h01;
+            m.h[0][2] = m.h[2][0] = h02;
+            m.h[1][2] = m.h[2][1] = h12;
+        }
+    } else {
+        T phi = T(0), g0 = T(0), g1 = T(0), h00 = T(0), h11 = T(0), h01 = T(0);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const T* p = f + t0 + i * TE;
+            const T f0 = p[0], f1 = p[1], f2 = p[2];
+            const T zw = w[1][0] * f0 + w[1][1] * f1 + w[1][2] * f2;
+            const T zdw = dw[1][0] * f0 + dw[1][1] * f1 + dw[1][2] * f2;
+            if constexpr (PHI)
+                phi += w[0][i] * zw;
+            g0 += dw[0][i] * zw;
+            g1 += w[0][i] * zdw;
+            if constexpr (HES) {
+                const T zdd = (f0 + f2) - T(2) * f1;
+                h00 += (i == 1 ? T(-2) : T(1)) * zw;
+                h11 += w[0][i] * zdd;
+                h01 += dw[0][i] * zdw;
+            }
+        }
+        m.phi = phi;
+        m.g[0] = g0;
+        m.g[1] = g1;
+        if constexpr (HES) {
+            m.h[0][0] = h00 * idh2;
+            m.h[1][1] = h11 * idh2;
+            m.h[0][1] = m.h[1][0] = h01;
+        }
+    }
+}
+
 // ---- K5a: G2P-transpose gather + constitutive VJP ------------------------------------------
+// Cotangents live in state-storage order: co (cot at t+1) is indexed by the sorted slot i (the
+// storage order of S^{t+1}, which the forward G2P wrote in this step's sort order) and ci (cot at
+// t) by src = perm[i] (the storage slot of S^t). Both are streamed, not gathered through ids.
+// GVZ: co.grad_v is known zero (FLIP/PIC chains and seeded losses) and ci.grad_v is left to the
+// caller's zero flag unless TPIC accumulates into it in K7.
 template <class T, int D, bool APIC>
 __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf<T, D> Pin, GBuf<T, D> G,
                                                          const int* __restrict__ perm, const int* __restrict__ bstart,
                                                          const int* __restrict__ bend, const int* __restrict__ occ,
                                                          const int* __restrict__ n_occ, CBuf<T, D> co, CBuf<T, D> ci,
-                                                         SBuf<T, D> S, T* __restrict__ pg_block, DevStatus* st)
+                                                         SBuf<T, D> S, T* __restrict__ pg_block, DevStatus* st,
+                                                         int co_gv_zero, int ci_gv_write)
 {
     using C = Cfg<D>;
     constexpr int TE = C::TE, TN = C::TN;
     extern __shared__ unsigned char smem_raw[];
-    T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]
+    T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]: v, v - v_old
     __shared__ T red[256];
     if (st->abort)
         return;
@@ -333,18 +436,19 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
             const size_t gi = (size_t)nid * C::NB + loc;
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-                tile[a * TN + t] = ok ? G.v[a][gi] : T(0);
-                tile[(D + a) * TN + t] = ok ? G.vold[a][gi] : T(0);
+                const T vn = ok ? G.v[a][gi] : T(0), vo = ok ? G.vold[a][gi] : T(0);
+                tile[a * TN + t] = vn;
+                tile[(D + a) * TN + t] = vn - vo;
             }
         }
         __syncthreads();
         T c_acc = T(0), mu_acc = T(0);
+        const T idh2 = sc.inv_dh * sc.inv_dh;
         // process the segment in rounds so every thread reaches the block reductions
         for (int base = s0; base < s1; base += blockDim.x) {
             const int i = base + threadIdx.x;
             if (i < s1) {
                 const int src = perm[i];
-                const int pid = Pin.pid[src];
                 T x[D];
 #pragma unroll
                 for (int a = 0; a < D; ++a)
@@ -365,51 +469,90 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
                     dw[a][2] = h2 * sc.inv_dh;
                     tb[a] = int(fl) - qc[a] * C::B;
                 }
-                // forward gather: grad v_new (transfer.hpp:476)
+                // co.* at the sorted slot i, ci.* at the storage slot src (see the kernel comment)
+                T vc[D], xc[D], pic[D], inc[D], xp[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    vc[a] = co.v[a][i];
+                    xc[a] = co.x[a][i];
+                    pic[a] = (T(1) - alpha) * vc[a] + sc.dt * xc[a];
+                    inc[a] = alpha * vc[a];
+                    xp[a] = T(0);
+                }
                 T L[D * D];
+                T HM[D][D][D]; // HM[c][a][b] = sum_o H_ab(o) v_c(o)   (non-APIC)
+                int t0 = 0;
 #pragma unroll
-                for (int k = 0; k < D * D; ++k)
-                    L[k] = T(0);
-                for (int k = 0; k < C::NOFF; ++k) {
-                    int o[D], kk = k, ti = 0;
+                for (int a = 0; a < D; ++a)
+                    t0 = t0 * TE + tb[a];
+                if constexpr (!APIC) {
+                    // forward gather grad v_new = sum v (x) grad phi (transfer.hpp:476) and every
+                    // stencil sum of the G2P transpose, as moments of the v and v - v_old fields:
+                    //   sum_o grad phi (pic.v + inc.(v - v_old)) = sum_c pic_c G1[c] + inc_c Gd[c]
+                    //   sum_o H (L^T v)                          = sum_bc L_cb HM[c][:, b]
 #pragma unroll
-                    for (int a = D - 1; a >= 0; --a) {
-                        o[a] = kk % 3;
-                        kk /= 3;
+                    for (int c = 0; c < D; ++c) {
+                        Mom<T, D> m;
+                        stencil_moments<T, D, false, true>(tile + c * TN, t0, w, dw, idh2, m);
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            L[c * D + a] = m.g[a];
+                            xp[a] += pic[c] * m.g[a];
+#pragma unroll
+                            for (int b = 0; b < D; ++b)
+                                HM[c][a][b] = m.h[a][b];
+                        }
+                        Mom<T, D> md;
+                        stencil_moments<T, D, false, false>(tile + (D + c) * TN, t0, w, dw, idh2, md);
+#pragma unroll
+                        for (int a = 0; a < D; ++a)
+                            xp[a] += inc[c] * md.g[a];
                     }
+                } else {
 #pragma unroll
-                    for (int a = 0; a < D; ++a)
-                        ti = ti * TE + tb[a] + o[a];
-                    T gw[D];
+                    for (int k = 0; k < D * D; ++k)
+                        L[k] = T(0);
+                    for (int k = 0; k < C::NOFF; ++k) {
+                        int o[D], kk = k, ti = 0;
 #pragma unroll
-                    for (int a = 0; a < D; ++a) {
-                        T r = dw[a][o[a]];
+                        for (int a = D - 1; a >= 0; --a) {
+                            o[a] = kk % 3;
+                            kk /= 3;
+                        }
 #pragma unroll
-                        for (int b = 0; b < D; ++b)
-                            if (b != a)
-                                r *= w[b][o[b]];
-                        gw[a] = r;
-                    }
+                        for (int a = 0; a < D; ++a)
+                            ti = ti * TE + tb[a] + o[a];
+                        T gw[D];
 #pragma unroll
-                    for (int a = 0; a < D; ++a) {
-                        const T nv = tile[a * TN + ti];
+                        for (int a = 0; a < D; ++a) {
+                            T r = dw[a][o[a]];
 #pragma unroll
-                        for (int b = 0; b < D; ++b)
-                            L[a * D + b] += nv * gw[b];
+                            for (int b = 0; b < D; ++b)
+                                if (b != a)
+                                    r *= w[b][o[b]];
+                            gw[a] = r;
+                        }
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            const T nv = tile[a * TN + ti];
+#pragma unroll
+                            for (int b = 0; b < D; ++b)
+                                L[a * D + b] += nv * gw[b];
+                        }
                     }
                 }
                 // (1) constitutive transpose (adjoint.hpp:374-400)
                 T sgc[D * D], gvn_c[D * D], sig_in_c[D * D];
 #pragma unroll
                 for (int k = 0; k < D * D; ++k) {
-                    sgc[k] = co.sig[k][pid];
+                    sgc[k] = co.sig[k][i];
                     gvn_c[k] = T(0);
                     sig_in_c[k] = T(0);
                 }
                 T rho_in_c = T(0), V_in_c = T(0), szz_in_c = T(0);
                 const T rho = Pin.rho[src], V = Pin.V[src];
                 if (sc.material == 0) {
-                    fluid_vjp_dev<T, D>(sc, rho, V, L, sgc, co.rho[pid], co.V[pid], gvn_c, rho_in_c, V_in_c, c_acc,
+                    fluid_vjp_dev<T, D>(sc, rho, V, L, sgc, co.rho[i], co.V[i], gvn_c, rho_in_c, V_in_c, c_acc,
                                         mu_acc);
                 } else {
                     T Sm[3][3];
@@ -420,29 +563,30 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
                             Sm[a][b] = (a < D && b < D) ? Pin.sig[sym_idx<D>(a, b)][src] : T(0);
                     if (D == 2)
                         Sm[2][2] = Pin.szz[src];
-                    dp_vjp_dev<T, D>(sc, Sm, L, sgc, D == 2 ? co.szz[pid] : T(0), co.rho[pid], co.V[pid], rho, V,
+                    dp_vjp_dev<T, D>(sc, Sm, L, sgc, D == 2 ? co.szz[i] : T(0), co.rho[i], co.V[i], rho, V,
                                      gvn_c, sig_in_c, szz_in_c, rho_in_c, V_in_c);
                 }
                 // cot_out.grad_v joins (adjoint.hpp:398-400)
+                if (!co_gv_zero)
 #pragma unroll
-                for (int k = 0; k < D * D; ++k)
-                    gvn_c[k] += co.gv[k][pid];
+                    for (int k = 0; k < D * D; ++k)
+                        gvn_c[k] += co.gv[k][i];
                 // (2) G2P transpose, gather half (adjoint.hpp:405-439)
-                T vc[D], xc[D], pic[D], inc[D], xp[D];
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    vc[a] = co.v[a][pid];
-                    xc[a] = co.x[a][pid];
-                    pic[a] = (T(1) - alpha) * vc[a] + sc.dt * xc[a];
-                    inc[a] = alpha * vc[a];
-                    xp[a] = T(0);
-                }
                 T Bc[D * D];
                 if constexpr (APIC) {
 #pragma unroll
                     for (int k = 0; k < D * D; ++k)
-                        Bc[k] = co.aff[k][pid];
+                        Bc[k] = co.aff[k][i];
                 }
+                if constexpr (!APIC) {
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+#pragma unroll
+                            for (int c = 0; c < D; ++c)
+                                xp[a] += gvn_c[c * D + b] * HM[c][a][b];
+                } else {
                 for (int k = 0; k < C::NOFF; ++k) {
                     int o[D], kk = k, ti = 0;
 #pragma unroll
@@ -473,8 +617,7 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
                     for (int a = 0; a < D; ++a)
 #pragma unroll
                         for (int b = a; b < D; ++b) {
-                            T r = a == b ? (o[a] == 1 ? -T(2) * sc.inv_dh * sc.inv_dh : sc.inv_dh * sc.inv_dh)
-                                         : dw[a][o[a]] * dw[b][o[b]];
+                            T r = a == b ? (o[a] == 1 ? -T(2) * idh2 : idh2) : dw[a][o[a]] * dw[b][o[b]];
 #pragma unroll
                             for (int c = 0; c < D; ++c)
                                 if (c != a && c != b)
@@ -482,17 +625,17 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
                             H[a][b] = r;
                             H[b][a] = r;
                         }
-                    T wv[D], uv[D];
+                    T wv[D], dv[D];
 #pragma unroll
                     for (int a = 0; a < D; ++a) {
                         wv[a] = tile[a * TN + ti];
-                        uv[a] = tile[(D + a) * TN + ti];
+                        dv[a] = tile[(D + a) * TN + ti]; // v - v_old
                     }
                     T s1 = T(0), s2 = T(0);
 #pragma unroll
                     for (int a = 0; a < D; ++a) {
                         s1 += pic[a] * wv[a];
-                        s2 += inc[a] * (wv[a] - uv[a]);
+                        s2 += inc[a] * dv[a];
                     }
                     T LTw[D];
 #pragma unroll
@@ -512,48 +655,48 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
                         xp[a] += gw[a] * (s1 + s2);
                         xp[a] += hs;
                     }
-                    if constexpr (APIC) {
-                        T r[D];
+                    T r[D];
 #pragma unroll
-                        for (int a = 0; a < D; ++a)
-                            r[a] = (sc.origin[a] + T(qc[a] * C::B + tb[a] + o[a]) * sc.dh) - x[a];
-                        T Bcr[D], BcTw[D], wBr = T(0);
+                    for (int a = 0; a < D; ++a)
+                        r[a] = (sc.origin[a] + T(qc[a] * C::B + tb[a] + o[a]) * sc.dh) - x[a];
+                    T Bcr[D], BcTw[D], wBr = T(0);
 #pragma unroll
-                        for (int a = 0; a < D; ++a) {
-                            T s = T(0), s2b = T(0);
+                    for (int a = 0; a < D; ++a) {
+                        T s = T(0), s2b = T(0);
 #pragma unroll
-                            for (int b = 0; b < D; ++b) {
-                                s += Bc[a * D + b] * r[b];
-                                s2b += Bc[b * D + a] * wv[b];
-                            }
-                            Bcr[a] = s;
-                            BcTw[a] = s2b;
+                        for (int b = 0; b < D; ++b) {
+                            s += Bc[a * D + b] * r[b];
+                            s2b += Bc[b * D + a] * wv[b];
                         }
-#pragma unroll
-                        for (int a = 0; a < D; ++a)
-                            wBr += wv[a] * Bcr[a];
-#pragma unroll
-                        for (int a = 0; a < D; ++a)
-                            xp[a] += gw[a] * wBr - phi * BcTw[a];
+                        Bcr[a] = s;
+                        BcTw[a] = s2b;
                     }
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        wBr += wv[a] * Bcr[a];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        xp[a] += gw[a] * wBr - phi * BcTw[a];
                 }
-                // write cot_in (overwrites: this kernel is the first writer of every field)
+                }
+                // write cot_in at the storage slot (overwrites: this kernel is the first writer;
+                // the eps cotangent is discarded, adjoint.hpp:399-400, and never stored)
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
-                    ci.v[a][pid] = alpha * vc[a];
-                    ci.x[a][pid] = xc[a] + xp[a];
+                    ci.v[a][src] = alpha * vc[a];
+                    ci.x[a][src] = xc[a] + xp[a];
                 }
-                ci.rho[pid] = rho_in_c;
-                ci.V[pid] = V_in_c;
-                ci.eps[pid] = T(0);
+                ci.rho[src] = rho_in_c;
+                ci.V[src] = V_in_c;
                 if (D == 2)
-                    ci.szz[pid] = szz_in_c;
+                    ci.szz[src] = szz_in_c;
 #pragma unroll
                 for (int k = 0; k < D * D; ++k) {
-                    ci.sig[k][pid] = sig_in_c[k];
-                    ci.gv[k][pid] = T(0);
+                    ci.sig[k][src] = sig_in_c[k];
+                    if (ci_gv_write)
+                        ci.gv[k][src] = T(0);
                     if constexpr (APIC)
-                        ci.aff[k][pid] = T(0);
+                        ci.aff[k][src] = T(0);
                 }
                 // scatter records (sorted slot i)
 #pragma unroll
@@ -1420,7 +1563,6 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
         __syncthreads();
         for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
             const int src = perm[i];
-            const int pid = Pin.pid[src];
             T x[D], v[D], sig[D][D];
 #pragma unroll
             for (int a = 0; a < D; ++a) {
@@ -1525,6 +1667,51 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
 #pragma unroll
             for (int k = 0; k < D * D; ++k)
                 sigc[k] = Ac[k] = T(0);
+            if constexpr (!AFF) {
+                // every stencil sum of the P2G transpose as moments of the node cotangent fields:
+                //   v:     m sum phi gmom
+                //   sigma: -V sum gf (x) grad phi;  V: -sum (sigma grad phi).gf
+                //   x:     m sum grad phi (gm + v.gmom + g.gf) - V sum H (sigma gf)
+                int t0 = 0;
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+                    t0 = t0 * TE + tb[a];
+                const T idh2 = sc.inv_dh * sc.inv_dh;
+                {
+                    Mom<T, D> m;
+                    stencil_moments<T, D, false, false>(tile, t0, w, dw, idh2, m);
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        xpc[a] += mass * m.g[a];
+                }
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    Mom<T, D> m;
+                    stencil_moments<T, D, true, false>(tile + (1 + c) * TN, t0, w, dw, idh2, m);
+                    vcot[c] = mass * m.phi;
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+                        xpc[a] += (mass * v[c]) * m.g[a];
+                }
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    Mom<T, D> m;
+                    stencil_moments<T, D, false, true>(tile + (1 + D + c) * TN, t0, w, dw, idh2, m);
+#pragma unroll
+                    for (int b = 0; b < D; ++b) {
+                        sigc[c * D + b] = -vol * m.g[b];
+                        Vc -= sig[c][b] * m.g[b];
+                    }
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        T hs = T(0);
+#pragma unroll
+                        for (int b = 0; b < D; ++b)
+                            hs += sig[b][c] * m.h[a][b];
+                        xpc[a] += (mass * sc.gravity[c]) * m.g[a] - vol * hs;
+                    }
+                }
+            } else {
             for (int k = 0; k < C::NOFF; ++k) {
                 int o[D], kk = k, ti = 0;
 #pragma unroll
@@ -1634,20 +1821,21 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
                     xpc[a] += -vol * hs;
                 }
             }
+            }
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-                ci.v[a][pid] += vcot[a];
-                ci.x[a][pid] += xpc[a];
+                ci.v[a][src] += vcot[a];
+                ci.x[a][src] += xpc[a];
             }
-            ci.V[pid] += Vc;
+            ci.V[src] += Vc;
 #pragma unroll
             for (int k = 0; k < D * D; ++k)
-                ci.sig[k][pid] += sigc[k];
+                ci.sig[k][src] += sigc[k];
             if constexpr (AFF) {
                 if (sc.tpic) {
 #pragma unroll
                     for (int k = 0; k < D * D; ++k)
-                        ci.gv[k][pid] += Ac[k];
+                        ci.gv[k][src] += Ac[k];
                 } else {
 #pragma unroll
                     for (int a = 0; a < D; ++a)
@@ -1657,7 +1845,7 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
 #pragma unroll
                             for (int k = 0; k < D; ++k)
                                 s += Ac[a * D + k] * Dinv[k * D + b];
-                            ci.aff[a * D + b][pid] += s;
+                            ci.aff[a * D + b][src] += s;
                         }
                 }
             }
@@ -1702,7 +1890,7 @@ __global__ void __launch_bounds__(1024) k_pg_reduce(const T* __restrict__ pg_blo
 }
 
 // ---- Lagrangian least-squares seeder (SPEC observe_lagrangian + loss) -------------------------
-// loss += sum ||z - target||^2, cot.z[pid] += 2 (z - target), z = x or v. Grid-wide: one
+// loss += sum ||z - target||^2, cot.z[slot of pid] += 2 (z - target), z = x or v. Grid-wide: one
 // selection entry per thread, per-block sums (fixed tree), then k_seed_sum adds the blocks in order.
 template <class T, int D>
 __global__ void __launch_bounds__(256) k_seed_lagrangian(PBuf<T, D> P, int n, const int* __restrict__ slot_of_pid,
@@ -1723,7 +1911,7 @@ __global__ void __launch_bounds__(256) k_seed_lagrangian(PBuf<T, D> P, int n, co
             acc += r * r;
             if (do_cot) {
                 T* zc = field == 0 ? cot.x[a] : cot.v[a];
-                zc[pid] += T(2) * r;
+                zc[s] += T(2) * r; // cot in the storage order of P
             }
         }
     }
@@ -1829,7 +2017,7 @@ __global__ void k_eul_final(const T* __restrict__ partials, int nblocks, int nre
     }
 }
 
-// cot.z[pid] += g_l for every region containing the particle (region order)
+// cot.z[i] += g_l (storage order) for every region containing the particle (region order)
 template <class T, int D>
 __global__ void k_eul_seed(PBuf<T, D> P, int n, const T* __restrict__ centers, const T* __restrict__ half, int nreg,
                            const T* __restrict__ g, int field, CBuf<T, D> cot)
@@ -1837,7 +2025,6 @@ __global__ void k_eul_seed(PBuf<T, D> P, int n, const T* __restrict__ centers, c
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || P.pid[i] < 0)
         return;
-    const int pid = P.pid[i];
     T x[D];
 #pragma unroll
     for (int a = 0; a < D; ++a)
@@ -1851,7 +2038,7 @@ __global__ void k_eul_seed(PBuf<T, D> P, int n, const T* __restrict__ centers, c
 #pragma unroll
             for (int a = 0; a < D; ++a) {
                 T* zc = field == 0 ? cot.x[a] : cot.v[a];
-                zc[pid] += g[l * D + a];
+                zc[i] += g[l * D + a];
             }
     }
 }
@@ -1861,35 +2048,38 @@ __global__ void k_eul_seed(PBuf<T, D> P, int n, const T* __restrict__ centers, c
 enum CotField { CF_X = 1, CF_V = 2, CF_RHO = 4, CF_VOL = 8, CF_EPS = 16, CF_SZZ = 32, CF_SIG = 64, CF_GV = 128,
                 CF_AFF = 256 };
 template <class T, int D>
-__global__ void k_cot_in(Stage<T, D> S, CBuf<T, D> k, int n, int mask, int has_aff)
+__global__ void k_cot_in(Stage<T, D> S, CBuf<T, D> k, int n, int mask, int has_aff, const int* __restrict__ perm)
 {
+    // host row j pairs with the uploaded state's storage slot j; with perm the cotangent is placed
+    // at the sorted slot i (perm[i] = j), the storage order of the step's output state
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n)
         return;
+    const int j = perm ? perm[i] : i;
     auto get = [&](int f, int bit, size_t idx) { return (mask & bit) ? S.f[f][idx] : T(0); };
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        k.x[a][i] = get(S_X, CF_X, (size_t)i * D + a);
-        k.v[a][i] = get(S_V, CF_V, (size_t)i * D + a);
+        k.x[a][i] = get(S_X, CF_X, (size_t)j * D + a);
+        k.v[a][i] = get(S_V, CF_V, (size_t)j * D + a);
     }
-    k.rho[i] = get(S_RHO, CF_RHO, i);
-    k.V[i] = get(S_VOL, CF_VOL, i);
-    k.eps[i] = T(0); // the eps cotangent is discarded (adjoint.hpp:399-400)
+    k.rho[i] = get(S_RHO, CF_RHO, j);
+    k.V[i] = get(S_VOL, CF_VOL, j);
     if (D == 2)
-        k.szz[i] = get(S_SZZ, CF_SZZ, i);
+        k.szz[i] = get(S_SZZ, CF_SZZ, j);
 #pragma unroll
     for (int r = 0; r < D; ++r)
 #pragma unroll
         for (int q = 0; q < D; ++q) {
-            const size_t m = (size_t)i * D * D + q * D + r; // column-major (r, q)
+            const size_t m = (size_t)j * D * D + q * D + r; // column-major (r, q)
             k.sig[r * D + q][i] = get(S_SIG, CF_SIG, m);
-            k.gv[r * D + q][i] = get(S_GV, CF_GV, m);
+            if (mask & CF_GV)
+                k.gv[r * D + q][i] = S.f[S_GV][m];
             if (has_aff)
                 k.aff[r * D + q][i] = get(S_AFF, CF_AFF, m);
         }
 }
 template <class T, int D>
-__global__ void k_cot_out(Stage<T, D> S, CBuf<T, D> k, int n, int has_aff)
+__global__ void k_cot_out(Stage<T, D> S, CBuf<T, D> k, int n, int has_aff, int gv_zero)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n)
@@ -1901,7 +2091,7 @@ __global__ void k_cot_out(Stage<T, D> S, CBuf<T, D> k, int n, int has_aff)
     }
     S.f[S_RHO][i] = k.rho[i];
     S.f[S_VOL][i] = k.V[i];
-    S.f[S_EPS][i] = k.eps[i];
+    S.f[S_EPS][i] = T(0); // the eps cotangent is discarded (adjoint.hpp:399-400)
     if (D == 2)
         S.f[S_SZZ][i] = k.szz[i];
 #pragma unroll
@@ -1910,7 +2100,7 @@ __global__ void k_cot_out(Stage<T, D> S, CBuf<T, D> k, int n, int has_aff)
         for (int q = 0; q < D; ++q) {
             const size_t m = (size_t)i * D * D + q * D + r;
             S.f[S_SIG][m] = k.sig[r * D + q][i];
-            S.f[S_GV][m] = k.gv[r * D + q][i];
+            S.f[S_GV][m] = gv_zero ? T(0) : k.gv[r * D + q][i];
             if (has_aff)
                 S.f[S_AFF][m] = k.aff[r * D + q][i];
         }
@@ -1936,6 +2126,7 @@ template <class T, int D> struct AdjWork {
     double* pg_acc = nullptr;
     double* loss_acc = nullptr;
     int* slot_of_pid = nullptr;
+    bool gvz[2] = {true, true}; // cot[b].grad_v is known zero (not stored)
     std::vector<void*> allocs;
     bool ready = false;
     int64_t cap = 0;
@@ -1964,7 +2155,7 @@ template <class T, int D> struct AdjWork {
             }
             k.rho = al<T>(cap);
             k.V = al<T>(cap);
-            k.eps = al<T>(cap);
+            k.eps = nullptr; // discarded cotangent (adjoint.hpp:399-400): never stored
             k.szz = D == 2 ? al<T>(cap) : nullptr;
             for (int q = 0; q < D * D; ++q) {
                 k.sig[q] = al<T>(cap);
@@ -2020,7 +2211,9 @@ template <class T, int D> struct AdjWork {
     }
 
     // upload / download a host cotangent view (reference layout, id order) <-> cot[b]
-    template <class Ctx> void cot_upload(Ctx& c, const mpm_cot_view* v, int b)
+    // perm: place row j at the sorted slot i with perm[i] = j (cot_out of a step whose replay has
+    // sorted the input state); nullptr: storage order of the uploaded state
+    template <class Ctx> void cot_upload(Ctx& c, const mpm_cot_view* v, int b, const int* perm)
     {
         const int64_t n = c.n;
         if (n == 0)
@@ -2036,8 +2229,10 @@ template <class T, int D> struct AdjWork {
                 mask |= bit[f];
             }
         c.launch("k_cot_in", [&] {
-            k_cot_in<T, D><<<c.grid_for(n, 256), 256, 0, c.stream>>>(c.stage, cot[b], int(n), mask, c.has_aff);
+            k_cot_in<T, D><<<c.grid_for(n, 256), 256, 0, c.stream>>>(c.stage, cot[b], int(n), mask, c.has_aff,
+                                                                     perm);
         });
+        gvz[b] = !(mask & CF_GV);
         c.sync(); // the staging buffer is reused by the next transfer
     }
     template <class Ctx> void cot_zero(Ctx& c, int b)
@@ -2050,15 +2245,14 @@ template <class T, int D> struct AdjWork {
         }
         c.zero(k.rho, n);
         c.zero(k.V, n);
-        c.zero(k.eps, n);
         if (D == 2)
             c.zero(k.szz, n);
         for (int q = 0; q < D * D; ++q) {
             c.zero(k.sig[q], n);
-            c.zero(k.gv[q], n);
             if (c.has_aff)
                 c.zero(k.aff[q], n);
         }
+        gvz[b] = true;
     }
 
     template <class Ctx> void cot_download(Ctx& c, mpm_cot_view* v, int b)
@@ -2067,7 +2261,7 @@ template <class T, int D> struct AdjWork {
         if (n == 0)
             return;
         c.launch("k_cot_out", [&] {
-            k_cot_out<T, D><<<c.grid_for(n, 256), 256, 0, c.stream>>>(c.stage, cot[b], int(n), c.has_aff);
+            k_cot_out<T, D><<<c.grid_for(n, 256), 256, 0, c.stream>>>(c.stage, cot[b], int(n), c.has_aff, gvz[b]);
         });
         void* dst[S_NFIELDS] = {v->x, v->v, nullptr, v->volume, v->rho, v->eps_eq, D == 2 ? v->sigma_zz : nullptr,
                                 v->sigma, v->grad_v, c.has_aff ? v->affine : nullptr, nullptr};
@@ -2078,14 +2272,23 @@ template <class T, int D> struct AdjWork {
         c.sync();
     }
 
-    // one reverse step on the state currently in c.buf[c.cur]: cot[bo] (out) -> cot[bi] (in)
+    // one reverse step on the state currently in c.buf[c.cur]: cot[bo] (out, storage order of the
+    // step's output state = this replay's sort order) -> cot[bi] (in, storage order of the input)
     template <class Ctx> void vjp_enqueue(Ctx& c, int bo, int bi)
     {
         ensure(c);
-        // forward replay with the full grid stored (m, p, f, v, v_old)
+        vjp_replay(c);
+        vjp_reverse(c, bo, bi);
+    }
+    // forward replay with the full grid stored (m, p, f, v, v_old)
+    template <class Ctx> void vjp_replay(Ctx& c)
+    {
         c.sort_and_segment();
         c.p2g_kernel();
         c.template grid_kernel<G_SUM | G_MOM | G_CORR | G_STORE>();
+    }
+    template <class Ctx> void vjp_reverse(Ctx& c, int bo, int bi)
+    {
         k5(c, bo, bi);
         c.launch("k_adj_grid", [&] {
             k_adj_grid<T, D><<<c.persistent(4), C::NB, 0, c.stream>>>(c.sc, c.G, gc, partials, c.bstart, c.act,
@@ -2099,10 +2302,10 @@ template <class T, int D> struct AdjWork {
     template <class Ctx> void slab_vjp_begin(Ctx& c, const mpm_cot_view* co)
     {
         ensure(c);
-        cot_upload(c, co, 0);
         pg_reset(c, nullptr); // this rank's partial; the caller sums the ranks
         c.reset_status();
         c.sort_and_segment();
+        cot_upload(c, co, 0, c.perm);
         c.p2g_kernel();
         c.template grid_kernel<G_BANDONLY | G_SUM | G_NOGRAV | G_STORE>();
     }
@@ -2151,17 +2354,19 @@ template <class T, int D> struct AdjWork {
         auto& Pin = c.buf[c.cur];
         const unsigned gr = c.persistent(4);
         const size_t sm5 = sizeof(T) * 2 * D * C::TN;
+        const int gvw = c.sc.tpic ? 1 : 0; // only TPIC accumulates a grad_v cotangent (K7)
+        gvz[bi] = !gvw;
         if (c.has_aff)
             c.launch("k_adj_g2pT_gather", [&] {
                 k_adj_g2pT_gather<T, D, true><<<gr, 256, sm5, c.stream>>>(c.sc, Pin, c.G, c.perm, c.bstart, c.bend,
                                                                            c.occ, c.counts, cot[bo], cot[bi], sb,
-                                                                           pg_block, c.st);
+                                                                           pg_block, c.st, gvz[bo], gvw);
             });
         else
             c.launch("k_adj_g2pT_gather", [&] {
                 k_adj_g2pT_gather<T, D, false><<<gr, 256, sm5, c.stream>>>(c.sc, Pin, c.G, c.perm, c.bstart, c.bend,
                                                                             c.occ, c.counts, cot[bo], cot[bi], sb,
-                                                                            pg_block, c.st);
+                                                                            pg_block, c.st, gvz[bo], gvw);
             });
         const int tpb = D == 2 ? 160 : 256;
         if constexpr (D == 3) {
@@ -2244,10 +2449,11 @@ template <class T, int D> struct AdjWork {
     {
         c.upload(s);
         ensure(c);
-        cot_upload(c, co, 0);
         pg_reset(c, pg);
         c.reset_status();
-        vjp_enqueue(c, 0, 1);
+        vjp_replay(c);
+        cot_upload(c, co, 0, c.perm);
+        vjp_reverse(c, 0, 1);
         c.check_status(c.step);
         cot_download(c, ci, 1);
         pg_download(c, pg);
