@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--adj-steps", type=int, default=20, help="fwd+adjoint sample: backprop steps (0: skip)")
+    ap.add_argument("--adj-segments", type=int, default=2)
     ap.add_argument("--mode", default="auto", choices=["auto", "plain", "slab"],
                     help="auto: one context at N=1, slab decomposition for N>1")
     return ap.parse_args()
@@ -196,6 +198,75 @@ def cpu_baseline(cfg, dtype, steps=1):
             if kind == "ref" else "oracle restatement (C++20 -O3, serial)"}
 
 
+def _cpu_adj_worker(args):
+    """One host core: the reference's backprop_trajectory (checkpoint.hpp:72-143) on the full scene."""
+    cfg, dtype, kind, steps, nseg = args
+    sys.path.insert(0, str(ROOT))
+    from oracle import CpuOracle  # test infrastructure: the CPU baseline, never the product path
+    from paper_2507_04192_b200.presets import CONFIGS
+    s = CONFIGS[cfg](dtype=dtype)
+    o = CpuOracle(kind)
+    st = o.init_scene(s)
+    sd = {"field": "x", "obs_steps": [steps], "sel": None, "target": st.particles.x[None] + 1e-3}
+    t0 = time.perf_counter()
+    o.backprop(s, st, steps, nseg, sd)
+    return st.particles.size() * steps, time.perf_counter() - t0
+
+
+def cpu_baseline_adj(cfg, dtype, steps=2, nseg=1):
+    """fwd+adjoint on the host cores: the reference's backprop_trajectory over `steps` steps (forward
+    sweep + replay + step_vjp per step), one process per core, capped by host memory."""
+    import multiprocessing as mp
+    import oracle
+    kind = "ref" if oracle.available("ref") else "orc"
+    cores = os.cpu_count() or 1
+    per_proc_gb = {"C4": 14.0, "C5": 100.0}.get(cfg, 2.0) * (0.5 if dtype == "f32" else 1.0)
+    procs = max(1, min(cores, int(_mem_available_gb() * 0.6 / per_proc_gb)))
+    with mp.get_context("spawn").Pool(procs) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_adj_worker, [(cfg, dtype, kind, steps, nseg)] * procs)
+        wall = time.perf_counter() - t0
+    per_proc = [r[0] / r[1] for r in res]
+    n = int(res[0][0] / steps)
+    return {"value": sum(per_proc), "unit": UNIT, "cores": procs, "host_cores": cores,
+            "kind": "reference" if kind == "ref" else "port",
+            "sample": (f"{procs} concurrent replicas (of {cores} host cores, capped by host memory) of the full "
+                       f"{cfg} scene ({n} particles): backprop_trajectory over {steps} steps, {nseg} segment(s), "
+                       f"Lagrangian least-squares loss on the final positions, wall clock of the call; "
+                       f"value = sum of per-process particle-steps/s"),
+            "single_process": per_proc[0], "wall_s": wall}
+
+
+def bench_fwd_adj(ctx, s, st, n, steps, nseg):
+    """fwd+adjoint (BASELINE metric, second half): one checkpointed backprop_trajectory through the
+    C ABI -- forward sweep, segment replays, step_vjp per step (checkpoint.hpp:72-143) -- with the
+    device Lagrangian least-squares seeder on the final positions. Device time from CUDA events on
+    the context stream around the sweep (mpm_backprop_result.device_ms); the S0 upload and the
+    cotangent download are outside it. Roofline: B_fwd+adj = 2 B_fwd + B_vjp."""
+    from paper_2507_04192_b200.seeders import LagrangianLeastSquares
+    st0 = ctx.download(st)
+    sd = LagrangianLeastSquares([steps], st0.particles.x[None] + 1e-3, "x")
+    ctx.backprop(st0, steps, nseg, sd.desc())  # allocates the checkpoint / replay pool
+    t0 = time.perf_counter()
+    _, _, res = ctx.backprop(st0, steps, nseg, sd.desc())
+    wall = time.perf_counter() - t0
+    ms = res.device_ms
+    ctx.profile(True)
+    ctx.profile_reset()
+    ctx.backprop(st0, steps, nseg, sd.desc())
+    kern = {}
+    for k in ("k_p2g", "k_grid", "k_g2p", "k_adj_g2pT_gather", "k_adj_scatter", "k_adj_grid", "k_adj_p2gT",
+              "k_seed"):
+        t, c = ctx.profile_query(k)
+        if c:
+            kern[k] = {"ms_per_launch": t / c, "launches": c}
+    ctx.profile(False)
+    return {"value": n * steps / (ms / 1e3), "unit": UNIT, "steps": steps, "n_segments": nseg,
+            "device_ms": ms, "ms_per_step": ms / steps, "wall_s_incl_host_transfers": wall,
+            "loss": res.loss, "kernels": kern,
+            "timing": "CUDA events on the library stream around forward sweep + replays + VJPs"}
+
+
 # ---- GPU arm -----------------------------------------------------------------------------------
 def bench_b200(a, rank, world, local):
     import ctypes as C
@@ -268,6 +339,22 @@ def bench_b200(a, rank, world, local):
     if rank == 0:
         e2e = bench_e2e(ctx, s, st, a.steps)
 
+    # ---- fwd+adjoint (checkpointed backprop_trajectory), device-timed
+    fwd_adj = None
+    if a.adj_steps > 0:
+        fwd_adj = bench_fwd_adj(ctx, s, st, n, a.adj_steps, a.adj_segments)
+        d = s.dim
+        sz = 8 if s.dtype == "f64" else 4
+        ns = 3 if d == 2 else 6
+        dp = s.material.__class__.__name__ == "DruckerPragerParams"
+        COT = 2 * d + 2 + ns + (1 if (dp and d == 2) else 0)
+        A_np = active_nodes_step / n
+        B_vjp = (IN + 2 * COT) * sz + A_np * (2 * (1 + 2 * d) + 8 * d) * sz
+        B_fa = 2 * B_fwd + B_vjp
+        gbs = n * B_fa / (fwd_adj["ms_per_step"] / 1e3) / 1e9
+        fwd_adj["roofline"] = {"bound": "hbm", "bytes_per_particle_step": B_fa, "achieved": gbs, "peak": peak,
+                               "unit": "GB/s", "frac": gbs / peak}
+
     ctx.close()
     if world > 1:
         import torch.distributed as dist
@@ -291,7 +378,7 @@ def bench_b200(a, rank, world, local):
                               "bytes_per_particle_step": B_fwd}},
         "fp64": fp64_for(prof, a),
         "kernels": prof, "profiled_step_ms": total_ms / 3,
-        "clocks": ck, "gpu_launches": launches, "e2e": e2e,
+        "clocks": ck, "gpu_launches": launches, "e2e": e2e, "fwd_adj": fwd_adj,
     }
     return line
 
@@ -535,6 +622,11 @@ def main():
                 line["cpu_baseline"] = cpu_baseline(a.config, a.dtype, 1)
             except Exception as e:  # the baseline is reported, never the target
                 line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+            if line.get("fwd_adj"):
+                try:
+                    line["fwd_adj"]["cpu_baseline"] = cpu_baseline_adj(a.config, a.dtype)
+                except Exception as e:
+                    line["fwd_adj"]["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
         print(json.dumps(line), flush=True)
 
 

@@ -169,6 +169,8 @@ typedef struct mpm_backprop_result {
     double loss;
     int64_t checkpoints_stored;
     int64_t peak_replay_states;
+    double device_ms; /* device time of the sweep (forward sweep, segment replays, VJPs; CUDA events on
+                         the context stream), excluding the S0 upload and the cotangent download */
 } mpm_backprop_result;
 
 /* advance flags */

@@ -159,6 +159,7 @@ class BackpropResultView(C.Structure):
         ("loss", C.c_double),
         ("checkpoints_stored", C.c_int64),
         ("peak_replay_states", C.c_int64),
+        ("device_ms", C.c_double),
     ]
 
 

@@ -1560,6 +1560,12 @@ template <class T, int D> struct Ctx : CtxBase {
                 replay[j] = pool_buf(size_t(nseg + j));
             std::vector<uint64_t> bhash(nseg + 1);
             CK(cudaMemsetAsync(aw.loss_acc, 0, sizeof(double), stream));
+            struct Ev { // released on every exit path
+                cudaEvent_t e{};
+                Ev() { CK(cudaEventCreate(&e)); }
+                ~Ev() { cudaEventDestroy(e); }
+            } ev0, ev1;
+            CK(cudaEventRecord(ev0.e, stream));
             // forward sweep
             reset_status();
             if (obs_index(0) >= 0)
@@ -1611,13 +1617,17 @@ template <class T, int D> struct Ctx : CtxBase {
             }
             if (obs_index(0) >= 0)
                 seed(ckpt[0], obs_index(0), cb, 1);
+            CK(cudaEventRecord(ev1.e, stream));
             CK(cudaStreamSynchronize(stream));
+            float dev_ms = 0;
+            CK(cudaEventElapsedTime(&dev_ms, ev0.e, ev1.e));
             aw.cot_download(*this, c0, cb);
             aw.pg_download(*this, pg);
             if (res) {
                 res->loss = loss;
                 res->checkpoints_stored = nseg;
                 res->peak_replay_states = peak;
+                res->device_ms = dev_ms;
             }
             // restore the context's own buffers holding S0
             buf[0] = own0;
