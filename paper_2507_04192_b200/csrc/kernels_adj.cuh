@@ -1575,6 +1575,17 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
                 for (int b = 0; b < D; ++b)
                     sig[a][b] = Pin.sig[sym_idx<D>(a, b)][src];
             const T mass = Pin.m[src], vol = Pin.V[src];
+            // cot_in as K5a left it, read up front so that its latency overlaps the gather
+            T ox[D], ov[D], oV, osg[D * D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                ox[a] = ci.x[a][src];
+                ov[a] = ci.v[a][src];
+            }
+            oV = ci.V[src];
+#pragma unroll
+            for (int k = 0; k < D * D; ++k)
+                osg[k] = ci.sig[k][src];
             T w[D][3], dw[D][3];
             int tb[D], base[D];
 #pragma unroll
@@ -1824,13 +1835,13 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
             }
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-                ci.v[a][src] += vcot[a];
-                ci.x[a][src] += xpc[a];
+                ci.v[a][src] = ov[a] + vcot[a];
+                ci.x[a][src] = ox[a] + xpc[a];
             }
-            ci.V[src] += Vc;
+            ci.V[src] = oV + Vc;
 #pragma unroll
             for (int k = 0; k < D * D; ++k)
-                ci.sig[k][src] += sigc[k];
+                ci.sig[k][src] = osg[k] + sigc[k];
             if constexpr (AFF) {
                 if (sc.tpic) {
 #pragma unroll
