@@ -284,6 +284,7 @@ template <class T, int D> struct Ctx : CtxBase {
         drop_slab_graphs();
         for (void* p : bp_pool_mem)
             cudaFree(p);
+        tape_free();
         for (auto& e : events) {
             cudaEventDestroy(e.a);
             cudaEventDestroy(e.b);
@@ -1416,6 +1417,90 @@ template <class T, int D> struct Ctx : CtxBase {
     // GB per call dominated a short backprop); released with the context
     std::vector<PBuf<T, D>> bp_pool;
     std::vector<void*> bp_pool_mem;
+
+    // ---- replay tape (backprop): per segment-replay step, the sort arrays (pointer-swapped in,
+    // no copies) and the active grid blocks, so that step_vjp skips its forward replay
+    // (sort + P2G + grid); a step whose grid outgrew its slot falls back to the replay
+    struct SortSet {
+        int *keys_sorted, *perm, *bstart, *bend, *lstart, *occ, *act, *counts;
+        unsigned char* nflag;
+    };
+    SortSet sort_set() const { return {keys_sorted, perm, bstart, bend, lstart, occ, act, counts, nflag}; }
+    void use_sort_set(const SortSet& s)
+    {
+        keys_sorted = s.keys_sorted;
+        perm = s.perm;
+        bstart = s.bstart;
+        bend = s.bend;
+        lstart = s.lstart;
+        occ = s.occ;
+        act = s.act;
+        counts = s.counts;
+        nflag = s.nflag;
+    }
+    struct TapeSlot {
+        SortSet ss{};
+        T* grid = nullptr;
+    };
+    std::vector<TapeSlot> tape;
+    bool tape_enabled = !(std::getenv("MPM_TAPE") && std::getenv("MPM_TAPE")[0] == '0');
+    std::vector<void*> tape_mem;
+    int64_t tape_grid_cap = 0; // node blocks per slot
+    int* tape_over = nullptr;  // [slots] overflow flags
+    void tape_free()
+    {
+        for (void* p : tape_mem)
+            cudaFree(p);
+        tape_mem.clear();
+        tape.clear();
+        tape_over = nullptr;
+        tape_grid_cap = 0;
+    }
+    size_t tape_slot_bytes(int64_t grid_cap) const
+    {
+        return sizeof(int) * (2 * size_t(cap) + size_t(sc.nb_total) * (3 + C::B + 1) + size_t(sc.nnb_total) + 4) +
+               size_t(sc.nnb_total) + sizeof(T) * size_t(grid_cap) * C::NB * (1 + 4 * D);
+    }
+    // slots for `L` replay steps with `grid_cap` node blocks each; false when HBM is short
+    bool tape_reserve(int64_t L, int64_t grid_cap)
+    {
+        if (int64_t(tape.size()) >= L && tape_grid_cap >= grid_cap)
+            return true;
+        tape_free();
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        if (double(tape_slot_bytes(grid_cap)) * double(L) > 0.5 * double(fr))
+            return false;
+        auto al = [&](auto*& p, size_t k) {
+            CK(cudaMalloc(reinterpret_cast<void**>(&p), (k ? k : 1) * sizeof(*p)));
+            tape_mem.push_back(p);
+        };
+        tape.resize(L);
+        for (auto& t : tape) {
+            al(t.ss.keys_sorted, cap);
+            al(t.ss.perm, cap);
+            al(t.ss.bstart, sc.nb_total);
+            al(t.ss.bend, sc.nb_total);
+            al(t.ss.lstart, (size_t)sc.nb_total * (C::B + 1));
+            al(t.ss.occ, sc.nb_total);
+            al(t.ss.act, sc.nnb_total);
+            al(t.ss.counts, 4);
+            al(t.ss.nflag, sc.nnb_total);
+            al(t.grid, (size_t)grid_cap * C::NB * (1 + 4 * D));
+        }
+        al(tape_over, L);
+        tape_grid_cap = grid_cap;
+        return true;
+    }
+    template <bool SAVE> void tape_grid(int j)
+    {
+        const int64_t per = tape_grid_cap * C::NB * (1 + 4 * D);
+        const unsigned blocks = unsigned(std::min<int64_t>((per + 255) / 256, int64_t(nsm) * 16));
+        launch(SAVE ? "k_tape_save" : "k_tape_load", [&] {
+            k_grid_tape<T, D, SAVE><<<std::max(1u, blocks), 256, 0, stream>>>(G, act, counts + 1, tape[j].grid,
+                                                                             int(tape_grid_cap), tape_over + j);
+        });
+    }
     PBuf<T, D> pool_buf(size_t k)
     {
         while (bp_pool.size() <= k)
@@ -1552,6 +1637,7 @@ template <class T, int D> struct Ctx : CtxBase {
             });
             launch("k_seed", [&] { k_seed_sum<T><<<1, 1024, 0, stream>>>(d_lblk, sb, aw.loss_acc); });
         };
+        const SortSet own_ss = sort_set();
         try {
             std::vector<PBuf<T, D>> ckpt(nseg), replay(Lmax + 1);
             for (int k = 0; k < nseg; ++k) // checkpoint and replay slots persist across calls
@@ -1583,6 +1669,16 @@ template <class T, int D> struct Ctx : CtxBase {
             check_status(step0);
             double loss = 0;
             d2h_raw(&loss, aw.loss_acc, sizeof(double));
+            // replay tape, sized by the last forward step's active node blocks (+25 %)
+            int n_act_last = 0;
+            d2h_raw(&n_act_last, counts + 1, sizeof(int));
+            const char* cap_env = std::getenv("MPM_TAPE_CAP"); // test hook: force slot overflows
+            const int64_t grid_cap = cap_env ? std::max<int64_t>(1, std::atoll(cap_env))
+                                             : std::min<int64_t>(sc.nnb_total, (int64_t(n_act_last) * 5 / 4 + 255) / 256 * 256);
+            const bool use_tape = tape_enabled && n > 0 && tape_reserve(Lmax, grid_cap);
+            if (use_tape)
+                CK(cudaMemsetAsync(tape_over, 0, sizeof(int) * Lmax, stream));
+            std::vector<int> over(Lmax, 1);
             // backward sweep
             aw.cot_zero(*this, 0);
             aw.pg_reset(*this, pg);
@@ -1596,23 +1692,42 @@ template <class T, int D> struct Ctx : CtxBase {
                     buf[1] = replay[j + 1];
                     cur = 0;
                     keys_valid = false;
-                    step_once(false);
+                    if (use_tape) {
+                        use_sort_set(tape[j].ss);
+                        step_once(false, true);
+                        tape_grid<true>(int(j));
+                    } else {
+                        step_once(false);
+                    }
                 }
                 peak = std::max(peak, len + 1);
                 if (digest_of(replay[len]) != bhash[k + 1])
                     throw ApiError(MPM_ERR_CHECKPOINT,
                                    "checkpoint mismatch: recomputed segment end differs from the recorded state at step "
                                        + std::to_string(step0 + b1));
+                if (use_tape) { // the digest read synchronised the stream
+                    d2h_raw(over.data(), tape_over, sizeof(int) * len);
+                    CK(cudaMemsetAsync(tape_over, 0, sizeof(int) * len, stream));
+                }
                 for (int64_t t = b1; t > b0; --t) {
                     if (obs_index(t) >= 0)
                         seed(replay[t - b0], obs_index(t), cb, 1);
-                    buf[0] = replay[t - b0 - 1];
-                    buf[1] = replay[t - b0];
+                    const int64_t j = t - b0 - 1;
+                    buf[0] = replay[j];
+                    buf[1] = replay[j + 1];
                     cur = 0;
                     keys_valid = false;
-                    aw.vjp_enqueue(*this, cb, cb ^ 1);
+                    if (use_tape && !over[j]) { // the step's sort and grid from the replay
+                        use_sort_set(tape[j].ss);
+                        tape_grid<false>(int(j));
+                        aw.vjp_reverse(*this, cb, cb ^ 1);
+                    } else {
+                        use_sort_set(own_ss);
+                        aw.vjp_enqueue(*this, cb, cb ^ 1);
+                    }
                     cb ^= 1;
                 }
+                use_sort_set(own_ss);
                 check_status(step);
             }
             if (obs_index(0) >= 0)
@@ -1638,6 +1753,7 @@ template <class T, int D> struct Ctx : CtxBase {
             keys_valid = false;
             CK(cudaStreamSynchronize(stream));
         } catch (...) {
+            use_sort_set(own_ss);
             buf[0] = own0;
             buf[1] = own1;
             cur = cur0;

@@ -2124,6 +2124,49 @@ template <class T, int D> __global__ void k_slot_of_pid(PBuf<T, D> P, int n, int
         slot_of_pid[P.pid[i]] = i;
 }
 
+// ---- replay tape: a step's forward grid kept from the segment replay --------------------------
+// field f of the dense grid: m, p[D], f[D], v[D], v_old[D]
+template <class T, int D> __device__ __forceinline__ T* grid_field(const GBuf<T, D>& G, int f)
+{
+    if (f == 0)
+        return G.m;
+    if (f <= D)
+        return G.p[f - 1];
+    if (f <= 2 * D)
+        return G.f[f - 1 - D];
+    if (f <= 3 * D)
+        return G.v[f - 1 - 2 * D];
+    return G.vold[f - 1 - 3 * D];
+}
+// SAVE: active node blocks of G -> dst[w][field][node]; LOAD: the reverse. A step whose active
+// block count exceeds the slot capacity is flagged (the VJP then recomputes its grid).
+template <class T, int D, bool SAVE>
+__global__ void __launch_bounds__(256) k_grid_tape(GBuf<T, D> G, const int* __restrict__ act,
+                                                   const int* __restrict__ n_act, T* __restrict__ tape, int cap_blocks,
+                                                   int* overflow)
+{
+    using C = Cfg<D>;
+    constexpr int NFLD = 1 + 4 * D;
+    const int na = *n_act;
+    if (na > cap_blocks) {
+        if (SAVE && blockIdx.x == 0 && threadIdx.x == 0)
+            *overflow = 1;
+        return;
+    }
+    const long long total = (long long)na * NFLD * C::NB;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int loc = int(e % C::NB);
+        const long long r = e / C::NB;
+        const int f = int(r % NFLD), w = int(r / NFLD);
+        T* g = grid_field<T, D>(G, f) + (size_t)act[w] * C::NB + loc;
+        if (SAVE)
+            tape[e] = *g;
+        else
+            *g = tape[e];
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Adjoint workspace + drivers (host side, templated on the context type)
 template <class T, int D> struct AdjWork {

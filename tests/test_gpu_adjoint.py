@@ -227,3 +227,39 @@ def test_finite_difference_initial_velocity():
         fd = (loss(st.particles.v + h * d) - loss(st.particles.v - h * d)) / (2 * h)
         an = float((c.v * d).sum())
         assert abs(fd - an) <= 1e-5 * (abs(fd) + 1e-12), (fd, an)
+
+
+@pytest.mark.parametrize("name", ["fluid2-flip", "fluid2-tpic-rate", "dp2-coulomb-obstacle", "dp3-coulomb",
+                                  "fluid3-apic"])
+@pytest.mark.parametrize("cap", [None, "1"])
+def test_backprop_replay_tape_bitwise(name, cap, monkeypatch):
+    """The replay tape (the segment replay's sort and grid reused by step_vjp) changes nothing:
+    bit-identical to recomputing the forward replay inside every step_vjp. cap=1 forces every
+    step's grid to overflow its slot (the recompute fallback)."""
+    s = SCENES[name]()
+    st = init_scene(s)
+    ctx = Context(s, st.particles.size())
+    ctx.upload(st)
+    ctx.advance(9)
+    seeder = _seeder_final_x(ctx.download(st.copy()), 9)
+    ctx.close()
+    monkeypatch.setenv("MPM_TAPE", "0")
+    ctx0 = Context(s, st.particles.size())
+    c_ref, pg_ref, r_ref = ctx0.backprop(st, 9, 2, seeder)
+    ctx0.close()
+    monkeypatch.setenv("MPM_TAPE", "1")
+    if cap:
+        monkeypatch.setenv("MPM_TAPE_CAP", cap)
+    ctx1 = Context(s, st.particles.size())
+    for _ in range(2):  # the second call reuses the persistent tape slots
+        c, pg, r = ctx1.backprop(st, 9, 2, seeder)
+        for f in StateCotangent.FIELDS:
+            a, b = getattr(c, f), getattr(c_ref, f)
+            if a is not None:
+                assert np.array_equal(a, b), f
+        assert r.loss == r_ref.loss
+        assert pg.sound_speed == pg_ref.sound_speed and pg.viscosity == pg_ref.viscosity
+        for w in range(2 * s.dim):
+            if pg_ref.wall_friction[w] is not None:
+                assert np.array_equal(pg.wall_friction[w], pg_ref.wall_friction[w])
+    ctx1.close()

@@ -49,8 +49,8 @@ ctx.backprop(st, N, nseg, sd.desc())  # first call allocates the checkpoint / re
 t0 = time.perf_counter()
 c0, pg, res = ctx.backprop(st, N, nseg, sd.desc())
 wall = time.perf_counter() - t0
-print(f"{cfg} backprop N={N} nseg={nseg}: {wall * 1e3:.1f} ms wall = {n * N / wall / 1e9:.3f} G particle-steps/s "
-      f"(fwd sweep + replay + VJP per step)")
+print(f"{cfg} backprop N={N} nseg={nseg}: device {res.device_ms:.2f} ms = {n * N / res.device_ms / 1e6:.3f} "
+      f"G particle-steps/s (fwd sweep + replay + VJP per step); wall incl. host transfers {wall * 1e3:.1f} ms")
 ctx.profile(True)
 ctx.profile_reset()
 ctx.backprop(st, N, nseg, sd.desc())
