@@ -1166,9 +1166,34 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
 }
 
 // ---- K6: per node: sum partials, correction-chain VJP, momentum-update transpose ------------
+// a node's friction-gradient terms: at most one segment per Coulomb wall it lies in the band of
+template <class T, int D> struct FricAcc {
+    int n = 0;
+    int k[2 * D];
+    T v[2 * D];
+    __device__ __forceinline__ void add(int slot, T x)
+    {
+        for (int i = 0; i < n; ++i)
+            if (k[i] == slot) {
+                v[i] += x;
+                return;
+            }
+        k[n] = slot;
+        v[n] = x;
+        ++n;
+    }
+    __device__ __forceinline__ T get(int slot) const
+    {
+        T r = T(0);
+        for (int i = 0; i < n; ++i)
+            if (k[i] == slot)
+                r = v[i];
+        return r;
+    }
+};
 template <class T, int D>
 __device__ __forceinline__ void corr_vjp_chain(const DevScene<T, D>& sc, const int* n, const T* vtilde, T* cot,
-                                               T* fr_acc)
+                                               FricAcc<T, D>& fr_acc)
 {
     // forward replay of the chain (contact.hpp:141-224): record inputs of each correction
     constexpr int MAXC = 2 * D + MAX_OBST + 2 * D;
@@ -1345,7 +1370,7 @@ __device__ __forceinline__ void corr_vjp_chain(const DevScene<T, D>& sc, const i
                 const T nb = b == r.axis ? r.nrm : T(0);
                 out[b] = s * (cot[b] - nb * ncd) + tc * (-(r.mu / tn) * nb + (r.mu * vn / (tn * tn)) * that[b]);
             }
-            fr_acc[r.fidx] += -vn * thc;
+            fr_acc.add(r.fidx, -vn * thc);
 #pragma unroll
             for (int b = 0; b < D; ++b)
                 cot[b] = out[b];
@@ -1367,7 +1392,9 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf
 {
     using C = Cfg<D>;
     constexpr int NF = 2 * D;
+    static_assert(MAX_FRIC <= 64, "segment slots are tracked in a 64-bit mask");
     __shared__ T red[C::NB];
+    __shared__ unsigned long long fr_mask;
     if (st->abort)
         return;
     const int nact = *n_act;
@@ -1456,9 +1483,7 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf
             continue;
         }
         const T m = G.m[gi];
-        T fr_acc[MAX_FRIC];
-        for (int k = 0; k < nfr; ++k)
-            fr_acc[k] = T(0);
+        FricAcc<T, D> fr_acc;
         T gm = T(0), gmom[D], gf[D];
 #pragma unroll
         for (int a = 0; a < D; ++a)
@@ -1500,17 +1525,32 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf
             }
         }
         if (!owned)
-            for (int k = 0; k < nfr; ++k)
-                fr_acc[k] = T(0);
-        // friction gradient partials per node block (fixed-order tree); the band pass adds to the
-        // interior pass's value of the same block
-        for (int k = 0; k < nfr; ++k) {
-            const T s = block_sum_fixed<T, C::NB>(fr_acc[k], red);
-            if (tid == 0) {
-                if constexpr (MODE == ADJ_BAND_LOAD)
-                    fr_block[(size_t)q * MAX_FRIC + k] += s;
-                else
-                    fr_block[(size_t)q * MAX_FRIC + k] = s;
+            fr_acc.n = 0;
+        // friction gradient partials per node block: a fixed-order tree per segment slot the block
+        // touched (a block meets at most a few of a wall's segments); untouched slots are zero.
+        // The band pass adds to the interior pass's value of the same block.
+        if (nfr > 0) {
+            __syncthreads(); // the previous block's readers of fr_mask are done
+            if (tid == 0)
+                fr_mask = 0ull;
+            __syncthreads();
+            for (int i = 0; i < fr_acc.n; ++i)
+                atomicOr(&fr_mask, 1ull << fr_acc.k[i]);
+            __syncthreads();
+            const unsigned long long mask = fr_mask;
+            if constexpr (MODE != ADJ_BAND_LOAD) {
+                if (tid < nfr && !((mask >> tid) & 1ull))
+                    fr_block[(size_t)q * MAX_FRIC + tid] = T(0);
+            }
+            for (unsigned long long rest = mask; rest; rest &= rest - 1) {
+                const int k = __ffsll((long long)rest) - 1;
+                const T s = block_sum_fixed<T, C::NB>(fr_acc.get(k), red);
+                if (tid == 0) {
+                    if constexpr (MODE == ADJ_BAND_LOAD)
+                        fr_block[(size_t)q * MAX_FRIC + k] += s;
+                    else
+                        fr_block[(size_t)q * MAX_FRIC + k] = s;
+                }
             }
         }
     }
