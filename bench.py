@@ -430,11 +430,15 @@ def bench_slab(a, rank, world, local):
     dist.barrier()
     ck = clocks.stop()
     launches = dom.ctx.launch_count() - l0
+    an1, _, _ = dom.ctx.grid_stats()
     t = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     mig = torch.tensor([stp.migrated], device="cuda", dtype=torch.int64)
     dist.all_reduce(mig)
+    # the slab path resets the device status every step: the counter holds the last step's nodes
+    act = torch.tensor([float(an1)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(act)
     # e2e: rank-local upload from pinned host + K decomposed steps + compact download, max over ranks
     e2e = bench_slab_e2e(dom, stp, a.steps)
     te = torch.tensor([e2e["seconds"], e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]], device="cuda",
@@ -446,6 +450,14 @@ def bench_slab(a, rank, world, local):
     dist.barrier()
     if rank != 0:
         return None
+    # step-level roofline per GPU: B_fwd over each GPU's share of the particles
+    B_fwd, _, _ = bytes_model(s, n_total, float(act.item()))
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    gbs = n_total / world * B_fwd / (ms / a.steps / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "step (per GPU)", "achieved": gbs, "peak": peak, "unit": "GB/s",
+            "frac": gbs / peak, "traffic": None, "bytes_per_particle_step": B_fwd,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s"}
     e2e_line = {"value": n_total * a.steps / float(te[0].item()), "unit": UNIT,
                 "h2d_bytes_per_step": float(tb[0].item()), "d2h_bytes_per_step": float(tb[1].item()),
                 "call": e2e["call"], "seconds": float(te[0].item())}
@@ -458,7 +470,7 @@ def bench_slab(a, rank, world, local):
                    "particles_total": n_total, "parallelism": f"slab x{world} (NCCL halo + migration)",
                    "slab_bounds": plan.bounds, "migrated_particles": int(mig.item()),
                    "l2_policy": "inputs larger than the 126 MB L2; no flush"},
-        "clocks": ck, "gpu_launches": launches, "e2e": e2e_line,
+        "roofline": roof, "clocks": ck, "gpu_launches": launches, "e2e": e2e_line,
     }
 
 
@@ -487,7 +499,13 @@ def bench_slab_e2e(dom, stp, steps):
     lib, h = dom.lib, dom.h
     out = SimState.zeros(k + dom.capacity // 4, sub.dim, sub.dtype)
     ov, okeep = out.output_view()
-    oids = np.empty(k + dom.capacity // 4, np.int64)
+    for name, arr in okeep.items():  # pinned download buffers, as the upload's
+        if arr is None or not arr.size:
+            continue
+        t = torch.empty(arr.shape, dtype=torch.from_numpy(arr[:0]).dtype, pin_memory=True).numpy()
+        okeep[name] = t
+        setattr(ov, name, t.ctypes.data)
+    oids = torch.empty(k + dom.capacity // 4, dtype=torch.int64, pin_memory=True).numpy()
     torch.cuda.synchronize()
     import torch.distributed as dist
     dist.barrier()
