@@ -264,7 +264,10 @@ def bench_fwd_adj(ctx, s, st, n, steps, nseg):
     return {"value": n * steps / (ms / 1e3), "unit": UNIT, "steps": steps, "n_segments": nseg,
             "device_ms": ms, "ms_per_step": ms / steps, "wall_s_incl_host_transfers": wall,
             "loss": res.loss, "kernels": kern,
-            "timing": "CUDA events on the library stream around forward sweep + replays + VJPs"}
+            "timing": "CUDA events on the library stream around forward sweep + replays + VJPs",
+            # the last segment runs in the replay slots during the forward sweep and is not
+            # replayed (bit-identical states): forward passes per step = 1 + (steps - L_last) / steps
+            "forward_passes_per_step": 1 + (steps - (steps // nseg)) / steps if nseg >= 2 else 2.0}
 
 
 # ---- GPU arm -----------------------------------------------------------------------------------

@@ -1652,13 +1652,54 @@ template <class T, int D> struct Ctx : CtxBase {
                 ~Ev() { cudaEventDestroy(e); }
             } ev0, ev1;
             CK(cudaEventRecord(ev0.e, stream));
-            // forward sweep
+            // replay tape, sized by the active node blocks of the latest forward step (+25 %)
+            bool use_tape = false;
+            auto reserve_tape = [&]() {
+                int n_act_now = 0;
+                d2h_raw(&n_act_now, counts + 1, sizeof(int));
+                const char* cap_env = std::getenv("MPM_TAPE_CAP"); // test hook: force slot overflows
+                const int64_t grid_cap =
+                    cap_env ? std::max<int64_t>(1, std::atoll(cap_env))
+                            : std::min<int64_t>(sc.nnb_total, (int64_t(n_act_now) * 5 / 4 + 255) / 256 * 256);
+                use_tape = tape_enabled && n > 0 && tape_reserve(Lmax, grid_cap);
+                if (use_tape)
+                    CK(cudaMemsetAsync(tape_over, 0, sizeof(int) * Lmax, stream));
+            };
+            // one step of a segment kept in the replay slots: S^j -> S^{j+1}, with its tape entry
+            auto slot_step = [&](int64_t j) {
+                buf[0] = replay[j];
+                buf[1] = replay[j + 1];
+                cur = 0;
+                keys_valid = false;
+                if (use_tape) {
+                    use_sort_set(tape[j].ss);
+                    step_once(false, true);
+                    tape_grid<true>(int(j));
+                    use_sort_set(own_ss);
+                } else {
+                    step_once(false);
+                }
+            };
+            // forward sweep. With 2+ segments the last one runs directly in the replay slots (and
+            // fills the tape): its states are the ones a replay would recompute bit for bit, so
+            // the reverse sweep starts without replaying it.
+            const bool last_kept = nseg >= 2 && tape_enabled && n > 0;
             reset_status();
             if (obs_index(0) >= 0)
                 seed(buf[cur], obs_index(0), 0, 0);
             for (int k = 0; k < nseg; ++k) {
                 pbuf_copy(ckpt[k], buf[cur]);
                 bhash[k] = digest_of(buf[cur]);
+                if (k == nseg - 1 && last_kept) {
+                    reserve_tape();
+                    pbuf_copy(replay[0], buf[cur]);
+                    for (int64_t t = bnd[k]; t < bnd[k + 1]; ++t) {
+                        slot_step(t - bnd[k]);
+                        if (obs_index(t + 1) >= 0)
+                            seed(buf[cur], obs_index(t + 1), 0, 0);
+                    }
+                    continue;
+                }
                 for (int64_t t = bnd[k]; t < bnd[k + 1]; ++t) {
                     step_once(false);
                     if (obs_index(t + 1) >= 0)
@@ -1669,15 +1710,8 @@ template <class T, int D> struct Ctx : CtxBase {
             check_status(step0);
             double loss = 0;
             d2h_raw(&loss, aw.loss_acc, sizeof(double));
-            // replay tape, sized by the last forward step's active node blocks (+25 %)
-            int n_act_last = 0;
-            d2h_raw(&n_act_last, counts + 1, sizeof(int));
-            const char* cap_env = std::getenv("MPM_TAPE_CAP"); // test hook: force slot overflows
-            const int64_t grid_cap = cap_env ? std::max<int64_t>(1, std::atoll(cap_env))
-                                             : std::min<int64_t>(sc.nnb_total, (int64_t(n_act_last) * 5 / 4 + 255) / 256 * 256);
-            const bool use_tape = tape_enabled && n > 0 && tape_reserve(Lmax, grid_cap);
-            if (use_tape)
-                CK(cudaMemsetAsync(tape_over, 0, sizeof(int) * Lmax, stream));
+            if (!last_kept)
+                reserve_tape();
             std::vector<int> over(Lmax, 1);
             // backward sweep
             aw.cot_zero(*this, 0);
@@ -1686,22 +1720,14 @@ template <class T, int D> struct Ctx : CtxBase {
             int64_t peak = 0;
             for (int k = nseg - 1; k >= 0; --k) {
                 const int64_t b0 = bnd[k], b1 = bnd[k + 1], len = b1 - b0;
-                pbuf_copy(replay[0], ckpt[k]);
-                for (int64_t j = 0; j < len; ++j) {
-                    buf[0] = replay[j];
-                    buf[1] = replay[j + 1];
-                    cur = 0;
-                    keys_valid = false;
-                    if (use_tape) {
-                        use_sort_set(tape[j].ss);
-                        step_once(false, true);
-                        tape_grid<true>(int(j));
-                    } else {
-                        step_once(false);
-                    }
+                const bool kept = k == nseg - 1 && last_kept;
+                if (!kept) {
+                    pbuf_copy(replay[0], ckpt[k]);
+                    for (int64_t j = 0; j < len; ++j)
+                        slot_step(j);
                 }
                 peak = std::max(peak, len + 1);
-                if (digest_of(replay[len]) != bhash[k + 1])
+                if (!kept && digest_of(replay[len]) != bhash[k + 1])
                     throw ApiError(MPM_ERR_CHECKPOINT,
                                    "checkpoint mismatch: recomputed segment end differs from the recorded state at step "
                                        + std::to_string(step0 + b1));
