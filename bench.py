@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--adj-steps", type=int, default=20, help="fwd+adjoint sample: backprop steps (0: skip)")
-    ap.add_argument("--adj-segments", type=int, default=2)
+    ap.add_argument("--adj-segments", type=int, default=0,
+                    help="checkpoint segments of the fwd+adjoint sample (0: fewest that fit in HBM)")
     ap.add_argument("--mode", default="auto", choices=["auto", "plain", "slab"],
                     help="auto: one context at N=1, slab decomposition for N>1")
     return ap.parse_args()
@@ -267,7 +268,27 @@ def bench_fwd_adj(ctx, s, st, n, steps, nseg):
             "timing": "CUDA events on the library stream around forward sweep + replays + VJPs",
             # the last segment runs in the replay slots during the forward sweep and is not
             # replayed (bit-identical states): forward passes per step = 1 + (steps - L_last) / steps
-            "forward_passes_per_step": 1 + (steps - (steps // nseg)) / steps if nseg >= 2 else 2.0}
+            "forward_passes_per_step": 1 + (steps - (steps // nseg)) / steps}
+
+
+def hbm_plan(s, n, steps, active_nodes):
+    """Fewest checkpoint segments whose HBM footprint fits: n_seg checkpoints + L_max + 1 replay
+    slots (checkpoint.hpp:50's planned_peak_states) + L_max replay-tape entries, within 70 % of
+    the free device memory. B200-first: 180 GB holds a C4 20-step trajectory whole (one segment,
+    nothing replayed), where a CPU-sized plan would recompute half of it."""
+    import torch
+    d = s.dim
+    sz = 8 if s.dtype == "f64" else 4
+    fields = (2 * d + 4 + (1 if d == 2 else 0) + (3 if d == 2 else 6) + d * d)
+    state = n * (fields * sz + 4)
+    tape = n * 8 + 1.25 * active_nodes * (1 + 4 * d) * sz
+    free = torch.cuda.mem_get_info()[0]
+    for nseg in range(1, steps + 1):
+        L = -(-steps // nseg)
+        if (nseg + L + 1) * state + L * tape <= 0.7 * free:
+            return nseg, {"n_segments": nseg, "rule": "fewest segments whose checkpoints + replay slots + tape "
+                          "fit in 70% of free HBM", "state_bytes": state, "free_hbm_bytes": free}
+    return steps, {"n_segments": steps, "rule": "HBM-bound: one step per segment"}
 
 
 # ---- GPU arm -----------------------------------------------------------------------------------
@@ -345,7 +366,13 @@ def bench_b200(a, rank, world, local):
     # ---- fwd+adjoint (checkpointed backprop_trajectory), device-timed
     fwd_adj = None
     if a.adj_steps > 0:
-        fwd_adj = bench_fwd_adj(ctx, s, st, n, a.adj_steps, a.adj_segments)
+        nseg, plan = (a.adj_segments, {"n_segments": a.adj_segments, "rule": "--adj-segments"}) \
+            if a.adj_segments > 0 else hbm_plan(s, n, a.adj_steps, active_nodes_step)
+        fwd_adj = bench_fwd_adj(ctx, s, st, n, a.adj_steps, nseg)
+        fwd_adj["plan"] = plan
+        if nseg != 2 and a.adj_steps >= 2:  # the two-segment plan beside it (same loss, more replay)
+            alt = bench_fwd_adj(ctx, s, st, n, a.adj_steps, 2)
+            fwd_adj["two_segments"] = {k: alt[k] for k in ("value", "ms_per_step", "forward_passes_per_step", "loss")}
         d = s.dim
         sz = 8 if s.dtype == "f64" else 4
         ns = 3 if d == 2 else 6

@@ -28,6 +28,17 @@
 
 using namespace mpmgpu;
 
+#ifndef P2G_ABL
+#define P2G_ABL 0 // timing-ablation builds only (tools/p2g_ablate.py)
+#endif
+#if P2G_ABL == 16
+__global__ void k_spin_abl(long long cycles) // idle the SMs (no memory traffic) in front of P2G
+{
+    const long long t0 = clock64();
+    while (clock64() - t0 < cycles)
+        __nanosleep(1000);
+}
+#endif
 #ifndef P2G_WIDE
 #define P2G_WIDE false
 #endif
@@ -463,6 +474,10 @@ template <class T, int D> struct Ctx : CtxBase {
         if constexpr (D == 3) {
             CK(cudaFuncSetAttribute(k_p2g_pipe3<T, P2G_WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(Pipe3Cfg<T, P2G_WIDE>::SMEM)));
+#if P2G_ABL
+            CK(cudaFuncSetAttribute(k_p2g_pipe3<T, P2G_WIDE, P2G_ABL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(Pipe3Cfg<T, P2G_WIDE>::SMEM)));
+#endif
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2g_ctas_per_sm, k_p2g_pipe3<T, P2G_WIDE>,
                                                              Pipe3Cfg<T, P2G_WIDE>::THREADS, Pipe3Cfg<T, P2G_WIDE>::SMEM));
             CK(cudaFuncSetAttribute(k_p2g_lanes3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -542,6 +557,14 @@ template <class T, int D> struct Ctx : CtxBase {
             if constexpr (D == 3) {
                 if (p2g_impl == 1) {
                     using S = Pipe3Cfg<T, P2G_WIDE>;
+#if P2G_ABL == 16
+                    launch("k_p2g_abl", [&] { k_spin_abl<<<nsm, 32, 0, stream>>>(600000); });
+#elif P2G_ABL
+                    launch("k_p2g_abl", [&] {
+                        k_p2g_pipe3<T, P2G_WIDE, P2G_ABL><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
+                            sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st);
+                    });
+#endif
                     launch("k_p2g", [&] {
                         k_p2g_pipe3<T, P2G_WIDE><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
                             sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st);
@@ -1689,10 +1712,11 @@ template <class T, int D> struct Ctx : CtxBase {
                     step_once(false);
                 }
             };
-            // forward sweep. With 2+ segments the last one runs directly in the replay slots (and
-            // fills the tape): its states are the ones a replay would recompute bit for bit, so
-            // the reverse sweep starts without replaying it.
-            const bool last_kept = nseg >= 2 && tape_enabled && n > 0;
+            // forward sweep. The last segment runs directly in the replay slots (and fills the
+            // tape): its states are the ones a replay would recompute bit for bit, so the reverse
+            // sweep starts without replaying it. With one segment (a plan whose L_max + 1 replay
+            // slots fit in HBM) nothing is replayed at all.
+            const bool last_kept = tape_enabled && n > 0;
             reset_status();
             if (obs_index(0) >= 0)
                 seed(buf[cur], obs_index(0), 0, 0);

@@ -694,7 +694,9 @@ template <class T> __device__ __forceinline__ void cp_async_t(T* smem, const T* 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-template <class T, bool WIDE>
+// ABL != 0: timing ablation only (1 skip reduce, 2 skip convert, 4 skip march), launched in
+// front of the real kernel by ablation builds (-DP2G_ABL=...), never on its own
+template <class T, bool WIDE, int ABL = 0>
 __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     k_p2g_pipe3(DevScene<T, 3> sc, PBuf<T, 3> P, const int* __restrict__ perm, const int* __restrict__ keys,
                 const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ lstart,
@@ -827,7 +829,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
             }
             __syncthreads(); // slots complete
             // one (node column, field) per task: 700 short fixed-order sums over all threads
-            for (int t = tid; t < C::NCOL * NF; t += blockDim.x) {
+            for (int t = tid; t < ((ABL & 1) ? 0 : C::NCOL * NF); t += blockDim.x) {
                 const int c = t / NF, f = t - c * NF;
                 const int n0 = c / TE, n1 = c - n0 * TE;
                 T sum = T(0);
@@ -862,6 +864,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                 T* Rw = raw + (j & 1) * NRAW * CAP;
                 for (int r = tid; r < len; r += blockDim.x) {
                     atomicAdd(&cnt[col[r] & (NBC - 1)], 1);
+                    if (ABL & 2)
+                        continue;
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         const T u = (Rw[(RX + a) * CAP + r] - sc.origin[a]) * sc.inv_dh;
@@ -899,7 +903,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                 ke = kb + ((bc & 1) ? a1 : a0);
             }
             const T* R = raw + (j & 1) * NRAW * CAP;
-            for (int k = kb; k < ke; ++k) {
+            for (int k = kb; k < ((ABL & 4) ? kb : ke); ++k) {
                 T f[3];
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
