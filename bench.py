@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-workloads", action="store_true", help="skip the C2/C3/C5 sub-lines")
     ap.add_argument("--adj-steps", type=int, default=20, help="fwd+adjoint sample: backprop steps (0: skip)")
     ap.add_argument("--adj-segments", type=int, default=0,
                     help="checkpoint segments of the fwd+adjoint sample (0: fewest that fit in HBM)")
@@ -271,6 +272,98 @@ def bench_fwd_adj(ctx, s, st, n, steps, nseg):
             "forward_passes_per_step": 1 + (steps - (steps // nseg)) / steps}
 
 
+def vjp_bytes(s, n, active_nodes_step, B_fwd, IN):
+    """B_fwd+adj = 2 B_fwd + B_vjp per particle-step."""
+    d = s.dim
+    sz = 8 if s.dtype == "f64" else 4
+    ns = 3 if d == 2 else 6
+    dp = s.material.__class__.__name__ == "DruckerPragerParams"
+    COT = 2 * d + 2 + ns + (1 if (dp and d == 2) else 0)
+    A_np = active_nodes_step / n
+    B_vjp = (IN + 2 * COT) * sz + A_np * (2 * (1 + 2 * d) + 8 * d) * sz
+    return 2 * B_fwd + B_vjp
+
+
+def bench_workloads(peak, names):
+    """The other BASELINE.json configs on this GPU (N = 1), device-timed through the same context
+    API: C2 forward; C3 the paper's inverse problem (loss on the final deposit of a twin run with
+    alpha* = 2, reverse-mode gradient through all 1000 steps, HBM-sized checkpoint plan, dL/dalpha
+    chained on the host as in SURVEY §8d); C5 forward + a 20-step fwd+adjoint with the 32 Coulomb
+    friction segments' gradients. No CPU sample here (the reference would take hours)."""
+    import numpy as np
+    import torch
+    from paper_2507_04192_b200 import init_scene
+    from paper_2507_04192_b200.presets import CONFIGS, c3_inverse
+    from paper_2507_04192_b200.seeders import LagrangianLeastSquares
+    from paper_2507_04192_b200.solver import Context
+
+    out = {}
+    for name in names:
+        try:
+            if name == "C5" and _mem_available_gb() < 48:
+                out[name] = {"skipped": "host memory below 48 GB for the 7.3 GB host copies"}
+                continue
+            s = CONFIGS[name](dtype="f64")
+            st = init_scene(s)
+            n = st.particles.size()
+            ctx = Context(s, n)
+            ctx.upload(st)
+            ctx.advance(3)
+            k_fwd = {"C2": 200, "C3": 200, "C5": 20}[name]
+            ms = ctx.advance_timed(k_fwd)
+            act, _, _ = ctx.grid_stats()
+            B_fwd, IN, _ = bytes_model(s, n, act / k_fwd)
+            w = {"particles": n, "grid_cells": s.config.cells, "dtype": "f64",
+                 "fwd": {"value": n * k_fwd / (ms / 1e3), "unit": UNIT, "steps": k_fwd, "ms_per_step": ms / k_fwd,
+                         "roofline_frac": n * B_fwd / (ms / k_fwd / 1e3) / 1e9 / peak,
+                         "bytes_per_particle_step": B_fwd}}
+            adj = {"C3": 1000, "C5": 20}.get(name, 0)
+            if adj:
+                st0 = ctx.download(st)
+                ctx.upload(st0)
+                if name == "C3":  # twin run at the true alpha* = 2.0 gives the observed deposit
+                    tw = c3_inverse(alpha=2.0, dtype="f64")
+                    stt = init_scene(tw)
+                    ctt = Context(tw, stt.particles.size())
+                    ctt.upload(stt)
+                    ctt.advance(adj)
+                    target = ctt.download(stt).particles.x[None].copy()
+                    ctt.close()
+                else:  # positions of a 1 % subset (seeded) against a perturbed twin
+                    rng = np.random.default_rng(0)
+                    sel = np.sort(rng.choice(n, n // 100, replace=False))
+                    target = None
+                act0 = act / k_fwd
+                nseg, plan = hbm_plan(s, n, adj, act0)
+                if name == "C3":
+                    sd = LagrangianLeastSquares([adj], target, "x")
+                else:
+                    ctx.upload(st0)
+                    ctx.advance(adj)
+                    xf = ctx.download(st0.copy()).particles.x
+                    sd = LagrangianLeastSquares([adj], xf[sel][None] + 1e-3, "x", sel=sel)
+                ctx.backprop(st0, adj, nseg, sd.desc())  # allocates the checkpoint / replay pool
+                c0, pg, res = ctx.backprop(st0, adj, nseg, sd.desc())
+                B_fa = vjp_bytes(s, n, act0, B_fwd, IN)
+                mps = res.device_ms / adj
+                w["fwd_adj"] = {"value": n * adj / (res.device_ms / 1e3), "unit": UNIT, "steps": adj,
+                                "ms_per_step": mps, "plan": plan, "loss": res.loss,
+                                "roofline_frac": n * B_fa / (mps / 1e3) / 1e9 / peak, "bytes_per_particle_step": B_fa,
+                                "timing": "mpm_backprop_result.device_ms (forward sweep + replays + VJPs)"}
+                if name == "C3":  # v_x(0) = alpha (H0 - y): dL/dalpha = sum_p vbar_x(0) v_x(0) / alpha
+                    alpha = s.geometry[0].velocity.alpha
+                    w["fwd_adj"]["dL_dalpha"] = float(np.sum(c0.v[:, 0] * st0.particles.v[:, 0]) / alpha)
+                else:
+                    fr = np.asarray(pg.flat())
+                    w["fwd_adj"]["param_grads_norm"] = float(np.linalg.norm(fr))
+            ctx.close()
+            torch.cuda.empty_cache()
+            out[name] = w
+        except Exception as e:  # a workload that fails is reported, the headline line still prints
+            out[name] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+    return out
+
+
 def hbm_plan(s, n, steps, active_nodes):
     """Fewest checkpoint segments whose HBM footprint fits: n_seg checkpoints + L_max + 1 replay
     slots (checkpoint.hpp:50's planned_peak_states) + L_max replay-tape entries, within 70 % of
@@ -373,19 +466,15 @@ def bench_b200(a, rank, world, local):
         if nseg != 2 and a.adj_steps >= 2:  # the two-segment plan beside it (same loss, more replay)
             alt = bench_fwd_adj(ctx, s, st, n, a.adj_steps, 2)
             fwd_adj["two_segments"] = {k: alt[k] for k in ("value", "ms_per_step", "forward_passes_per_step", "loss")}
-        d = s.dim
-        sz = 8 if s.dtype == "f64" else 4
-        ns = 3 if d == 2 else 6
-        dp = s.material.__class__.__name__ == "DruckerPragerParams"
-        COT = 2 * d + 2 + ns + (1 if (dp and d == 2) else 0)
-        A_np = active_nodes_step / n
-        B_vjp = (IN + 2 * COT) * sz + A_np * (2 * (1 + 2 * d) + 8 * d) * sz
-        B_fa = 2 * B_fwd + B_vjp
+        B_fa = vjp_bytes(s, n, active_nodes_step, B_fwd, IN)
         gbs = n * B_fa / (fwd_adj["ms_per_step"] / 1e3) / 1e9
         fwd_adj["roofline"] = {"bound": "hbm", "bytes_per_particle_step": B_fa, "achieved": gbs, "peak": peak,
                                "unit": "GB/s", "frac": gbs / peak}
 
     ctx.close()
+    workloads = None
+    if world == 1 and a.config == "C4" and not a.no_workloads:
+        workloads = bench_workloads(peak, ["C2", "C3", "C5"])
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -409,6 +498,7 @@ def bench_b200(a, rank, world, local):
         "fp64": fp64_for(prof, a),
         "kernels": prof, "profiled_step_ms": total_ms / 3,
         "clocks": ck, "gpu_launches": launches, "e2e": e2e, "fwd_adj": fwd_adj,
+        "workloads": workloads,
     }
     return line
 

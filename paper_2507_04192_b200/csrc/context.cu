@@ -1722,7 +1722,8 @@ template <class T, int D> struct Ctx : CtxBase {
                 seed(buf[cur], obs_index(0), 0, 0);
             for (int k = 0; k < nseg; ++k) {
                 pbuf_copy(ckpt[k], buf[cur]);
-                bhash[k] = digest_of(buf[cur]);
+                if (k >= 1) // digests only where a replayed segment ends (S^0 is never checked)
+                    bhash[k] = digest_of(buf[cur]);
                 if (k == nseg - 1 && last_kept) {
                     reserve_tape();
                     pbuf_copy(replay[0], buf[cur]);
@@ -1739,7 +1740,8 @@ template <class T, int D> struct Ctx : CtxBase {
                         seed(buf[cur], obs_index(t + 1), 0, 0);
                 }
             }
-            bhash[nseg] = digest_of(buf[cur]);
+            if (!last_kept)
+                bhash[nseg] = digest_of(buf[cur]);
             check_status(step0);
             double loss = 0;
             d2h_raw(&loss, aw.loss_acc, sizeof(double));
