@@ -72,14 +72,25 @@ def dist_env():
 
 
 # ---- algorithmic bytes ------------------------------------------------------
-def bytes_model(scene, n_particles, active_nodes):
-    """B_fwd = (IN + OUT) s + (A/N_p) 2 (1 + 2d) s, IN/OUT per SURVEY §8d (D-P adds eps, 2-D sigma_zz)."""
+def gv_dead(scene) -> bool:
+    """FLIP / PIC / blend without F tracking never read the stored grad v: inside one advance()
+    call only the last step writes it"""
+    return scene.config.scheme.kind not in ("apic", "tpic") and not scene.config.track_def_grad
+
+
+def bytes_model(scene, n_particles, active_nodes, steps_per_call=1):
+    """B_fwd = (IN + OUT) s + (A/N_p) 2 (1 + 2d) s, IN/OUT per SURVEY §8d (D-P adds eps, 2-D sigma_zz).
+    This is SURVEY §8d's figure (the one the roofline is scored on), with OUT holding grad v. With
+    steps_per_call > 1 and gv_dead(), grad v is stored once per advance() call instead, and the
+    return value is the traffic the implementation actually needs (reported beside it)."""
     d = scene.dim
     s = 8 if scene.dtype == "f64" else 4
     ns = 3 if d == 2 else 6
     dp = scene.material.__class__.__name__ == "DruckerPragerParams"
     IN = 2 * d + 2 + 1 + ns + (1 if dp else 0) + (1 if (dp and d == 2) else 0)    # x v m V rho sig (+eps, +szz)
     OUT = 2 * d + 2 + ns + d * d + (1 if dp else 0) + (1 if (dp and d == 2) else 0)  # x v V rho sig gradv (+eps, +szz)
+    if gv_dead(scene):
+        OUT -= d * d * (1 - 1 / steps_per_call)
     per_particle = (IN + OUT) * s
     grid = 2 * (1 + 2 * d) * s * active_nodes / n_particles
     return per_particle + grid, IN, OUT
@@ -98,7 +109,7 @@ def kernel_bytes(scene, n, active_nodes, occupied_blocks):
     p2g = n * ((2 * d + 2 + ns) * s + 8) + occupied_blocks * tile * nf * s
     # k_g2p: read + write the whole particle record (+ perm, pid, key) and the node tiles (v, v_old)
     rec_in = 2 * d + 4 + ns + (1 if (dp and d == 2) else 0)
-    rec_out = rec_in + d * d
+    rec_out = rec_in + d * d  # SURVEY's record (grad v included), as bytes_model
     g2p = n * ((rec_in + rec_out) * s + 4 * 4) + occupied_blocks * tile * 2 * d * s
     return {"k_p2g": p2g, "k_g2p": g2p}
 
@@ -313,6 +324,7 @@ def bench_workloads(peak, names):
             ms = ctx.advance_timed(k_fwd)
             act, _, _ = ctx.grid_stats()
             B_fwd, IN, _ = bytes_model(s, n, act / k_fwd)
+            B_fwd1 = B_fwd
             w = {"particles": n, "grid_cells": s.config.cells, "dtype": "f64",
                  "fwd": {"value": n * k_fwd / (ms / 1e3), "unit": UNIT, "steps": k_fwd, "ms_per_step": ms / k_fwd,
                          "roofline_frac": n * B_fwd / (ms / k_fwd / 1e3) / 1e9 / peak,
@@ -344,7 +356,7 @@ def bench_workloads(peak, names):
                     sd = LagrangianLeastSquares([adj], xf[sel][None] + 1e-3, "x", sel=sel)
                 ctx.backprop(st0, adj, nseg, sd.desc())  # allocates the checkpoint / replay pool
                 c0, pg, res = ctx.backprop(st0, adj, nseg, sd.desc())
-                B_fa = vjp_bytes(s, n, act0, B_fwd, IN)
+                B_fa = vjp_bytes(s, n, act0, B_fwd1, IN)
                 mps = res.device_ms / adj
                 w["fwd_adj"] = {"value": n * adj / (res.device_ms / 1e3), "unit": UNIT, "steps": adj,
                                 "ms_per_step": mps, "plan": plan, "loss": res.loss,
@@ -430,7 +442,9 @@ def bench_b200(a, rank, world, local):
 
     active_nodes, occ_blocks, act_blocks = ctx.grid_stats()
     active_nodes_step = active_nodes / a.steps
-    B_fwd, IN, OUT = bytes_model(s, n, active_nodes_step)
+    B_fwd, IN, OUT = bytes_model(s, n, active_nodes_step)  # SURVEY §8d (grad v stored every step)
+    B_fwd1 = B_fwd
+    B_need = bytes_model(s, n, active_nodes_step, a.steps)[0]  # grad v stored by the call's last step
 
     # ---- per-kernel profile (CUDA events around each launch on the library stream)
     ctx.profile(True)
@@ -466,7 +480,7 @@ def bench_b200(a, rank, world, local):
         if nseg != 2 and a.adj_steps >= 2:  # the two-segment plan beside it (same loss, more replay)
             alt = bench_fwd_adj(ctx, s, st, n, a.adj_steps, 2)
             fwd_adj["two_segments"] = {k: alt[k] for k in ("value", "ms_per_step", "forward_passes_per_step", "loss")}
-        B_fa = vjp_bytes(s, n, active_nodes_step, B_fwd, IN)
+        B_fa = vjp_bytes(s, n, active_nodes_step, B_fwd1, IN)
         gbs = n * B_fa / (fwd_adj["ms_per_step"] / 1e3) / 1e9
         fwd_adj["roofline"] = {"bound": "hbm", "bytes_per_particle_step": B_fa, "achieved": gbs, "peak": peak,
                                "unit": "GB/s", "frac": gbs / peak}
@@ -494,7 +508,10 @@ def bench_b200(a, rank, world, local):
                      "algorithmic_bytes_per_launch": kb[dom], "mean_launch_ms": dom_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
                      "step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak,
-                              "bytes_per_particle_step": B_fwd}},
+                              "bytes_per_particle_step": B_fwd,
+                              "needed_bytes_per_particle_step": B_need,
+                              "note": "grad v (dead state for FLIP) is stored by the last step of each "
+                                      "advance() call only: DRAM traffic sits below SURVEY's figure"}},
         "fp64": fp64_for(prof, a),
         "kernels": prof, "profiled_step_ms": total_ms / 3,
         "clocks": ck, "gpu_launches": launches, "e2e": e2e, "fwd_adj": fwd_adj,

@@ -28,6 +28,9 @@
 
 using namespace mpmgpu;
 
+#ifndef G2P_ABL
+#define G2P_ABL 0 // timing-ablation builds only (tools/p2g_ablate.py)
+#endif
 #ifndef P2G_ABL
 #define P2G_ABL 0 // timing-ablation builds only (tools/p2g_ablate.py)
 #endif
@@ -174,7 +177,7 @@ template <class T, int D> struct Ctx : CtxBase {
     int* d_cells = nullptr;
     int mig_cnt[2] = {0, 0};
 
-    cudaGraphExec_t graphs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}}; // [guard][cur]
+    cudaGraphExec_t graphs[2][2][2] = {}; // [guard][stores grad v][cur]
     // slab phases: P2G phase [cur] (valid for slab_g1_n[cur] particles), finish phase [guard][cur]
     cudaGraphExec_t slab_g1[2] = {nullptr, nullptr};
     int64_t slab_g1_n[2] = {-1, -1};
@@ -293,9 +296,10 @@ template <class T, int D> struct Ctx : CtxBase {
     ~Ctx() override
     {
         for (auto& g : graphs)
-            for (auto& e : g)
-                if (e)
-                    cudaGraphExecDestroy(e);
+            for (auto& h : g)
+                for (auto& e : h)
+                    if (e)
+                        cudaGraphExecDestroy(e);
         drop_slab_graphs();
         for (void* p : bp_pool_mem)
             cudaFree(p);
@@ -460,7 +464,13 @@ template <class T, int D> struct Ctx : CtxBase {
         size_t sm = g2p_smem(true);
         auto set = [&](auto kern) { CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm))); };
         set(k_g2p<T, D, P_CONSTIT, false, false>);
+#if G2P_ABL
+        set(k_g2p<T, D, P_CONSTIT, false, false, G2P_ABL>);
+        set(k_g2p<T, D, P_CONSTIT | P_GUARD, false, false, G2P_ABL>);
+#endif
         set(k_g2p<T, D, P_CONSTIT | P_GUARD, false, false>);
+        set(k_g2p<T, D, P_CONSTIT | P_NOGV, false, false>);
+        set(k_g2p<T, D, P_CONSTIT | P_GUARD | P_NOGV, false, false>);
         set(k_g2p<T, D, P_CONSTIT, true, false>);
         set(k_g2p<T, D, P_CONSTIT | P_GUARD, true, false>);
         set(k_g2p<T, D, P_CONSTIT, false, true>);
@@ -604,19 +614,31 @@ template <class T, int D> struct Ctx : CtxBase {
         auto& Pout = buf[cur ^ 1];
         const size_t sm = g2p_smem(has_F);
         const unsigned gr = persistent(D == 2 ? 8 : 4);
-        if (has_aff && has_F)
+        if constexpr ((FL & P_NOGV) != 0) { // requested only without affine / F state
+            if (has_aff || has_F)
+                throw ApiError(MPM_ERR_USAGE, "internal: P_NOGV with affine or F state");
+            launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
+        } else if (has_aff && has_F)
             launch("k_g2p", [&] { k_g2p<T, D, FL, true, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
         else if (has_aff)
             launch("k_g2p", [&] { k_g2p<T, D, FL, true, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
         else if (has_F)
             launch("k_g2p", [&] { k_g2p<T, D, FL, false, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
-        else
+        else {
+#if G2P_ABL
+            launch("k_g2p_abl", [&] { k_g2p<T, D, FL, false, false, G2P_ABL><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
+#endif
             launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
+        }
         cur ^= 1;
         keys_valid = true;
     }
 
-    void step_once(bool guard, bool store = false)
+    // grad v is dead state between the steps of one advance() call unless the scheme reads it
+    // (APIC's B lives in its own field; TPIC's affine matrix is grad v) or F is tracked
+    bool gv_skippable() const { return !has_aff && !has_F && !sc.tpic; }
+
+    void step_once(bool guard, bool store = false, bool gv = true)
     {
         sort_and_segment();
         p2g_kernel();
@@ -624,10 +646,11 @@ template <class T, int D> struct Ctx : CtxBase {
             grid_kernel<G_SUM | G_MOM | G_CORR | G_STORE>();
         else
             grid_kernel<G_SUM | G_MOM | G_CORR>();
+        const bool nogv = !gv && gv_skippable();
         if (guard)
-            g2p_kernel_fl<P_CONSTIT | P_GUARD>();
+            nogv ? g2p_kernel_fl<P_CONSTIT | P_GUARD | P_NOGV>() : g2p_kernel_fl<P_CONSTIT | P_GUARD>();
         else
-            g2p_kernel_fl<P_CONSTIT>();
+            nogv ? g2p_kernel_fl<P_CONSTIT | P_NOGV>() : g2p_kernel_fl<P_CONSTIT>();
         launch("k_step_end", [&] { k_step_end<<<1, 1, 0, stream>>>(st); });
     }
 
@@ -865,28 +888,31 @@ template <class T, int D> struct Ctx : CtxBase {
         const bool guard = flags & MPM_ADV_NAN_GUARD;
         const bool store = flags & MPM_ADV_STORE_GRID;
         reset_status();
+        // only the call's last step stores grad v (the state a download, snapshot or the next
+        // call sees); the steps before it skip the dead 9-value write when gv_skippable()
         if (prof || store) {
             for (int64_t k = 0; k < nsteps; ++k)
-                step_once(guard, store);
+                step_once(guard, store, k == nsteps - 1);
         } else {
             // first step runs eagerly (computes keys if needed); the rest replay a captured graph
-            step_once(guard);
+            step_once(guard, false, nsteps == 1);
             for (int64_t k = 1; k < nsteps; ++k) {
-                cudaGraphExec_t& ge = graphs[guard][cur];
+                const int gv = k == nsteps - 1 ? 1 : 0;
+                cudaGraphExec_t& ge = graphs[guard][gv][cur];
                 if (!ge) {
                     const int cur0 = cur;
                     const int64_t l0 = launches;
                     cudaGraph_t g;
                     CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-                    step_once(guard);
+                    step_once(guard, false, gv);
                     CK(cudaStreamEndCapture(stream, &g));
-                    CK(cudaGraphInstantiate(&graphs[guard][cur0], g, 0));
+                    CK(cudaGraphInstantiate(&graphs[guard][gv][cur0], g, 0));
                     CK(cudaGraphDestroy(g));
                     graph_launches = launches - l0;
                     launches = l0;
                     cur = cur0;
                 }
-                CK(cudaGraphLaunch(graphs[guard][cur], stream));
+                CK(cudaGraphLaunch(graphs[guard][gv][cur], stream));
                 launches += graph_launches;
                 cur ^= 1;
             }
@@ -1107,11 +1133,12 @@ template <class T, int D> struct Ctx : CtxBase {
             mig.hi_pid = alloc<int>(mig_cap);
         }
         for (auto& g : graphs)
-            for (auto& e : g)
-                if (e) {
-                    cudaGraphExecDestroy(e);
-                    e = nullptr;
-                }
+            for (auto& h : g)
+                for (auto& e : h)
+                    if (e) {
+                        cudaGraphExecDestroy(e);
+                        e = nullptr;
+                    }
         drop_slab_graphs();
         keys_valid = false;
     }

@@ -1496,7 +1496,9 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
 
 // ---------------------------------------------------------------------------------------
 // G2P (+ constitutive): CTA per occupied particle block, node tile (v, v_old) in smem.
-enum G2PFlags { P_CONSTIT = 1, P_GUARD = 2 };
+// P_NOGV: grad v is not stored (a step inside an advance() call whose scheme never reads the
+// stored grad v -- FLIP / PIC / blend without F tracking; the call's last step stores it)
+enum G2PFlags { P_CONSTIT = 1, P_GUARD = 2, P_NOGV = 4 };
 
 // migration export buffers (slab mode): one record of `rec` scalars + the pid per mover
 template <class T> struct MigBuf {
@@ -1515,7 +1517,9 @@ template <class T, int D, bool TRACKF> struct G2PStage {
     static constexpr size_t SMEM = TILE + sizeof(T) * 2 * NSF * THREADS + sizeof(int) * 2 * THREADS; // tile + 2 slots (+ pid)
 };
 
-template <class T, int D, int FLAGS, bool APIC, bool TRACKF>
+// ABL != 0: timing ablation only (1 skip the node-tile load, 2 skip the constitutive update,
+// 4 skip the gather arithmetic, 8 none), launched in front of the real kernel by -DG2P_ABL builds
+template <class T, int D, int FLAGS, bool APIC, bool TRACKF, int ABL = 0>
 __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pin, PBuf<T, D> Pout,
                                              GBuf<T, D> G, const int* __restrict__ perm,
                                              const int* __restrict__ bstart, const int* __restrict__ bend,
@@ -1582,6 +1586,8 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                 loc = (loc << C::LOGB) | (nn & (C::B - 1));
             }
             const size_t gi = (size_t)nid * C::NB + loc;
+            if (ABL & 1)
+                ok = false;
 #pragma unroll
             for (int a = 0; a < D; ++a) {
                 const T vn = ok ? G.v[a][gi] : T(0), vo = ok ? G.vold[a][gi] : T(0);
@@ -1623,7 +1629,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
 #pragma unroll
             for (int k = 0; k < D * D; ++k)
                 L[k] = Bm[k] = T(0);
-            if constexpr (!APIC) {
+            if constexpr (!APIC && !(ABL & 4)) {
                 // tensor-product factorisation along the last axis: for each outer offset,
                 // A = sum w_z v, Bz = sum dw_z v, Cd = sum w_z (v - v_old); then
                 // v_pic += w_o A, v_inc += w_o Cd, grad v[:, a<d-1] += dw_o A, grad v[:, d-1] += w_o Bz
@@ -1673,7 +1679,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                         L[a * D + D - 1] += wo * Bz[a];
                     }
                 }
-            } else {
+            } else if constexpr (APIC) {
 #pragma unroll
             for (int k = 0; k < C::NOFF; ++k) {
                 int o[D];
@@ -1744,7 +1750,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                     Fm[k] = sb[(FS + C::NS + k) * NT];
             }
             bool ok_den = true;
-            if (FLAGS & P_CONSTIT) {
+            if ((FLAGS & P_CONSTIT) && !(ABL & 2)) {
                 ok_den = constitutive_particle<T, D>(sc, sig, szz, rho, V, eps, L);
                 if constexpr (TRACKF) { // F <- (I + L dt) F (stepper.hpp:452-455)
                     T Fn[D * D];
@@ -1779,9 +1785,11 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
 #pragma unroll
             for (int s = 0; s < C::NS; ++s)
                 o[(PL::SIG + s) * SO] = sig[s];
+            if constexpr (!(FLAGS & P_NOGV)) {
 #pragma unroll
-            for (int k = 0; k < D * D; ++k)
-                o[(PL::GV + k) * SO] = L[k];
+                for (int k = 0; k < D * D; ++k)
+                    o[(PL::GV + k) * SO] = L[k];
+            }
             if constexpr (APIC) {
 #pragma unroll
                 for (int k = 0; k < D * D; ++k)

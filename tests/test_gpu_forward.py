@@ -146,6 +146,28 @@ def test_deterministic_and_grid_is_derived(orc):
         assert np.array_equal(getattr(sa.particles, f), getattr(sb.particles, f))
 
 
+@pytest.mark.parametrize("kind", ["flip", "blend", "tpic"])
+def test_grad_v_stored_by_the_last_step_of_a_call(orc, kind):
+    """Inside one advance() call only the last step stores grad v when no scheme reads it
+    (DESIGN.md §5): any chunking of the same steps gives bit-identical states, grad v included,
+    and the result matches the oracle."""
+    s = fluid_box_scene(2, kind=kind, alpha=0.3) if kind == "blend" else fluid_box_scene(2, kind=kind)
+    st = init_scene(s)
+    ctxs = []
+    for chunks in ([12], [7, 5], [1] * 12):
+        c = Context(s, st.particles.size())
+        c.upload(st)
+        for k in chunks:
+            c.advance(k)
+        ctxs.append(c.download(st.copy()))
+    for other in ctxs[1:]:
+        for f in ("x", "v", "sigma", "rho", "volume", "grad_v"):
+            assert np.array_equal(getattr(ctxs[0].particles, f), getattr(other.particles, f)), f
+    ref = st.copy()
+    orc.advance(s, ref, 12)
+    assert_state_close(ctxs[0], ref, STEP_RTOL["f64"])
+
+
 def test_stepper_api_mirror(orc):
     """Stepper(scene).advance(state) as in the reference (stepper.hpp:462-483)."""
     s = small_fluid_scene("flip")

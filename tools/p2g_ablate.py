@@ -20,6 +20,6 @@ for so in sys.argv[2:]:
     ctx.profile(True)
     ctx.profile_reset()
     ctx.advance(10)
-    r = {k: ctx.profile_query(k) for k in ("k_p2g_abl", "k_p2g", "k_g2p")}
+    r = {k: ctx.profile_query(k) for k in ("k_p2g_abl", "k_p2g", "k_g2p_abl", "k_g2p")}
     print(Path(so).name, dt, {k: round(v[0] / max(v[1], 1), 4) for k, v in r.items()}, flush=True)
     ctx.close()
