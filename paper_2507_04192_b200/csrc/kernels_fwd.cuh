@@ -664,8 +664,14 @@ template <class T> __device__ __forceinline__ void quad_w(T fx, int o, T inv_dh,
 // are in flight while item j is marched, so the dependent gathers through the sort
 // permutation never stall the CTA. Raw fields are staged (x, v, m, V, sigma); fractional
 // offsets, m v and V sigma are formed per visit. One CTA per SM, full register file.
+#ifndef P2G_SPLIT
+#define P2G_SPLIT 1 // f64: the narrow mapping's 7 node fields split over two thread groups
+#endif
+// SPLIT (f64 only; bit-identical sums): 12 warps of <= 45 accumulators instead of 6 warps of 63.
+// MEASURED C4: f64 k_p2g 0.517-0.523 -> 0.508 ms; f32 0.262 -> 0.318 ms (so f32 stays narrow).
 template <class T, bool WIDE = true> struct Pipe3Cfg {
-    static constexpr int LANES = WIDE ? 576 : 192;
+    static constexpr bool SPLIT = !WIDE && P2G_SPLIT && sizeof(T) == 8;
+    static constexpr int LANES = WIDE ? 576 : (SPLIT ? 384 : 192);
     static constexpr int NBC = 64, THREADS = LANES, NSRC = 9, NRAW = 14, MAXIT = 64;
     static constexpr int CAP = 640;
     static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
@@ -706,7 +712,10 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     using S = Pipe3Cfg<T, WIDE>;
     constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW;
     constexpr int NO1 = WIDE ? 1 : 3; // y-offsets handled per thread
-    constexpr int NA = NF; // accumulated fields per thread
+    constexpr bool SPLIT = S::SPLIT;
+    // SPLIT: thread group 0 accumulates m, p and f_x (5 fields), group 1 f_y and f_z (2 fields):
+    // 12 warps with <= 45 accumulators each instead of 6 warps with 63
+    constexpr int NA = SPLIT ? 5 : NF; // accumulated fields per thread
     // raw field rows: x0..2, v0..2, m, V, sig0..5
     constexpr int RX = 0, RV = 3, RM = 6, RVOL = 7, RS = 8;
     extern __shared__ unsigned char smem_raw[];
@@ -719,7 +728,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
         return;
     const int nocc = *n_occ;
     const int tid = threadIdx.x;
-    const int lt = tid;
+    const int grp = SPLIT ? tid / 192 : 0; // warp-uniform
+    const int lt = SPLIT ? tid - 192 * grp : tid;
     const int bc = WIDE ? lt / 9 : lt / 3;
     const int o0 = WIDE ? (lt % 9) / 3 : lt % 3;
     const int o1t = WIDE ? lt % 3 : 0; // WIDE: this thread's y-offset
@@ -821,7 +831,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                 const int ncol = (bc0 + o0) * TE + bc1 + o1;
 #pragma unroll
                 for (int f = 0; f < NA; ++f) {
-                    slots[(ncol * NSRC + o0 * 3 + o1) * NF + f] = acc[i1][0][f];
+                    if (!SPLIT || grp == 0 || f < 2)
+                        slots[(ncol * NSRC + o0 * 3 + o1) * NF + (SPLIT && grp ? 5 + f : f)] = acc[i1][0][f];
                     acc[i1][0][f] = acc[i1][1][f];
                     acc[i1][1][f] = acc[i1][2][f];
                     acc[i1][2][f] = T(0);
@@ -929,6 +940,24 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
 #pragma unroll
                 for (int q = 0; q < 6; ++q)
                     vs[q] = R[(RS + q) * CAP + k];
+                if (SPLIT && grp == 1) { // f_y, f_z into acc[..][..][0..1]
+#pragma unroll
+                    for (int o1 = 0; o1 < NO1; ++o1) {
+                        const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
+                        T u[2], t[2];
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            u[r] = vs[sym_idx<3>(r + 1, 0)] * p1 + vs[sym_idx<3>(r + 1, 1)] * p2;
+                            t[r] = vs[sym_idx<3>(r + 1, 2)] * pw;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 3; ++q)
+#pragma unroll
+                            for (int a = 0; a < 2; ++a)
+                                acc[o1][q][a] = acc[o1][q][a] - wz[q] * u[a] - dwz[q] * t[a];
+                    }
+                    continue;
+                }
                 {
 #pragma unroll
                     for (int o1 = 0; o1 < NO1; ++o1) {
@@ -944,7 +973,17 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                         }
                     }
                 }
-                {
+                if constexpr (SPLIT) { // group 0: f_x into acc[..][..][4]
+#pragma unroll
+                    for (int o1 = 0; o1 < NO1; ++o1) {
+                        const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
+                        const T u = vs[sym_idx<3>(0, 0)] * p1 + vs[sym_idx<3>(0, 1)] * p2;
+                        const T t = vs[sym_idx<3>(0, 2)] * pw;
+#pragma unroll
+                        for (int q = 0; q < 3; ++q)
+                            acc[o1][q][4] = acc[o1][q][4] - wz[q] * u - dwz[q] * t;
+                    }
+                } else {
                     constexpr int FO = 4; // force slots in acc
 #pragma unroll
                     for (int o1 = 0; o1 < NO1; ++o1) {
