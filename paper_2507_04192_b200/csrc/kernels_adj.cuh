@@ -921,8 +921,15 @@ __global__ void __launch_bounds__(256) k_adj_scatter(DevScene<T, D> sc, PBuf<T, 
 // column, x-offset), 3 y-offsets x a rolling 3-node z window x 6 fields. Per node
 // (adjoint.hpp:427-436): gv_cot += phi a + L grad(phi) = wz u + dwz t with u = pw a + L[:,0] p1 +
 // L[:,1] p2, t = L[:,2] pw; gvold_cot -= phi inc. Fixed-order slot reduction into the partial tiles.
+// SPLIT (f64): the 6 node fields over two thread groups, (gv_x, gv_y) and (gv_z, gvold_xyz), as
+// the forward P2G's split: 12 warps with <= 36 accumulators (bit-identical sums)
+#ifndef ADJ_SPLIT
+#define ADJ_SPLIT P2G_SPLIT
+#endif
 template <class T> struct AdjScatterCfg {
-    static constexpr int THREADS = 192, NBC = 64, NSRC = 9, NRAW = 18, MAXIT = 64, CAP = 512, NF = 6;
+    static constexpr bool SPLIT = ADJ_SPLIT && sizeof(T) == 8;
+    static constexpr int THREADS = SPLIT ? 384 : 192, NBC = 64, NSRC = 9, NRAW = 18, MAXIT = 64, CAP = 512, NF = 6;
+    static constexpr int NA = SPLIT ? 4 : NF; // accumulated fields per thread
     static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
     static constexpr size_t SMEM_PK = sizeof(int) * 3 * 2 * CAP;
     static constexpr size_t SMEM_SLOT = sizeof(T) * Cfg<3>::NCOL * NSRC * NF;
@@ -950,7 +957,12 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
         return;
     const int nocc = *n_occ;
     const int tid = threadIdx.x;
-    const int bc = tid / 3, o0 = tid % 3;
+    constexpr bool SPLIT = S::SPLIT;
+    constexpr int NA = S::NA;
+    const int grp = SPLIT ? tid / 192 : 0; // warp-uniform
+    const int lt = SPLIT ? tid - 192 * grp : tid;
+    const int f0 = SPLIT && grp ? 2 : 0;   // first slot field of this thread's group
+    const int bc = lt / 3, o0 = lt % 3;
     const bool mid = o0 == 1;
     const T xoff = o0 == 0 ? T(1.5) : (o0 == 1 ? T(1) : T(0.5));
     const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
@@ -1030,13 +1042,13 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
         cp_async_commit();
 
         T* part = partials + (size_t)Q * NF * C::TN;
-        T acc[3][3][NF];
+        T acc[3][3][NA];
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
             for (int k = 0; k < 3; ++k)
 #pragma unroll
-                for (int f = 0; f < NF; ++f)
+                for (int f = 0; f < NA; ++f)
                     acc[a][k][f] = T(0);
 
         auto emit_and_reduce = [&](int z) {
@@ -1044,8 +1056,9 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
             for (int o1 = 0; o1 < 3; ++o1) {
                 const int ncol = (bc0 + o0) * TE + bc1 + o1;
 #pragma unroll
-                for (int f = 0; f < NF; ++f) {
-                    slots[(ncol * NSRC + o0 * 3 + o1) * NF + f] = acc[o1][0][f];
+                for (int f = 0; f < NA; ++f) {
+                    if (!SPLIT || grp == 1 || f < 2)
+                        slots[(ncol * NSRC + o0 * 3 + o1) * NF + f0 + f] = acc[o1][0][f];
                     acc[o1][0][f] = acc[o1][1][f];
                     acc[o1][1][f] = acc[o1][2][f];
                     acc[o1][2][f] = T(0);
@@ -1134,6 +1147,36 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
 #pragma unroll
                 for (int q = 0; q < 9; ++q)
                     L[q] = R[(RL + q) * CAP + k];
+                if constexpr (SPLIT) {
+#pragma unroll
+                    for (int o1 = 0; o1 < 3; ++o1) {
+                        const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
+                        if (grp == 0) { // gv_x, gv_y
+#pragma unroll
+                            for (int a = 0; a < 2; ++a) {
+                                const T u = pw * av[a] + L[a * 3 + 0] * p1 + L[a * 3 + 1] * p2;
+                                const T t = L[a * 3 + 2] * pw;
+#pragma unroll
+                                for (int q = 0; q < 3; ++q)
+                                    acc[o1][q][a] = acc[o1][q][a] + wz[q] * u + dwz[q] * t;
+                            }
+                        } else { // gv_z, gvold_xyz
+                            const T u = pw * av[2] + L[6] * p1 + L[7] * p2;
+                            const T t = L[8] * pw;
+                            T ui[3];
+#pragma unroll
+                            for (int a = 0; a < 3; ++a)
+                                ui[a] = pw * iv[a];
+#pragma unroll
+                            for (int q = 0; q < 3; ++q) {
+                                acc[o1][q][0] = acc[o1][q][0] + wz[q] * u + dwz[q] * t;
+#pragma unroll
+                                for (int a = 0; a < 3; ++a)
+                                    acc[o1][q][1 + a] = acc[o1][q][1 + a] - wz[q] * ui[a];
+                            }
+                        }
+                    }
+                } else {
 #pragma unroll
                 for (int o1 = 0; o1 < 3; ++o1) {
                     // grad phi = (p1 wz, p2 wz, pw dwz) with pw = wx wy, p1 = dwx wy, p2 = wx dwy
@@ -1152,6 +1195,7 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
                             acc[o1][q][a] = acc[o1][q][a] + wz[q] * u[a] + dwz[q] * t[a];
                             acc[o1][q][3 + a] = acc[o1][q][3 + a] - wz[q] * ui[a];
                         }
+                }
                 }
             }
             if (it_last[j])
