@@ -921,10 +921,11 @@ __global__ void __launch_bounds__(256) k_adj_scatter(DevScene<T, D> sc, PBuf<T, 
 // column, x-offset), 3 y-offsets x a rolling 3-node z window x 6 fields. Per node
 // (adjoint.hpp:427-436): gv_cot += phi a + L grad(phi) = wz u + dwz t with u = pw a + L[:,0] p1 +
 // L[:,1] p2, t = L[:,2] pw; gvold_cot -= phi inc. Fixed-order slot reduction into the partial tiles.
-// SPLIT (f64): the 6 node fields over two thread groups, (gv_x, gv_y) and (gv_z, gvold_xyz), as
-// the forward P2G's split: 12 warps with <= 36 accumulators (bit-identical sums)
+// SPLIT (f64, A/B only): the 6 node fields over two thread groups, (gv_x, gv_y) and
+// (gv_z, gvold_xyz), as the forward P2G's split: 12 warps with <= 36 accumulators. MEASURED C4:
+// 0.54 -> 0.67 ms (slower, unlike the forward P2G), so it is off by default.
 #ifndef ADJ_SPLIT
-#define ADJ_SPLIT P2G_SPLIT
+#define ADJ_SPLIT 0
 #endif
 template <class T> struct AdjScatterCfg {
     static constexpr bool SPLIT = ADJ_SPLIT && sizeof(T) == 8;
