@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-workloads", action="store_true", help="skip the C2/C3/C5 sub-lines")
+    ap.add_argument("--slab-adj", action="store_true",
+                    help="slab mode: also time the host-orchestrated decomposed backprop (slow; DESIGN.md §7)")
     ap.add_argument("--adj-steps", type=int, default=20, help="fwd+adjoint sample: backprop steps (0: skip)")
     ap.add_argument("--adj-segments", type=int, default=0,
                     help="checkpoint segments of the fwd+adjoint sample (0: fewest that fit in HBM)")
@@ -583,6 +585,9 @@ def bench_slab(a, rank, world, local):
     dist.all_reduce(te[:1], op=dist.ReduceOp.MAX)
     tb = te[1:].clone()
     dist.all_reduce(tb)
+    fwd_adj = None
+    if a.config == "C4" and a.slab_adj:
+        fwd_adj = bench_slab_fwd_adj(s, st, dom, rank, world, n, min(a.adj_steps, 2))
     dom.close()
     dist.barrier()
     if rank != 0:
@@ -607,8 +612,39 @@ def bench_slab(a, rank, world, local):
                    "particles_total": n_total, "parallelism": f"slab x{world} (NCCL halo + migration)",
                    "slab_bounds": plan.bounds, "migrated_particles": int(mig.item()),
                    "l2_policy": "inputs larger than the 126 MB L2; no flush"},
-        "roofline": roof, "clocks": ck, "gpu_launches": launches, "e2e": e2e_line,
+        "roofline": roof, "clocks": ck, "gpu_launches": launches, "e2e": e2e_line, "fwd_adj": fwd_adj,
     }
+
+
+def bench_slab_fwd_adj(s, st, dom, rank, world, n, steps):
+    """fwd+adjoint over the slab decomposition (slab_backprop_trajectory: per-rank checkpoints,
+    digest-checked replay, slab_step_vjp with two halo exchanges per step). It is host-orchestrated:
+    replay states and migrants' cotangent rows pass through host memory every step,
+    so this is the protocol's number, wall clock max over ranks, not the device path's.
+    Loss: positions of every 100th particle (global ids) at the last step."""
+    import torch
+    import torch.distributed as dist
+    from paper_2507_04192_b200.distributed import TorchTransport, slab_backprop_trajectory
+    from paper_2507_04192_b200.seeders import LagrangianLeastSquares
+    from paper_2507_04192_b200.solver import CheckpointPlan
+
+    try:
+        n_total = n * world
+        sel = np.arange(0, n_total, 100, dtype=np.int64)
+        x0 = st.particles.x[sel % n].copy()  # every rank's column is the same seeding, shifted in x
+        x0[:, 0] += 256 * (sel // n - rank) * s.config.dh
+        seeder = LagrangianLeastSquares([steps], x0[None] + 1e-3, "x", sel=sel)
+        dist.barrier()
+        t0 = time.perf_counter()
+        res = slab_backprop_trajectory(s, CheckpointPlan.make(steps, 1), seeder, [dom], TorchTransport(), n_total)
+        wall = time.perf_counter() - t0
+        t = torch.tensor([wall], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+        return {"value": n_total * steps / wall, "unit": UNIT, "steps": steps, "n_segments": 1, "seconds": wall,
+                "loss": res.loss, "timing": "wall clock, max over ranks (host-orchestrated decomposed backprop)"}
+    except Exception as e:  # reported, the forward line still prints
+        return {"value": None, "error": f"{type(e).__name__}: {str(e)[:200]}"}
 
 
 def bench_slab_e2e(dom, stp, steps):
