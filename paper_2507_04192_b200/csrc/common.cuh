@@ -33,6 +33,35 @@ template <int D> struct Cfg {
     static constexpr int SEGS = D == 2 ? 8 : 2;            // march segments (B % SEGS == 0, >= 2 levels each)
 };
 
+// occupied-block list buckets and work counters (the list kernels are in kernels_util.cuh)
+constexpr int OCC_NBUCKET = 64;
+constexpr int WQ_HIST = 0, WQ_CUR = OCC_NBUCKET, WQ_CTR = 2 * OCC_NBUCKET; // scratch layout
+constexpr int WQ_P2G = WQ_CTR, WQ_G2P = WQ_CTR + 2, WQ_K5A = WQ_CTR + 4, WQ_K5B = WQ_CTR + 6, WQ_K7 = WQ_CTR + 8;
+constexpr int WQ_INTS = WQ_CTR + 16; // one counter pair per kernel
+
+__device__ __forceinline__ int occ_bucket(int cnt) // cnt >= 1
+{
+    const int L = 31 - __clz(cnt);
+    const int half = L > 0 ? (cnt >> (L - 1)) & 1 : 0;
+    return min(2 * L + half, OCC_NBUCKET - 1);
+}
+
+// A CTA's exit from a work-counter loop: the last CTA out resets the pair (next item, CTAs done)
+// for the next launch. Every CTA must call it exactly once, after its final fetch.
+// wq == nullptr: the plain static stride (blockIdx.x, + gridDim.x, ...), no counter.
+__device__ __forceinline__ int wq_first(int* wq) { return wq ? atomicAdd(wq, 1) : int(blockIdx.x); }
+__device__ __forceinline__ int wq_next(int* wq, int w) { return wq ? atomicAdd(wq, 1) : w + int(gridDim.x); }
+__device__ __forceinline__ void wq_finish(int* pair)
+{
+    if (pair && threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(pair + 1, 1) == int(gridDim.x) - 1) {
+            atomicExch(pair, 0);
+            atomicExch(pair + 1, 0);
+        }
+    }
+}
+
 // index of node (tile level z, node column col) inside a P2G partial tile: z fastest, so that
 // k_grid's threads (node-block-local index, z fastest) read consecutive addresses
 template <int D> __host__ __device__ __forceinline__ int ptile(int z, int col) { return col * Cfg<D>::TE + z; }

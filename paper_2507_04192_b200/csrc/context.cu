@@ -152,6 +152,7 @@ template <class T, int D> struct Ctx : CtxBase {
     size_t cub_bytes = 0;
     int *bstart = nullptr, *bend = nullptr, *lstart = nullptr, *occ = nullptr, *act = nullptr, *counts = nullptr; // counts[0]=n_occ, [1]=n_act
     unsigned char* nflag = nullptr;
+    int* wq = nullptr; // [WQ_INTS]: occupancy-bucket histogram and cursors, work-counter pairs (kernels_util.cuh)
     int *d_nb = nullptr, *d_nnb = nullptr;
     T* partials = nullptr;
     GBuf<T, D> G{};
@@ -165,6 +166,9 @@ template <class T, int D> struct Ctx : CtxBase {
     bool grid_touched_all = false;
     int nsm = 148;
     int p2g_ctas_per_sm = 1;
+    // occupied blocks listed heaviest first and taken through work counters (MPM_OCC_ORDER=index:
+    // the plain compaction, for A/B)
+    bool occ_lpt = !(std::getenv("MPM_OCC_ORDER") && std::getenv("MPM_OCC_ORDER")[0] == 'i');
     // 2-D P2G: the column-march kernel k_p2g (several CTAs' worth of warps per block) by default;
     // the staged variant (48 threads per block) is kept for A/B with MPM_P2G2D=staged. Measured
     // (C3, 102k particles): 25.7 vs 58.5 us; C2 (250k): 32 vs 72 us.
@@ -257,6 +261,8 @@ template <class T, int D> struct Ctx : CtxBase {
         occ = alloc<int>(sc.nb_total);
         act = alloc<int>(sc.nnb_total);
         counts = alloc<int>(4);
+        wq = alloc<int>(WQ_INTS);
+        CK(cudaMemsetAsync(wq, 0, sizeof(int) * WQ_INTS, stream));
         nflag = alloc<unsigned char>(sc.nnb_total);
         d_nb = alloc<int>(D);
         d_nnb = alloc<int>(D);
@@ -526,6 +532,11 @@ template <class T, int D> struct Ctx : CtxBase {
         CK(cudaGetLastError());
     }
 
+    // a kernel's work-counter pair when the occupied-block list is heaviest-first (3-D), else
+    // nullptr: the static CTA stride. MEASURED (C4 f64): G2P 0.410 -> 0.352 ms, step 1.102 -> 1.030 ms;
+    // in 2-D (C2/C3: small blocks, latency-bound steps) the extra list pass cost 5-7 us per step.
+    int* wq_ptr(int pair) const { return (occ_lpt && D == 3) ? wq + pair : nullptr; }
+
     unsigned grid_for(int64_t k, int tpb) const { return k > 0 ? unsigned((k + tpb - 1) / tpb) : 1u; } // n may be 0 on a slab
     unsigned persistent(int per_sm) const { return unsigned(nsm * per_sm); }
 
@@ -550,7 +561,13 @@ template <class T, int D> struct Ctx : CtxBase {
         CK(cudaMemsetAsync(counts, 0, sizeof(int) * 4, stream));
         CK(cudaMemsetAsync(nflag, 0, sc.nnb_total, stream));
         launch("k_seg", [&] { k_seg<D><<<grid_for(n, 256), 256, 0, stream>>>(keys_sorted, int(n), sc.nb_total, bstart, bend, lstart); });
-        launch("k_compact", [&] { k_compact_pos<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, sc.nb_total, occ, counts); });
+        if (occ_lpt && D == 3) { // heaviest blocks first (kernels_util.cuh)
+            CK(cudaMemsetAsync(wq, 0, sizeof(int) * WQ_CTR, stream));
+            launch("k_occ", [&] { k_occ_hist<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, bend, sc.nb_total, wq); });
+            launch("k_occ", [&] { k_occ_scatter<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, bend, sc.nb_total, wq, occ, counts); });
+        } else {
+            launch("k_compact", [&] { k_compact_pos<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, sc.nb_total, occ, counts); });
+        }
         launch("k_mark_nodes", [&] { k_mark_nodes<D><<<grid_for(sc.nb_total, 128), 128, 0, stream>>>(occ, counts, d_nb, d_nnb, nflag); });
         launch("k_compact", [&] { k_compact_flag<<<grid_for(sc.nnb_total, 256), 256, 0, stream>>>(nflag, sc.nnb_total, act, counts + 1); });
     }
@@ -572,12 +589,12 @@ template <class T, int D> struct Ctx : CtxBase {
 #elif P2G_ABL
                     launch("k_p2g_abl", [&] {
                         k_p2g_pipe3<T, P2G_WIDE, P2G_ABL><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
-                            sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st);
+                            sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st, wq_ptr(WQ_P2G));
                     });
 #endif
                     launch("k_p2g", [&] {
                         k_p2g_pipe3<T, P2G_WIDE><<<unsigned(nsm * p2g_ctas_per_sm), S::THREADS, S::SMEM, stream>>>(
-                            sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st);
+                            sc, buf[cur], perm, keys_sorted, bstart, bend, lstart, occ, counts, partials, st, wq_ptr(WQ_P2G));
                     });
                 } else {
                     using S = Lane3Cfg<T>;
@@ -617,18 +634,18 @@ template <class T, int D> struct Ctx : CtxBase {
         if constexpr ((FL & P_NOGV) != 0) { // requested only without affine / F state
             if (has_aff || has_F)
                 throw ApiError(MPM_ERR_USAGE, "internal: P_NOGV with affine or F state");
-            launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
+            launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig, wq_ptr(WQ_G2P)); });
         } else if (has_aff && has_F)
-            launch("k_g2p", [&] { k_g2p<T, D, FL, true, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
+            launch("k_g2p", [&] { k_g2p<T, D, FL, true, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig, wq_ptr(WQ_G2P)); });
         else if (has_aff)
-            launch("k_g2p", [&] { k_g2p<T, D, FL, true, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
+            launch("k_g2p", [&] { k_g2p<T, D, FL, true, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig, wq_ptr(WQ_G2P)); });
         else if (has_F)
-            launch("k_g2p", [&] { k_g2p<T, D, FL, false, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
+            launch("k_g2p", [&] { k_g2p<T, D, FL, false, true><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig, wq_ptr(WQ_G2P)); });
         else {
 #if G2P_ABL
-            launch("k_g2p_abl", [&] { k_g2p<T, D, FL, false, false, G2P_ABL><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
+            launch("k_g2p_abl", [&] { k_g2p<T, D, FL, false, false, G2P_ABL><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig, wq_ptr(WQ_G2P)); });
 #endif
-            launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig); });
+            launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig, wq_ptr(WQ_G2P)); });
         }
         cur ^= 1;
         keys_valid = true;

@@ -400,23 +400,27 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
                                                          const int* __restrict__ bend, const int* __restrict__ occ,
                                                          const int* __restrict__ n_occ, CBuf<T, D> co, CBuf<T, D> ci,
                                                          SBuf<T, D> S, T* __restrict__ pg_block, DevStatus* st,
-                                                         int co_gv_zero, int ci_gv_write)
+                                                         int co_gv_zero, int ci_gv_write, int* __restrict__ wq)
 {
     using C = Cfg<D>;
     constexpr int TE = C::TE, TN = C::TN;
     extern __shared__ unsigned char smem_raw[];
     T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]: v, v - v_old
     __shared__ T red[256];
-    if (st->abort)
-        return;
-    const int nocc = *n_occ;
+    __shared__ int w_s; // next list entry (work counter, common.cuh)
+    const int nocc = st->abort ? 0 : *n_occ; // every CTA still passes wq_finish
+    if (threadIdx.x == 0)
+        w_s = wq_first(wq);
     const T alpha = sc.alpha;
-    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+    for (;;) {
+        __syncthreads(); // w_s published; the previous block's shared-memory readers are done
+        const int w = w_s;
+        if (w >= nocc)
+            break;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
         int qc[D];
         block_coords<D>(Q, sc.nb, qc);
-        __syncthreads();
         for (int t = threadIdx.x; t < TN; t += blockDim.x) {
             int tl[D], rem = t, nid = 0, loc = 0;
             bool ok = true;
@@ -442,6 +446,8 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
             }
         }
         __syncthreads();
+        if (threadIdx.x == 0) // every thread read w_s before the barrier above
+            w_s = wq_next(wq, w);
         T c_acc = T(0), mu_acc = T(0);
         const T idh2 = sc.inv_dh * sc.inv_dh;
         // process the segment in rounds so every thread reaches the block reductions
@@ -722,6 +728,7 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
             }
         }
     }
+    wq_finish(wq);
 }
 
 // ---- K5b: G2P-transpose scatter (node-column march over the sorted records) ----------------
@@ -942,7 +949,7 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
     k_adj_scatter_pipe3(DevScene<T, 3> sc, PBuf<T, 3> P, SBuf<T, 3> Sb, const int* __restrict__ perm,
                         const int* __restrict__ keys, const int* __restrict__ bstart, const int* __restrict__ bend,
                         const int* __restrict__ lstart, const int* __restrict__ occ, const int* __restrict__ n_occ,
-                        T* __restrict__ partials, const DevStatus* st)
+                        T* __restrict__ partials, const DevStatus* st, int* __restrict__ wq)
 {
     using C = Cfg<3>;
     using S = AdjScatterCfg<T>;
@@ -954,9 +961,10 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
     T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_RAW + S::SMEM_PK); // [NCOL][NSRC][NF]
     __shared__ int it_start[S::MAXIT], it_len[S::MAXIT], it_lvl[S::MAXIT], it_last[S::MAXIT];
     __shared__ int nit_s, ccount[2][NBC];
-    if (st->abort)
-        return;
-    const int nocc = *n_occ;
+    __shared__ int w_s; // next list entry (work counter, common.cuh)
+    const int nocc = st->abort ? 0 : *n_occ; // every CTA still passes wq_finish
+    if (threadIdx.x == 0)
+        w_s = wq_first(wq);
     const int tid = threadIdx.x;
     constexpr bool SPLIT = S::SPLIT;
     constexpr int NA = S::NA;
@@ -969,10 +977,13 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
     const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
     const long long SI = P.S;
 
-    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+    for (;;) {
+        __syncthreads(); // w_s published; the previous block's shared-memory readers are done
+        const int w = w_s;
+        if (w >= nocc)
+            break;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
-        __syncthreads();
         if (tid == 0) { // level starts -> work items (as k_p2g_pipe3)
             int lv[B + 1];
             int nxt = s1;
@@ -1000,6 +1011,8 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
         }
         __syncthreads();
         int nit = nit_s;
+        if (tid == 0) // every thread read w_s before the barrier above
+            w_s = wq_next(wq, w);
         if (nit < 0) // the forward refused this block already (far_flag); nothing consistent to do
             nit = 0;
         auto issue_pk = [&](int j) {
@@ -1208,6 +1221,7 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
         __syncthreads();
         emit_and_reduce(B + 1);
     }
+    wq_finish(wq);
 }
 
 // ---- K6: per node: sum partials, correction-chain VJP, momentum-update transpose ------------
@@ -1606,21 +1620,25 @@ template <class T, int D, bool AFF>
 __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> Pin, GCBuf<T, D> GC,
                                                   const int* __restrict__ perm, const int* __restrict__ bstart,
                                                   const int* __restrict__ bend, const int* __restrict__ occ,
-                                                  const int* __restrict__ n_occ, CBuf<T, D> ci, const DevStatus* st)
+                                                  const int* __restrict__ n_occ, CBuf<T, D> ci, const DevStatus* st, int* __restrict__ wq)
 {
     using C = Cfg<D>;
     constexpr int TE = C::TE, TN = C::TN; // tile fields: 1 + 2 D
     extern __shared__ unsigned char smem_raw[];
     T* tile = reinterpret_cast<T*>(smem_raw); // [NF][TN]: gm, gmom[D], gf[D]
-    if (st->abort)
-        return;
-    const int nocc = *n_occ;
-    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+    __shared__ int w_s; // next list entry (work counter, common.cuh)
+    const int nocc = st->abort ? 0 : *n_occ; // every CTA still passes wq_finish
+    if (threadIdx.x == 0)
+        w_s = wq_first(wq);
+    for (;;) {
+        __syncthreads(); // w_s published; the previous block's shared-memory readers are done
+        const int w = w_s;
+        if (w >= nocc)
+            break;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
         int qc[D];
         block_coords<D>(Q, sc.nb, qc);
-        __syncthreads();
         for (int t = threadIdx.x; t < TN; t += blockDim.x) {
             int tl[D], rem = t, nid = 0, loc = 0;
             bool ok = true;
@@ -1646,6 +1664,8 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
             }
         }
         __syncthreads();
+        if (threadIdx.x == 0) // every thread read w_s before the barrier above
+            w_s = wq_next(wq, w);
         for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
             const int src = perm[i];
             T x[D], v[D], sig[D][D];
@@ -1947,6 +1967,7 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
             }
         }
     }
+    wq_finish(wq);
 }
 
 // ---- parameter-gradient reductions (fixed order over dense block ids) ------------------------
@@ -2499,13 +2520,13 @@ template <class T, int D> struct AdjWork {
             c.launch("k_adj_g2pT_gather", [&] {
                 k_adj_g2pT_gather<T, D, true><<<gr, 256, sm5, c.stream>>>(c.sc, Pin, c.G, c.perm, c.bstart, c.bend,
                                                                            c.occ, c.counts, cot[bo], cot[bi], sb,
-                                                                           pg_block, c.st, gvz[bo], gvw);
+                                                                           pg_block, c.st, gvz[bo], gvw, c.wq_ptr(WQ_K5A));
             });
         else
             c.launch("k_adj_g2pT_gather", [&] {
                 k_adj_g2pT_gather<T, D, false><<<gr, 256, sm5, c.stream>>>(c.sc, Pin, c.G, c.perm, c.bstart, c.bend,
                                                                             c.occ, c.counts, cot[bo], cot[bi], sb,
-                                                                            pg_block, c.st, gvz[bo], gvw);
+                                                                            pg_block, c.st, gvz[bo], gvw, c.wq_ptr(WQ_K5A));
             });
         const int tpb = D == 2 ? 160 : 256;
         if constexpr (D == 3) {
@@ -2514,7 +2535,7 @@ template <class T, int D> struct AdjWork {
                 c.launch("k_adj_scatter", [&] {
                     k_adj_scatter_pipe3<T><<<c.persistent(1), SC::THREADS, SC::SMEM, c.stream>>>(
                         c.sc, Pin, sb, c.perm, c.keys_sorted, c.bstart, c.bend, c.lstart, c.occ, c.counts, partials,
-                        c.st);
+                        c.st, c.wq_ptr(WQ_K5B));
                 });
                 return;
             }
@@ -2543,12 +2564,12 @@ template <class T, int D> struct AdjWork {
         if (aff)
             c.launch("k_adj_p2gT", [&] {
                 k_adj_p2gT<T, D, true><<<gr, 256, sm7, c.stream>>>(c.sc, Pin, gc, c.perm, c.bstart, c.bend, c.occ,
-                                                                   c.counts, cot[bi], c.st);
+                                                                   c.counts, cot[bi], c.st, c.wq_ptr(WQ_K7));
             });
         else
             c.launch("k_adj_p2gT", [&] {
                 k_adj_p2gT<T, D, false><<<gr, 256, sm7, c.stream>>>(c.sc, Pin, gc, c.perm, c.bstart, c.bend, c.occ,
-                                                                    c.counts, cot[bi], c.st);
+                                                                    c.counts, cot[bi], c.st, c.wq_ptr(WQ_K7));
             });
         int nfr = 0;
         for (int w = 0; w < 2 * D; ++w)

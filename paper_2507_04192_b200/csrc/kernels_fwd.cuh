@@ -706,7 +706,8 @@ template <class T, bool WIDE, int ABL = 0>
 __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     k_p2g_pipe3(DevScene<T, 3> sc, PBuf<T, 3> P, const int* __restrict__ perm, const int* __restrict__ keys,
                 const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ lstart,
-                const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials, DevStatus* st)
+                const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials, DevStatus* st,
+                int* __restrict__ wq)
 {
     using C = Cfg<3>;
     using S = Pipe3Cfg<T, WIDE>;
@@ -724,9 +725,10 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_RAW + S::SMEM_PK);      // [NCOL][NSRC][NF]
     __shared__ int it_start[S::MAXIT], it_len[S::MAXIT], it_lvl[S::MAXIT], it_last[S::MAXIT];
     __shared__ int nit_s, ccount[2][NBC]; // per-item column counts, double-buffered
-    if (st->abort)
-        return;
-    const int nocc = *n_occ;
+    __shared__ int w_s;                   // next list entry (work counter, kernels_util.cuh)
+    const int nocc = st->abort ? 0 : *n_occ; // every CTA still passes wq_finish
+    if (threadIdx.x == 0)
+        w_s = wq_first(wq);
     const int tid = threadIdx.x;
     const int grp = SPLIT ? tid / 192 : 0; // warp-uniform
     const int lt = SPLIT ? tid - 192 * grp : tid;
@@ -742,12 +744,15 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     static_assert(PL::M == RM && PL::VOL == RVOL && PL::SIG == RS + 2 && RS + 6 == NRAW, "raw row map");
     const long long SI = P.S;
 
-    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+    for (;;) {
+        __syncthreads(); // w_s published; the previous block's shared-memory readers are done
+        const int w = w_s;
+        if (w >= nocc)
+            break;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
         int qc[3];
         block_coords<3>(Q, sc.nb, qc);
-        __syncthreads();
         if (tid == 0) { // level starts (suffix minimum) -> work items
             int lv[B + 1];
             int nxt = s1;
@@ -780,6 +785,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
         }
         __syncthreads();
         const int nit = nit_s;
+        if (tid == 0) // every thread read w_s before the barrier above
+            w_s = wq_next(wq, w);
         auto issue_pk = [&](int j) {
             int* dp = pk + (j % 3) * 2 * CAP;
             const int b = s0 + it_start[j];
@@ -1012,6 +1019,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
         __syncthreads(); // slots reused by the next emit right away
         emit_and_reduce(B + 1);
     }
+    wq_finish(wq);
 }
 
 // 3-D P2G, lane-per-stencil-offset (PIC / FLIP / blend). A warp owns 4 particle columns of
@@ -1563,7 +1571,8 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                                              GBuf<T, D> G, const int* __restrict__ perm,
                                              const int* __restrict__ bstart, const int* __restrict__ bend,
                                              const int* __restrict__ occ, const int* __restrict__ n_occ,
-                                             int* __restrict__ keys_out, DevStatus* st, MigBuf<T> MG)
+                                             int* __restrict__ keys_out, DevStatus* st, MigBuf<T> MG,
+                                             int* __restrict__ wq)
 {
     using C = Cfg<D>;
     using SG = G2PStage<T, D, TRACKF>;
@@ -1572,9 +1581,10 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
     T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]: v[0..D), v - vold[0..D) (formed once per node)
     T* stg = tile + 2 * D * TN;               // [2][NSF][NT]: this thread's column only
     int* stg_pid = reinterpret_cast<int*>(stg + 2 * NSF * NT); // [2][NT]
-    if (st->abort)
-        return;
-    const int nocc = *n_occ;
+    __shared__ int w_s; // next list entry (work counter, kernels_util.cuh)
+    const int nocc = st->abort ? 0 : *n_occ; // every CTA still passes wq_finish
+    if (threadIdx.x == 0)
+        w_s = wq_first(wq);
     const T alpha = sc.alpha;
     const int tid = threadIdx.x;
     // cp.async of particle `src`'s inputs into slot `slot` (each thread its own column: no barrier)
@@ -1594,13 +1604,16 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
         cp_async4(stg_pid + slot * NT + tid, Pin.pid + src); // its id too: no exposed load before the stores
     };
     static_assert(PL::SIG + C::NS + (TRACKF ? D * D : 0) == NSF, "staging mirrors the PLay field order");
-    for (int w = blockIdx.x; w < nocc; w += gridDim.x) {
+    for (;;) {
+        cp_async_wait_all();
+        __syncthreads(); // w_s published; the previous block's tile readers are done
+        const int w = w_s;
+        if (w >= nocc)
+            break;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
         int qc[D];
         block_coords<D>(Q, sc.nb, qc);
-        cp_async_wait_all();
-        __syncthreads();
         // first particle of this thread in flight while the node tile loads
         int i0 = s0 + tid;
         int src_a = i0 < s1 ? perm[i0] : -1;                    // particle i0
@@ -1635,6 +1648,8 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
             }
         }
         __syncthreads();
+        if (threadIdx.x == 0) // every thread read w_s before the barrier above
+            w_s = wq_next(wq, w);
         int slot = 0;
         for (int i = i0; i < s1; i += NT) {
             // keep the next particle's fields and the one after's index in flight
@@ -1914,6 +1929,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
             keys_out[i] = key;
         }
     }
+    wq_finish(wq);
 }
 
 // constitutive-only phase (constitutive_update on the stored grad_v), in place

@@ -373,6 +373,48 @@ struct AliveSlot {
     __device__ __forceinline__ bool operator()(int i) const { return pid[i] >= 0; }
 };
 
+// ---- occupied-block list, heaviest blocks first, taken through a work counter ----------------
+// The list order is free: every listed block's outputs depend only on the block, not on which
+// CTA runs it or when. So it is chosen for load balance. Blocks are bucketed by particle count
+// (two buckets per octave) and listed heaviest bucket first; the persistent kernels take blocks
+// from the list through an atomic counter (longest-processing-time first), so a launch's tail is
+// made of light blocks instead of whichever blocks a static CTA stride happened to leave last.
+__global__ void k_occ_hist(const int* __restrict__ bstart, const int* __restrict__ bend, int n, int* __restrict__ wq)
+{
+    __shared__ int h[OCC_NBUCKET];
+    for (int t = threadIdx.x; t < OCC_NBUCKET; t += blockDim.x)
+        h[t] = 0;
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && bstart[i] >= 0)
+        atomicAdd(&h[occ_bucket(bend[i] - bstart[i])], 1);
+    __syncthreads();
+    for (int t = threadIdx.x; t < OCC_NBUCKET; t += blockDim.x)
+        if (h[t])
+            atomicAdd(&wq[WQ_HIST + t], h[t]);
+}
+
+__global__ void k_occ_scatter(const int* __restrict__ bstart, const int* __restrict__ bend, int n, int* __restrict__ wq,
+                              int* __restrict__ list, int* __restrict__ count)
+{
+    __shared__ int off[OCC_NBUCKET];
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int b = OCC_NBUCKET - 1; b >= 0; --b) {
+            off[b] = s;
+            s += wq[WQ_HIST + b];
+        }
+        if (blockIdx.x == 0)
+            *count = s;
+    }
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && bstart[i] >= 0) {
+        const int b = occ_bucket(bend[i] - bstart[i]);
+        list[off[b] + atomicAdd(&wq[WQ_CUR + b], 1)] = i;
+    }
+}
+
 // unordered compaction of a dense predicate (list order does not affect results: every
 // listed block is processed independently)
 __global__ void k_compact_pos(const int* __restrict__ dense, int n, int* __restrict__ list, int* __restrict__ count)
