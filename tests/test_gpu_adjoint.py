@@ -263,3 +263,49 @@ def test_backprop_replay_tape_bitwise(name, cap, monkeypatch):
             if pg_ref.wall_friction[w] is not None:
                 assert np.array_equal(pg.wall_friction[w], pg_ref.wall_friction[w])
     ctx1.close()
+
+
+def _dp3_many_blocks():
+    s = dp_block_scene(3, coulomb=True, cells=[200, 100, 110])
+    s.config.dh = 0.005  # 2.24 M particles in ~630 occupied blocks: several blocks per CTA
+    return s
+
+
+@pytest.mark.parametrize("name", ["dp3-coulomb", "fluid3-apic", "dp3-many-blocks"])
+def test_block_scheduling_bitwise(name, monkeypatch):
+    """3-D kernels take occupied blocks heaviest first through work counters (common.cuh).
+    Every block's outputs depend only on the block, so the forward state and the backprop
+    results are bit-identical to the static CTA stride (MPM_OCC_ORDER=index); a second call
+    checks that the counters were reset by the last CTA of every launch."""
+    s = _dp3_many_blocks() if name == "dp3-many-blocks" else SCENES[name]()
+    st = init_scene(s)
+    ctx = Context(s, st.particles.size())
+    ctx.upload(st)
+    ctx.advance(9)
+    seeder = _seeder_final_x(ctx.download(st.copy()), 9)
+    ctx.close()
+    out = {}
+    for order in ("index", "lpt"):
+        monkeypatch.setenv("MPM_OCC_ORDER", order)
+        c1 = Context(s, st.particles.size())
+        runs = []
+        for _ in range(2):
+            c1.upload(st)
+            c1.advance(7)
+            fwd = c1.download(st.copy())
+            runs.append((fwd, c1.backprop(st, 9, 2, seeder)))
+        c1.close()
+        out[order] = runs
+    ref_fwd, (c_ref, pg_ref, r_ref) = out["index"][0]
+    for fwd, (c, pg, r) in out["index"][1:] + out["lpt"]:
+        for f in ("x", "v", "sigma", "rho", "volume", "grad_v"):
+            assert np.array_equal(getattr(fwd.particles, f), getattr(ref_fwd.particles, f)), f
+        for f in StateCotangent.FIELDS:
+            a, b = getattr(c, f), getattr(c_ref, f)
+            if a is not None:
+                assert np.array_equal(a, b), f
+        assert r.loss == r_ref.loss
+        assert pg.sound_speed == pg_ref.sound_speed and pg.viscosity == pg_ref.viscosity
+        for w in range(2 * s.dim):
+            if pg_ref.wall_friction[w] is not None:
+                assert np.array_equal(pg.wall_friction[w], pg_ref.wall_friction[w])
