@@ -669,16 +669,71 @@ template <class T> __device__ __forceinline__ void quad_w(T fx, int o, T inv_dh,
 #endif
 // SPLIT (f64 only; bit-identical sums): 12 warps of <= 45 accumulators instead of 6 warps of 63.
 // MEASURED C4: f64 k_p2g 0.517-0.523 -> 0.508 ms; f32 0.262 -> 0.318 ms (so f32 stays narrow).
-template <class T, bool WIDE = true> struct Pipe3Cfg {
-    static constexpr bool SPLIT = !WIDE && P2G_SPLIT && sizeof(T) == 8;
-    static constexpr int LANES = WIDE ? 576 : (SPLIT ? 384 : 192);
+template <class T, bool WIDE = true, int NGR = 2> struct Pipe3Cfg {
+    // NG thread groups of 192 lanes split the 7 node fields (m, p[3], f[3]); f64 only
+    static constexpr int NG = (!WIDE && P2G_SPLIT && sizeof(T) == 8) ? NGR : 1;
+    static constexpr bool SPLIT = NG > 1;
+    static constexpr int LANES = WIDE ? 576 : 192 * NG;
     static constexpr int NBC = 64, THREADS = LANES, NSRC = 9, NRAW = 14, MAXIT = 64;
     static constexpr int CAP = 640;
     static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
     static constexpr size_t SMEM_PK = sizeof(int) * 3 * 2 * CAP;
     static constexpr size_t SMEM_SLOT = sizeof(T) * Cfg<3>::NCOL * NSRC * Cfg<3>::NF;
     static constexpr size_t SMEM = SMEM_RAW + SMEM_PK + SMEM_SLOT;
+    // field range [fb(g), fb(g + 1)) of group g in the order m, p0..2, f0..2.
+    // NG 2: {m, p, f_x} {f_y, f_z}; NG 3: {m, p} {f_x, f_y} {f_z} (FP64 work per lane-particle
+    // ~73 / 85 / 58 instead of ~106 / 85). MEASURED C4 f64: NG 3 (18 warps) 0.98 ms against NG 2's
+    // 0.49 ms -- ptxas caps it at 96 registers with 120 B of spills -- so NG 2 is the default.
+    static constexpr int fb(int g) { return NG == 1 ? (g ? 7 : 0) : NG == 2 ? (g == 0 ? 0 : g == 1 ? 5 : 7) : (g == 0 ? 0 : g == 1 ? 4 : g == 2 ? 6 : 7); }
+    static constexpr int NA = NG == 1 ? 7 : NG == 2 ? 5 : 4; // accumulated fields per thread (largest group)
 };
+
+// one staged particle's contributions to this lane's 3 x NO1 x 3 nodes, fields [FB, FE) only.
+// The arithmetic per field is the same expression whatever the grouping (bit-identical sums).
+template <int FB, int FE, int NO1, int NA, class T>
+__device__ __forceinline__ void p2g_visit(T (&acc)[NO1][3][NA], T wx, T dwx, const T (&wy)[NO1], const T (&dwy)[NO1],
+                                          const T (&wz)[3], const T (&dwz)[3], const T* __restrict__ R, int k, int CAP)
+{
+    constexpr int RV = 3, RM = 6, RS = 8;
+    constexpr bool HM = FB == 0, HP = FB < 4 && FE > 1, HF = FE > 4;
+#pragma unroll
+    for (int o1 = 0; o1 < NO1; ++o1) {
+        const T pw = wx * wy[o1];
+        if constexpr (HM || HP) {
+            T m = T(0), mv[3];
+            if constexpr (HM)
+                m = R[RM * CAP + k];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                mv[a] = R[(RV + a) * CAP + k];
+            const T mpw = m * pw;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const T phi = pw * wz[q];
+                if constexpr (HM)
+                    acc[o1][q][0] += mpw * wz[q];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    if (1 + a >= FB && 1 + a < FE)
+                        acc[o1][q][1 + a - FB] += phi * mv[a];
+            }
+        }
+        if constexpr (HF) {
+            // grad phi = (dwx wy wz, wx dwy wz, wx wy dwz): V sigma grad phi = wz u + dwz t
+            const T p1 = dwx * wy[o1], p2 = wx * dwy[o1];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                if (4 + r >= FB && 4 + r < FE) {
+                    const T u = R[(RS + sym_idx<3>(r, 0)) * CAP + k] * p1 + R[(RS + sym_idx<3>(r, 1)) * CAP + k] * p2;
+                    const T t = R[(RS + sym_idx<3>(r, 2)) * CAP + k] * pw;
+#pragma unroll
+                    for (int q = 0; q < 3; ++q)
+                        acc[o1][q][4 + r - FB] = acc[o1][q][4 + r - FB] - wz[q] * u - dwz[q] * t; // two FMAs
+                }
+            }
+        }
+    }
+}
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
 {
@@ -702,21 +757,21 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // ABL != 0: timing ablation only (1 skip reduce, 2 skip convert, 4 skip march), launched in
 // front of the real kernel by ablation builds (-DP2G_ABL=...), never on its own
-template <class T, bool WIDE, int ABL = 0>
-__global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
+template <class T, bool WIDE, int ABL = 0, int NGR = 2>
+__global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
     k_p2g_pipe3(DevScene<T, 3> sc, PBuf<T, 3> P, const int* __restrict__ perm, const int* __restrict__ keys,
                 const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ lstart,
                 const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials, DevStatus* st,
                 int* __restrict__ wq)
 {
     using C = Cfg<3>;
-    using S = Pipe3Cfg<T, WIDE>;
+    using S = Pipe3Cfg<T, WIDE, NGR>;
     constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW;
     constexpr int NO1 = WIDE ? 1 : 3; // y-offsets handled per thread
-    constexpr bool SPLIT = S::SPLIT;
-    // SPLIT: thread group 0 accumulates m, p and f_x (5 fields), group 1 f_y and f_z (2 fields):
+    // NG > 1: the node fields are split over NG groups of 192 lanes (S::fb): e.g. NG 2 gives
     // 12 warps with <= 45 accumulators each instead of 6 warps with 63
-    constexpr int NA = SPLIT ? 5 : NF; // accumulated fields per thread
+    constexpr int NG = S::NG;
+    constexpr int NA = S::NA; // accumulated fields per thread
     // raw field rows: x0..2, v0..2, m, V, sig0..5
     constexpr int RX = 0, RV = 3, RM = 6, RVOL = 7, RS = 8;
     extern __shared__ unsigned char smem_raw[];
@@ -730,8 +785,9 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
     if (threadIdx.x == 0)
         w_s = wq_first(wq);
     const int tid = threadIdx.x;
-    const int grp = SPLIT ? tid / 192 : 0; // warp-uniform
-    const int lt = SPLIT ? tid - 192 * grp : tid;
+    const int grp = NG > 1 ? tid / 192 : 0; // warp-uniform
+    const int lt = tid - 192 * grp;
+    const int gfb = S::fb(grp), gfn = S::fb(grp + 1) - gfb; // this group's fields
     const int bc = WIDE ? lt / 9 : lt / 3;
     const int o0 = WIDE ? (lt % 9) / 3 : lt % 3;
     const int o1t = WIDE ? lt % 3 : 0; // WIDE: this thread's y-offset
@@ -838,8 +894,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
                 const int ncol = (bc0 + o0) * TE + bc1 + o1;
 #pragma unroll
                 for (int f = 0; f < NA; ++f) {
-                    if (!SPLIT || grp == 0 || f < 2)
-                        slots[(ncol * NSRC + o0 * 3 + o1) * NF + (SPLIT && grp ? 5 + f : f)] = acc[i1][0][f];
+                    if (f < gfn)
+                        slots[(ncol * NSRC + o0 * 3 + o1) * NF + gfb + f] = acc[i1][0][f];
                     acc[i1][0][f] = acc[i1][1][f];
                     acc[i1][1][f] = acc[i1][2][f];
                     acc[i1][2][f] = T(0);
@@ -939,75 +995,13 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE>::THREADS, 1)
 #pragma unroll
                 for (int q = 0; q < 3; ++q)
                     quad_w<T>(f[2], q, sc.inv_dh, wz[q], dwz[q]);
-                const T m = R[RM * CAP + k];
-                T mv[3], vs[6];
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-                    mv[a] = R[(RV + a) * CAP + k];
-#pragma unroll
-                for (int q = 0; q < 6; ++q)
-                    vs[q] = R[(RS + q) * CAP + k];
-                if (SPLIT && grp == 1) { // f_y, f_z into acc[..][..][0..1]
-#pragma unroll
-                    for (int o1 = 0; o1 < NO1; ++o1) {
-                        const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
-                        T u[2], t[2];
-#pragma unroll
-                        for (int r = 0; r < 2; ++r) {
-                            u[r] = vs[sym_idx<3>(r + 1, 0)] * p1 + vs[sym_idx<3>(r + 1, 1)] * p2;
-                            t[r] = vs[sym_idx<3>(r + 1, 2)] * pw;
-                        }
-#pragma unroll
-                        for (int q = 0; q < 3; ++q)
-#pragma unroll
-                            for (int a = 0; a < 2; ++a)
-                                acc[o1][q][a] = acc[o1][q][a] - wz[q] * u[a] - dwz[q] * t[a];
-                    }
-                    continue;
-                }
-                {
-#pragma unroll
-                    for (int o1 = 0; o1 < NO1; ++o1) {
-                        const T pw = wx * wy[o1];
-                        const T mpw = m * pw;
-#pragma unroll
-                        for (int q = 0; q < 3; ++q) {
-                            const T phi = pw * wz[q];
-                            acc[o1][q][0] += mpw * wz[q];
-#pragma unroll
-                            for (int a = 0; a < 3; ++a)
-                                acc[o1][q][1 + a] += phi * mv[a];
-                        }
-                    }
-                }
-                if constexpr (SPLIT) { // group 0: f_x into acc[..][..][4]
-#pragma unroll
-                    for (int o1 = 0; o1 < NO1; ++o1) {
-                        const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
-                        const T u = vs[sym_idx<3>(0, 0)] * p1 + vs[sym_idx<3>(0, 1)] * p2;
-                        const T t = vs[sym_idx<3>(0, 2)] * pw;
-#pragma unroll
-                        for (int q = 0; q < 3; ++q)
-                            acc[o1][q][4] = acc[o1][q][4] - wz[q] * u - dwz[q] * t;
-                    }
-                } else {
-                    constexpr int FO = 4; // force slots in acc
-#pragma unroll
-                    for (int o1 = 0; o1 < NO1; ++o1) {
-                        // grad phi = (dwx wy wz, wx dwy wz, wx wy dwz): V sigma grad phi = wz u + dwz t
-                        const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
-                        T u[3], t[3];
-#pragma unroll
-                        for (int r = 0; r < 3; ++r) {
-                            u[r] = vs[sym_idx<3>(r, 0)] * p1 + vs[sym_idx<3>(r, 1)] * p2;
-                            t[r] = vs[sym_idx<3>(r, 2)] * pw;
-                        }
-#pragma unroll
-                        for (int q = 0; q < 3; ++q)
-#pragma unroll
-                            for (int a = 0; a < 3; ++a)
-                                acc[o1][q][FO + a] = acc[o1][q][FO + a] - wz[q] * u[a] - dwz[q] * t[a]; // two FMAs
-                    }
+                if (grp == 0)
+                    p2g_visit<S::fb(0), S::fb(1)>(acc, wx, dwx, wy, dwy, wz, dwz, R, k, CAP);
+                else if constexpr (NG > 1) {
+                    if (NG == 2 || grp == 1)
+                        p2g_visit<S::fb(1), S::fb(2)>(acc, wx, dwx, wy, dwy, wz, dwz, R, k, CAP);
+                    else if constexpr (NG > 2)
+                        p2g_visit<S::fb(2), S::fb(3)>(acc, wx, dwx, wy, dwy, wz, dwz, R, k, CAP);
                 }
             }
             if (it_last[j]) // slots were last read before the previous emit's closing barrier
