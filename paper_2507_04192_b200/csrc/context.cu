@@ -560,7 +560,7 @@ template <class T, int D> struct Ctx : CtxBase {
         CK(cudaMemsetAsync(lstart, 0xff, sizeof(int) * sc.nb_total * (C::B + 1), stream));
         CK(cudaMemsetAsync(counts, 0, sizeof(int) * 4, stream));
         CK(cudaMemsetAsync(nflag, 0, sc.nnb_total, stream));
-        launch("k_seg", [&] { k_seg<D><<<grid_for(n, 256), 256, 0, stream>>>(keys_sorted, int(n), sc.nb_total, bstart, bend, lstart); });
+        launch("k_seg", [&] { k_seg4<D><<<grid_for((n + 3) / 4, 256), 256, 0, stream>>>(keys_sorted, int(n), sc.nb_total, bstart, bend, lstart); });
         if (occ_lpt && D == 3) { // heaviest blocks first (kernels_util.cuh)
             CK(cudaMemsetAsync(wq, 0, sizeof(int) * WQ_CTR, stream));
             launch("k_occ", [&] { k_occ_hist<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, bend, sc.nb_total, wq); });

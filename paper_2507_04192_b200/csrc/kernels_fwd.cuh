@@ -78,6 +78,54 @@ __global__ void k_seg(const int* keys, int n, int nb_total, int* bstart, int* be
         lstart[b * (C::B + 1) + z] = i;
 }
 
+// k_seg over 4 sorted keys per thread (one 16-byte load; the neighbours across threads come by
+// shuffle): the same tables, 4x fewer threads and loads
+template <int D>
+__global__ void k_seg4(const int* __restrict__ keys, int n, int nb_total, int* __restrict__ bstart,
+                       int* __restrict__ bend, int* __restrict__ lstart)
+{
+    using C = Cfg<D>;
+    constexpr int LVLBITS = (D - 1) * C::LOGB;
+    const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    int k[6]; // keys i0 - 1 .. i0 + 4; -1 where out of range
+    if (i0 + 3 < n) {
+        const int4 v = *reinterpret_cast<const int4*>(keys + i0);
+        k[1] = v.x;
+        k[2] = v.y;
+        k[3] = v.z;
+        k[4] = v.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            k[1 + j] = i0 + j < n ? keys[i0 + j] : -1;
+    }
+    const int lane = threadIdx.x & 31;
+    k[0] = __shfl_up_sync(0xffffffffu, k[4], 1);
+    k[5] = __shfl_down_sync(0xffffffffu, k[1], 1);
+    if (lane == 0)
+        k[0] = (i0 > 0 && i0 - 1 < n) ? keys[i0 - 1] : -1;
+    if (lane == 31)
+        k[5] = i0 + 4 < n ? keys[i0 + 4] : -1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int i = i0 + j;
+        const int kk = k[j + 1];
+        const int b = kk >> C::LOGNB;
+        if (i >= n || b >= nb_total)
+            continue;
+        const int kp = k[j];
+        const int bp = kp >> C::LOGNB; // -1 for i == 0
+        const int bn = k[j + 2] >> C::LOGNB;
+        if (b != bp)
+            bstart[b] = i;
+        if (b != bn)
+            bend[b] = i + 1;
+        const int z = (kk & (C::NB - 1)) >> LVLBITS;
+        if (b != bp || z != ((kp & (C::NB - 1)) >> LVLBITS))
+            lstart[b * (C::B + 1) + z] = i;
+    }
+}
+
 // node blocks touched by occupied particle block Q: Q + s, s in {0,1}^D
 template <int D>
 __global__ void k_mark_nodes(const int* occ, const int* n_occ, const int* nb, const int* nnb, unsigned char* nflag)
