@@ -696,12 +696,18 @@ def bench_slab_e2e(dom, stp, steps):
 def fp64_for(prof, a):
     """The f64 kernels are co-limited by FP64 issue, not HBM: FP64 flops per launch
     (ncu SASS op counts, profiles/fp64.json: 2 x DFMA + DMUL + DADD) over the live mean launch time,
-    against the datasheet FP64 vector peak (not measured on this pool; MEASURED_PEAKS has no FP64)."""
+    against the FP64 DFMA ceiling measured on this pool by tools/fp64_peak.cu (profiles/fp64_peak.json;
+    MEASURED_PEAKS has no FP64), else the datasheet FP64 vector peak."""
     p = ROOT / "profiles" / "fp64.json"
     if a.config != "C4" or a.dtype != "f64" or not p.exists():
         return None
     ref = json.loads(p.read_text())
     out = {"peak_tflops": 37.0, "peak_source": "HGX B200 datasheet FP64 (not measured)", "unit": "TFLOP/s"}
+    pk = ROOT / "profiles" / "fp64_peak.json"
+    if pk.exists():
+        meas = json.loads(pk.read_text())
+        out["peak_tflops"] = float(meas["fp64_tflops"])
+        out["peak_source"] = "profiles/fp64_peak.json (measured: tools/fp64_peak.cu DFMA chains)"
     for k in ("k_p2g", "k_g2p"):
         if k in ref and k in prof:
             tf = ref[k]["fp64_flops"] / (prof[k]["ms_per_launch"] * 1e-3) / 1e12
