@@ -371,6 +371,12 @@ class SlabStepper:
             raise PeerFailure("step aborted on another rank")
         if rep.get(0, (0, 0, 0))[1] or rep.get(n_ranks - 1, (0, 0, 0))[2]:
             raise NumericalError("a particle left the outermost slab")  # OOD catches this first
+        if not any(v[1] or v[2] for v in rep.values()):
+            # no rank exported a particle (every rank holds the same gathered report, so all skip
+            # together): the export/exchange/import would move nothing. MEASURED at C4 N=1: 19 us of
+            # host time per step, all of it exposed behind the report's synchronisation.
+            self.steps_done += 1
+            return
         # migration of particles that left their slab
         sends = {}
         for r, d in doms.items():
