@@ -214,7 +214,21 @@ template <class T, int D> struct Ctx : CtxBase {
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
         f();
         CK(cudaStreamEndCapture(stream, &g));
-        CK(cudaGraphInstantiate(&out, g, 0));
+        // an existing executable graph of the same phase (the slab P2G phase after the particle
+        // count changed) is updated in place: same topology, new launch dimensions. A topology or
+        // node-type change (cub's tile count moving a memset's size, say) falls back to instantiation.
+        bool updated = false;
+        if (out) {
+            cudaGraphExecUpdateResultInfo info{};
+            updated = cudaGraphExecUpdate(out, g, &info) == cudaSuccess;
+            if (!updated) {
+                (void)cudaGetLastError(); // cudaErrorGraphExecUpdateFailure is not sticky
+                CK(cudaGraphExecDestroy(out));
+                out = nullptr;
+            }
+        }
+        if (!updated)
+            CK(cudaGraphInstantiate(&out, g, 0));
         CK(cudaGraphDestroy(g));
         const int64_t k = launches - l0;
         launches = l0;
@@ -1270,9 +1284,6 @@ template <class T, int D> struct Ctx : CtxBase {
         }
         // replay a graph of the phase; recapture when the particle count changed (migration)
         if (!slab_g1[cur] || slab_g1_n[cur] != n) {
-            if (slab_g1[cur])
-                cudaGraphExecDestroy(slab_g1[cur]);
-            slab_g1[cur] = nullptr;
             slab_g1_launches = capture(slab_g1[cur], [&] { p2g_phase(); });
             slab_g1_n[cur] = n;
         }
