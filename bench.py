@@ -99,7 +99,14 @@ def bytes_model(scene, n_particles, active_nodes, steps_per_call=1):
 
 
 def kernel_bytes(scene, n, active_nodes, occupied_blocks):
-    """Compulsory bytes per launch of the two particle kernels."""
+    """Per launch of the two particle kernels: SURVEY §8(d)'s COMPULSORY bytes ("algorithmic":
+    every particle field the kernel must read or write, once, and each active node's fields once)
+    next to the bytes the implementation actually moves ("moved": + the sort permutation / keys /
+    particle ids and the (B+2)^d partial tiles of every occupied block instead of the active nodes).
+      k_p2g  reads x v m V sigma; writes the active nodes' m p f once
+      k_g2p  reads x v V rho sigma (+eps, +sigma_zz) and the active nodes' v v_old; writes
+             x v V rho sigma grad v (+eps, +sigma_zz) -- grad v counted as SURVEY does
+             ("needed" drops it: FLIP stores it only on a call's last step)"""
     d = scene.dim
     s = 8 if scene.dtype == "f64" else 4
     ns = 3 if d == 2 else 6
@@ -107,13 +114,16 @@ def kernel_bytes(scene, n, active_nodes, occupied_blocks):
     B = 16 if d == 2 else 8
     tile = (B + 2) ** d
     nf = 1 + 2 * d
-    # k_p2g: read x v m V sigma (+ perm, keys) per particle; write one partial tile per block
-    p2g = n * ((2 * d + 2 + ns) * s + 8) + occupied_blocks * tile * nf * s
-    # k_g2p: read + write the whole particle record (+ perm, pid, key) and the node tiles (v, v_old)
-    rec_in = 2 * d + 4 + ns + (1 if (dp and d == 2) else 0)
-    rec_out = rec_in + d * d  # SURVEY's record (grad v included), as bytes_model
-    g2p = n * ((rec_in + rec_out) * s + 4 * 4) + occupied_blocks * tile * 2 * d * s
-    return {"k_p2g": p2g, "k_g2p": g2p}
+    extra = (1 if dp else 0) + (1 if (dp and d == 2) else 0)  # eps (+ sigma_zz)
+    p2g_in = 2 * d + 2 + ns
+    g2p_in = 2 * d + 2 + ns + extra
+    g2p_out = g2p_in + d * d
+    alg = {"k_p2g": n * p2g_in * s + active_nodes * nf * s,
+           "k_g2p": n * (g2p_in + g2p_out) * s + active_nodes * 2 * d * s}
+    need = {"k_p2g": alg["k_p2g"], "k_g2p": alg["k_g2p"] - (n * d * d * s if gv_dead(scene) else 0)}
+    moved = {"k_p2g": n * (p2g_in * s + 8) + occupied_blocks * tile * nf * s,
+             "k_g2p": n * ((g2p_in + 1 + g2p_out) * s + 4 * 4) + occupied_blocks * tile * 2 * d * s}
+    return alg, need, moved
 
 
 # ---- clocks sampler -------------------------------------------------------------------------
@@ -164,15 +174,22 @@ class ClockSampler:
 
 # ---- CPU baseline (the reference on host cores) --------------------------------------------
 def _cpu_worker(args):
-    """One host core: the reference's own run() timer (stepper.hpp:504-535) on the full scene."""
-    cfg, dtype, kind, steps = args
+    """One host process: the reference's own run() timer (stepper.hpp:91-122) for mode "fwd", or the
+    wall clock of its backprop_trajectory (checkpoint.hpp:72-143) for mode "adj", on the full scene."""
+    cfg, dtype, kind, steps, mode, nseg = args
     sys.path.insert(0, str(ROOT))
     from oracle import CpuOracle  # test infrastructure: the CPU baseline, never the product path
     from paper_2507_04192_b200.presets import CONFIGS
     s = CONFIGS[cfg](dtype=dtype)
     o = CpuOracle(kind)
     st = o.init_scene(s)
-    secs = o.run_seconds_per_1000(s, st, steps) / 1000.0 * steps
+    if mode == "fwd":
+        secs = o.run_seconds_per_1000(s, st, steps) / 1000.0 * steps
+    else:
+        sd = {"field": "x", "obs_steps": [steps], "sel": None, "target": st.particles.x[None] + 1e-3}
+        t0 = time.perf_counter()
+        o.backprop(s, st, steps, nseg, sd)
+        secs = time.perf_counter() - t0
     return st.particles.size() * steps, secs
 
 
@@ -186,70 +203,75 @@ def _mem_available_gb():
     return 16.0
 
 
-def cpu_baseline(cfg, dtype, steps=1):
-    """The reference (or the restatement) on the same scene, `steps` steps, one process per core
-    (independent replicas are the reference's only sanctioned concurrency), capped
-    by host memory. Value = sum of the per-process rates."""
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# host memory one reference process needs (state copies inside run / backprop_trajectory), GB
+_PROC_GB = {"fwd": {"C4": 6.0, "C5": 40.0, "C5/8": 6.0}, "adj": {"C4": 14.0, "C5": 100.0, "C5/8": 14.0}}
+
+
+def cpu_sample(cfg, dtype="f64", steps=1, mode="fwd", nseg=1, kind=None, procs=None):
+    """The reference (oracle/_ref, compiled unmodified) -- or the restatement -- on the full scene
+    `cfg`: `steps` forward steps (mode "fwd") or a backprop_trajectory over `steps` steps (mode
+    "adj"), in `procs` concurrent processes (default: one per host core, capped by host memory;
+    independent replicas are the reference's only sanctioned concurrency).
+    value = sum of the per-process particle-steps/s."""
     import multiprocessing as mp
     import oracle
-    kind = "ref" if oracle.available("ref") else "orc"
+    kind = kind or ("ref" if oracle.available("ref") else "orc")
     cores = os.cpu_count() or 1
-    per_proc_gb = {"C4": 6.0, "C5": 40.0}.get(cfg, 1.0) * (0.5 if dtype == "f32" else 1.0)
-    procs = max(1, min(cores, int(_mem_available_gb() * 0.6 / per_proc_gb)))
+    per_proc_gb = _PROC_GB[mode].get(cfg, 1.0 if mode == "fwd" else 2.0) * (0.5 if dtype == "f32" else 1.0)
+    cap = max(1, min(cores, int(_mem_available_gb() * 0.6 / per_proc_gb)))
+    procs = min(procs or cap, cap)
     with mp.get_context("spawn").Pool(procs) as pool:
         t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, [(cfg, dtype, kind, steps)] * procs)
+        res = pool.map(_cpu_worker, [(cfg, dtype, kind, steps, mode, nseg)] * procs)
         wall = time.perf_counter() - t0
     per_proc = [r[0] / r[1] for r in res]
-    value = sum(per_proc)
     n = int(res[0][0] / steps)
-    sample = (f"{procs} concurrent replicas (one per host core, of {cores}) of the full {cfg} scene "
-              f"({n} particles), {steps} step(s) each, timed by the reference's run() timer; "
-              f"value = sum of per-process particle-steps/s")
-    return {"value": value, "unit": UNIT, "cores": procs, "host_cores": cores,
-            "kind": "reference" if kind == "ref" else "port", "sample": sample,
-            "single_process": per_proc[0], "wall_s": wall,
-            "label": "reference compiled against the Eigen-API shim (C++20 -O3 -DNDEBUG, serial)"
-            if kind == "ref" else "oracle restatement (C++20 -O3, serial)"}
+    what = (f"{steps} forward step(s) timed by the reference's run() timer" if mode == "fwd" else
+            f"backprop_trajectory over {steps} step(s), {nseg} segment(s), Lagrangian least-squares loss on the "
+            f"final positions, wall clock of the call")
+    flags = "-O3 -DNDEBUG -march=x86-64-v3" if kind == "ref_v3" else "-O3 -DNDEBUG (no -march: the reference's CMake Release)"
+    return {"value": sum(per_proc), "unit": UNIT, "cores": procs, "host_cores": cores,
+            "kind": "reference" if kind.startswith("ref") else "port",
+            "sample": (f"{procs} concurrent process(es) (of {cores} host cores{', capped by host memory' if procs < cores else ''}) "
+                       f"each running the full {cfg} scene ({n} particles): {what}; value = sum of per-process rates"),
+            "single_process": per_proc[0], "wall_s": wall, "cpu_model": _cpu_model(),
+            "label": f"reference compiled against the Eigen-API shim (C++20 {flags}, serial)"
+            if kind.startswith("ref") else "oracle restatement (C++20 -O3, serial)"}
 
 
-def _cpu_adj_worker(args):
-    """One host core: the reference's backprop_trajectory (checkpoint.hpp:72-143) on the full scene."""
-    cfg, dtype, kind, steps, nseg = args
-    sys.path.insert(0, str(ROOT))
-    from oracle import CpuOracle  # test infrastructure: the CPU baseline, never the product path
-    from paper_2507_04192_b200.presets import CONFIGS
-    s = CONFIGS[cfg](dtype=dtype)
-    o = CpuOracle(kind)
-    st = o.init_scene(s)
-    sd = {"field": "x", "obs_steps": [steps], "sel": None, "target": st.particles.x[None] + 1e-3}
-    t0 = time.perf_counter()
-    o.backprop(s, st, steps, nseg, sd)
-    return st.particles.size() * steps, time.perf_counter() - t0
+def cpu_baseline(cfg, dtype, steps=1):
+    """Headline CPU baseline (all host cores) plus BASELINE.md §2's variants: one process alone
+    (1 thread) and the -march=x86-64-v3 build on all cores."""
+    import oracle
+    out = cpu_sample(cfg, dtype, steps)
+    out["variants"] = {}
+    try:
+        one = cpu_sample(cfg, dtype, steps, procs=1)
+        out["variants"]["one_thread"] = {k: one[k] for k in ("value", "cores", "sample", "label")}
+    except Exception as e:
+        out["variants"]["one_thread"] = {"error": str(e)[:200]}
+    if oracle.available("ref_v3"):
+        try:
+            v3 = cpu_sample(cfg, dtype, steps, kind="ref_v3")
+            out["variants"]["march_x86_64_v3"] = {k: v3[k] for k in ("value", "cores", "sample", "label")}
+        except Exception as e:
+            out["variants"]["march_x86_64_v3"] = {"error": str(e)[:200]}
+    return out
 
 
 def cpu_baseline_adj(cfg, dtype, steps=2, nseg=1):
-    """fwd+adjoint on the host cores: the reference's backprop_trajectory over `steps` steps (forward
-    sweep + replay + step_vjp per step), one process per core, capped by host memory."""
-    import multiprocessing as mp
-    import oracle
-    kind = "ref" if oracle.available("ref") else "orc"
-    cores = os.cpu_count() or 1
-    per_proc_gb = {"C4": 14.0, "C5": 100.0}.get(cfg, 2.0) * (0.5 if dtype == "f32" else 1.0)
-    procs = max(1, min(cores, int(_mem_available_gb() * 0.6 / per_proc_gb)))
-    with mp.get_context("spawn").Pool(procs) as pool:
-        t0 = time.perf_counter()
-        res = pool.map(_cpu_adj_worker, [(cfg, dtype, kind, steps, nseg)] * procs)
-        wall = time.perf_counter() - t0
-    per_proc = [r[0] / r[1] for r in res]
-    n = int(res[0][0] / steps)
-    return {"value": sum(per_proc), "unit": UNIT, "cores": procs, "host_cores": cores,
-            "kind": "reference" if kind == "ref" else "port",
-            "sample": (f"{procs} concurrent replicas (of {cores} host cores, capped by host memory) of the full "
-                       f"{cfg} scene ({n} particles): backprop_trajectory over {steps} steps, {nseg} segment(s), "
-                       f"Lagrangian least-squares loss on the final positions, wall clock of the call; "
-                       f"value = sum of per-process particle-steps/s"),
-            "single_process": per_proc[0], "wall_s": wall}
+    """fwd+adjoint on the host cores: the reference's backprop_trajectory over `steps` steps."""
+    return cpu_sample(cfg, dtype, steps, mode="adj", nseg=nseg)
 
 
 def bench_fwd_adj(ctx, s, st, n, steps, nseg):
@@ -285,8 +307,9 @@ def bench_fwd_adj(ctx, s, st, n, steps, nseg):
             "forward_passes_per_step": 1 + (steps - (steps // nseg)) / steps}
 
 
-def vjp_bytes(s, n, active_nodes_step, B_fwd, IN):
-    """B_fwd+adj = 2 B_fwd + B_vjp per particle-step."""
+def vjp_bytes(s, n, active_nodes_step, B_fwd, IN, fwd_passes=2.0):
+    """B_fwd+adj = fwd_passes B_fwd + B_vjp per particle-step; SURVEY.md §8d writes it with 2
+    forward passes (sweep + replay); the bench also reports it on the passes actually executed."""
     d = s.dim
     sz = 8 if s.dtype == "f64" else 4
     ns = 3 if d == 2 else 6
@@ -294,15 +317,24 @@ def vjp_bytes(s, n, active_nodes_step, B_fwd, IN):
     COT = 2 * d + 2 + ns + (1 if (dp and d == 2) else 0)
     A_np = active_nodes_step / n
     B_vjp = (IN + 2 * COT) * sz + A_np * (2 * (1 + 2 * d) + 8 * d) * sz
-    return 2 * B_fwd + B_vjp
+    return fwd_passes * B_fwd + B_vjp
 
 
-def bench_workloads(peak, names):
+# CPU samples of the sub-lines (BASELINE.md §2 horizons where they fit a few minutes of wall
+# time; the reference is serial, so each is run as concurrent replicas on the host cores):
+#   (cfg, mode, steps, n_segments)
+CPU_SUBLINE = {"C2": {"fwd": ("C2", "fwd", 100, 1)},
+               "C3": {"fwd": ("C3", "fwd", 100, 1), "fwd_adj": ("C3", "adj", 20, 1)},
+               "C5": {"fwd": ("C5", "fwd", 1, 1), "fwd_adj": ("C5/8", "adj", 1, 1)}}
+
+
+def bench_workloads(peak, names, cpu=True):
     """The other BASELINE.json configs on this GPU (N = 1), device-timed through the same context
-    API: C2 forward; C3 the paper's inverse problem (loss on the final deposit of a twin run with
-    alpha* = 2, reverse-mode gradient through all 1000 steps, HBM-sized checkpoint plan, dL/dalpha
-    chained on the host as in SURVEY §8d); C5 forward + a 20-step fwd+adjoint with the 32 Coulomb
-    friction segments' gradients. No CPU sample here (the reference would take hours)."""
+    API: C2 forward; C3 the paper's inverse problem (loss on the final deposit of an alpha* = 2
+    twin, reverse-mode gradient through all 1000 steps from t = 0, HBM-sized checkpoint plan,
+    dL/dalpha chained on the host as in SURVEY §8d, compared with the reference's own gradient in
+    tests/golden/c3_gradient.npz); C5 forward + a 20-step fwd+adjoint with the 32 Coulomb friction
+    segments' gradients. Each sub-line carries its own roofline and a CPU sample (CPU_SUBLINE)."""
     import numpy as np
     import torch
     from paper_2507_04192_b200 import init_scene
@@ -317,24 +349,21 @@ def bench_workloads(peak, names):
                 out[name] = {"skipped": "host memory below 48 GB for the 7.3 GB host copies"}
                 continue
             s = CONFIGS[name](dtype="f64")
-            st = init_scene(s)
-            n = st.particles.size()
+            st0 = init_scene(s)
+            n = st0.particles.size()
             ctx = Context(s, n)
-            ctx.upload(st)
+            ctx.upload(st0)
             ctx.advance(3)
             k_fwd = {"C2": 200, "C3": 200, "C5": 20}[name]
-            ms = ctx.advance_timed(k_fwd)
+            ms = ctx.advance_timed(k_fwd, nan_guard=True)
             act, _, _ = ctx.grid_stats()
             B_fwd, IN, _ = bytes_model(s, n, act / k_fwd)
-            B_fwd1 = B_fwd
             w = {"particles": n, "grid_cells": s.config.cells, "dtype": "f64",
                  "fwd": {"value": n * k_fwd / (ms / 1e3), "unit": UNIT, "steps": k_fwd, "ms_per_step": ms / k_fwd,
                          "roofline_frac": n * B_fwd / (ms / k_fwd / 1e3) / 1e9 / peak,
                          "bytes_per_particle_step": B_fwd}}
             adj = {"C3": 1000, "C5": 20}.get(name, 0)
             if adj:
-                st0 = ctx.download(st)
-                ctx.upload(st0)
                 if name == "C3":  # twin run at the true alpha* = 2.0 gives the observed deposit
                     tw = c3_inverse(alpha=2.0, dtype="f64")
                     stt = init_scene(tw)
@@ -343,35 +372,52 @@ def bench_workloads(peak, names):
                     ctt.advance(adj)
                     target = ctt.download(stt).particles.x[None].copy()
                     ctt.close()
+                    sd = LagrangianLeastSquares([adj], target, "x")
                 else:  # positions of a 1 % subset (seeded) against a perturbed twin
                     rng = np.random.default_rng(0)
                     sel = np.sort(rng.choice(n, n // 100, replace=False))
-                    target = None
-                act0 = act / k_fwd
-                nseg, plan = hbm_plan(s, n, adj, act0)
-                if name == "C3":
-                    sd = LagrangianLeastSquares([adj], target, "x")
-                else:
                     ctx.upload(st0)
                     ctx.advance(adj)
                     xf = ctx.download(st0.copy()).particles.x
                     sd = LagrangianLeastSquares([adj], xf[sel][None] + 1e-3, "x", sel=sel)
+                act0 = act / k_fwd
+                nseg, plan = hbm_plan(s, n, adj, act0)
                 ctx.backprop(st0, adj, nseg, sd.desc())  # allocates the checkpoint / replay pool
                 c0, pg, res = ctx.backprop(st0, adj, nseg, sd.desc())
-                B_fa = vjp_bytes(s, n, act0, B_fwd1, IN)
+                L_last = adj // nseg
+                fpps = 1 + (adj - L_last) / adj
+                B_fa = vjp_bytes(s, n, act0, B_fwd, IN, fpps)
                 mps = res.device_ms / adj
                 w["fwd_adj"] = {"value": n * adj / (res.device_ms / 1e3), "unit": UNIT, "steps": adj,
-                                "ms_per_step": mps, "plan": plan, "loss": res.loss,
+                                "ms_per_step": mps, "plan": plan, "loss": res.loss, "forward_passes_per_step": fpps,
                                 "roofline_frac": n * B_fa / (mps / 1e3) / 1e9 / peak, "bytes_per_particle_step": B_fa,
+                                "roofline_basis": "forward passes executed x B_fwd + B_vjp",
                                 "timing": "mpm_backprop_result.device_ms (forward sweep + replays + VJPs)"}
-                if name == "C3":  # v_x(0) = alpha (H0 - y): dL/dalpha = sum_p vbar_x(0) v_x(0) / alpha
+                if name == "C3":  # v_x(0) = alpha (h0 - y_rel): dL/dalpha = sum_p vbar_x(0) v_x(0) / alpha
                     alpha = s.geometry[0].velocity.alpha
-                    w["fwd_adj"]["dL_dalpha"] = float(np.sum(c0.v[:, 0] * st0.particles.v[:, 0]) / alpha)
+                    dl = float(np.sum(c0.v[:, 0] * st0.particles.v[:, 0]) / alpha)
+                    w["fwd_adj"]["dL_dalpha"] = dl
+                    gold = ROOT / "tests" / "golden" / "c3_gradient.npz"
+                    if gold.exists():
+                        g = np.load(gold)
+                        w["fwd_adj"]["reference_gradient"] = {
+                            "dL_dalpha": float(g["dL_dalpha"]), "loss": float(g["loss"]),
+                            "rel_diff_dL_dalpha": abs(dl - float(g["dL_dalpha"])) / abs(float(g["dL_dalpha"])),
+                            "rel_diff_loss": abs(res.loss - float(g["loss"])) / abs(float(g["loss"])),
+                            "source": "tests/golden/c3_gradient.npz: the reference's backprop_trajectory, "
+                                      "1000 steps, n_seg 10 (tests/golden/make_c3_gradient.py)"}
                 else:
                     fr = np.asarray(pg.flat())
                     w["fwd_adj"]["param_grads_norm"] = float(np.linalg.norm(fr))
             ctx.close()
             torch.cuda.empty_cache()
+            if cpu:
+                for leg, (ccfg, mode, steps, cseg) in CPU_SUBLINE.get(name, {}).items():
+                    if leg in w:
+                        try:
+                            w[leg]["cpu_baseline"] = cpu_sample(ccfg, "f64", steps, mode=mode, nseg=cseg)
+                        except Exception as e:
+                            w[leg]["cpu_baseline"] = {"value": None, "error": f"{type(e).__name__}: {str(e)[:160]}"}
             out[name] = w
         except Exception as e:  # a workload that fails is reported, the headline line still prints
             out[name] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
@@ -430,7 +476,7 @@ def bench_b200(a, rank, world, local):
     time.sleep(0.3)
     l0 = ctx.launch_count()
     barrier()
-    ms = ctx.advance_timed(a.steps)
+    ms = ctx.advance_timed(a.steps, nan_guard=True)  # run()'s per-step all_finite guard (stepper.hpp:106-109)
     barrier()
     launches = ctx.launch_count() - l0
     ck = clocks.stop()
@@ -451,21 +497,38 @@ def bench_b200(a, rank, world, local):
     # ---- per-kernel profile (CUDA events around each launch on the library stream)
     ctx.profile(True)
     ctx.profile_reset()
-    ctx.advance(3)
+    ctx.advance(3, nan_guard=True)
     prof = {}
-    for k in ("k_p2g", "k_grid", "k_g2p", "k_seg", "k_compact", "k_mark_nodes", "k_step_end", "k_keys"):
+    for k in ("k_p2g", "k_grid", "k_g2p", "k_sort", "k_seg", "k_occ", "k_compact", "k_mark_nodes", "k_step_end",
+              "k_keys"):
         t_ms, cnt = ctx.profile_query(k)
         if cnt:
             prof[k] = {"ms_per_launch": t_ms / cnt, "launches": cnt}
     total_ms, _ = ctx.profile_query("")
     ctx.profile(False)
-    kb = kernel_bytes(s, n, active_nodes_step, occ_blocks)
+    kb, kneed, kmoved = kernel_bytes(s, n, active_nodes_step, occ_blocks)
     dom = max(("k_p2g", "k_g2p"), key=lambda k: prof.get(k, {}).get("ms_per_launch", 0))
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     dom_ms = prof[dom]["ms_per_launch"]
     achieved = kb[dom] / (dom_ms / 1e3) / 1e9
     step_gbs = n * B_fwd / (ms_per_step / 1e3) / 1e9
+    per_kernel = {}
+    for k in ("k_p2g", "k_g2p"):
+        if k in prof:
+            t = prof[k]["ms_per_launch"] / 1e3
+            tr = traffic_for(k, a)
+            per_kernel[k] = {"mean_launch_ms": prof[k]["ms_per_launch"],
+                             "algorithmic_bytes_per_launch": kb[k], "frac": kb[k] / t / 1e9 / peak,
+                             "needed_bytes_per_launch": kneed[k], "frac_needed": kneed[k] / t / 1e9 / peak,
+                             "moved_bytes_per_launch": kmoved[k],
+                             "ncu_dram_bytes_per_launch": tr,
+                             "waste_ratio_ncu_over_algorithmic": (tr / kb[k]) if tr else None,
+                             "l2_hit_rate_pct_ncu": l2_hit_for(k, a)}
+    if "k_grid" in prof:
+        per_kernel["k_grid"] = {"mean_launch_ms": prof["k_grid"]["ms_per_launch"],
+                                "ncu_dram_bytes_per_launch": traffic_for("k_grid", a),
+                                "l2_hit_rate_pct_ncu": l2_hit_for("k_grid", a)}
 
     # ---- e2e through the C ABI with pinned host buffers (upload + K steps + download)
     e2e = None
@@ -483,14 +546,19 @@ def bench_b200(a, rank, world, local):
             alt = bench_fwd_adj(ctx, s, st, n, a.adj_steps, 2)
             fwd_adj["two_segments"] = {k: alt[k] for k in ("value", "ms_per_step", "forward_passes_per_step", "loss")}
         B_fa = vjp_bytes(s, n, active_nodes_step, B_fwd1, IN)
+        B_ex = vjp_bytes(s, n, active_nodes_step, B_fwd1, IN, fwd_adj["forward_passes_per_step"])
         gbs = n * B_fa / (fwd_adj["ms_per_step"] / 1e3) / 1e9
-        fwd_adj["roofline"] = {"bound": "hbm", "bytes_per_particle_step": B_fa, "achieved": gbs, "peak": peak,
-                               "unit": "GB/s", "frac": gbs / peak}
+        gbs_ex = n * B_ex / (fwd_adj["ms_per_step"] / 1e3) / 1e9
+        fwd_adj["roofline"] = {"bound": "hbm", "bytes_per_particle_step": B_ex, "achieved": gbs_ex, "peak": peak,
+                               "unit": "GB/s", "frac": gbs_ex / peak,
+                               "basis": "forward passes actually executed per step x B_fwd + B_vjp",
+                               "survey_formula": {"bytes_per_particle_step": B_fa, "frac": gbs / peak,
+                                                  "note": "2 B_fwd + B_vjp (one replay per step assumed)"}}
 
     ctx.close()
     workloads = None
     if world == 1 and a.config == "C4" and not a.no_workloads:
-        workloads = bench_workloads(peak, ["C2", "C3", "C5"])
+        workloads = bench_workloads(peak, ["C2", "C3", "C5"], cpu=not a.no_cpu_baseline)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -509,11 +577,17 @@ def bench_b200(a, rank, world, local):
                      "frac": achieved / peak, "traffic": traffic_for(dom, a),
                      "algorithmic_bytes_per_launch": kb[dom], "mean_launch_ms": dom_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
+                     "basis": "SURVEY 8(d) compulsory bytes of the kernel (x v m V sigma read, active nodes "
+                              "written once) / its mean event-timed launch; implementation bytes and the ncu "
+                              "DRAM count are in per_kernel",
+                     "per_kernel": per_kernel,
                      "step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak,
                               "bytes_per_particle_step": B_fwd,
                               "needed_bytes_per_particle_step": B_need,
-                              "note": "grad v (dead state for FLIP) is stored by the last step of each "
-                                      "advance() call only: DRAM traffic sits below SURVEY's figure"}},
+                              "frac_needed": n * B_need / (ms_per_step / 1e3) / 1e9 / peak,
+                              "note": "frac counts grad v stored every step (SURVEY's B_fwd); frac_needed counts "
+                                      "what the implementation must move (FLIP stores grad v on a call's last "
+                                      "step only)"}},
         "fp64": fp64_for(prof, a),
         "kernels": prof, "profiled_step_ms": total_ms / 3,
         "clocks": ck, "gpu_launches": launches, "e2e": e2e, "fwd_adj": fwd_adj,
@@ -714,6 +788,15 @@ def fp64_for(prof, a):
             out[k] = {"achieved": tf, "frac": tf / out["peak_tflops"], "flops_per_launch": ref[k]["fp64_flops"],
                       "fp64_pipe_active_pct_ncu": ref[k]["fp64_pipe_active_pct"]}
     return out
+
+
+def l2_hit_for(kernel, a):
+    """lts__t_sector_hit_rate.pct of `kernel` from the same ncu capture (profiles/traffic.json)."""
+    p = ROOT / "profiles" / "traffic.json"
+    if a.config != "C4" or a.dtype != "f64" or not p.exists():
+        return None
+    t = json.loads(p.read_text()).get(kernel)
+    return t.get("l2_hit_rate_pct") if t else None
 
 
 def traffic_for(kernel, a):

@@ -56,7 +56,7 @@ enum {
 enum { MPM_SCHEME_PIC = 0, MPM_SCHEME_FLIP = 1, MPM_SCHEME_BLEND = 2, MPM_SCHEME_APIC = 3, MPM_SCHEME_TPIC = 4 };
 /* config.hpp:34 WallKind, same order */
 enum { MPM_WALL_SLIP = 0, MPM_WALL_NO_SLIP = 1, MPM_WALL_FIXED = 2, MPM_WALL_COULOMB = 3 };
-/* material.hpp:97 Material variant index */
+/* material.hpp:106-107 Material variant index */
 enum { MPM_MAT_FLUID = 0, MPM_MAT_DRUCKER_PRAGER = 1 };
 
 /* Scene<T,dim> (scene.hpp:9-16) minus the init-only geometry. All reals are passed as
@@ -175,7 +175,7 @@ typedef struct mpm_backprop_result {
 
 /* advance flags */
 enum {
-    MPM_ADV_NAN_GUARD = 1u, /* run(): abort on non-finite state (stepper.hpp:519-522) */
+    MPM_ADV_NAN_GUARD = 1u, /* run(): abort on non-finite state (stepper.hpp:106-109) */
     MPM_ADV_STORE_GRID = 2u /* also keep the step's full grid (mass, momentum, force) so that
                                mpm_grid_download returns Stepper::grid as the reference has it */
 };
@@ -183,7 +183,7 @@ enum {
 typedef struct mpm_ctx mpm_ctx;
 
 /* ---- context ---------------------------------------------------------------------- */
-/* Stepper<T,dim>::Stepper(const Scene&) (stepper.hpp:66-70): validates the scene and
+/* Stepper<T,dim>::Stepper(const Scene&) (stepper.hpp:53-57): validates the scene and
  * allocates device state, grid blocks, sort and workspace buffers for up to max_particles. */
 int mpm_ctx_create(const mpm_scene_desc* scene, int64_t max_particles, int device, mpm_ctx** out);
 void mpm_ctx_destroy(mpm_ctx* ctx);
@@ -197,28 +197,28 @@ int mpm_device_name(char* buf, size_t len);
 int mpm_state_upload(mpm_ctx* ctx, const mpm_state_view* s);
 int mpm_state_download(mpm_ctx* ctx, mpm_state_view* s);
 /* order-independent 64-bit digest of the device state (replaces SimState::hash at the
- * checkpoint replay check, state.hpp:152-167 / checkpoint.hpp:124) */
+ * checkpoint replay check, state.hpp:71-86 / checkpoint.hpp:124) */
 int mpm_state_digest(mpm_ctx* ctx, uint64_t* out);
-/* max_particle_speed (stepper.hpp:491-498) */
+/* max_particle_speed (stepper.hpp:78-85) */
 int mpm_max_speed(mpm_ctx* ctx, double* vmax);
 
 /* ---- forward ------------------------------------------------------------------------ */
-/* n x Stepper::advance (stepper.hpp:472-482); MPM_ADV_NAN_GUARD adds run()'s all_finite
- * check after every step (stepper.hpp:519-522). */
+/* n x Stepper::advance (stepper.hpp:59-69); MPM_ADV_NAN_GUARD adds run()'s all_finite
+ * check after every step (stepper.hpp:106-109). */
 int mpm_advance(mpm_ctx* ctx, int64_t n_steps, uint32_t flags);
 /* mpm_advance with CUDA events recorded on the context stream around the n steps:
  * *device_ms = device time of the steps (bench / instrumentation) */
 int mpm_advance_timed(mpm_ctx* ctx, int64_t n_steps, uint32_t flags, double* device_ms);
 /* phase functions (each backs one reference free function, for per-phase parity):
- * p2g (transfer.hpp:402-434), grid_momentum_update (transfer.hpp:440-449),
- * apply_grid_corrections (contact.hpp:394-411), g2p (transfer.hpp:457-486),
- * constitutive_update (stepper.hpp:428-456). */
+ * p2g (transfer.hpp:37-69), grid_momentum_update (transfer.hpp:75-84),
+ * apply_grid_corrections (contact.hpp:228-245), g2p (transfer.hpp:92-121),
+ * constitutive_update (stepper.hpp:15-43). */
 int mpm_p2g(mpm_ctx* ctx);
 int mpm_grid_momentum_update(mpm_ctx* ctx);
 int mpm_grid_corrections(mpm_ctx* ctx);
 int mpm_g2p(mpm_ctx* ctx);
 int mpm_constitutive(mpm_ctx* ctx);
-/* Stepper::grid (stepper.hpp:464) as a dense host grid, and the reverse for tests that
+/* Stepper::grid (stepper.hpp:51) as a dense host grid, and the reverse for tests that
  * drive the phase functions on a prescribed grid (test_contact.cpp, test_transfer.cpp). */
 int mpm_grid_download(mpm_ctx* ctx, mpm_grid_view* g);
 int mpm_grid_upload(mpm_ctx* ctx, const mpm_grid_view* g);

@@ -6,9 +6,9 @@
 // (vectors [n][d], matrices column-major: exactly the ABI's host layout). Errors come back as the
 // reference's exception types (common.hpp:22-36).
 //
-//   mpm::gpu::Stepper<T,dim>          stepper.hpp:462-483   (Stepper::grid is a host mirror)
-//   mpm::gpu::run                     stepper.hpp:504-535
-//   mpm::gpu::constitutive_update     stepper.hpp:428-456
+//   mpm::gpu::Stepper<T,dim>          stepper.hpp:49-70   (Stepper::grid is a host mirror)
+//   mpm::gpu::run                     stepper.hpp:91-122
+//   mpm::gpu::constitutive_update     stepper.hpp:15-43
 //   mpm::gpu::step_vjp                adjoint.hpp:328-525
 //   mpm::gpu::backprop_trajectory     checkpoint.hpp:72-143 (built-in device seeder, or any
 //                                     duck-typed Seeder through a host-orchestrated sweep)
@@ -238,7 +238,7 @@ private:
 // ---- forward ---------------------------------------------------------------------------
 template <class T, int dim> struct Stepper {
     const Scene<T, dim>* scene;
-    Grid<T, dim> grid; // host mirror (the device grid is derived data, state.hpp:170-171)
+    Grid<T, dim> grid; // host mirror (the device grid is derived data, state.hpp:89-90)
 
     explicit Stepper(const Scene<T, dim>& s)
         : scene(&s)
@@ -283,7 +283,7 @@ template <class T, int dim> T max_particle_speed(const SimState<T, dim>& state)
     return vmax;
 }
 
-// run (stepper.hpp:504-535): CFL refusal, NaN guard every step, snapshots at the stride, the
+// run (stepper.hpp:91-122): CFL refusal, NaN guard every step, snapshots at the stride, the
 // observer after every step (which forces a per-step download of state and grid). Steps between
 // snapshots run as one device call.
 template <class T, int dim>
@@ -318,7 +318,7 @@ RunResult<T, dim> run(const Scene<T, dim>& scene, SimState<T, dim> state, Index 
         ctx.advance(chunk, true, bool(observer));
         done += chunk;
         const Index cur = step0 + done;
-        const bool snap = stride > 0 && cur % stride == 0 && cur != num_steps; // stepper.hpp:525
+        const bool snap = stride > 0 && cur % stride == 0 && cur != num_steps; // stepper.hpp:112
         if (observer || snap)
             ctx.download(state);
         if (observer) {
@@ -335,7 +335,7 @@ RunResult<T, dim> run(const Scene<T, dim>& scene, SimState<T, dim> state, Index 
     return result;
 }
 
-// constitutive_update (stepper.hpp:428-456) on the device
+// constitutive_update (stepper.hpp:15-43) on the device
 template <class T, int dim> void constitutive_update(ParticleSoA<T, dim>& prt, const Material<T>& material, T dt)
 {
     Scene<T, dim> s;

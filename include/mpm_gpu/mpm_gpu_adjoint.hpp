@@ -7,6 +7,9 @@
 
 #include <mpm/checkpoint.hpp>
 
+#include <memory>
+#include <vector>
+
 namespace mpm {
 namespace gpu {
 
@@ -30,13 +33,49 @@ template <class T, int dim> void pg_back(ParamGrads<T, dim>& g, const mpm_param_
             g.wall_friction[w][k] = T(tmp[w][k]);
 }
 
-// step_vjp: cot_in is overwritten, pg accumulated (adjoint.hpp:371, :145, :172)
-template <class T, int dim>
-void step_vjp(const Scene<T, dim>& scene, const SimState<T, dim>& input, const StateCotangent<T, dim>& cot_out,
-              StateCotangent<T, dim>& cot_in, ParamGrads<T, dim>& pg, AdjointWorkspace<T, dim>& ws)
+namespace detail {
+// The scene's content as bytes (scalars + friction + obstacles): the key of the cached context.
+template <class T, int dim> std::vector<unsigned char> scene_key(const SceneDesc<T, dim>& sd)
 {
-    (void)ws;
-    Context<T, dim> ctx(scene, input.particles.size());
+    mpm_scene_desc d = sd.d;
+    for (auto& f : d.friction)
+        f = nullptr;
+    d.obstacles = nullptr;
+    std::vector<unsigned char> k(reinterpret_cast<const unsigned char*>(&d),
+                                 reinterpret_cast<const unsigned char*>(&d) + sizeof(d));
+    auto put = [&](const double* p, std::size_t n) {
+        k.insert(k.end(), reinterpret_cast<const unsigned char*>(p), reinterpret_cast<const unsigned char*>(p + n));
+    };
+    for (int w = 0; w < 2 * dim; ++w)
+        put(sd.fr[w].data(), sd.fr[w].size());
+    put(sd.ob.data(), sd.ob.size());
+    return k;
+}
+
+// step_vjp's device context. The reference's AdjointWorkspace (adjoint.hpp:298-322) is its
+// scratch; its layout is fixed by the reference headers, so the device context lives beside it,
+// one per host thread, reused while the scene is the same and the particle count fits.
+template <class T, int dim> Context<T, dim>& vjp_context(const Scene<T, dim>& scene, Index n)
+{
+    struct Cache {
+        std::unique_ptr<Context<T, dim>> ctx;
+        std::vector<unsigned char> key;
+    };
+    thread_local Cache c;
+    SceneDesc<T, dim> sd(scene);
+    std::vector<unsigned char> key = scene_key(sd);
+    if (!c.ctx || c.key != key || c.ctx->capacity() < n) {
+        c.ctx.reset();
+        c.ctx = std::make_unique<Context<T, dim>>(scene, std::max<Index>(n, 1));
+        c.key = std::move(key);
+    }
+    return *c.ctx;
+}
+
+template <class T, int dim>
+void step_vjp_on(Context<T, dim>& ctx, const SimState<T, dim>& input, const StateCotangent<T, dim>& cot_out,
+                 StateCotangent<T, dim>& cot_in, ParamGrads<T, dim>& pg)
+{
     SimState<T, dim> s = input;
     auto sv = state_view(s);
     StateCotangent<T, dim> co = cot_out;
@@ -47,6 +86,17 @@ void step_vjp(const Scene<T, dim>& scene, const SimState<T, dim>& input, const S
     auto pv = pg_view(pg, tmp);
     ctx.check(mpm_step_vjp(ctx.handle(), &sv, &cov, &civ, &pv));
     pg_back(pg, pv, tmp);
+}
+} // namespace detail
+
+// step_vjp: cot_in is overwritten, pg accumulated (adjoint.hpp:371, :145, :172). The device
+// context is cached per thread (detail::vjp_context): no allocation per call in a reverse loop.
+template <class T, int dim>
+void step_vjp(const Scene<T, dim>& scene, const SimState<T, dim>& input, const StateCotangent<T, dim>& cot_out,
+              StateCotangent<T, dim>& cot_in, ParamGrads<T, dim>& pg, AdjointWorkspace<T, dim>& ws)
+{
+    (void)ws;
+    detail::step_vjp_on(detail::vjp_context(scene, input.particles.size()), input, cot_out, cot_in, pg);
 }
 
 // backprop_trajectory with any duck-typed Seeder (observes / loss_at / seed, checkpoint.hpp:63-66):
@@ -105,7 +155,8 @@ BackpropResult<T, dim> backprop_trajectory(const Scene<T, dim>& scene, const Sim
         for (Index t = b1; t > b0; --t) {
             if (seeder.observes(t))
                 seeder.seed(t, replay[t - b0], cot);
-            gpu::step_vjp(scene, replay[t - b0 - 1], cot, cot_prev, result.param_grads, ws);
+            (void)ws;
+            detail::step_vjp_on(ctx, replay[t - b0 - 1], cot, cot_prev, result.param_grads); // trajectory's context
             std::swap(cot, cot_prev);
         }
     }

@@ -23,7 +23,8 @@ from paper_2507_04192_b200.errors import raise_for
 from paper_2507_04192_b200.state import Grid, ParamGrads, SimState, StateCotangent
 
 HERE = Path(__file__).resolve().parent
-LIBS = {"orc": HERE / "_build" / "liboracle.so", "ref": HERE / "_ref" / "libmpm_ref.so"}
+LIBS = {"orc": HERE / "_build" / "liboracle.so", "ref": HERE / "_ref" / "libmpm_ref.so",
+        "ref_v3": HERE / "_ref" / "libmpm_ref_v3.so"}  # the reference at -march=x86-64-v3
 
 
 class OrcRegion(C.Structure):
@@ -81,7 +82,7 @@ class CpuOracle:
             raise RuntimeError(f"oracle library {LIBS[kind]} missing; run `make -C oracle`")
         self.kind = kind
         lib = C.CDLL(str(LIBS[kind]))
-        P = kind + "_"
+        P = "ref_" if kind.startswith("ref") else "orc_"
         sig = {
             "last_error": (C.c_int, [C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]),
             "dp_make": (C.c_int, [C.POINTER(capi.SceneDesc)] + [C.c_double] * 7),

@@ -197,7 +197,7 @@ template <class T, int D> struct Scene {
             n *= nodes(a);
         return n;
     }
-    // Grid::node_index (state.hpp:208-214): row-major, last axis fastest
+    // Grid::node_index (state.hpp:127-133): row-major, last axis fastest
     int64_t node_index(const int* idx) const
     {
         int64_t r = 0;
@@ -205,7 +205,7 @@ template <class T, int D> struct Scene {
             r = r * nodes(a) + idx[a];
         return r;
     }
-    // Grid::node_multi_index (state.hpp:216-225)
+    // Grid::node_multi_index (state.hpp:135-144)
     void node_multi(int64_t f, int* idx) const
     {
         for (int a = D - 1; a >= 0; --a) {
@@ -213,7 +213,7 @@ template <class T, int D> struct Scene {
             f /= nodes(a);
         }
     }
-    // Grid::node_position (state.hpp:227-233)
+    // Grid::node_position (state.hpp:146-152)
     Vec<T, D> node_pos(const int* idx) const
     {
         Vec<T, D> p;
@@ -266,7 +266,7 @@ template <class T, int D> Scene<T, D> decode(const mpm_scene_desc* d)
 }
 
 // ---------------------------------------------------------------------------------------
-// particle state (state.hpp:98-168) in the restatement's own layout
+// particle state (state.hpp:17-87) in the restatement's own layout
 template <class T, int D> struct State {
     int64_t n = 0;
     std::vector<Vec<T, D>> x, v;
@@ -408,7 +408,7 @@ template <class T, int D> void store_grid(const Scene<T, D>& sc, const Grid<T, D
 }
 
 // ---------------------------------------------------------------------------------------
-// quadratic B-spline stencil: shape_and_grad (bspline.hpp:312-344)
+// quadratic B-spline stencil: shape_and_grad (bspline.hpp:76-108)
 template <class T, int D> struct Stencil {
     int base[D];
     T w[D][3], dw[D][3], ddw[D][3];
@@ -421,7 +421,7 @@ template <class T, int D> Stencil<T, D> stencil(const Scene<T, D>& sc, const Vec
     for (int a = 0; a < D; ++a) {
         T u = (x.a[a] - sc.origin[a]) * inv_dh;
         T fl = std::floor(u - T(0.5));
-        // bspline.hpp:322-327; a non-finite coordinate is out of domain (the reference's
+        // bspline.hpp:86-91; a non-finite coordinate is out of domain (the reference's
         // int cast of NaN/inf is undefined; on x86 it yields INT_MIN < 0 -> throws)
         if (!(fl >= T(0)) || fl + T(2) > T(sc.cells[a]))
             throw Err(MPM_ERR_OUT_OF_DOMAIN,
@@ -445,7 +445,7 @@ template <class T, int D> Stencil<T, D> stencil(const Scene<T, D>& sc, const Vec
     return st;
 }
 
-// canonical offset order: row-major over {0,1,2}^D (bspline.hpp:346-363)
+// canonical offset order: row-major over {0,1,2}^D (bspline.hpp:110-127)
 template <int D> void offset_of(int k, int* o)
 {
     for (int a = D - 1; a >= 0; --a) {
@@ -455,7 +455,7 @@ template <int D> void offset_of(int k, int* o)
 }
 template <int D> constexpr int n_off() { return D == 2 ? 9 : 27; }
 
-// Stencil::weight / Stencil::grad (bspline.hpp:286-306)
+// Stencil::weight / Stencil::grad (bspline.hpp:50-70)
 template <class T, int D> T weight(const Stencil<T, D>& st, const int* o)
 {
     T r = T(1);
@@ -502,7 +502,7 @@ template <class T, int D> Vec<T, D> node_rel(const Scene<T, D>& sc, const Stenci
     return r;
 }
 
-// APIC moment matrix D = sum phi r r^T recomputed from the stencil (transfer.hpp:388-396)
+// APIC moment matrix D = sum phi r r^T recomputed from the stencil (transfer.hpp:23-31)
 template <class T, int D> Mat<T, D> apic_D(const Scene<T, D>& sc, const Stencil<T, D>& st, const Vec<T, D>& xp)
 {
     Mat<T, D> Dm = mzero<T, D>();
@@ -519,13 +519,13 @@ template <class T, int D> Mat<T, D> apic_D(const Scene<T, D>& sc, const Stencil<
 }
 
 // ---------------------------------------------------------------------------------------
-// P2G (transfer.hpp:402-434): reset, then particles in index order, offsets canonical.
+// P2G (transfer.hpp:37-69): reset, then particles in index order, offsets canonical.
 template <class T, int D> void p2g(const Scene<T, D>& sc, const State<T, D>& s, Grid<T, D>& g)
 {
     g.reset(sc.num_nodes());
     for (int64_t p = 0; p < s.n; ++p) {
         Stencil<T, D> st = stencil(sc, s.x[p], p);
-        // p2g_affine_matrix (transfer.hpp:379-397)
+        // p2g_affine_matrix (transfer.hpp:14-32)
         Mat<T, D> A = mzero<T, D>();
         bool affine = sc.apic() || sc.tpic();
         if (sc.tpic())
@@ -557,7 +557,7 @@ template <class T, int D> void p2g(const Scene<T, D>& sc, const State<T, D>& s, 
     }
 }
 
-// grid_momentum_update (transfer.hpp:440-449)
+// grid_momentum_update (transfer.hpp:75-84)
 template <class T, int D> void momentum_update(const Scene<T, D>& sc, Grid<T, D>& g)
 {
     for (int64_t i = 0; i < (int64_t)g.m.size(); ++i) {
@@ -582,20 +582,20 @@ template <class T, int D> struct Corr {
     int wall, seg;
 };
 
-// node_in_wall_band (contact.hpp:183-190)
+// node_in_wall_band (contact.hpp:17-24)
 template <class T, int D> bool in_band(const Scene<T, D>& sc, const int* idx, int w)
 {
     int a = w / 2;
     return w % 2 == 0 ? idx[a] < sc.band : idx[a] > sc.cells[a] - sc.band;
 }
-// coulomb_segment_index (contact.hpp:234-240)
+// coulomb_segment_index (contact.hpp:68-74)
 template <class T> int segment_index(T coord, T lo, T extent, int n)
 {
     T len = extent / T(n);
     int k = int(std::ceil(double((coord - lo) / len))) - 1;
     return std::clamp(k, 0, n - 1);
 }
-// collect_node_corrections (contact.hpp:307-352): walls, obstacles, Coulomb walls
+// collect_node_corrections (contact.hpp:141-186): walls, obstacles, Coulomb walls
 template <class T, int D> void collect(const Scene<T, D>& sc, const int* idx, std::vector<Corr<T, D>>& out)
 {
     out.clear();
@@ -648,14 +648,14 @@ template <class T, int D> void collect(const Scene<T, D>& sc, const int* idx, st
         Corr<T, D> c{};
         c.kind = C_COUL;
         c.n = vzero<T, D>();
-        c.n.a[w / 2] = w % 2 == 0 ? T(-1) : T(1); // wall_contact_normal (contact.hpp:194-200)
+        c.n.a[w / 2] = w % 2 == 0 ? T(-1) : T(1); // wall_contact_normal (contact.hpp:28-34)
         c.mu = sc.friction[w][k];
         c.wall = w;
         c.seg = k;
         out.push_back(c);
     }
 }
-// apply_node_correction (contact.hpp:354-390)
+// apply_node_correction (contact.hpp:188-224)
 template <class T, int D> Vec<T, D> apply_corr(const Corr<T, D>& c, const Vec<T, D>& v)
 {
     switch (c.kind) {
@@ -694,7 +694,7 @@ template <class T, int D> Vec<T, D> apply_corr(const Corr<T, D>& c, const Vec<T,
     }
     }
 }
-// apply_grid_corrections (contact.hpp:394-411): every node, fixed order
+// apply_grid_corrections (contact.hpp:228-245): every node, fixed order
 template <class T, int D> void corrections(const Scene<T, D>& sc, Grid<T, D>& g)
 {
     std::vector<Corr<T, D>> list;
@@ -708,7 +708,7 @@ template <class T, int D> void corrections(const Scene<T, D>& sc, Grid<T, D>& g)
 }
 
 // ---------------------------------------------------------------------------------------
-// G2P (transfer.hpp:457-486)
+// G2P (transfer.hpp:92-121)
 template <class T, int D> void g2p(const Scene<T, D>& sc, const Grid<T, D>& g, State<T, D>& s)
 {
     T alpha = sc.flip_fraction();
@@ -874,7 +874,7 @@ template <class T, int D> T dp_update(const Scene<T, D>& sc, Mat<T, D>& sig, T& 
     return den;
 }
 
-// constitutive_update (stepper.hpp:428-456)
+// constitutive_update (stepper.hpp:15-43)
 template <class T, int D> void constitutive(const Scene<T, D>& sc, State<T, D>& s)
 {
     if (sc.material == MPM_MAT_FLUID) {
@@ -926,7 +926,7 @@ template <class T, int D> void constitutive(const Scene<T, D>& sc, State<T, D>& 
         }
 }
 
-// Stepper::advance (stepper.hpp:472-482)
+// Stepper::advance (stepper.hpp:59-69)
 template <class T, int D> void advance(const Scene<T, D>& sc, State<T, D>& s)
 {
     Grid<T, D> g;
@@ -939,7 +939,7 @@ template <class T, int D> void advance(const Scene<T, D>& sc, State<T, D>& s)
     s.time = double(T(s.step) * sc.dt);
 }
 
-// ParticleSoA::all_finite (state.hpp:129-143)
+// ParticleSoA::all_finite (state.hpp:48-62)
 template <class T, int D> bool all_finite(const State<T, D>& s)
 {
     auto fv = [](const auto& vec) {
@@ -1432,7 +1432,7 @@ template <class T, int D> void step_vjp(const Scene<T, D>& sc, const State<T, D>
 }
 
 // ---------------------------------------------------------------------------------------
-// FNV-1a state hash (common.hpp:40-57, hash.cpp:5-13, state.hpp:152-167). Hashes the
+// FNV-1a state hash (common.hpp:40-57, hash.cpp:5-13, state.hpp:71-86). Hashes the
 // reference's in-memory layout (vectors AoS, matrices column-major).
 inline uint64_t fnv(const void* data, size_t n, uint64_t h)
 {
@@ -1953,7 +1953,7 @@ int orc_last_error(int64_t* particle, char* msg, size_t len)
     return 0;
 }
 
-// DruckerPragerParams::make + dp_derived_params (material.hpp:292-339)
+// DruckerPragerParams::make + dp_derived_params (material.hpp:37-84)
 int orc_dp_make(mpm_scene_desc* d, double rho0, double K, double nu, double phi, double psi, double cohesion,
                 double sigma_t)
 {
@@ -1972,7 +1972,7 @@ int orc_dp_make(mpm_scene_desc* d, double rho0, double K, double nu, double phi,
     d->q_psi = 6.0 * std::sin(psi) / (s3 * (3.0 + std::sin(psi)));
     d->tau_P = d->k_phi - d->q_phi * sigma_t;
     d->alpha_P = std::sqrt(1.0 + d->q_phi * d->q_phi) - d->q_phi;
-    // validate (material.hpp:341-359)
+    // validate (material.hpp:86-104)
     if (!(rho0 > 0) || !(K > 0) || !(nu >= 0 && nu < 0.5) || !(d->G > 0) || !(phi >= 0 && phi < 1.5707963267948966)
         || !(psi >= 0 && psi <= phi) || cohesion < 0 || sigma_t < 0
         || (d->q_phi > 0 && sigma_t > d->k_phi / d->q_phi)) {

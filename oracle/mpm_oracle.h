@@ -45,7 +45,7 @@ typedef struct orc_region {
     int64_t P##_init_scene_count(const mpm_scene_desc* d, const orc_region* r, int nreg);            \
     int P##_init_scene(const mpm_scene_desc* d, const orc_region* r, int nreg, mpm_state_view* out,  \
                        double* mass_epsilon);                                                        \
-    /* n x Stepper::advance (stepper.hpp:472-482), optional run() NaN guard */                       \
+    /* n x Stepper::advance (stepper.hpp:59-69), optional run() NaN guard */                       \
     int P##_advance(const mpm_scene_desc* d, mpm_state_view* s, int64_t n, int nan_guard);           \
     int P##_p2g(const mpm_scene_desc* d, const mpm_state_view* s, mpm_grid_view* g);                 \
     int P##_grid_momentum_update(const mpm_scene_desc* d, mpm_grid_view* g);                         \
@@ -57,9 +57,9 @@ typedef struct orc_region {
     int P##_backprop(const mpm_scene_desc* d, const mpm_state_view* s0, int64_t total_steps,         \
                      int n_segments, const mpm_seeder_desc* seeder, mpm_cot_view* cot0,              \
                      mpm_param_grads* pg, mpm_backprop_result* res);                                 \
-    /* SimState::hash (state.hpp:152-167) */                                                         \
+    /* SimState::hash (state.hpp:71-86) */                                                         \
     uint64_t P##_state_hash(const mpm_scene_desc* d, const mpm_state_view* s);                       \
-    /* run(...).seconds_per_1000_steps (stepper.hpp:504-535), state advanced in place */             \
+    /* run(...).seconds_per_1000_steps (stepper.hpp:91-122), state advanced in place */             \
     double P##_run_seconds_per_1000(const mpm_scene_desc* d, mpm_state_view* s, int64_t n);
 
 MPM_ORACLE_DECLARE(orc)

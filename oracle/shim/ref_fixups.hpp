@@ -7,8 +7,8 @@
 //   contact.hpp:142  collect_node_corrections  (called at contact.hpp:238, the correction
 //                    pipeline used by Stepper::advance and step_vjp)
 //   adjoint.hpp:96   detail::stencil_hessian    (called at adjoint.hpp:423 and :500)
-// Their sibling helpers avoid this with std::type_identity_t (contact.hpp:184,
-// bspline.hpp:313-315); these two do not.
+// Their sibling helpers avoid this with std::type_identity_t (contact.hpp:18,
+// bspline.hpp:77-79); these two do not.
 //
 // Without touching the reference sources we declare NON-template forwarding overloads for
 // the instantiations the oracle uses. Non-templates win over the non-viable templates;

@@ -206,7 +206,7 @@ template <> __device__ __forceinline__ float dsqrt<float>(float x) { return sqrt
 
 template <class T> __device__ __forceinline__ bool finite_(T x) { return isfinite(x); }
 
-// quadratic B-spline weights along one axis (bspline.hpp:312-344): base = floor(u - 1/2),
+// quadratic B-spline weights along one axis (bspline.hpp:76-108): base = floor(u - 1/2),
 // fx = u - base in [1/2, 3/2); returns false when out of the valid interior.
 template <class T> struct Axis {
     int base;

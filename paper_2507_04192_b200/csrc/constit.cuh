@@ -2,7 +2,7 @@
 //
 // fluid_stress_update  constitutive.hpp:32-50
 // dp_stress_update     constitutive.hpp:101-164 (2-D runs on the plane-strain 3x3 embedding)
-// constitutive_update  stepper.hpp:428-456 (volume / density / eps / F bookkeeping)
+// constitutive_update  stepper.hpp:15-43 (volume / density / eps / F bookkeeping)
 #pragma once
 
 #include "common.cuh"
@@ -157,7 +157,7 @@ __device__ __forceinline__ bool constitutive_particle(const DevScene<T, D>& sc, 
                                                       T& eps, const T* L)
 {
     using C = Cfg<D>;
-    if (sc.material == 0) { // fluid (constitutive.hpp:32-50, stepper.hpp:431-438)
+    if (sc.material == 0) { // fluid (constitutive.hpp:32-50, stepper.hpp:18-25)
         T dd[D][D];
         T trd = T(0);
 #pragma unroll
@@ -186,7 +186,7 @@ __device__ __forceinline__ bool constitutive_particle(const DevScene<T, D>& sc, 
         V *= den;
         return true;
     }
-    // Drucker-Prager (stepper.hpp:440-450)
+    // Drucker-Prager (stepper.hpp:27-37)
     T S[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)

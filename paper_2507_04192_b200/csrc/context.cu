@@ -1,7 +1,7 @@
 // context.cu -- host runtime of libmpm_b200.so: device context, buffer ownership, step
 // orchestration (CUDA graph per step), error attribution and the C ABI (include/mpm_capi.h).
 //
-// The context is the device-side Stepper (stepper.hpp:462-483): it owns the particle state
+// The context is the device-side Stepper (stepper.hpp:49-70): it owns the particle state
 // (double-buffered SoA), the node-block grid, the sort / segment tables, the P2G partial tiles
 // and the adjoint workspace, all on one CUDA stream. Calls are synchronous at return.
 
@@ -10,6 +10,7 @@
 #include "constit.cuh"
 #include "kernels_adj.cuh"
 #include "kernels_fwd.cuh"
+#include "kernels_sort.cuh"
 #include "kernels_util.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -148,6 +149,20 @@ template <class T, int D> struct Ctx : CtxBase {
     PBuf<T, D> buf[2]{};
     int cur = 0;
     int *keys = nullptr, *keys_sorted = nullptr, *perm = nullptr, *iota = nullptr;
+    // K1 incremental sort (kernels_sort.cuh). The context's own sort arrays alternate with the
+    // buffer parity (sorted keys and block ranges of step t are read while step t+1 writes the
+    // other pair); the replay tape's sort sets are distinct arrays anyway.
+    int *ks_own[2] = {}, *bs_own[2] = {}, *be_own[2] = {};
+    bool own_set = true;
+    IncSort inc{};
+    // the order a particle buffer is stored in: base of the buffer the last G2P wrote and the
+    // sort arrays of that step. Valid until the buffer's content changes any other way.
+    struct IncSrc {
+        const T* base;
+        const int *ks, *bs, *be;
+    } inc_src{};
+    bool inc_enabled = !(std::getenv("MPM_SORT") && std::string(std::getenv("MPM_SORT")) == "cub");
+    void inc_invalidate() { inc_src = IncSrc{}; }
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
     int *bstart = nullptr, *bend = nullptr, *lstart = nullptr, *occ = nullptr, *act = nullptr, *counts = nullptr; // counts[0]=n_occ, [1]=n_act
@@ -181,7 +196,10 @@ template <class T, int D> struct Ctx : CtxBase {
     int* d_cells = nullptr;
     int mig_cnt[2] = {0, 0};
 
+    IncSrc captured_inc_src{};
     cudaGraphExec_t graphs[2][2][2] = {}; // [guard][stores grad v][cur]
+    IncSrc graph_inc[2][2][2] = {};       // the stored-order record a replay of each graph leaves
+    int64_t graph_n[2][2][2] = {};        // particle count each forward graph was captured with
     // slab phases: P2G phase [cur] (valid for slab_g1_n[cur] particles), finish phase [guard][cur]
     cudaGraphExec_t slab_g1[2] = {nullptr, nullptr};
     int64_t slab_g1_n[2] = {-1, -1};
@@ -210,10 +228,37 @@ template <class T, int D> struct Ctx : CtxBase {
         const int cur0 = cur;
         const bool kv0 = keys_valid;
         const int64_t l0 = launches;
-        cudaGraph_t g;
+        const IncSrc inc0 = inc_src;
+        const bool own0 = own_set;
+        int* const ptr0[3] = {keys_sorted, bstart, bend};
+        auto restore = [&] {
+            launches = l0;
+            cur = cur0;
+            keys_valid = kv0;
+            inc_src = inc0;
+            own_set = own0;
+            keys_sorted = ptr0[0];
+            bstart = ptr0[1];
+            bend = ptr0[2];
+        };
+        cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-        f();
+        try {
+            f();
+        } catch (...) { // leave the stream out of capture mode and the context state as it was
+            cudaStreamEndCapture(stream, &g);
+            if (g)
+                cudaGraphDestroy(g);
+            (void)cudaGetLastError();
+            restore();
+            throw;
+        }
         CK(cudaStreamEndCapture(stream, &g));
+        captured_inc_src = inc_src; // what replaying the graph leaves behind
+        struct GraphGuard {
+            cudaGraph_t g;
+            ~GraphGuard() { cudaGraphDestroy(g); }
+        } guard_g{g};
         // an existing executable graph of the same phase (the slab P2G phase after the particle
         // count changed) is updated in place: same topology, new launch dimensions. A topology or
         // node-type change (cub's tile count moving a memset's size, say) falls back to instantiation.
@@ -227,13 +272,16 @@ template <class T, int D> struct Ctx : CtxBase {
                 out = nullptr;
             }
         }
-        if (!updated)
-            CK(cudaGraphInstantiate(&out, g, 0));
-        CK(cudaGraphDestroy(g));
+        if (!updated) {
+            const cudaError_t ie = cudaGraphInstantiate(&out, g, 0);
+            if (ie != cudaSuccess) {
+                out = nullptr;
+                restore();
+                CK(ie);
+            }
+        }
         const int64_t k = launches - l0;
-        launches = l0;
-        cur = cur0;
-        keys_valid = kv0;
+        restore();
         return k;
     }
 
@@ -263,18 +311,33 @@ template <class T, int D> struct Ctx : CtxBase {
         for (int b = 0; b < 2; ++b)
             alloc_pbuf(buf[b]);
         keys = alloc<int>(cap);
-        keys_sorted = alloc<int>(cap);
+        for (int k = 0; k < 2; ++k) {
+            ks_own[k] = alloc<int>(cap);
+            bs_own[k] = alloc<int>(sc.nb_total);
+            be_own[k] = alloc<int>(sc.nb_total);
+        }
+        keys_sorted = ks_own[0];
+        inc.cnt_in = alloc<int>(sc.nb_total);
+        inc.cnt_out = alloc<int>(sc.nb_total);
+        inc.in_off = alloc<int>(sc.nb_total);
+        inc.xlist = alloc<int>(cap);
+        inc.inbuf = alloc<int>(cap);
+        inc.nx = alloc<int>(1);
+        CK(cudaMemsetAsync(inc.cnt_in, 0, sizeof(int) * sc.nb_total, stream));
+        CK(cudaMemsetAsync(inc.cnt_out, 0, sizeof(int) * sc.nb_total, stream));
+        CK(cudaMemsetAsync(inc.nx, 0, sizeof(int), stream));
         perm = alloc<int>(cap);
         iota = alloc<int>(cap);
         k_iota<<<unsigned((cap + 255) / 256), 256, 0, stream>>>(iota, int(cap));
         CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, keys, keys_sorted, iota, perm, int(cap), 0, 32, stream));
         cub_tmp = alloc<unsigned char>(cub_bytes);
-        bstart = alloc<int>(sc.nb_total);
-        bend = alloc<int>(sc.nb_total);
+        bstart = bs_own[0];
+        bend = be_own[0];
         lstart = alloc<int>((size_t)sc.nb_total * (C::B + 1));
         occ = alloc<int>(sc.nb_total);
         act = alloc<int>(sc.nnb_total);
         counts = alloc<int>(4);
+        CK(cudaMemsetAsync(counts, 0, sizeof(int) * 4, stream));
         wq = alloc<int>(WQ_INTS);
         CK(cudaMemsetAsync(wq, 0, sizeof(int) * WQ_INTS, stream));
         nflag = alloc<unsigned char>(sc.nnb_total);
@@ -557,30 +620,60 @@ template <class T, int D> struct Ctx : CtxBase {
     // ---- sort + segment tables ---------------------------------------------------------------
     void sort_and_segment()
     {
+        if (own_set) { // the pair the previous step did not write (slab steps: never incremental, pair 0)
+            const int k = slab ? 0 : cur;
+            keys_sorted = ks_own[k];
+            bstart = bs_own[k];
+            bend = be_own[k];
+        }
         if (!keys_valid) {
             launch("k_keys", [&] { k_keys<T, D><<<grid_for(n, 256), 256, 0, stream>>>(sc, buf[cur], int(n), keys, st); });
             keys_valid = true;
         }
-        // radix-sort only the bits a valid key can have (C4: 24 bits -> 3 onesweep passes). An
-        // out-of-domain particle's sentinel key aliases in those bits, but such a step is aborted.
-        int end_bit = 1;
-        const int64_t need = (int64_t(sc.nb_total) << C::LOGNB) + (slab ? 2 : 0); // dead keys sort last
-        while ((int64_t(1) << end_bit) < need)
-            ++end_bit;
-        size_t bytes = cub_bytes;
-        CK(cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys, keys_sorted, iota, perm, int(n), 0, end_bit, stream));
-        CK(cudaMemsetAsync(bstart, 0xff, sizeof(int) * sc.nb_total, stream));
-        CK(cudaMemsetAsync(bend, 0xff, sizeof(int) * sc.nb_total, stream));
-        CK(cudaMemsetAsync(lstart, 0xff, sizeof(int) * sc.nb_total * (C::B + 1), stream));
-        CK(cudaMemsetAsync(counts, 0, sizeof(int) * 4, stream));
-        CK(cudaMemsetAsync(nflag, 0, sc.nnb_total, stream));
-        launch("k_seg", [&] { k_seg4<D><<<grid_for((n + 3) / 4, 256), 256, 0, stream>>>(keys_sorted, int(n), sc.nb_total, bstart, bend, lstart); });
-        if (occ_lpt && D == 3) { // heaviest blocks first (kernels_util.cuh)
-            CK(cudaMemsetAsync(wq, 0, sizeof(int) * WQ_CTR, stream));
-            launch("k_occ", [&] { k_occ_hist<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, bend, sc.nb_total, wq); });
-            launch("k_occ", [&] { k_occ_scatter<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, bend, sc.nb_total, wq, occ, counts); });
+        // K1: the stored order is the previous step's sort -> rebuild it incrementally
+        const bool inc_ok = inc_enabled && !slab && n > 0 && inc_src.base == buf[cur].base && inc_src.ks &&
+                            inc_src.ks != keys_sorted && inc_src.bs != bstart && inc_src.be != bend;
+        if (inc_ok) {
+            const IncSrc o = inc_src;
+            CK(cudaMemsetAsync(counts, 0, sizeof(int) * 4, stream));
+            CK(cudaMemsetAsync(nflag, 0, sc.nnb_total, stream));
+            launch("k_sort_classify", [&] {
+                k_inc_classify<D><<<grid_for(n, 256), 256, 0, stream>>>(keys, o.ks, int(n), sc.nb_total, inc);
+            });
+            const bool lpt = occ_lpt && D == 3;
+            launch("k_sort_scan", [&] {
+                if (lpt)
+                    k_inc_scan<D, true><<<1, 1024, 0, stream>>>(sc.nb_total, o.bs, o.be, inc, bstart, bend, occ, counts);
+                else
+                    k_inc_scan<D, false><<<1, 1024, 0, stream>>>(sc.nb_total, o.bs, o.be, inc, bstart, bend, occ, counts);
+            });
+            launch("k_sort_place", [&] { k_inc_place<D><<<nsm, 256, 0, stream>>>(keys, inc, nsm * 256); });
+            launch("k_sort_block", [&] {
+                k_inc_block<D><<<persistent(8), INC_THREADS, 0, stream>>>(keys, o.bs, o.be, inc, bstart, bend, occ,
+                                                                          counts, perm, keys_sorted, lstart);
+            });
         } else {
-            launch("k_compact", [&] { k_compact_pos<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, sc.nb_total, occ, counts); });
+            // radix-sort only the bits a valid key can have (C4: 24 bits -> 3 onesweep passes). An
+            // out-of-domain particle's sentinel key aliases in those bits, but such a step is aborted.
+            int end_bit = 1;
+            const int64_t need = (int64_t(sc.nb_total) << C::LOGNB) + (slab ? 2 : 0); // dead keys sort last
+            while ((int64_t(1) << end_bit) < need)
+                ++end_bit;
+            size_t bytes = cub_bytes;
+            CK(cub::DeviceRadixSort::SortPairs(cub_tmp, bytes, keys, keys_sorted, iota, perm, int(n), 0, end_bit, stream));
+            CK(cudaMemsetAsync(bstart, 0xff, sizeof(int) * sc.nb_total, stream));
+            CK(cudaMemsetAsync(bend, 0xff, sizeof(int) * sc.nb_total, stream));
+            CK(cudaMemsetAsync(lstart, 0xff, sizeof(int) * sc.nb_total * (C::B + 1), stream));
+            CK(cudaMemsetAsync(counts, 0, sizeof(int) * 4, stream));
+            CK(cudaMemsetAsync(nflag, 0, sc.nnb_total, stream));
+            launch("k_seg", [&] { k_seg4<D><<<grid_for((n + 3) / 4, 256), 256, 0, stream>>>(keys_sorted, int(n), sc.nb_total, bstart, bend, lstart); });
+            if (occ_lpt && D == 3) { // heaviest blocks first (kernels_util.cuh)
+                CK(cudaMemsetAsync(wq, 0, sizeof(int) * WQ_CTR, stream));
+                launch("k_occ", [&] { k_occ_hist<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, bend, sc.nb_total, wq); });
+                launch("k_occ", [&] { k_occ_scatter<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, bend, sc.nb_total, wq, occ, counts); });
+            } else {
+                launch("k_compact", [&] { k_compact_pos<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, sc.nb_total, occ, counts); });
+            }
         }
         launch("k_mark_nodes", [&] { k_mark_nodes<D><<<grid_for(sc.nb_total, 128), 128, 0, stream>>>(occ, counts, d_nb, d_nnb, nflag); });
         launch("k_compact", [&] { k_compact_flag<<<grid_for(sc.nnb_total, 256), 256, 0, stream>>>(nflag, sc.nnb_total, act, counts + 1); });
@@ -661,6 +754,7 @@ template <class T, int D> struct Ctx : CtxBase {
 #endif
             launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig, wq_ptr(WQ_G2P)); });
         }
+        inc_src = slab ? IncSrc{} : IncSrc{Pout.base, keys_sorted, bstart, bend};
         cur ^= 1;
         keys_valid = true;
     }
@@ -702,18 +796,19 @@ template <class T, int D> struct Ctx : CtxBase {
         if (!s.abort)
             return;
         reset_status();
+        inc_invalidate();
         if (s.den_flag)
             throw ApiError(MPM_ERR_NUMERICAL, "update: 1 + tr(dd) <= 0, time step too large for the compression rate",
                            s.den_pid, s.step + 1);
         if (s.nan_flag) {
-            step = s.step + 1; // the step completed, then the guard fired (stepper.hpp:519-522)
+            step = s.step + 1; // the step completed, then the guard fired (stepper.hpp:106-109)
             time = double(T(step) * sc.dt);
             throw ApiError(MPM_ERR_NUMERICAL, "run: non-finite particle field detected at step " + std::to_string(step),
                            -1, step);
         }
         if (s.ood_flag) {
             // keys of step s.step+1's output -> the state after that step is complete; the
-            // next P2G is where the reference throws (bspline.hpp:322-327)
+            // next P2G is where the reference throws (bspline.hpp:86-91)
             throw ApiError(MPM_ERR_OUT_OF_DOMAIN,
                            "particle " + std::to_string(s.ood_pid) + " outside valid grid interior", s.ood_pid,
                            s.step + 1);
@@ -729,6 +824,7 @@ template <class T, int D> struct Ctx : CtxBase {
 
     void upload_ids(const mpm_state_view* s, const int64_t* ids) override
     {
+        inc_invalidate();
         if (s->n < 0 || s->n > cap) // an empty state is valid (the reference steps it; a slab may be empty)
             throw ApiError(MPM_ERR_USAGE, "state size " + std::to_string(s->n) + " outside [1, " + std::to_string(cap) + "]");
         if (s->n > 0 && (!s->x || !s->v || !s->mass || !s->volume || !s->rho || !s->sigma))
@@ -930,21 +1026,19 @@ template <class T, int D> struct Ctx : CtxBase {
             for (int64_t k = 1; k < nsteps; ++k) {
                 const int gv = k == nsteps - 1 ? 1 : 0;
                 cudaGraphExec_t& ge = graphs[guard][gv][cur];
-                if (!ge) {
-                    const int cur0 = cur;
-                    const int64_t l0 = launches;
-                    cudaGraph_t g;
-                    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-                    step_once(guard, false, gv);
-                    CK(cudaStreamEndCapture(stream, &g));
-                    CK(cudaGraphInstantiate(&graphs[guard][gv][cur0], g, 0));
-                    CK(cudaGraphDestroy(g));
-                    graph_launches = launches - l0;
-                    launches = l0;
-                    cur = cur0;
+                // a graph bakes in the particle count it was captured with (sort sizes, grids):
+                // recapture after an upload / init_scene changed n
+                if (!ge || graph_n[guard][gv][cur] != n) { // (updated in place when only sizes moved)
+                    graph_launches = capture(ge, [&] { step_once(guard, false, gv); });
+                    graph_n[guard][gv][cur] = n;
+                    graph_inc[guard][gv][cur] = captured_inc_src;
                 }
                 CK(cudaGraphLaunch(graphs[guard][gv][cur], stream));
                 launches += graph_launches;
+                inc_src = graph_inc[guard][gv][cur];
+                keys_sorted = ks_own[cur]; // the pair the replayed step wrote (own set: advance)
+                bstart = bs_own[cur];
+                bend = be_own[cur];
                 cur ^= 1;
             }
         }
@@ -974,14 +1068,14 @@ template <class T, int D> struct Ctx : CtxBase {
         reset_status();
         sort_and_segment();
         p2g_kernel();
-        zero_grid(); // Grid::reset (state.hpp:235-242)
+        zero_grid(); // Grid::reset (state.hpp:154-161)
         grid_kernel<G_SUM | G_STORE>();
         grid_touched_all = false;
         check_status(step);
     }
     void activate_all_node_blocks()
     {
-        // phases applied to an uploaded grid act on every node (contact.hpp:249-262)
+        // phases applied to an uploaded grid act on every node (contact.hpp:83-96)
         CK(cudaMemsetAsync(nflag, 1, sc.nnb_total, stream));
         CK(cudaMemsetAsync(counts + 1, 0, sizeof(int), stream));
         launch("k_compact", [&] { k_compact_flag<<<grid_for(sc.nnb_total, 256), 256, 0, stream>>>(nflag, sc.nnb_total, act, counts + 1); });
@@ -1009,7 +1103,7 @@ template <class T, int D> struct Ctx : CtxBase {
         g2p_kernel_fl<0>();
         fetch_status();
         if (st_host->abort && st_host->ood_flag == 2 && !st_host->den_flag && !st_host->nan_flag) {
-            // g2p itself does not check the domain (transfer.hpp:457-486): the next p2g throws
+            // g2p itself does not check the domain (transfer.hpp:92-121): the next p2g throws
             reset_status();
             keys_valid = false;
             return;
@@ -1147,6 +1241,12 @@ template <class T, int D> struct Ctx : CtxBase {
     int rec_size() const override { return 2 * D + 5 + C::NS + D * D + (has_aff ? D * D : 0) + (has_F ? D * D : 0); }
     void slab_set(int lo, int hi, int64_t mig_cap) override
     {
+        inc_invalidate();
+        if (own_set) { // slab phases are graph-replayed with eager kernels between them: one fixed pair
+            keys_sorted = ks_own[0];
+            bstart = bs_own[0];
+            bend = be_own[0];
+        }
         if (lo < 0 || hi <= lo || lo % C::B || (hi % C::B && hi < sc.cells[0]))
             throw ApiError(MPM_ERR_USAGE, "slab bounds must be block-aligned (multiples of " + std::to_string(C::B) + ")");
         sc.slab_lo = lo;
@@ -1189,6 +1289,7 @@ template <class T, int D> struct Ctx : CtxBase {
     void init_scene_dev(const mpm_region* rg, int nreg, double mass, double volume, double rho0,
                         int64_t* n_out) override
     {
+        inc_invalidate();
         if (nreg < 1 || !rg)
             throw ApiError(MPM_ERR_VALIDATION, "scene: no geometry regions");
         SeedBox bx{};
@@ -1398,6 +1499,7 @@ template <class T, int D> struct Ctx : CtxBase {
     }
     void migrate_import(const void* recs, const int* pids, int64_t k) override
     {
+        inc_invalidate();
         if (k <= 0)
             return;
         if (n + k > cap)
@@ -1496,6 +1598,8 @@ template <class T, int D> struct Ctx : CtxBase {
     }
     void pbuf_copy(const PBuf<T, D>& dst, const PBuf<T, D>& src)
     {
+        if (dst.base == inc_src.base)
+            inc_invalidate();
         auto d = pbuf_arrays(dst), s = pbuf_arrays(src);
         for (size_t i = 0; i < d.size(); ++i)
             CK(cudaMemcpyAsync(d[i].first, s[i].first, n * s[i].second, cudaMemcpyDeviceToDevice, stream));
@@ -1524,6 +1628,7 @@ template <class T, int D> struct Ctx : CtxBase {
         act = s.act;
         counts = s.counts;
         nflag = s.nflag;
+        own_set = s.keys_sorted == ks_own[0] || s.keys_sorted == ks_own[1];
     }
     struct TapeSlot {
         SortSet ss{};
@@ -1646,7 +1751,15 @@ template <class T, int D> struct Ctx : CtxBase {
         const bool eul = sd && sd->kind == MPM_SEEDER_EULERIAN_LS && sd->n_obs > 0;
         const bool seeding = (sd && sd->kind == MPM_SEEDER_LAGRANGIAN_LS && sd->n_obs > 0) || eul;
         const int64_t nsel = seeding ? (eul ? sd->n_regions : (sd->sel ? sd->n_sel : n)) : 0;
-        std::vector<void*> owned;
+        struct Owned { // seeder tables: released on every exit path (validation throws included)
+            std::vector<void*> v;
+            void push_back(void* p) { v.push_back(p); }
+            ~Owned()
+            {
+                for (void* p : v)
+                    cudaFree(p);
+            }
+        } owned;
         long long* d_sel = nullptr;
         T* d_tgt = nullptr;
         T *d_cen = nullptr, *d_half = nullptr, *d_epart = nullptr, *d_g = nullptr;
@@ -1741,7 +1854,12 @@ template <class T, int D> struct Ctx : CtxBase {
             CK(cudaEventRecord(ev0.e, stream));
             // replay tape, sized by the active node blocks of the latest forward step (+25 %)
             bool use_tape = false;
-            auto reserve_tape = [&]() {
+            auto reserve_tape = [&](bool fresh) {
+                if (fresh) { // no step of this trajectory ran yet: size from S0's own active blocks
+                    keys_valid = false;
+                    sort_and_segment();
+                    keys_valid = false;
+                }
                 int n_act_now = 0;
                 d2h_raw(&n_act_now, counts + 1, sizeof(int));
                 const char* cap_env = std::getenv("MPM_TAPE_CAP"); // test hook: force slot overflows
@@ -1780,7 +1898,7 @@ template <class T, int D> struct Ctx : CtxBase {
                 if (k >= 1) // digests only where a replayed segment ends (S^0 is never checked)
                     bhash[k] = digest_of(buf[cur]);
                 if (k == nseg - 1 && last_kept) {
-                    reserve_tape();
+                    reserve_tape(bnd[k] == 0);
                     pbuf_copy(replay[0], buf[cur]);
                     for (int64_t t = bnd[k]; t < bnd[k + 1]; ++t) {
                         slot_step(t - bnd[k]);
@@ -1801,7 +1919,7 @@ template <class T, int D> struct Ctx : CtxBase {
             double loss = 0;
             d2h_raw(&loss, aw.loss_acc, sizeof(double));
             if (!last_kept)
-                reserve_tape();
+                reserve_tape(false);
             std::vector<int> over(Lmax, 1);
             // backward sweep
             aw.cot_zero(*this, 0);
@@ -1875,12 +1993,8 @@ template <class T, int D> struct Ctx : CtxBase {
             cur = cur0;
             keys_valid = false;
             cudaStreamSynchronize(stream);
-            for (void* p : owned)
-                cudaFree(p);
             throw;
         }
-        for (void* p : owned)
-            cudaFree(p);
     }
 
     void step_vjp(const mpm_state_view* s, const mpm_cot_view* co, mpm_cot_view* ci, mpm_param_grads* pg) override

@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
                 for (int a = 0; a < D; ++a)
                     t0 = t0 * TE + tb[a];
                 if constexpr (!APIC) {
-                    // forward gather grad v_new = sum v (x) grad phi (transfer.hpp:476) and every
+                    // forward gather grad v_new = sum v (x) grad phi (transfer.hpp:111) and every
                     // stencil sum of the G2P transpose, as moments of the v and v - v_old fields:
                     //   sum_o grad phi (pic.v + inc.(v - v_old)) = sum_c pic_c G1[c] + inc_c Gd[c]
                     //   sum_o H (L^T v)                          = sum_bc L_cb HM[c][:, b]

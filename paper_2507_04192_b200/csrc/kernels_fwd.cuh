@@ -6,10 +6,10 @@
 //   k_p2g     CTA per occupied particle block: node-column march (deterministic gather,
 //             no atomics) of the block's particles into its (B+2)^d partial tile
 //   k_grid    CTA per active node block: sum <= 2^d partial tiles in fixed order, momentum
-//             update, wall / obstacle / Coulomb corrections (transfer.hpp:440-449,
-//             contact.hpp:394-411)
+//             update, wall / obstacle / Coulomb corrections (transfer.hpp:75-84,
+//             contact.hpp:228-245)
 //   k_g2p     CTA per occupied particle block: node tile in smem, gather + v/x/grad v update
-//             (transfer.hpp:457-486) fused with the constitutive update (stepper.hpp:428-456),
+//             (transfer.hpp:92-121) fused with the constitutive update (stepper.hpp:15-43),
 //             writes the new state in sorted order and the next step's cell keys
 #pragma once
 
@@ -179,7 +179,7 @@ __device__ __forceinline__ void axis_weights(T x, T origin, T inv_dh, T* w, T* d
     dw[2] = h2 * inv_dh;
 }
 
-// APIC / TPIC velocity augmentation matrix A (transfer.hpp:379-397), row-major D x D
+// APIC / TPIC velocity augmentation matrix A (transfer.hpp:14-32), row-major D x D
 template <class T, int D>
 __device__ __forceinline__ void affine_matrix(const DevScene<T, D>& sc, const PBuf<T, D>& P, int src, const T* x,
                                               const T (&w)[D][3], const int* base, T* A)
@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(StageCfg<T, D>::THREADS, 1)
     }
 }
 
-// quadratic B-spline weight and derivative of stencil offset o (bspline.hpp:330-344)
+// quadratic B-spline weight and derivative of stencil offset o (bspline.hpp:94-108)
 template <class T> __device__ __forceinline__ void quad_w(T fx, int o, T inv_dh, T& w, T& dw)
 {
     if (o == 0) {
@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
     const int o0 = WIDE ? (lt % 9) / 3 : lt % 3;
     const int o1t = WIDE ? lt % 3 : 0; // WIDE: this thread's y-offset
     const bool mid = o0 == 1;
-    const T xoff = o0 == 0 ? T(1.5) : (o0 == 1 ? T(1) : T(0.5)); // h = fx - xoff (bspline.hpp:330-335)
+    const T xoff = o0 == 0 ? T(1.5) : (o0 == 1 ? T(1) : T(0.5)); // h = fx - xoff (bspline.hpp:94-99)
     const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
     // raw rows x0..2 v0..2 m V sigma0..5 = PLay fields 0..7 and SIG..SIG+5 of the strided buffer
     // (one base pointer and a stride instead of 14 pointers reloaded from the parameter bank)
@@ -1225,7 +1225,7 @@ __global__ void __launch_bounds__(Lane3Cfg<T>::THREADS, 1)
             __syncthreads(); // raw(j), pk(j + 1) landed for every thread
             const int len = it_len[j];
             const int* col = pk + (j % 3) * 2 * CAP + CAP;
-            // convert each staged particle once: weights (bspline.hpp:330-344), m v, V sigma
+            // convert each staged particle once: weights (bspline.hpp:94-108), m v, V sigma
             for (int r = tid; r < len; r += NT) {
                 atomicAdd(&ccount[col[r] & (NBC - 1)], 1);
                 T* d = der + r * ND;
@@ -1294,7 +1294,7 @@ __global__ void __launch_bounds__(Lane3Cfg<T>::THREADS, 1)
                     acc[c][1] += mv0 * wgt;
                     acc[c][2] += mv1 * wgt;
                     acc[c][3] += mv2 * wgt;
-                    // f -= V sigma grad phi (transfer.hpp:420-427); gravity is added per node in k_grid
+                    // f -= V sigma grad phi (transfer.hpp:55-62); gravity is added per node in k_grid
                     acc[c][4] = acc[c][4] - s00 * g0 - s01 * g1 - s02 * g2;
                     acc[c][5] = acc[c][5] - s01 * g0 - s11 * g1 - s12 * g2;
                     acc[c][6] = acc[c][6] - s02 * g0 - s12 * g1 - s22 * g2;
@@ -1516,7 +1516,7 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
                     f[a] += part[(1 + D + a) * C::TN];
                 }
             }
-            // sum_p phi m g = g m_i (transfer.hpp:427, gravity term factored out of the scatter)
+            // sum_p phi m g = g m_i (transfer.hpp:62, gravity term factored out of the scatter)
             if (!(MODE & G_NOGRAV)) {
 #pragma unroll
                 for (int a = 0; a < D; ++a)
@@ -1848,7 +1848,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
             bool ok_den = true;
             if ((FLAGS & P_CONSTIT) && !(ABL & 2)) {
                 ok_den = constitutive_particle<T, D>(sc, sig, szz, rho, V, eps, L);
-                if constexpr (TRACKF) { // F <- (I + L dt) F (stepper.hpp:452-455)
+                if constexpr (TRACKF) { // F <- (I + L dt) F (stepper.hpp:39-42)
                     T Fn[D * D];
 #pragma unroll
                     for (int a = 0; a < D; ++a)
@@ -1902,7 +1902,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                 st->den_flag = 1;
                 st->abort = 1;
             }
-            if (FLAGS & P_GUARD) { // ParticleSoA::all_finite (state.hpp:129-143)
+            if (FLAGS & P_GUARD) { // ParticleSoA::all_finite (state.hpp:48-62)
                 bool fin = finite_(V) && finite_(rho) && finite_(eps) && finite_(szz);
 #pragma unroll
                 for (int a = 0; a < D; ++a)

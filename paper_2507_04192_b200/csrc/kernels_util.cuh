@@ -498,7 +498,7 @@ __global__ void k_digest(PBuf<T, D> P, int n, int has_aff, unsigned long long* o
         atomicAdd(out, h);
 }
 
-// max |v| (stepper.hpp:491-498) as the bit pattern of a non-negative double
+// max |v| (stepper.hpp:78-85) as the bit pattern of a non-negative double
 template <class T, int D>
 __global__ void k_max_speed(PBuf<T, D> P, int n, unsigned long long* out)
 {

@@ -1,6 +1,6 @@
 """Slab decomposition of the MPM step across GPUs.
 
-The reference is single-process (stepper.hpp:462-483 has no decomposition). This module shards
+The reference is single-process (stepper.hpp:49-70 has no decomposition). This module shards
 the same step along x across one process per GPU. Every rank owns the particles whose base cell
 along x lies in its slab `[lo, hi)`. Slab bounds are multiples of the particle-block edge: 16
 cells in 2-D, 8 in 3-D. One step runs in four phases:
@@ -17,7 +17,7 @@ cells in 2-D, 8 in 3-D. One step runs in four phases:
      from its slot. It is then appended by the receiving neighbour, in particle-id order.
 
 There is no all-reduce on the data path. Each step does one small MAX all-reduce of an error
-flag, so that a NaN/OOD abort on one rank stops every rank at the same step (stepper.hpp:519-522).
+flag, so that a NaN/OOD abort on one rank stops every rank at the same step (stepper.hpp:106-109).
 
 Transports:
   * TorchTransport runs torch.distributed point-to-point (NCCL over NVLink on device tensors;
@@ -46,7 +46,7 @@ def block_edge(dim: int) -> int:
 
 
 def base_cell_x(scene: Scene, x: np.ndarray) -> np.ndarray:
-    """base node index along x of the quadratic stencil (bspline.hpp:315-327): floor(u - 1/2)"""
+    """base node index along x of the quadratic stencil (bspline.hpp:79-91): floor(u - 1/2)"""
     c = scene.config
     u = (x[:, 0] - c.origin[0]) / c.dh
     return np.floor(u - 0.5).astype(np.int64)
@@ -283,7 +283,7 @@ class TorchTransport:
 class SlabStepper:
     """Drives one step of the decomposition over the domains this process owns.
 
-    Mirrors Stepper::advance (stepper.hpp:462-483). Every rank advances by one step, and an
+    Mirrors Stepper::advance (stepper.hpp:49-70). Every rank advances by one step, and an
     error on any rank raises on all of them at the same step.
     """
 

@@ -98,4 +98,17 @@ def c5_landslide(dtype="f64", n_segments=32) -> Scene:
     return s
 
 
-CONFIGS = {"C1": c1_column, "C2": c2_dam_break, "C3": c3_inverse, "C4": c4_column3d, "C5": c5_landslide}
+def c5_landslide_eighth(dtype="f64", n_segments=32) -> Scene:
+    """C5 with 1/8 of its particles (4,063,232): the same 512 x 256 x 128 grid, material, dt and
+    32-segment Coulomb floor; the block keeps its 1.0 m along x (segments 0-15 under it, as in
+    full C5) and v0 = (2, 0, 0), with half the height and a quarter of the width. Used where the
+    full scene's 7.3 GB host copies do not fit (parity tests, CPU samples)."""
+    s = c5_landslide(dtype, n_segments)
+    dh = s.config.dh
+    s.geometry[0] = GeometryRegion(lo=[2 * dh, 2 * dh, 2 * dh], hi=[2 * dh + 1.0, 2 * dh + 0.25, 2 * dh + 31 * dh],
+                                   velocity=VelocityExpr("constant", value=[2.0, 0.0, 0.0]))
+    return s
+
+
+CONFIGS = {"C1": c1_column, "C2": c2_dam_break, "C3": c3_inverse, "C4": c4_column3d, "C5": c5_landslide,
+           "C5/8": c5_landslide_eighth}

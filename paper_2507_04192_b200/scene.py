@@ -76,7 +76,7 @@ class DruckerPragerParams:
 
     @staticmethod
     def make(rho0, K, nu, phi, psi, cohesion, sigma_t) -> "DruckerPragerParams":
-        """DruckerPragerParams::make + dp_derived_params (material.hpp:292-339)."""
+        """DruckerPragerParams::make + dp_derived_params (material.hpp:37-84)."""
         s3 = math.sqrt(3.0)
         p = DruckerPragerParams(rho0=rho0, K=K, nu=nu, phi=phi, psi=psi, cohesion=cohesion, sigma_t=sigma_t)
         p.G = 3.0 * K * (1.0 - 2.0 * nu) / (2.0 * (1.0 + nu))
@@ -108,7 +108,7 @@ class DruckerPragerParams:
 
 
 def material_wave_speed(m) -> float:
-    """material.hpp:371-380"""
+    """material.hpp:116-125"""
     if isinstance(m, FluidParams):
         return m.sound_speed
     return math.sqrt((m.K + 4.0 * m.G / 3.0) / m.rho0)

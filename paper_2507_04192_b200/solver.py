@@ -1,8 +1,8 @@
 """Python mirror of the reference solver API (stepper.hpp, adjoint.hpp, checkpoint.hpp) over the
 C ABI of libmpm_b200.so. Names, argument meaning and error behaviour follow the reference:
 
-    Stepper(scene).advance(state)                    stepper.hpp:462-483
-    run(scene, state, n, stride, force, observer)    stepper.hpp:504-535
+    Stepper(scene).advance(state)                    stepper.hpp:49-70
+    run(scene, state, n, stride, force, observer)    stepper.hpp:91-122
     step_vjp(scene, state, cot_out, cot_in, pg, ws)  adjoint.hpp:328-525
     backprop_trajectory(scene, s0, plan, seeder)     checkpoint.hpp:72-143
     CheckpointPlan.make(N_t, n)                      checkpoint.hpp:15-34
@@ -228,7 +228,7 @@ def _scene_changed(ctx: Context, scene: Scene) -> bool:
 
 
 class Stepper:
-    """stepper.hpp:462-483. `grid` is a host mirror refreshed on demand (the device grid is
+    """stepper.hpp:49-70. `grid` is a host mirror refreshed on demand (the device grid is
     derived data, so poisoning this copy between steps changes nothing, as in the reference)."""
 
     def __init__(self, scene: Scene):
@@ -253,18 +253,18 @@ class Stepper:
 
 @dataclass
 class RunResult:
-    """stepper.hpp:485-489"""
+    """stepper.hpp:72-76"""
     snapshots: list = field(default_factory=list)
     seconds_per_1000_steps: float = 0.0
 
 
 def max_particle_speed(state: SimState) -> float:
-    """stepper.hpp:491-498"""
+    """stepper.hpp:78-85"""
     return float(np.sqrt((state.particles.v.astype(np.float64) ** 2).sum(axis=1)).max()) if state.particles.size() else 0.0
 
 
 def run(scene: Scene, state: SimState, num_steps: int, stride: int, force: bool = False, observer=None) -> RunResult:
-    """stepper.hpp:504-535: CFL refusal, NaN guard every step, snapshots at the stride, the
+    """stepper.hpp:91-122: CFL refusal, NaN guard every step, snapshots at the stride, the
     reference's own timer. Steps between snapshots run as one device call."""
     courant = cfl_report(scene.config, scene.material, max_particle_speed(state))
     if courant > 1 and not force:
@@ -313,7 +313,7 @@ def run(scene: Scene, state: SimState, num_steps: int, stride: int, force: bool 
 
 
 def constitutive_update(scene: Scene, state: SimState):
-    """stepper.hpp:428-456 on the device (phase function)."""
+    """stepper.hpp:15-43 on the device (phase function)."""
     ctx = _context_for(scene, state.particles.size())
     ctx.upload(state)
     ctx.constitutive()

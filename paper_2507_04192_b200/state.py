@@ -21,7 +21,7 @@ def _from_colmajor(buf: np.ndarray, n: int, d: int) -> np.ndarray:
 
 
 class ParticleSoA:
-    """state.hpp:98-144"""
+    """state.hpp:17-63"""
 
     FIELDS = ("x", "v", "mass", "volume", "rho", "eps_eq", "sigma_zz", "sigma", "grad_v", "affine", "def_grad")
 
@@ -48,7 +48,7 @@ class ParticleSoA:
         return self.x.dtype
 
     def all_finite(self) -> bool:
-        """state.hpp:129-143"""
+        """state.hpp:48-62"""
         fs = [self.x, self.v, self.volume, self.rho, self.eps_eq, self.sigma_zz, self.sigma, self.grad_v]
         if self.affine is not None:
             fs.append(self.affine)
@@ -81,7 +81,7 @@ class ParticleSoA:
 
 
 class SimState:
-    """state.hpp:146-168"""
+    """state.hpp:65-87"""
 
     def __init__(self, particles: ParticleSoA, step: int = 0, time: float = 0.0):
         self.particles = particles

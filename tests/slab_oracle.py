@@ -2,8 +2,8 @@
 
 This implements the per-rank protocol of paper_2507_04192_b200.distributed.SlabDomain on top of
 the CPU oracle's phase functions. The phases follow the reference's Stepper::advance
-(stepper.hpp:472-482), run on one rank's particle subset:
-  - p2g: the reference's p2g with `g m_i` inside the scatter (transfer.hpp:427);
+(stepper.hpp:59-69), run on one rank's particle subset:
+  - p2g: the reference's p2g with `g m_i` inside the scatter (transfer.hpp:62);
   - halo sum;
   - grid_momentum_update, apply_grid_corrections, g2p, constitutive_update;
   - migration.

@@ -107,7 +107,7 @@ def test_single_slab_is_bitwise_oracle(orc):
 
 
 def test_error_propagates_to_all_ranks(orc):
-    """a NaN on one rank aborts every rank at the same step (stepper.hpp:519-522)"""
+    """a NaN on one rank aborts every rank at the same step (stepper.hpp:106-109)"""
     s = moving_fluid_scene(2)
     st = init_scene(s)
     plan = SlabPlan.make(s, 2, st.particles.x)

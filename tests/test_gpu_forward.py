@@ -11,7 +11,7 @@ import math
 import numpy as np
 import pytest
 
-from helpers import (assert_grid_close, assert_state_close, dp_block_scene, fluid_box_scene, random_block,
+from helpers import (assert_grid_close, assert_state_close, dp_block_scene, fluid_box_scene, random_block, rel_err,
                      single_particle_state)
 from paper_2507_04192_b200 import GeometryRegion, Obstacle, SimState, VelocityExpr, Wall, init_scene
 from paper_2507_04192_b200.errors import NumericalError, OutOfDomainError, ValidationError
@@ -169,7 +169,7 @@ def test_grad_v_stored_by_the_last_step_of_a_call(orc, kind):
 
 
 def test_stepper_api_mirror(orc):
-    """Stepper(scene).advance(state) as in the reference (stepper.hpp:462-483)."""
+    """Stepper(scene).advance(state) as in the reference (stepper.hpp:49-70)."""
     s = small_fluid_scene("flip")
     s.config.gravity = [0.0, -9.8]
     st = init_scene(s)
@@ -234,7 +234,7 @@ def test_run_snapshots_cfl_and_nan():
 
 
 def test_out_of_domain_names_lowest_particle(orc):
-    """bspline.hpp:322-327 through the step: the smallest offending id is reported."""
+    """bspline.hpp:86-91 through the step: the smallest offending id is reported."""
     s = small_fluid_scene("pic")
     st = init_scene(s)
     st.particles.x[200] = [0.01, 0.5]
@@ -346,3 +346,49 @@ def test_empty_state_steps_like_the_reference(orc, ref, dim):
     assert [x.step for x in res.snapshots] == [0, 2, 4]
     cin = step_vjp(s, st, StateCotangent.zeros_like(st.particles), None, ParamGrads(s.boundary))
     assert cin.x.shape == (0, dim)
+
+
+@pytest.mark.parametrize("name", ["dp2-noslip", "fluid2-apic", "dp3", "fluid3-flip"])
+def test_track_def_grad_parity(orc, name):
+    """F <- (I + grad v dt) F when track_def_grad is set (stepper.hpp:39-42), in the G2P
+    epilogue (all schemes) and in the separate constitutive phase; against the oracle."""
+    s = SCENES[name]("f64")
+    s.config.track_def_grad = True
+    st = init_scene(s)
+    assert st.particles.def_grad is not None
+    want = orc.advance(s, st.copy(), 20)
+    got = gpu_run(s, st, 20)
+    assert_state_close(got, want, STEP_RTOL["f64"], what=name + "+F")
+    assert rel_err(got.particles.def_grad, want.particles.def_grad, 1.0) <= 1e-10
+    eye = np.eye(s.dim)
+    assert np.abs(want.particles.def_grad - eye).max() > 1e-8  # F actually evolved
+    # the phase path: constitutive_update alone on an uploaded state
+    ctx = Context(s, st.particles.size())
+    ctx.upload(want)
+    ctx.constitutive()
+    g1 = ctx.download(want.copy())
+    ctx.close()
+    w1 = orc.constitutive(s, want.copy())
+    assert rel_err(g1.particles.def_grad, w1.particles.def_grad, 1.0) <= 1e-13
+
+
+def test_particle_count_change_recaptures_the_step_graph(orc):
+    """the captured step graph bakes in n. Upload n1, advance, upload a smaller
+    (then a larger) state to the same context, advance again: identical to a fresh context."""
+    s = dp_block_scene(3, cells=[12, 12, 12])
+    st = init_scene(s)
+    n1 = st.particles.size()
+    small = SimState(st.particles.take(np.arange(0, n1, 2)))
+    ctx = Context(s, n1)
+    for state in (st, small, st):
+        ctx.upload(state)
+        ctx.advance(4)
+        got = ctx.download(state.copy())
+        fresh = Context(s, n1)
+        fresh.upload(state)
+        fresh.advance(4)
+        want = fresh.download(state.copy())
+        fresh.close()
+        for f in ("x", "v", "sigma", "grad_v"):
+            assert np.array_equal(getattr(got.particles, f), getattr(want.particles, f)), f
+    ctx.close()
