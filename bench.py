@@ -61,8 +61,12 @@ def parse():
     ap.add_argument("--adj-steps", type=int, default=20, help="fwd+adjoint sample: backprop steps (0: skip)")
     ap.add_argument("--adj-segments", type=int, default=0,
                     help="checkpoint segments of the fwd+adjoint sample (0: fewest that fit in HBM)")
-    ap.add_argument("--mode", default="auto", choices=["auto", "plain", "slab"],
-                    help="auto: one context at N=1, slab decomposition for N>1")
+    ap.add_argument("--mode", default="auto", choices=["auto", "plain", "slab", "pyslab"],
+                    help="auto: one context at N=1, the library's slab decomposition (mpm_dist_*, NCCL) for "
+                         "N>1; slab: that path at any N; pyslab: the Python-orchestrated protocol reference")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1 with C4: weak = one C4 column per GPU (256N x 256 x 256 domain); strong = the one "
+                         "C4 scene split into N slabs")
     return ap.parse_args()
 
 
@@ -690,6 +694,154 @@ def bench_slab(a, rank, world, local):
     }
 
 
+def bench_dist(a, rank, world, local):
+    """The library-owned slab decomposition (mpm_dist_*: NCCL send/recv of the halo bands and the
+    fixed-capacity migration messages, device-resident counts, no host synchronisation inside the
+    K steps), one process per GPU. C4 weak scaling: one C4 column per rank in a 256N x 256 x 256
+    domain; strong scaling: the C4 scene itself split into N particle-balanced slabs. Time = CUDA
+    events around the K steps on each rank's library stream, max over ranks."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+    from paper_2507_04192_b200 import init_scene
+    from paper_2507_04192_b200.distributed import NcclSlabRank, SlabPlan, dist_unique_id
+    from paper_2507_04192_b200.presets import CONFIGS, c4_column3d
+
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    strong = a.scaling == "strong" or a.config != "C4"
+    if not strong:
+        s = c4_column3d(a.dtype, replicas_x=world)
+        st = init_scene(c4_column3d(a.dtype))  # this rank's column, shifted into its slab
+        n = st.particles.size()
+        st.particles.x[:, 0] += 256 * rank * s.config.dh
+        ids = np.arange(rank * n, (rank + 1) * n, dtype=np.int64)
+        plan = SlabPlan([256 * r for r in range(world + 1)], 8)
+        n_total = n * world
+        workload = (f"C4 x{world} (weak): 3-D D-P granular column collapse, one 128x64x64-cell column per GPU, "
+                    f"domain {s.config.cells}")
+    else:
+        s = CONFIGS[a.config](dtype=a.dtype)
+        full = init_scene(s)
+        plan = SlabPlan.make(s, world, full.particles.x)
+        ids = plan.partition(s, full)[rank]
+        st = SimState_take(full, ids)
+        n_total = full.particles.size()
+        workload = f"{a.config} (strong): the one scene split into {world} particle-balanced slabs along x"
+    obj = [dist_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    rk = NcclSlabRank(s, plan, rank, st, ids, obj[0], device=local, n_total=n_total)
+    rk.advance(a.warmup)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = rk.ctx.launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = rk.advance(a.steps, nan_guard=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ck = clocks.stop()
+    launches = rk.ctx.launch_count() - l0
+    an1, _, _ = rk.ctx.grid_stats()
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    cnt = torch.tensor([int(rk.lib.mpm_local_count(rk.h))], device="cuda", dtype=torch.int64)
+    dist.all_reduce(cnt)
+    act = torch.tensor([float(an1)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(act)
+    # e2e: rank-local upload from pinned host + K decomposed steps + compact download, max over ranks
+    e2e = dist_e2e(rk, st, ids, a.steps)
+    te = torch.tensor([e2e["seconds"], e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]], device="cuda",
+                      dtype=torch.float64)
+    dist.all_reduce(te[:1], op=dist.ReduceOp.MAX)
+    tb = te[1:].clone()
+    dist.all_reduce(tb)
+    rk.close()
+    dist.barrier()
+    if rank != 0:
+        return None
+    B_fwd, _, _ = bytes_model(s, n_total, float(act.item()))
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    gbs = n_total / world * B_fwd / (ms / a.steps / 1e3) / 1e9
+    return {
+        "metric": METRIC, "value": n_total * a.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": a.dtype,
+        "data": "synthetic (init_scene seeding of the named scene, deterministic)",
+        "config": {"workload": workload, "particles_total": n_total, "grid_cells": s.config.cells,
+                   "parallelism": f"slab x{world} (library-owned: NCCL halo + migration, device-resident counts)",
+                   "slab_bounds": plan.bounds, "particles_after": int(cnt.item()),
+                   "l2_policy": "inputs larger than the 126 MB L2; no flush"},
+        "roofline": {"bound": "hbm", "kernel": "step (per GPU)", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                     "frac": gbs / peak, "traffic": None, "bytes_per_particle_step": B_fwd,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s"},
+        "clocks": ck, "gpu_launches": launches,
+        "e2e": {"value": n_total * a.steps / float(te[0].item()), "unit": UNIT,
+                "h2d_bytes_per_step": float(tb[0].item()), "d2h_bytes_per_step": float(tb[1].item()),
+                "call": e2e["call"], "seconds": float(te[0].item())},
+    }
+
+
+def SimState_take(full, ids):
+    from paper_2507_04192_b200.state import SimState
+    return SimState(full.particles.take(ids), full.step, full.time)
+
+
+def dist_e2e(rk, st, ids, steps):
+    """mpm_state_upload_ids from pinned host buffers + K decomposed steps (mpm_dist_advance) +
+    mpm_state_download_local into pinned buffers, wall clock on this rank."""
+    import ctypes as C
+
+    import torch
+    from paper_2507_04192_b200 import capi
+
+    p = st.particles
+    d = p.dim
+    n = p.size()
+    tdt = torch.float64 if p.dtype == np.float64 else torch.float32
+
+    def pinned(shape):
+        return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+
+    fields = {"x": (n, d), "v": (n, d), "mass": (n,), "volume": (n,), "rho": (n,), "eps_eq": (n,),
+              "sigma": (n, d * d), "grad_v": (n, d * d)}
+    if d == 2:
+        fields["sigma_zz"] = (n,)
+    host = {k: pinned(sh) for k, sh in fields.items()}
+    for k in ("x", "v", "mass", "volume", "rho", "eps_eq") + (("sigma_zz",) if d == 2 else ()):
+        host[k][...] = getattr(p, k)
+    host["sigma"][...] = np.transpose(p.sigma, (0, 2, 1)).reshape(n, d * d)
+    host["grad_v"][...] = np.transpose(p.grad_v, (0, 2, 1)).reshape(n, d * d)
+    cap = rk.capacity
+    outb = {k: pinned((cap,) + sh[1:]) for k, sh in fields.items()}
+    ids_in = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int64)).pin_memory().numpy()
+    ids_out = torch.empty(cap, dtype=torch.int64, pin_memory=True).numpy()
+    view, out = capi.StateView(), capi.StateView()
+    view.n, out.n = n, cap
+    for k in fields:
+        setattr(view, k, host[k].ctypes.data)
+        setattr(out, k, outb[k].ctypes.data)
+    lib, h = rk.lib, rk.h
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rk.ctx.check(lib.mpm_state_upload_ids(h, C.byref(view), ids_in.ctypes.data_as(C.c_void_p)))
+    rk.ctx.check(lib.mpm_dist_advance(h, steps, 0, None))
+    rk.ctx.check(lib.mpm_state_download_local(h, C.byref(out), ids_out.ctypes.data_as(C.c_void_p)))
+    t1 = time.perf_counter()
+    h2d = sum(v.nbytes for v in host.values()) + ids_in.nbytes
+    d2h = out.n * (sum(v[0].nbytes for v in outb.values()) + 8)
+    return {"seconds": t1 - t0, "h2d_bytes_per_step": h2d / steps, "d2h_bytes_per_step": d2h / steps,
+            "call": f"mpm_state_upload_ids (pinned host) + mpm_dist_advance({steps}) + mpm_state_download_local, "
+                    "wall clock"}
+
+
 def bench_slab_fwd_adj(s, st, dom, rank, world, n, steps):
     """fwd+adjoint over the slab decomposition (slab_backprop_trajectory: per-rank checkpoints,
     digest-checked replay, slab_step_vjp with two halo exchanges per step). It is host-orchestrated:
@@ -894,8 +1046,12 @@ def main():
         if line:
             print(json.dumps(line), flush=True)
         return
-    slab = a.mode == "slab" or (a.mode == "auto" and world > 1)
-    line = bench_slab(a, rank, world, local) if slab else bench_b200(a, rank, world, local)
+    if a.mode == "pyslab":
+        line = bench_slab(a, rank, world, local)
+    elif a.mode == "slab" or (a.mode == "auto" and world > 1):
+        line = bench_dist(a, rank, world, local)
+    else:
+        line = bench_b200(a, rank, world, local)
     if line is not None:
         if not a.no_cpu_baseline:
             try:

@@ -312,6 +312,32 @@ int mpm_migrate_export(mpm_ctx* ctx, void* lo, int* lo_pid, void* hi, int* hi_pi
                        int64_t* n_hi);
 int mpm_migrate_import(mpm_ctx* ctx, const void* recs, const int* pids, int64_t n);
 
+/* ---- library-owned slab decomposition ---------------------------------- */
+/* The decomposed step of Stepper::advance (stepper.hpp:59-69) run entirely inside the library:
+ * one context per rank, rank r owning base cells [cell_lo, cell_hi) along x. Each step is
+ * sort + P2G + band sums -> halo exchange of the 2 shared node planes (overlapping the interior
+ * grid pass) -> fixed-order band import -> band update + G2P -> migration messages (count + up to
+ * mig_cap records per neighbour, fixed size) + a device max-reduction of the abort flag -> import.
+ * Particle counts stay on the device; there is no host synchronisation inside mpm_dist_advance,
+ * whose status (this rank's error, or "another rank aborted") is checked once at its end.
+ * Per-rank state goes in and out with mpm_state_upload_ids / mpm_state_download_local.
+ *
+ * NCCL ranks (one process per GPU): rank 0 makes an id with mpm_dist_unique_id, every rank
+ * receives it (any side channel) and calls mpm_dist_attach_nccl; the library then owns an
+ * ncclComm_t (ncclSend / ncclRecv to the x-neighbours, ncclAllReduce of the abort flag, on its
+ * own communication stream ordered by events against the context stream). */
+#define MPM_DIST_ID_BYTES 128
+int mpm_dist_unique_id(void* id_out);
+int mpm_dist_attach_nccl(mpm_ctx* ctx, int rank, int nranks, const void* nccl_id, int cell_lo, int cell_hi,
+                         int64_t mig_cap);
+/* n decomposed steps (MPM_ADV_NAN_GUARD as mpm_advance); *device_ms (may be NULL) = CUDA-event
+ * time of the steps on the context stream */
+int mpm_dist_advance(mpm_ctx* ctx, int64_t n_steps, uint32_t flags, double* device_ms);
+/* Same-process ranks (several contexts driven by one host thread, e.g. R slabs on one GPU): ctxs[r]
+ * is rank r of bounds[r]..bounds[r+1]; exchanges are device copies ordered by events. */
+int mpm_dist_attach_local(mpm_ctx* const* ctxs, int nranks, const int* bounds, int64_t mig_cap);
+int mpm_dist_advance_local(mpm_ctx* const* ctxs, int nranks, int64_t n_steps, uint32_t flags);
+
 /* ---- instrumentation (bench / tests) --------------------------------------------------- */
 /* enable per-kernel CUDA-event timing on the context stream */
 int mpm_profile_enable(mpm_ctx* ctx, int enable);

@@ -227,7 +227,13 @@ _PROTOS = {
     "mpm_profile_reset": (C.c_int, [C.c_void_p]),
     "mpm_launch_count": (C.c_int64, [C.c_void_p]),
     "mpm_grid_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "mpm_dist_unique_id": (C.c_int, [C.c_void_p]),
+    "mpm_dist_attach_nccl": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int64]),
+    "mpm_dist_advance": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint32, C.POINTER(C.c_double)]),
+    "mpm_dist_attach_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_int), C.c_int64]),
+    "mpm_dist_advance_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, C.c_uint32]),
 }
+DIST_ID_BYTES = 128
 
 _lib = None
 

@@ -11,6 +11,9 @@
 #include "kernels_adj.cuh"
 #include "kernels_fwd.cuh"
 #include "kernels_sort.cuh"
+#include "kernels_dist.cuh"
+
+#include <nccl.h>
 #include "kernels_util.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -57,6 +60,14 @@ struct ApiError : std::runtime_error {
     {
     }
 };
+
+#define NCK(call)                                                                                  \
+    do {                                                                                           \
+        ncclResult_t r_ = (call);                                                                  \
+        if (r_ != ncclSuccess)                                                                     \
+            throw ApiError(MPM_ERR_CUDA, std::string("NCCL error: ") + ncclGetErrorString(r_) + " at " \
+                                             + __FILE__ + ":" + std::to_string(__LINE__));         \
+    } while (0)
 
 #define CK(call)                                                                                   \
     do {                                                                                           \
@@ -115,6 +126,12 @@ struct CtxBase {
     virtual int64_t local_count() const = 0;
     virtual void set_stream(void* s) = 0;
     virtual void migrate_counts(int64_t* lo, int64_t* hi) const = 0;
+    // library-owned slab decomposition (kernels_dist.cuh)
+    virtual void dist_attach(int rank, int nranks, int lo, int hi, int64_t mig_cap, const void* nccl_id) = 0;
+    virtual void dist_advance(int64_t n, uint32_t flags, double* ms) = 0;
+    virtual int dist_device() const = 0;
+    virtual void dist_enqueue_local(std::vector<CtxBase*>& all, int64_t n, uint32_t flags) = 0;
+    virtual void dist_finish() = 0;
 
     // profiling
     bool prof = false;
@@ -163,6 +180,13 @@ template <class T, int D> struct Ctx : CtxBase {
     } inc_src{};
     bool inc_enabled = !(std::getenv("MPM_SORT") && std::string(std::getenv("MPM_SORT")) == "cub");
     void inc_invalidate() { inc_src = IncSrc{}; }
+    bool last_sort_full = true;
+    // the stored order is a previous sort's (decomposed steps always sort incrementally: their
+    // particle count is on the device, which the radix sort cannot take)
+    bool inc_source_ok() const
+    {
+        return (inc_enabled || dist.on) && (!slab || dist.on) && inc_src.base == buf[cur].base && inc_src.ks;
+    }
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
     int *bstart = nullptr, *bend = nullptr, *lstart = nullptr, *occ = nullptr, *act = nullptr, *counts = nullptr; // counts[0]=n_occ, [1]=n_act
@@ -191,6 +215,27 @@ template <class T, int D> struct Ctx : CtxBase {
     AdjWork<T, D> aw{};
     // slab decomposition (multi-GPU)
     bool slab = false;
+    // library-owned decomposition (mpm_dist_*): device-resident counts, NCCL or same-process peers
+    struct Dist {
+        bool on = false;
+        int rank = 0, nranks = 1, lo_peer = -1, hi_peer = -1;
+        ncclComm_t comm = nullptr;
+        cudaStream_t comm_stream = nullptr;
+        cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+        int64_t halo_elems = 0;            // 2 node planes x NF values
+        T* halo_send[2] = {nullptr, nullptr}; // [0] toward the lower neighbour, [1] the upper
+        T* halo_recv[2] = {nullptr, nullptr};
+        long long* cnt_send = nullptr;     // [2]
+        long long* cnt_recv = nullptr;     // [2]
+        T* recs_recv[2] = {nullptr, nullptr};
+        int* pid_recv[2] = {nullptr, nullptr};
+        int* d_n = nullptr;
+        int* d_nlive = nullptr;
+        int* abort_red = nullptr;          // [2]: [0] published (NCCL: reduced in place), [1] local max
+        cudaGraphExec_t graph[2][2] = {}; // [guard][cur]
+        int64_t graph_launches = 0;
+        IncSrc graph_inc[2][2] = {};
+    } dist;
     MigBuf<T> mig{};
     int64_t n_dead = 0;  // vacated slots (pid < 0) left in storage by the last G2P
     int* d_cells = nullptr;
@@ -323,6 +368,12 @@ template <class T, int D> struct Ctx : CtxBase {
         inc.xlist = alloc<int>(cap);
         inc.inbuf = alloc<int>(cap);
         inc.nx = alloc<int>(1);
+        inc.nlive = alloc<int>(1);
+        inc.part = alloc<int>(3 * ((sc.nb_total + 255) / 256));
+        inc.hist = alloc<int>(OCC_NBUCKET);
+        inc.bcur = alloc<int>(OCC_NBUCKET);
+        CK(cudaMemsetAsync(inc.hist, 0, sizeof(int) * OCC_NBUCKET, stream));
+        CK(cudaMemsetAsync(inc.bcur, 0, sizeof(int) * OCC_NBUCKET, stream));
         CK(cudaMemsetAsync(inc.cnt_in, 0, sizeof(int) * sc.nb_total, stream));
         CK(cudaMemsetAsync(inc.cnt_out, 0, sizeof(int) * sc.nb_total, stream));
         CK(cudaMemsetAsync(inc.nx, 0, sizeof(int), stream));
@@ -384,6 +435,18 @@ template <class T, int D> struct Ctx : CtxBase {
                     if (e)
                         cudaGraphExecDestroy(e);
         drop_slab_graphs();
+        for (auto& g : dist.graph)
+            for (auto& e : g)
+                if (e)
+                    cudaGraphExecDestroy(e);
+        if (dist.comm)
+            ncclCommDestroy(dist.comm);
+        if (dist.comm_stream)
+            cudaStreamDestroy(dist.comm_stream);
+        if (dist.ev_a)
+            cudaEventDestroy(dist.ev_a);
+        if (dist.ev_b)
+            cudaEventDestroy(dist.ev_b);
         for (void* p : bp_pool_mem)
             cudaFree(p);
         tape_free();
@@ -620,8 +683,8 @@ template <class T, int D> struct Ctx : CtxBase {
     // ---- sort + segment tables ---------------------------------------------------------------
     void sort_and_segment()
     {
-        if (own_set) { // the pair the previous step did not write (slab steps: never incremental, pair 0)
-            const int k = slab ? 0 : cur;
+        if (own_set) { // the pair the previous step did not write (host-orchestrated slab steps: pair 0)
+            const int k = (slab && !dist.on) ? 0 : cur;
             keys_sorted = ks_own[k];
             bstart = bs_own[k];
             bend = be_own[k];
@@ -631,26 +694,34 @@ template <class T, int D> struct Ctx : CtxBase {
             keys_valid = true;
         }
         // K1: the stored order is the previous step's sort -> rebuild it incrementally
-        const bool inc_ok = inc_enabled && !slab && n > 0 && inc_src.base == buf[cur].base && inc_src.ks &&
-                            inc_src.ks != keys_sorted && inc_src.bs != bstart && inc_src.be != bend;
+        const bool inc_ok = inc_source_ok() && (n > 0 || dist.on) && inc_src.ks != keys_sorted &&
+                            inc_src.bs != bstart && inc_src.be != bend;
+        last_sort_full = !inc_ok;
         if (inc_ok) {
             const IncSrc o = inc_src;
             CK(cudaMemsetAsync(counts, 0, sizeof(int) * 4, stream));
             CK(cudaMemsetAsync(nflag, 0, sc.nnb_total, stream));
+            IncSort is = inc;
+            is.d_n = dist.on ? dist.d_n : nullptr; // decomposed steps: the count lives on the device
+            const int64_t nthr = dist.on ? cap : n;
             launch("k_sort_classify", [&] {
-                k_inc_classify<D><<<grid_for(n, 256), 256, 0, stream>>>(keys, o.ks, int(n), sc.nb_total, inc);
+                k_inc_classify<D><<<grid_for((nthr + 3) / 4, 256), 256, 0, stream>>>(keys, o.ks, int(n), sc.nb_total, is);
             });
             const bool lpt = occ_lpt && D == 3;
-            launch("k_sort_scan", [&] {
+            const unsigned nbc = unsigned((sc.nb_total + 255) / 256);
+            launch("k_sort_count", [&] {
+                k_inc_count<D><<<nbc, 256, 0, stream>>>(sc.nb_total, o.bs, o.be, inc, bend);
+            });
+            launch("k_sort_offsets", [&] {
                 if (lpt)
-                    k_inc_scan<D, true><<<1, 1024, 0, stream>>>(sc.nb_total, o.bs, o.be, inc, bstart, bend, occ, counts);
+                    k_inc_offsets<D, true><<<nbc, 256, 0, stream>>>(sc.nb_total, inc, bstart, bend, occ, counts);
                 else
-                    k_inc_scan<D, false><<<1, 1024, 0, stream>>>(sc.nb_total, o.bs, o.be, inc, bstart, bend, occ, counts);
+                    k_inc_offsets<D, false><<<nbc, 256, 0, stream>>>(sc.nb_total, inc, bstart, bend, occ, counts);
             });
             launch("k_sort_place", [&] { k_inc_place<D><<<nsm, 256, 0, stream>>>(keys, inc, nsm * 256); });
             launch("k_sort_block", [&] {
-                k_inc_block<D><<<persistent(8), INC_THREADS, 0, stream>>>(keys, o.bs, o.be, inc, bstart, bend, occ,
-                                                                          counts, perm, keys_sorted, lstart);
+                k_inc_block<D><<<persistent(8), INC_THREADS, 0, stream>>>(keys, o.ks, o.bs, o.be, inc, bstart, bend,
+                                                                          occ, counts, perm, keys_sorted, lstart);
             });
         } else {
             // radix-sort only the bits a valid key can have (C4: 24 bits -> 3 onesweep passes). An
@@ -754,7 +825,7 @@ template <class T, int D> struct Ctx : CtxBase {
 #endif
             launch("k_g2p", [&] { k_g2p<T, D, FL, false, false><<<gr, 256, sm, stream>>>(sc, Pin, Pout, G, perm, bstart, bend, occ, counts, keys, st, mig, wq_ptr(WQ_G2P)); });
         }
-        inc_src = slab ? IncSrc{} : IncSrc{Pout.base, keys_sorted, bstart, bend};
+        inc_src = (slab && !dist.on) ? IncSrc{} : IncSrc{Pout.base, keys_sorted, bstart, bend};
         cur ^= 1;
         keys_valid = true;
     }
@@ -816,6 +887,11 @@ template <class T, int D> struct Ctx : CtxBase {
         if (s.far_flag)
             throw ApiError(MPM_ERR_NUMERICAL, "P2G: a particle block exceeds the staging capacity (extreme compression)",
                            -1, s.step + 1);
+        if (s.mig_over)
+            throw ApiError(MPM_ERR_CUDA, "slab migration buffer overflow (raise mig_cap)", -1, s.step + 1);
+        if (s.pad2)
+            throw ApiError(MPM_ERR_NUMERICAL, "slab: another rank aborted step " + std::to_string(s.step + 1), -1,
+                           s.step + 1);
         throw ApiError(MPM_ERR_NUMERICAL, "device step aborted", -1, s.step);
     }
 
@@ -1225,6 +1301,288 @@ template <class T, int D> struct Ctx : CtxBase {
         *lo = mig_cnt[0];
         *hi = mig_cnt[1];
     }
+    // ---- library-owned slab decomposition (kernels_dist.cuh) -----------------------
+    // One decomposed step, all on the device (no host synchronisation):
+    //   A  sort (incremental, device count) + P2G + band-only grid sum; pack both halo bands
+    //   X1 halo exchange with the x-neighbours (NCCL on the communication stream, or device copies)
+    //   B  interior grid pass while the bands travel; fixed-order import of the neighbours' bands
+    //      (lower rank's partial first); band grid update; G2P (exports leavers); publish the
+    //      export counts and the abort flag
+    //   X2 migration messages (count + fixed-capacity records) and the abort max-reduction
+    //   C  a peer's abort becomes this rank's; append the received migrants (particle-id order)
+    int dist_device() const override { return device; }
+    void dist_attach(int rank, int nranks, int lo, int hi, int64_t mig_cap, const void* nccl_id) override
+    {
+        if (nranks < 1 || rank < 0 || rank >= nranks)
+            throw ApiError(MPM_ERR_USAGE, "dist: rank outside [0, nranks)");
+        if (dist.on)
+            throw ApiError(MPM_ERR_USAGE, "dist: context already attached");
+        if (mig_cap < 1)
+            throw ApiError(MPM_ERR_USAGE, "dist: migration capacity must be positive");
+        slab_set(lo, hi, mig_cap);
+        dist.on = true;
+        dist.rank = rank;
+        dist.nranks = nranks;
+        dist.lo_peer = rank > 0 ? rank - 1 : -1;
+        dist.hi_peer = rank + 1 < nranks ? rank + 1 : -1;
+        int64_t plane = 1;
+        for (int a = 1; a < D; ++a)
+            plane *= sc.cells[a] + 1;
+        dist.halo_elems = 2 * plane * C::NF;
+        for (int k = 0; k < 2; ++k) {
+            dist.halo_send[k] = alloc<T>(dist.halo_elems);
+            dist.halo_recv[k] = alloc<T>(dist.halo_elems);
+            dist.recs_recv[k] = alloc<T>((size_t)mig.cap * mig.rec);
+            dist.pid_recv[k] = alloc<int>(mig.cap);
+        }
+        dist.cnt_send = alloc<long long>(2);
+        dist.cnt_recv = alloc<long long>(2);
+        dist.d_n = alloc<int>(1);
+        dist.d_nlive = inc.nlive;
+        dist.abort_red = alloc<int>(2);
+        CK(cudaMemsetAsync(dist.abort_red, 0, 2 * sizeof(int), stream));
+        CK(cudaMemsetAsync(dist.cnt_send, 0, 2 * sizeof(long long), stream));
+        CK(cudaMemsetAsync(dist.cnt_recv, 0, 2 * sizeof(long long), stream));
+        CK(cudaEventCreateWithFlags(&dist.ev_a, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&dist.ev_b, cudaEventDisableTiming));
+        if (nccl_id) {
+            CK(cudaStreamCreateWithFlags(&dist.comm_stream, cudaStreamNonBlocking));
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            CK(cudaSetDevice(device));
+            NCK(ncclCommInitRank(&dist.comm, nranks, id, rank));
+        }
+        CK(cudaStreamSynchronize(stream));
+    }
+    void dist_step_begin()
+    {
+        const int ni = int(n);
+        CK(cudaMemcpyAsync(dist.d_n, &ni, sizeof(int), cudaMemcpyHostToDevice, stream));
+    }
+    void dist_phase_a()
+    {
+        launch("k_dist", [&] { k_dist_step_begin<<<1, 1, 0, stream>>>(st); });
+        sort_and_segment();
+        if (last_sort_full) { // the radix sort path: the live count from the block tables
+            CK(cudaMemsetAsync(dist.d_nlive, 0, sizeof(int), stream));
+            launch("k_dist", [&] { k_dist_nlive<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bend, sc.nb_total, dist.d_nlive); });
+        }
+        p2g_kernel();
+        grid_kernel<G_BANDONLY | G_SUM | G_NOGRAV | G_STORE>();
+        if (dist.lo_peer >= 0)
+            halo(sc.slab_lo, 2, dist.halo_send[0], 0);
+        if (dist.hi_peer >= 0)
+            halo(sc.slab_hi, 2, dist.halo_send[1], 0);
+    }
+    void dist_phase_b(bool guard)
+    {
+        // (the interior pass ran while the bands were in flight)
+        if (dist.lo_peer >= 0) // the lower rank's partial first: received + own
+            halo(sc.slab_lo, 2, dist.halo_recv[0], 1);
+        if (dist.hi_peer >= 0) // own (lower) + received
+            halo(sc.slab_hi, 2, dist.halo_recv[1], 2);
+        finish_phase(guard);
+        launch("k_dist", [&] {
+            k_dist_publish<<<1, 1, 0, stream>>>(st, dist.cnt_send, dist.cnt_send + 1, dist.abort_red, mig.cap);
+        });
+    }
+    void dist_phase_c(const int* reduced)
+    {
+        launch("k_dist", [&] { k_dist_merge_abort<<<1, 1, 0, stream>>>(st, reduced); });
+        launch("k_dist", [&] {
+            k_dist_import<T, D><<<grid_for(2 * int64_t(mig.cap), 256), 256, 0, stream>>>(
+                sc, buf[cur], dist.d_nlive, dist.d_n, dist.cnt_recv, dist.recs_recv[0], dist.pid_recv[0],
+                dist.cnt_recv + 1, dist.recs_recv[1], dist.pid_recv[1], mig.cap, mig.rec, has_aff, has_F, keys,
+                const_cast<int*>(keys_sorted), int(cap), st);
+        });
+    }
+    // NCCL: both exchanges of a step on the communication stream, ordered by events
+    void dist_exchange_halo_nccl()
+    {
+        const size_t hb = sizeof(T) * dist.halo_elems;
+        CK(cudaEventRecord(dist.ev_a, stream));
+        CK(cudaStreamWaitEvent(dist.comm_stream, dist.ev_a, 0));
+        NCK(ncclGroupStart());
+        if (dist.lo_peer >= 0) {
+            NCK(ncclSend(dist.halo_send[0], hb, ncclUint8, dist.lo_peer, dist.comm, dist.comm_stream));
+            NCK(ncclRecv(dist.halo_recv[0], hb, ncclUint8, dist.lo_peer, dist.comm, dist.comm_stream));
+        }
+        if (dist.hi_peer >= 0) {
+            NCK(ncclSend(dist.halo_send[1], hb, ncclUint8, dist.hi_peer, dist.comm, dist.comm_stream));
+            NCK(ncclRecv(dist.halo_recv[1], hb, ncclUint8, dist.hi_peer, dist.comm, dist.comm_stream));
+        }
+        NCK(ncclGroupEnd());
+        CK(cudaEventRecord(dist.ev_b, dist.comm_stream));
+    }
+    void dist_exchange_mig_nccl()
+    {
+        const size_t rb = sizeof(T) * size_t(mig.rec) * mig.cap, pb = sizeof(int) * size_t(mig.cap);
+        CK(cudaEventRecord(dist.ev_a, stream));
+        CK(cudaStreamWaitEvent(dist.comm_stream, dist.ev_a, 0));
+        NCK(ncclGroupStart());
+        for (int side = 0; side < 2; ++side) {
+            const int peer = side == 0 ? dist.lo_peer : dist.hi_peer;
+            if (peer < 0)
+                continue;
+            NCK(ncclSend(dist.cnt_send + side, sizeof(long long), ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(ncclSend(side == 0 ? mig.lo : mig.hi, rb, ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(ncclSend(side == 0 ? mig.lo_pid : mig.hi_pid, pb, ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(ncclRecv(dist.cnt_recv + side, sizeof(long long), ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(ncclRecv(dist.recs_recv[side], rb, ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(ncclRecv(dist.pid_recv[side], pb, ncclUint8, peer, dist.comm, dist.comm_stream));
+        }
+        if (dist.nranks > 1)
+            NCK(ncclAllReduce(dist.abort_red, dist.abort_red, 1, ncclInt32, ncclMax, dist.comm, dist.comm_stream));
+        NCK(ncclGroupEnd());
+        CK(cudaEventRecord(dist.ev_b, dist.comm_stream));
+        CK(cudaStreamWaitEvent(stream, dist.ev_b, 0));
+    }
+    void dist_step_nccl(bool guard)
+    {
+        dist_phase_a();
+        dist_exchange_halo_nccl();
+        step_grid_interior(); // overlaps the band exchange
+        CK(cudaStreamWaitEvent(stream, dist.ev_b, 0));
+        dist_phase_b(guard);
+        dist_exchange_mig_nccl();
+        dist_phase_c(dist.abort_red);
+    }
+    // same-process ranks (tests, or several GPUs driven by one host thread): the same phases in
+    // lock-step, exchanges as device copies ordered by events; all[r] is rank r
+    void dist_enqueue_local(std::vector<CtxBase*>& all, int64_t nsteps, uint32_t flags) override
+    {
+        const int R = int(all.size());
+        if (R > DIST_MAX_LOCAL)
+            throw ApiError(MPM_ERR_USAGE, "dist: too many same-process ranks");
+        std::vector<Ctx*> cs(R);
+        for (int r = 0; r < R; ++r) {
+            cs[r] = dynamic_cast<Ctx*>(all[r]);
+            if (!cs[r] || !cs[r]->dist.on || cs[r]->dist.comm || cs[r]->dist.rank != r || cs[r]->dist.nranks != R)
+                throw ApiError(MPM_ERR_USAGE, "dist: contexts must be attached as same-process ranks 0..R-1 of one scene type");
+            if (!cs[r]->has_state)
+                throw ApiError(MPM_ERR_USAGE, "no state uploaded");
+        }
+        const bool guard = flags & MPM_ADV_NAN_GUARD;
+        AbortPtrs ap{};
+        ap.R = R;
+        for (int r = 0; r < R; ++r)
+            ap.p[r] = cs[r]->dist.abort_red;
+        for (Ctx* c : cs) {
+            c->reset_status();
+            c->dist_step_begin();
+        }
+        auto wait_on = [](Ctx* c, Ctx* peer) { CK(cudaStreamWaitEvent(c->stream, peer->dist.ev_a, 0)); };
+        for (int64_t k = 0; k < nsteps; ++k) {
+            for (Ctx* c : cs) {
+                c->dist_phase_a();
+                CK(cudaEventRecord(c->dist.ev_a, c->stream));
+            }
+            for (int r = 0; r < R; ++r) {
+                Ctx* c = cs[r];
+                const size_t hb = sizeof(T) * c->dist.halo_elems;
+                for (int side = 0; side < 2; ++side) {
+                    const int pr = side == 0 ? c->dist.lo_peer : c->dist.hi_peer;
+                    if (pr < 0)
+                        continue;
+                    wait_on(c, cs[pr]);
+                    CK(cudaMemcpyAsync(c->dist.halo_recv[side], cs[pr]->dist.halo_send[1 - side], hb,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+                }
+            }
+            for (Ctx* c : cs) {
+                c->step_grid_interior();
+                c->dist_phase_b(guard);
+                CK(cudaEventRecord(c->dist.ev_a, c->stream));
+            }
+            for (int r = 0; r < R; ++r) {
+                Ctx* c = cs[r];
+                const size_t rb = sizeof(T) * size_t(c->mig.rec) * c->mig.cap, pb = sizeof(int) * size_t(c->mig.cap);
+                for (int q = 0; q < R; ++q)
+                    if (q != r)
+                        wait_on(c, cs[q]);
+                for (int side = 0; side < 2; ++side) {
+                    const int pr = side == 0 ? c->dist.lo_peer : c->dist.hi_peer;
+                    if (pr < 0)
+                        continue;
+                    Ctx* p = cs[pr];
+                    CK(cudaMemcpyAsync(c->dist.cnt_recv + side, p->dist.cnt_send + (1 - side), sizeof(long long),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+                    CK(cudaMemcpyAsync(c->dist.recs_recv[side], side == 0 ? p->mig.hi : p->mig.lo, rb,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+                    CK(cudaMemcpyAsync(c->dist.pid_recv[side], side == 0 ? p->mig.hi_pid : p->mig.lo_pid, pb,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+                }
+                c->launch("k_dist", [&] { k_dist_abort_max<<<1, 1, 0, c->stream>>>(ap, c->dist.abort_red + 1); });
+                CK(cudaEventRecord(c->dist.ev_b, c->stream));
+            }
+            for (Ctx* c : cs) { // every rank has read its peers' messages before they are rewritten
+                for (Ctx* q : cs)
+                    if (q != c)
+                        CK(cudaStreamWaitEvent(c->stream, q->dist.ev_b, 0));
+                c->dist_phase_c(c->dist.abort_red + 1);
+            }
+        }
+    }
+    void dist_finish() override { dist_finish_call(); }
+    // n decomposed steps on an NCCL rank; graph-replayed after the first (its radix sort and the
+    // count upload run eagerly), no host synchronisation until the status check at the end
+    void dist_advance(int64_t nsteps, uint32_t flags, double* ms) override
+    {
+        if (!dist.on || !dist.comm)
+            throw ApiError(MPM_ERR_USAGE, "dist: context not attached to an NCCL communicator");
+        if (!has_state)
+            throw ApiError(MPM_ERR_USAGE, "no state uploaded");
+        const bool guard = flags & MPM_ADV_NAN_GUARD;
+        reset_status();
+        dist_step_begin();
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (ms) {
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            CK(cudaEventRecord(e0, stream));
+        }
+        for (int64_t k = 0; k < nsteps; ++k) {
+            const bool eager = prof || !inc_source_ok();
+            if (eager) {
+                dist_step_nccl(guard);
+                continue;
+            }
+            cudaGraphExec_t& ge = dist.graph[guard][cur];
+            if (!ge) {
+                dist.graph_launches = capture(ge, [&] { dist_step_nccl(guard); });
+                dist.graph_inc[guard][cur] = captured_inc_src;
+            }
+            CK(cudaGraphLaunch(ge, stream));
+            launches += dist.graph_launches;
+            inc_src = dist.graph_inc[guard][cur];
+            keys_sorted = ks_own[cur];
+            bstart = bs_own[cur];
+            bend = be_own[cur];
+            cur ^= 1;
+            keys_valid = true;
+        }
+        if (ms) {
+            CK(cudaEventRecord(e1, stream));
+            CK(cudaEventSynchronize(e1));
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, e0, e1));
+            *ms = t;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+        dist_finish_call();
+    }
+    // after a call: the device count and status come back once
+    void dist_finish_call()
+    {
+        int dn = 0;
+        CK(cudaMemcpyAsync(&dn, dist.d_n, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        n = dn;
+        n_dead = 0; // vacated slots are dropped by the next sort; download_local skips them (pid < 0)
+        check_status(step);
+    }
+
     void* ids_scratch = nullptr;
     size_t ids_scratch_bytes = 0;
     void* aw_ids_scratch(int64_t k)
@@ -2223,6 +2581,63 @@ int mpm_profile_query(mpm_ctx* c, const char* name, double* ms, int64_t* launche
 }
 
 int64_t mpm_launch_count(const mpm_ctx* c) { return c ? c->impl->launches : -1; }
+
+int mpm_dist_unique_id(void* id_out)
+{
+    if (!id_out)
+        return MPM_ERR_USAGE;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess)
+        return MPM_ERR_CUDA;
+    std::memcpy(id_out, &id, sizeof(id));
+    return MPM_OK;
+}
+int mpm_dist_attach_nccl(mpm_ctx* c, int rank, int nranks, const void* nccl_id, int cell_lo, int cell_hi,
+                         int64_t mig_cap)
+{
+    if (!nccl_id)
+        return MPM_ERR_USAGE;
+    MPM_CALL(c, c->impl->dist_attach(rank, nranks, cell_lo, cell_hi, mig_cap, nccl_id));
+}
+int mpm_dist_attach_local(mpm_ctx* const* ctxs, int nranks, const int* bounds, int64_t mig_cap)
+{
+    if (!ctxs || nranks < 1 || !bounds)
+        return MPM_ERR_USAGE;
+    for (int r = 0; r < nranks; ++r) {
+        const int rc = guarded(ctxs[r], [&] {
+            if (!ctxs[r])
+                throw ApiError(MPM_ERR_USAGE, "null context");
+            ctxs[r]->impl->dist_attach(r, nranks, bounds[r], bounds[r + 1], mig_cap, nullptr);
+        });
+        if (rc)
+            return rc;
+    }
+    return MPM_OK;
+}
+int mpm_dist_advance(mpm_ctx* c, int64_t n_steps, uint32_t flags, double* device_ms)
+{
+    MPM_CALL(c, c->impl->dist_advance(n_steps, flags, device_ms));
+}
+int mpm_dist_advance_local(mpm_ctx* const* ctxs, int nranks, int64_t n_steps, uint32_t flags)
+{
+    if (!ctxs || nranks < 1)
+        return MPM_ERR_USAGE;
+    std::vector<CtxBase*> all(nranks);
+    for (int r = 0; r < nranks; ++r) {
+        if (!ctxs[r])
+            return MPM_ERR_USAGE;
+        all[r] = ctxs[r]->impl.get();
+    }
+    int rc = guarded(ctxs[0], [&] { all[0]->dist_enqueue_local(all, n_steps, flags); });
+    if (rc)
+        return rc;
+    for (int r = 0; r < nranks; ++r) { // every rank's status once, after the call
+        const int e = guarded(ctxs[r], [&] { all[r]->dist_finish(); });
+        if (e && !rc)
+            rc = e;
+    }
+    return rc;
+}
 
 int mpm_grid_stats(mpm_ctx* c, int64_t* an, int64_t* ob, int64_t* anb) { MPM_CALL(c, c->impl->grid_stats(an, ob, anb)); }
 

@@ -835,3 +835,144 @@ def local_slab_run(scene: Scene, state: SimState, n_ranks: int, steps: int, nan_
 
 __all__ = ["SlabPlan", "SlabDomain", "SlabStepper", "LocalTransport", "TorchTransport", "GpuSlabDomain",
            "PeerFailure", "local_slab_run", "slab_step_vjp", "slab_backprop_trajectory", "block_edge", "base_cell_x"]
+
+
+# ---------------------------------------------------------------------------------------------
+# The library-owned decomposition (include/mpm_capi.h, mpm_dist_*): the same slab step, run
+# inside libmpm_b200 with device-resident counts and no host synchronisation inside a call. The
+# classes above orchestrate the step from Python (the protocol reference, and the decomposed
+# adjoint); these drive the C++ path.
+def dist_unique_id() -> bytes:
+    """An NCCL unique id from the library (rank 0 makes it, every rank receives it)."""
+    from . import capi
+
+    lib = capi.load_library()
+    buf = (C.c_ubyte * capi.DIST_ID_BYTES)()
+    rc = lib.mpm_dist_unique_id(buf)
+    if rc:
+        raise MPMError(f"mpm_dist_unique_id failed ({rc})")
+    return bytes(buf)
+
+
+def _dist_capacity(n_local: int, n_total: int, n_ranks: int, mig_cap: int) -> int:
+    """room for particles arriving from the neighbours: a quarter of an average slab, plus one
+    step's worst-case arrivals (2 mig_cap)"""
+    return max(1024, int(1.25 * n_local) + n_total // (4 * n_ranks) + 2 * mig_cap)
+
+
+class NcclSlabRank:
+    """This process's rank of the decomposition (one process per GPU): a context owning particles
+    [lo, hi) of the plan and an NCCL communicator (mpm_dist_attach_nccl)."""
+
+    def __init__(self, scene: Scene, plan: SlabPlan, rank: int, state: SimState, ids: np.ndarray, nccl_id: bytes,
+                 device: int = 0, n_total: int | None = None, mig_cap: int | None = None, capacity: int | None = None):
+        from .solver import Context
+
+        self.scene, self.plan, self.rank = scene, plan, rank
+        n_local = state.particles.size()
+        n_total = int(n_total or n_local * plan.n_ranks)
+        self.mig_cap = int(mig_cap or max(1024, n_total // (256 * plan.n_ranks)))
+        self.capacity = int(capacity or _dist_capacity(n_local, n_total, plan.n_ranks, self.mig_cap))
+        self.ctx = Context(scene, self.capacity, device)
+        self.lib, self.h = self.ctx.lib, self.ctx.h
+        v, keep = state.to_view()
+        ids64 = np.ascontiguousarray(ids, dtype=np.int64)
+        self.ctx.check(self.lib.mpm_state_upload_ids(self.h, C.byref(v), ids64.ctypes.data_as(C.c_void_p)))
+        idb = (C.c_ubyte * len(nccl_id)).from_buffer_copy(nccl_id)
+        self.ctx.check(self.lib.mpm_dist_attach_nccl(self.h, rank, plan.n_ranks, idb, plan.lo(rank), plan.hi(rank),
+                                                     self.mig_cap))
+        self._template = state
+
+    def advance(self, n: int, nan_guard: bool = False) -> float:
+        """n decomposed steps; returns their device time (ms, CUDA events on the context stream)"""
+        from . import capi
+
+        ms = C.c_double()
+        self.ctx.check(self.lib.mpm_dist_advance(self.h, int(n), capi.MPM_ADV_NAN_GUARD if nan_guard else 0,
+                                                 C.byref(ms)))
+        return ms.value
+
+    def gather(self):
+        """(particles, global ids, (step, time)) of this rank's live particles"""
+        k = int(self.lib.mpm_local_count(self.h))
+        p = self._template.particles
+        sub = SimState(ParticleSoA(k, p.dim, p.dtype, p.affine is not None, p.def_grad is not None))
+        v, keep = sub.output_view()
+        ids = np.empty(max(k, 1), np.int64)
+        self.ctx.check(self.lib.mpm_state_download_local(self.h, C.byref(v), ids.ctypes.data_as(C.c_void_p)))
+        sub.sync_from(v, keep)
+        return sub.particles.take(np.arange(v.n)), ids[:v.n], (sub.step, sub.time)
+
+    def close(self):
+        self.ctx.close()
+
+
+class LocalSlabGroup:
+    """All ranks of the decomposition in this process (mpm_dist_attach_local): R contexts, stepped
+    in lock-step by the library with device-copy exchanges -- the single-GPU test bed of the NCCL
+    path (same phases, same kernels, only the transport differs)."""
+
+    def __init__(self, scene: Scene, plan: SlabPlan, state: SimState, device: int = 0, mig_cap: int | None = None):
+        from .solver import Context
+
+        self.scene, self.plan = scene, plan
+        parts = plan.partition(scene, state)
+        n_total = state.particles.size()
+        R = plan.n_ranks
+        self.mig_cap = int(mig_cap or max(256, n_total // (64 * R)))
+        self.ctxs = []
+        for r in range(R):
+            ids = parts[r]
+            sub = SimState(state.particles.take(ids), state.step, state.time)
+            ctx = Context(scene, _dist_capacity(len(ids), n_total, R, self.mig_cap), device)
+            v, keep = sub.to_view()
+            ids64 = np.ascontiguousarray(ids, dtype=np.int64)
+            ctx.check(ctx.lib.mpm_state_upload_ids(ctx.h, C.byref(v), ids64.ctypes.data_as(C.c_void_p)))
+            self.ctxs.append(ctx)
+        self.lib = self.ctxs[0].lib
+        self._arr = (C.c_void_p * R)(*[c.h for c in self.ctxs])
+        bounds = (C.c_int * (R + 1))(*plan.bounds)
+        rc = self.lib.mpm_dist_attach_local(self._arr, R, bounds, self.mig_cap)
+        if rc:
+            self.ctxs[0].check(rc)
+        self._template = state
+        self.n_total = n_total
+
+    def advance(self, n: int, nan_guard: bool = False):
+        from . import capi
+
+        rc = self.lib.mpm_dist_advance_local(self._arr, len(self.ctxs), int(n),
+                                             capi.MPM_ADV_NAN_GUARD if nan_guard else 0)
+        if rc:  # every rank raises at the same step; report the failing rank's own error first
+            errs = []
+            for c in self.ctxs:
+                code = C.c_int()
+                buf = C.create_string_buffer(1024)
+                c.lib.mpm_last_error(c.h, C.byref(code), None, None, buf, 1024)
+                if code.value:
+                    errs.append((b"another rank" in buf.value, c, code.value))
+            errs.sort(key=lambda e: e[0])
+            if errs:
+                errs[0][1].check(errs[0][2])
+            self.ctxs[0].check(rc)
+
+    def gather(self) -> SimState:
+        """the global state in particle-id order"""
+        out = self._template.copy()
+        step = None
+        for c in self.ctxs:
+            k = int(c.lib.mpm_local_count(c.h))
+            p = self._template.particles
+            sub = SimState(ParticleSoA(k, p.dim, p.dtype, p.affine is not None, p.def_grad is not None))
+            v, keep = sub.output_view()
+            ids = np.empty(max(k, 1), np.int64)
+            c.check(c.lib.mpm_state_download_local(c.h, C.byref(v), ids.ctypes.data_as(C.c_void_p)))
+            sub.sync_from(v, keep)
+            out.particles.put(ids[:v.n], sub.particles.take(np.arange(v.n)))
+            step = (v.step, v.time)
+        out.step, out.time = step
+        return out
+
+    def close(self):
+        for c in self.ctxs:
+            c.close()

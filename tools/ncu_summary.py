@@ -16,7 +16,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__block_size",
         "launch__grid_size", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
-        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem"]
+        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "lts__t_sector_hit_rate.pct",
+        "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+        "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"]
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -40,8 +42,11 @@ def main():
         b = 0.0
         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             b += float(d[k]) * SCALE.get(units[hdr.index(k)], 1.0)
-        short = "k_p2g" if name.startswith("k_p2g") else ("k_g2p" if name.startswith("k_g2p") else name)
+        short = next((k for k in ("k_p2g", "k_g2p", "k_grid", "k_inc_block", "k_inc_scan", "k_inc_classify")
+                      if name.startswith(k)), name)
         traffic[short] = {"dram_bytes": b, "kernel": name, "source": Path(rep).name}
+        if d.get("lts__t_sector_hit_rate.pct") not in (None, ""):
+            traffic[short]["l2_hit_rate_pct"] = float(d["lts__t_sector_hit_rate.pct"])
     out.write_text(json.dumps(summary, indent=1))
     tp = out.parent / "traffic.json"
     old = json.loads(tp.read_text()) if tp.exists() else {}

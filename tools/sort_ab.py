@@ -23,7 +23,7 @@ for cfg in sys.argv[1:] or ["C4", "C3", "C2"]:
         ctx.profile_reset()
         ctx.advance(10)
         parts = {}
-        for name in ("k_keys", "k_sort_classify", "k_sort_scan", "k_sort_place", "k_sort_block", "k_seg", "k_occ", "k_compact", "k_mark_nodes", "k_p2g", "k_grid", "k_g2p"):
+        for name in ("k_keys", "k_sort_classify", "k_sort_count", "k_sort_offsets", "k_sort_place", "k_sort_block", "k_seg", "k_occ", "k_compact", "k_mark_nodes", "k_p2g", "k_grid", "k_g2p"):
             t, nl = ctx.profile_query(name)
             if nl:
                 parts[name] = round(t / 10 * 1e3, 1)
