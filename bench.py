@@ -130,6 +130,43 @@ def kernel_bytes(scene, n, active_nodes, occupied_blocks):
     return alg, need, moved
 
 
+# particle counts of the configs' init_scene seeding (pinned by tests/test_gpu_configs.py)
+N_PARTICLES = {"C1": 20_000, "C2": 250_000, "C3": 102_400, "C4": 4_194_304, "C5": 32_505_856}
+GRID = {"C1": [128, 128], "C2": [512, 512], "C3": [480, 192], "C4": [256, 256, 256], "C5": [512, 256, 128]}
+DESC = {"C4": "3-D D-P granular column collapse, FLIP, 128x64x64-cell column on a 256^3 grid, dt 1e-5, f64",
+        "C1": "2-D D-P column (Bui), 20k particles, 128^2", "C2": "2-D dam break, fluid, 250k particles, 512^2",
+        "C3": "2-D inverse-velocity scene, fluid, 102k particles, 480x192",
+        "C5": "3-D landslide, D-P + 32-segment Coulomb floor, 32.5M particles, 512x256x128"}
+
+
+def run_mode(a, world):
+    if a.mode == "pyslab":
+        return "pyslab"
+    return "dist" if (a.mode == "slab" or (a.mode == "auto" and world > 1)) else "plain"
+
+
+def workload_config(a, world):
+    """The line's `config`: the static description of the workload, identical in both arms
+    (--impl b200 and --impl reference) at the same N. Measured quantities (active nodes, bytes,
+    slab bounds after balancing, migration counts) live in `roofline` / `slab`, not here."""
+    mode = run_mode(a, world)
+    n = N_PARTICLES[a.config]
+    cells = list(GRID[a.config])
+    l2 = "inputs larger than the 126 MB L2 (state >= 0.9 GB f64 per GPU at C4); no flush"
+    if mode == "plain":
+        return {"workload": f"{a.config}: {DESC[a.config]}", "particles_per_gpu": n, "grid_cells": cells,
+                "parallelism": f"replicas x{world}", "l2_policy": l2}
+    weak = a.config == "C4" and a.scaling == "weak"
+    if weak:
+        cells[0] *= world
+        return {"workload": f"C4 x{world} (weak scaling): one C4 column per GPU, {DESC['C4']}",
+                "particles_total": n * world, "particles_per_gpu": n, "grid_cells": cells,
+                "parallelism": f"slab x{world} along x (library-owned NCCL halo + migration)", "l2_policy": l2}
+    return {"workload": f"{a.config} (strong scaling): the one scene split into {world} particle-balanced slabs, "
+                        f"{DESC[a.config]}", "particles_total": n, "grid_cells": cells,
+            "parallelism": f"slab x{world} along x (library-owned NCCL halo + migration)", "l2_policy": l2}
+
+
 # ---- clocks sampler -------------------------------------------------------------------------
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -180,13 +217,16 @@ class ClockSampler:
 def _cpu_worker(args):
     """One host process: the reference's own run() timer (stepper.hpp:91-122) for mode "fwd", or the
     wall clock of its backprop_trajectory (checkpoint.hpp:72-143) for mode "adj", on the full scene."""
-    cfg, dtype, kind, steps, mode, nseg = args
+    cfg, dtype, kind, steps, mode, nseg = args[:6]
+    warm = args[6] if len(args) > 6 else 0
     sys.path.insert(0, str(ROOT))
     from oracle import CpuOracle  # test infrastructure: the CPU baseline, never the product path
     from paper_2507_04192_b200.presets import CONFIGS
     s = CONFIGS[cfg](dtype=dtype)
     o = CpuOracle(kind)
     st = o.init_scene(s)
+    if warm and mode == "fwd":
+        o.advance(s, st, warm)  # untimed warm-up steps
     if mode == "fwd":
         secs = o.run_seconds_per_1000(s, st, steps) / 1000.0 * steps
     else:
@@ -221,7 +261,7 @@ def _cpu_model():
 _PROC_GB = {"fwd": {"C4": 6.0, "C5": 40.0, "C5/8": 6.0}, "adj": {"C4": 14.0, "C5": 100.0, "C5/8": 14.0}}
 
 
-def cpu_sample(cfg, dtype="f64", steps=1, mode="fwd", nseg=1, kind=None, procs=None):
+def cpu_sample(cfg, dtype="f64", steps=1, mode="fwd", nseg=1, kind=None, procs=None, warm=0):
     """The reference (oracle/_ref, compiled unmodified) -- or the restatement -- on the full scene
     `cfg`: `steps` forward steps (mode "fwd") or a backprop_trajectory over `steps` steps (mode
     "adj"), in `procs` concurrent processes (default: one per host core, capped by host memory;
@@ -236,7 +276,7 @@ def cpu_sample(cfg, dtype="f64", steps=1, mode="fwd", nseg=1, kind=None, procs=N
     procs = min(procs or cap, cap)
     with mp.get_context("spawn").Pool(procs) as pool:
         t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, [(cfg, dtype, kind, steps, mode, nseg)] * procs)
+        res = pool.map(_cpu_worker, [(cfg, dtype, kind, steps, mode, nseg, warm)] * procs)
         wall = time.perf_counter() - t0
     per_proc = [r[0] / r[1] for r in res]
     n = int(res[0][0] / steps)
@@ -572,11 +612,7 @@ def bench_b200(a, rank, world, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": a.dtype, "data": "synthetic (init_scene seeding of the named scene, deterministic)",
-        "config": {"workload": f"{a.config}: 3-D D-P granular column collapse, FLIP, 128x64x64-cell column on 256^3 "
-                               f"grid, dt 1e-5" if a.config == "C4" else a.config,
-                   "particles_per_gpu": n, "grid_cells": s.config.cells, "parallelism": f"replicas x{world}",
-                   "l2_policy": "inputs (state ~1.4 GB f64) larger than the 126 MB L2; no flush",
-                   "algorithmic_bytes_per_particle_step": B_fwd, "active_nodes_per_particle": active_nodes_step / n},
+        "config": workload_config(a, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_for(dom, a),
                      "algorithmic_bytes_per_launch": kb[dom], "mean_launch_ms": dom_ms,
@@ -586,7 +622,7 @@ def bench_b200(a, rank, world, local):
                               "DRAM count are in per_kernel",
                      "per_kernel": per_kernel,
                      "step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak,
-                              "bytes_per_particle_step": B_fwd,
+                              "bytes_per_particle_step": B_fwd, "active_nodes_per_particle": active_nodes_step / n,
                               "needed_bytes_per_particle_step": B_need,
                               "frac_needed": n * B_need / (ms_per_step / 1e3) / 1e9 / peak,
                               "note": "frac counts grad v stored every step (SURVEY's B_fwd); frac_needed counts "
@@ -654,7 +690,7 @@ def bench_slab(a, rank, world, local):
     mig = torch.tensor([stp.migrated], device="cuda", dtype=torch.int64)
     dist.all_reduce(mig)
     # the slab path resets the device status every step: the counter holds the last step's nodes
-    act = torch.tensor([float(an1)], device="cuda", dtype=torch.float64)
+    act = torch.tensor([float(an1) / a.steps], device="cuda", dtype=torch.float64)  # counted over the K steps
     dist.all_reduce(act)
     # e2e: rank-local upload from pinned host + K decomposed steps + compact download, max over ranks
     e2e = bench_slab_e2e(dom, stp, a.steps)
@@ -753,7 +789,7 @@ def bench_dist(a, rank, world, local):
     ms = float(t.item())
     cnt = torch.tensor([int(rk.lib.mpm_local_count(rk.h))], device="cuda", dtype=torch.int64)
     dist.all_reduce(cnt)
-    act = torch.tensor([float(an1)], device="cuda", dtype=torch.float64)
+    act = torch.tensor([float(an1) / a.steps], device="cuda", dtype=torch.float64)  # counted over the K steps
     dist.all_reduce(act)
     # e2e: rank-local upload from pinned host + K decomposed steps + compact download, max over ranks
     e2e = dist_e2e(rk, st, ids, a.steps)
@@ -775,10 +811,9 @@ def bench_dist(a, rank, world, local):
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
         "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": a.dtype,
         "data": "synthetic (init_scene seeding of the named scene, deterministic)",
-        "config": {"workload": workload, "particles_total": n_total, "grid_cells": s.config.cells,
-                   "parallelism": f"slab x{world} (library-owned: NCCL halo + migration, device-resident counts)",
-                   "slab_bounds": plan.bounds, "particles_after": int(cnt.item()),
-                   "l2_policy": "inputs larger than the 126 MB L2; no flush"},
+        "config": workload_config(a, world),
+        "slab": {"workload": workload, "bounds": plan.bounds, "particles_after": int(cnt.item()),
+                 "path": "mpm_dist_advance: device-resident counts, no host synchronisation inside the K steps"},
         "roofline": {"bound": "hbm", "kernel": "step (per GPU)", "achieved": gbs, "peak": peak, "unit": "GB/s",
                      "frac": gbs / peak, "traffic": None, "bytes_per_particle_step": B_fwd,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s"},
@@ -1022,20 +1057,33 @@ def bench_e2e(ctx, s, st, steps):
 
 
 def bench_reference(a, rank, world):
-    """--impl reference: the reference's own CPU implementation of the step (oracle/_ref, compiled
-    unmodified against the Eigen shim) on all host cores, rank 0 only; each process runs
-    the full scene for 2 steps (a bounded sample: ~10-30 s per step per core at C4)."""
+    """--impl reference: the reference's own CPU implementation of the step (oracle/_ref: the
+    reference's headers compiled unmodified against the Eigen shim), rank 0 only, on all host
+    cores: P processes (one per core, capped by host memory) each run the full scene -- the
+    reference is serial and independent scenes are its only concurrency -- with
+    ceil(W / P) untimed and ceil(K / P) timed steps (the reference's run() timer), so the whole
+    run stays within a few minutes. value = sum of the per-process rates; `config` is the GPU
+    arm's (workload_config)."""
     if rank != 0:
         return None
-    res = cpu_baseline(a.config, a.dtype, 2)
+    import oracle
+    cores = os.cpu_count() or 1
+    per_proc_gb = _PROC_GB["fwd"].get(a.config, 1.0) * (0.5 if a.dtype == "f32" else 1.0)
+    procs = max(1, min(cores, int(_mem_available_gb() * 0.6 / per_proc_gb)))
+    k_each = max(1, -(-a.steps // procs))
+    res = cpu_sample(a.config, a.dtype, k_each, procs=procs, warm=max(0, -(-a.warmup // procs)))
     value = res["value"]
+    n = N_PARTICLES[a.config]
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": a.dtype, "data": "synthetic (init_scene seeding)",
-            "config": {"workload": a.config, "sample": res["sample"]},
+            "steps": k_each * res["cores"], "warmup": a.warmup, "ms_per_step": n / value * 1e3,
+            "higher_is_better": True, "scaling": "weak" if (world == 1 or a.scaling == "weak") else "strong",
+            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic (init_scene seeding, the reference's own)",
+            "config": workload_config(a, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
-                             "sample": res["sample"]},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": res["sample"], "cpu_model": res["cpu_model"], "label": res["label"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "steps = full-scene steps executed in total over the concurrent processes; ms_per_step = one "
+                    "full-scene step at the aggregate rate"}
 
 
 def main():

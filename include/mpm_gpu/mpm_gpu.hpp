@@ -25,7 +25,10 @@
 #include <mpm/scene.hpp>
 #include <mpm/transfer.hpp>
 
+#include <array>
 #include <chrono>
+#include <cmath>
+#include <cstring>
 #include <functional>
 #include <memory>
 #include <string>
@@ -367,6 +370,225 @@ template <class T, int dim> void constitutive_update(ParticleSoA<T, dim>& prt, c
             prt.def_grad[p] = st.particles.def_grad[p];
     }
 }
+
+// ---- multi-GPU: the library-owned slab decomposition (mpm_dist_*) -------------
+// The decomposed Stepper::advance (stepper.hpp:59-69) for a C++ caller: rank r owns the particles
+// whose base cell along x, floor((x - o) / dh - 1/2) (bspline.hpp:79-91), lies in
+// [bounds[r], bounds[r + 1]) -- bounds are multiples of the particle-block edge (16 cells in 2-D,
+// 8 in 3-D). The library does the halo exchange, the migration and the error reduction on the
+// device; a call of advance(n) has no host synchronisation inside.
+template <class T, int dim>
+std::vector<std::vector<Index>> slab_partition(const Scene<T, dim>& scene, const SimState<T, dim>& s,
+                                               const std::vector<int>& bounds)
+{
+    const int R = int(bounds.size()) - 1;
+    std::vector<std::vector<Index>> out(R);
+    for (Index i = 0; i < s.particles.size(); ++i) {
+        const double u = double((s.particles.x[i][0] - scene.config.origin[0]) / scene.config.dh);
+        const int b = int(std::floor(u - 0.5));
+        int r = 0;
+        while (r + 1 < R && b >= bounds[r + 1])
+            ++r;
+        out[r].push_back(i);
+    }
+    return out;
+}
+
+template <class T, int dim> SimState<T, dim> take_rows(const SimState<T, dim>& s, const std::vector<Index>& ids)
+{
+    SimState<T, dim> o;
+    const auto& p = s.particles;
+    auto& q = o.particles;
+    q.resize(Index(ids.size()), !p.affine.empty(), !p.def_grad.empty());
+    for (std::size_t k = 0; k < ids.size(); ++k) {
+        const Index i = ids[k];
+        q.x[k] = p.x[i];
+        q.v[k] = p.v[i];
+        q.mass[k] = p.mass[i];
+        q.volume[k] = p.volume[i];
+        q.rho[k] = p.rho[i];
+        q.eps_eq[k] = p.eps_eq[i];
+        if (dim == 2)
+            q.sigma_zz[k] = p.sigma_zz[i];
+        q.sigma[k] = p.sigma[i];
+        q.grad_v[k] = p.grad_v[i];
+        if (!p.affine.empty())
+            q.affine[k] = p.affine[i];
+        if (!p.def_grad.empty())
+            q.def_grad[k] = p.def_grad[i];
+    }
+    o.step = s.step;
+    o.time = s.time;
+    return o;
+}
+
+template <class T, int dim> void put_rows(SimState<T, dim>& s, const SimState<T, dim>& sub, const std::vector<Index>& ids)
+{
+    auto& p = s.particles;
+    const auto& q = sub.particles;
+    for (std::size_t k = 0; k < ids.size(); ++k) {
+        const Index i = ids[k];
+        p.x[i] = q.x[k];
+        p.v[i] = q.v[k];
+        p.mass[i] = q.mass[k];
+        p.volume[i] = q.volume[k];
+        p.rho[i] = q.rho[k];
+        p.eps_eq[i] = q.eps_eq[k];
+        if (dim == 2)
+            p.sigma_zz[i] = q.sigma_zz[k];
+        p.sigma[i] = q.sigma[k];
+        p.grad_v[i] = q.grad_v[k];
+        if (!p.affine.empty())
+            p.affine[i] = q.affine[k];
+        if (!p.def_grad.empty())
+            p.def_grad[i] = q.def_grad[k];
+    }
+    s.step = sub.step;
+    s.time = sub.time;
+}
+
+// one rank's context: upload of its subset (with global ids) and the compact download
+template <class T, int dim> class SlabContext : public Context<T, dim> {
+public:
+    SlabContext(const Scene<T, dim>& s, Index capacity, int device)
+        : Context<T, dim>(s, capacity, device)
+    {
+    }
+    void upload_subset(SimState<T, dim>& sub, const std::vector<Index>& ids)
+    {
+        auto v = state_view(sub);
+        std::vector<int64_t> id64(ids.begin(), ids.end());
+        this->check(mpm_state_upload_ids(this->handle(), &v, id64.data()));
+    }
+    // this rank's live particles and their global ids
+    SimState<T, dim> download_subset(std::vector<Index>& ids, bool with_affine, bool with_def_grad)
+    {
+        const Index k = Index(mpm_local_count(this->handle()));
+        SimState<T, dim> sub;
+        sub.particles.resize(k, with_affine, with_def_grad);
+        auto v = state_view(sub);
+        std::vector<int64_t> id64(std::max<Index>(k, 1));
+        this->check(mpm_state_download_local(this->handle(), &v, id64.data()));
+        auto& q = sub.particles; // keep the first v.n rows
+        const std::size_t m = std::size_t(v.n);
+        q.x.resize(m);
+        q.v.resize(m);
+        q.mass.resize(m);
+        q.volume.resize(m);
+        q.rho.resize(m);
+        q.eps_eq.resize(m);
+        q.sigma_zz.resize(dim == 2 ? m : 0);
+        q.sigma.resize(m);
+        q.grad_v.resize(m);
+        q.affine.resize(with_affine ? m : 0);
+        q.def_grad.resize(with_def_grad ? m : 0);
+        ids.assign(id64.begin(), id64.begin() + v.n);
+        sub.step = v.step;
+        sub.time = T(v.time);
+        return sub;
+    }
+};
+
+inline Index slab_capacity(Index n_local, Index n_total, int R, Index mig_cap)
+{
+    return std::max<Index>(1024, Index(1.25 * double(n_local)) + n_total / (4 * R) + 2 * mig_cap);
+}
+
+// all ranks in this process (R contexts, e.g. R slabs on one GPU): the library steps them in
+// lock-step with device-copy exchanges (mpm_dist_attach_local / mpm_dist_advance_local)
+template <class T, int dim> class SlabGroup {
+public:
+    SlabGroup(const Scene<T, dim>& scene, const SimState<T, dim>& state, std::vector<int> bounds, Index mig_cap = 0,
+              int device = 0)
+        : bounds_(std::move(bounds)), template_(state)
+    {
+        const int R = int(bounds_.size()) - 1;
+        const Index n = state.particles.size();
+        mig_cap_ = mig_cap > 0 ? mig_cap : std::max<Index>(256, n / (64 * R));
+        const auto parts = slab_partition(scene, state, bounds_);
+        for (int r = 0; r < R; ++r) {
+            ctxs_.push_back(std::make_unique<SlabContext<T, dim>>(
+                scene, slab_capacity(Index(parts[r].size()), n, R, mig_cap_), device));
+            SimState<T, dim> sub = take_rows(state, parts[r]);
+            ctxs_.back()->upload_subset(sub, parts[r]);
+            handles_.push_back(ctxs_.back()->handle());
+        }
+        int rc = mpm_dist_attach_local(handles_.data(), R, bounds_.data(), mig_cap_);
+        if (rc)
+            ctxs_[0]->check(rc);
+    }
+    void advance(Index n, bool nan_guard = false)
+    {
+        const int rc = mpm_dist_advance_local(handles_.data(), int(handles_.size()), n,
+                                              nan_guard ? MPM_ADV_NAN_GUARD : 0u);
+        if (!rc)
+            return;
+        for (auto& c : ctxs_) { // the failing rank's own error first, then the peer report
+            int code = 0;
+            char msg[512];
+            mpm_last_error(c->handle(), &code, nullptr, nullptr, msg, sizeof(msg));
+            if (code && !std::strstr(msg, "another rank"))
+                c->check(code);
+        }
+        ctxs_[0]->check(rc);
+    }
+    // the global state in particle-index order
+    SimState<T, dim> gather()
+    {
+        SimState<T, dim> out = template_;
+        const bool aff = !template_.particles.affine.empty(), F = !template_.particles.def_grad.empty();
+        for (auto& c : ctxs_) {
+            std::vector<Index> ids;
+            SimState<T, dim> sub = c->download_subset(ids, aff, F);
+            put_rows(out, sub, ids);
+        }
+        return out;
+    }
+    int ranks() const { return int(ctxs_.size()); }
+
+private:
+    std::vector<int> bounds_;
+    SimState<T, dim> template_;
+    Index mig_cap_ = 0;
+    std::vector<std::unique_ptr<SlabContext<T, dim>>> ctxs_;
+    std::vector<mpm_ctx*> handles_;
+};
+
+// this process's rank of an NCCL-connected decomposition (one process per GPU)
+template <class T, int dim> class SlabRank {
+public:
+    using Id = std::array<unsigned char, MPM_DIST_ID_BYTES>;
+    static Id unique_id()
+    {
+        Id id{};
+        const int rc = mpm_dist_unique_id(id.data());
+        if (rc)
+            rethrow(nullptr, rc);
+        return id;
+    }
+    SlabRank(const Scene<T, dim>& scene, SimState<T, dim> local, const std::vector<Index>& ids, int rank, int nranks,
+             const Id& id, int cell_lo, int cell_hi, Index n_total, Index mig_cap = 0, int device = 0)
+        : aff_(!local.particles.affine.empty()), F_(!local.particles.def_grad.empty())
+    {
+        mig_cap = mig_cap > 0 ? mig_cap : std::max<Index>(1024, n_total / (256 * nranks));
+        ctx_ = std::make_unique<SlabContext<T, dim>>(
+            scene, slab_capacity(local.particles.size(), n_total, nranks, mig_cap), device);
+        ctx_->upload_subset(local, ids);
+        ctx_->check(mpm_dist_attach_nccl(ctx_->handle(), rank, nranks, id.data(), cell_lo, cell_hi, mig_cap));
+    }
+    // n steps; returns their device time (ms)
+    double advance(Index n, bool nan_guard = false)
+    {
+        double ms = 0;
+        ctx_->check(mpm_dist_advance(ctx_->handle(), n, nan_guard ? MPM_ADV_NAN_GUARD : 0u, &ms));
+        return ms;
+    }
+    SimState<T, dim> download(std::vector<Index>& ids) { return ctx_->download_subset(ids, aff_, F_); }
+
+private:
+    bool aff_, F_;
+    std::unique_ptr<SlabContext<T, dim>> ctx_;
+};
 
 } // namespace gpu
 } // namespace mpm

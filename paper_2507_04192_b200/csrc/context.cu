@@ -645,6 +645,8 @@ template <class T, int D> struct Ctx : CtxBase {
             if (const char* e = std::getenv("MPM_P2G_IMPL")) // A/B measurement only
                 p2g_impl = std::string(e) == "lanes3" ? 0 : 1;
         } else {
+            CK(cudaFuncSetAttribute(k_p2g<T, D, false, D == 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(p2g2_smem<T>())));
             CK(cudaFuncSetAttribute(k_p2g_staged<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(StageCfg<T, D>::SMEM)));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2g_ctas_per_sm, k_p2g_staged<T, D>, StageCfg<T, D>::THREADS,
@@ -783,8 +785,12 @@ template <class T, int D> struct Ctx : CtxBase {
                 }
             } else if (p2g2d_generic) {
                 launch("k_p2g", [&] {
-                    k_p2g<T, D, false><<<persistent(8), 160, 0, stream>>>(sc, buf[cur], perm, keys_sorted, bstart, bend,
-                                                                          occ, counts, partials, st);
+                    if constexpr (D == 2)
+                        k_p2g<T, D, false, true><<<persistent(2), 160, p2g2_smem<T>(), stream>>>(
+                            sc, buf[cur], perm, keys_sorted, bstart, bend, occ, counts, partials, st);
+                    else
+                        k_p2g<T, D, false><<<persistent(8), 160, 0, stream>>>(sc, buf[cur], perm, keys_sorted, bstart,
+                                                                              bend, occ, counts, partials, st);
                 });
             } else {
                 using S = StageCfg<T, D>;
@@ -1368,11 +1374,21 @@ template <class T, int D> struct Ctx : CtxBase {
             launch("k_dist", [&] { k_dist_nlive<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bend, sc.nb_total, dist.d_nlive); });
         }
         p2g_kernel();
+        if (!dist_has_peers()) // one rank: the fused grid pass of the plain step
+            return;
         grid_kernel<G_BANDONLY | G_SUM | G_NOGRAV | G_STORE>();
         if (dist.lo_peer >= 0)
             halo(sc.slab_lo, 2, dist.halo_send[0], 0);
         if (dist.hi_peer >= 0)
             halo(sc.slab_hi, 2, dist.halo_send[1], 0);
+    }
+    bool dist_has_peers() const { return dist.lo_peer >= 0 || dist.hi_peer >= 0; }
+    void dist_grid_interior()
+    {
+        if (dist_has_peers())
+            step_grid_interior();
+        else
+            grid_kernel<G_SUM | G_MOM | G_CORR>();
     }
     void dist_phase_b(bool guard)
     {
@@ -1381,14 +1397,24 @@ template <class T, int D> struct Ctx : CtxBase {
             halo(sc.slab_lo, 2, dist.halo_recv[0], 1);
         if (dist.hi_peer >= 0) // own (lower) + received
             halo(sc.slab_hi, 2, dist.halo_recv[1], 2);
-        finish_phase(guard);
-        launch("k_dist", [&] {
-            k_dist_publish<<<1, 1, 0, stream>>>(st, dist.cnt_send, dist.cnt_send + 1, dist.abort_red, mig.cap);
-        });
+        if (dist_has_peers()) {
+            finish_phase(guard);
+        } else {
+            if (guard)
+                g2p_kernel_fl<P_CONSTIT | P_GUARD>();
+            else
+                g2p_kernel_fl<P_CONSTIT>();
+            launch("k_step_end", [&] { k_step_end<<<1, 1, 0, stream>>>(st); });
+        }
+        if (dist.nranks > 1)
+            launch("k_dist", [&] {
+                k_dist_publish<<<1, 1, 0, stream>>>(st, dist.cnt_send, dist.cnt_send + 1, dist.abort_red, mig.cap);
+            });
     }
     void dist_phase_c(const int* reduced)
     {
-        launch("k_dist", [&] { k_dist_merge_abort<<<1, 1, 0, stream>>>(st, reduced); });
+        if (dist.nranks > 1)
+            launch("k_dist", [&] { k_dist_merge_abort<<<1, 1, 0, stream>>>(st, reduced); });
         launch("k_dist", [&] {
             k_dist_import<T, D><<<grid_for(2 * int64_t(mig.cap), 256), 256, 0, stream>>>(
                 sc, buf[cur], dist.d_nlive, dist.d_n, dist.cnt_recv, dist.recs_recv[0], dist.pid_recv[0],
@@ -1440,11 +1466,14 @@ template <class T, int D> struct Ctx : CtxBase {
     void dist_step_nccl(bool guard)
     {
         dist_phase_a();
-        dist_exchange_halo_nccl();
-        step_grid_interior(); // overlaps the band exchange
-        CK(cudaStreamWaitEvent(stream, dist.ev_b, 0));
+        if (dist.nranks > 1)
+            dist_exchange_halo_nccl();
+        dist_grid_interior(); // overlaps the band exchange
+        if (dist.nranks > 1)
+            CK(cudaStreamWaitEvent(stream, dist.ev_b, 0));
         dist_phase_b(guard);
-        dist_exchange_mig_nccl();
+        if (dist.nranks > 1)
+            dist_exchange_mig_nccl();
         dist_phase_c(dist.abort_red);
     }
     // same-process ranks (tests, or several GPUs driven by one host thread): the same phases in
@@ -1490,7 +1519,7 @@ template <class T, int D> struct Ctx : CtxBase {
                 }
             }
             for (Ctx* c : cs) {
-                c->step_grid_interior();
+                c->dist_grid_interior();
                 c->dist_phase_b(guard);
                 CK(cudaEventRecord(c->dist.ev_a, c->stream));
             }

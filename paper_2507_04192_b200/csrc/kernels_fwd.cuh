@@ -253,7 +253,16 @@ __device__ __forceinline__ void affine_matrix(const DevScene<T, D>& sc, const PB
         }
 }
 
-template <class T, int D, bool AFF>
+// STAGED (2-D PIC / FLIP / blend): a block of up to P2G2_CAP particles is first gathered through
+// the permutation into shared memory by all threads at once (independent loads, several in
+// flight per thread), so the column march below reads shared memory instead of issuing a
+// dependent global load chain per visited particle (the 2-D steps are latency-bound: C2 / C3
+// have 100-1000 occupied blocks, under one wave). Larger blocks read global memory as before.
+// The arithmetic is the same expression in the same order: results are bit-identical.
+constexpr int P2G2_CAP = 1280;
+template <class T> constexpr size_t p2g2_smem() { return sizeof(T) * 9 * P2G2_CAP + sizeof(int) * P2G2_CAP; }
+
+template <class T, int D, bool AFF, bool STAGED = false>
 __global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, const int* __restrict__ perm,
                                              const int* __restrict__ keys, const int* __restrict__ bstart,
                                              const int* __restrict__ bend, const int* __restrict__ occ,
@@ -262,7 +271,11 @@ __global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, co
 {
     using C = Cfg<D>;
     constexpr int B = C::B, TE = C::TE, NF = C::NF;
+    static_assert(!STAGED || (D == 2 && !AFF), "staged P2G: 2-D without affine transfer");
     __shared__ int cst[C::NB + 1];
+    extern __shared__ unsigned char p2g2_raw[];
+    T* rec = reinterpret_cast<T*>(p2g2_raw);                                   // [9][CAP]: x v m V sigma
+    int* lc = reinterpret_cast<int*>(p2g2_raw + sizeof(T) * 9 * P2G2_CAP);    // [CAP] local cell
     if (st->abort)
         return;
     const int nocc = *n_occ;
@@ -286,12 +299,43 @@ __global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, co
         const int s0 = bstart[Q], s1 = bend[Q], len = s1 - s0;
         int qc[D];
         block_coords<D>(Q, sc.nb, qc);
+        const bool staged = STAGED && len <= P2G2_CAP;
+        if (staged) { // gather the block through the permutation: 4 particles in flight per thread
+            for (int r0 = 0; r0 < len; r0 += 4 * int(blockDim.x)) {
+                int src[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = r0 + j * int(blockDim.x) + tid;
+                    src[j] = r < len ? __ldg(perm + s0 + r) : 0;
+                    if (r < len)
+                        lc[r] = __ldg(keys + s0 + r) & (C::NB - 1);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = r0 + j * int(blockDim.x) + tid;
+                    if (r >= len)
+                        continue;
+                    const int q = src[j];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        rec[a * P2G2_CAP + r] = __ldg(P.x[a] + q);
+                        rec[(D + a) * P2G2_CAP + r] = __ldg(P.v[a] + q);
+                    }
+                    rec[2 * D * P2G2_CAP + r] = __ldg(P.m + q);
+                    rec[(2 * D + 1) * P2G2_CAP + r] = __ldg(P.V + q);
+#pragma unroll
+                    for (int q2 = 0; q2 < C::NS; ++q2)
+                        rec[(2 * D + 2 + q2) * P2G2_CAP + r] = __ldg(P.sig[q2] + q);
+                }
+            }
+            __syncthreads();
+        }
         // cell ranges: cst[c] = first index (segment-relative) with local cell >= c
         for (int c = tid; c <= C::NB; c += blockDim.x) {
             int lo = 0, hi = len;
             while (lo < hi) {
                 int mid = (lo + hi) >> 1;
-                if ((keys[s0 + mid] & (C::NB - 1)) < c)
+                if ((staged ? lc[mid] : (keys[s0 + mid] & (C::NB - 1))) < c)
                     lo = mid + 1;
                 else
                     hi = mid;
@@ -333,18 +377,33 @@ __global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, co
                     bcell |= z << ((D - 1) * C::LOGB); // level-major local cell (common.cuh)
                     const int kb = cst[bcell], ke = cst[bcell + 1];
                     for (int k = kb; k < ke; ++k) {
-                        const int src = __ldg(perm + s0 + k);
-                        T x[D], v[D];
+                        int src = 0;
+                        T x[D], v[D], m, V, sig[C::NS];
+                        if (staged) {
 #pragma unroll
-                        for (int a = 0; a < D; ++a) {
-                            x[a] = __ldg(P.x[a] + src);
-                            v[a] = __ldg(P.v[a] + src);
+                            for (int a = 0; a < D; ++a) {
+                                x[a] = rec[a * P2G2_CAP + k];
+                                v[a] = rec[(D + a) * P2G2_CAP + k];
+                            }
+                            m = rec[2 * D * P2G2_CAP + k];
+                            V = rec[(2 * D + 1) * P2G2_CAP + k];
+#pragma unroll
+                            for (int q2 = 0; q2 < C::NS; ++q2)
+                                sig[q2] = rec[(2 * D + 2 + q2) * P2G2_CAP + k];
+                        } else {
+                            src = __ldg(perm + s0 + k);
+#pragma unroll
+                            for (int a = 0; a < D; ++a) {
+                                x[a] = __ldg(P.x[a] + src);
+                                v[a] = __ldg(P.v[a] + src);
+                            }
+                            m = __ldg(P.m + src);
+                            V = __ldg(P.V + src);
+#pragma unroll
+                            for (int q2 = 0; q2 < C::NS; ++q2)
+                                sig[q2] = __ldg(P.sig[q2] + src);
                         }
-                        const T m = __ldg(P.m + src), V = __ldg(P.V + src);
-                        T sig[C::NS];
-#pragma unroll
-                        for (int s = 0; s < C::NS; ++s)
-                            sig[s] = __ldg(P.sig[s] + src);
+                        (void)src;
                         T w[D][3], dw[D][3];
 #pragma unroll
                         for (int a = 0; a < D; ++a)

@@ -153,3 +153,57 @@ TEST_CASE("gpu::backprop_trajectory with a duck-typed Seeder matches the referen
     CHECK(rel(r_gpu.initial_state_cot.v, r_cpu.initial_state_cot.v) < 1e-8);
     CHECK(rel(r_gpu.initial_state_cot.x, r_cpu.initial_state_cot.x) < 1e-8);
 }
+
+TEST_CASE("gpu::SlabGroup (library-owned slab decomposition, 1-3 ranks on one GPU) matches gpu::Stepper")
+{
+    Scene<double, 2> scene = dp_scene();
+    scene.config.cells = {64, 20};
+    scene.geometry[0].lo = Vec<double, 2>(0.6, 0.1); // spans the slab bound at x = 16 cells
+    scene.geometry[0].hi = Vec<double, 2>(1.0, 0.35);
+    SimState<double, 2> state = init_scene(scene);
+    SimState<double, 2> ref = state;
+    gpu::Stepper<double, 2> stepper(scene);
+    const int N = 30;
+    for (int k = 0; k < N; ++k)
+        stepper.advance(ref);
+    for (int R = 1; R <= 3; ++R) {
+        std::vector<int> bounds;
+        for (int r = 0; r <= R; ++r)
+            bounds.push_back(r == R ? 64 : 16 * ((4 * r) / R));
+        gpu::SlabGroup<double, 2> group(scene, state, bounds);
+        group.advance(1);
+        group.advance(N - 1, true);
+        SimState<double, 2> got = group.gather();
+        CHECK(got.step == N);
+        CHECK(rel(got.particles.x, ref.particles.x) < 1e-12);
+        CHECK(rel(got.particles.v, ref.particles.v) < 1e-9);
+        CHECK(rel(got.particles.sigma, ref.particles.sigma) < 1e-9);
+        if (R == 1) { // one slab: the same operations in the same order as the plain step
+            CHECK(rel(got.particles.x, ref.particles.x) == 0.0);
+            CHECK(rel(got.particles.sigma, ref.particles.sigma) == 0.0);
+        }
+    }
+}
+
+TEST_CASE("gpu::SlabRank: a 1-rank NCCL communicator owned by the library")
+{
+    Scene<double, 2> scene = dp_scene();
+    SimState<double, 2> state = init_scene(scene);
+    SimState<double, 2> ref = state;
+    gpu::Stepper<double, 2> stepper(scene);
+    for (int k = 0; k < 12; ++k)
+        stepper.advance(ref);
+    std::vector<Index> ids(state.particles.size());
+    for (std::size_t i = 0; i < ids.size(); ++i)
+        ids[i] = Index(i);
+    gpu::SlabRank<double, 2> rank(scene, state, ids, 0, 1, gpu::SlabRank<double, 2>::unique_id(), 0,
+                                  scene.config.cells[0], state.particles.size());
+    CHECK(rank.advance(12) > 0.0);
+    std::vector<Index> got_ids;
+    SimState<double, 2> sub = rank.download(got_ids);
+    SimState<double, 2> got = state;
+    gpu::put_rows(got, sub, got_ids);
+    CHECK(got.step == 12);
+    CHECK(rel(got.particles.x, ref.particles.x) == 0.0);
+    CHECK(rel(got.particles.sigma, ref.particles.sigma) == 0.0);
+}
