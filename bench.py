@@ -798,11 +798,22 @@ def bench_dist(a, rank, world, local):
     dist.all_reduce(te[:1], op=dist.ReduceOp.MAX)
     tb = te[1:].clone()
     dist.all_reduce(tb)
+    # fwd+adjoint over the decomposition (mpm_dist_backprop: device-resident per-rank checkpoints,
+    # replay, cotangent rows of migrants returned, decomposed step_vjp)
+    fwd_adj = None
+    if a.adj_steps > 0 and not strong:
+        fwd_adj = dist_fwd_adj(rk, s, st, rank, world, n, n_total, a.adj_steps)
     rk.close()
     dist.barrier()
     if rank != 0:
         return None
-    B_fwd, _, _ = bytes_model(s, n_total, float(act.item()))
+    B_fwd, IN, _ = bytes_model(s, n_total, float(act.item()))
+    if fwd_adj and fwd_adj.get("value"):
+        B_fa = vjp_bytes(s, n_total, float(act.item()), B_fwd, IN, fwd_adj["forward_passes_per_step"])
+        gbs_fa = n_total / world * B_fa / (fwd_adj["ms_per_step"] / 1e3) / 1e9
+        peaks0 = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        fwd_adj["roofline"] = {"bound": "hbm", "bytes_per_particle_step": B_fa, "achieved": gbs_fa, "unit": "GB/s",
+                               "frac": gbs_fa / peaks0.get("hbm_gbs", 6650.0), "per": "GPU"}
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     gbs = n_total / world * B_fwd / (ms / a.steps / 1e3) / 1e9
@@ -817,11 +828,41 @@ def bench_dist(a, rank, world, local):
         "roofline": {"bound": "hbm", "kernel": "step (per GPU)", "achieved": gbs, "peak": peak, "unit": "GB/s",
                      "frac": gbs / peak, "traffic": None, "bytes_per_particle_step": B_fwd,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s"},
-        "clocks": ck, "gpu_launches": launches,
+        "clocks": ck, "gpu_launches": launches, "fwd_adj": fwd_adj,
         "e2e": {"value": n_total * a.steps / float(te[0].item()), "unit": UNIT,
                 "h2d_bytes_per_step": float(tb[0].item()), "d2h_bytes_per_step": float(tb[1].item()),
                 "call": e2e["call"], "seconds": float(te[0].item())},
     }
+
+
+def dist_fwd_adj(rk, s, st, rank, world, n, n_total, steps):
+    """mpm_dist_backprop on every rank: `steps` steps, the fewest checkpoint segments that fit in
+    HBM, Lagrangian least squares on the final positions of every 100th particle (global ids).
+    Time = the library's CUDA-event time of the call, max over ranks (the S0 upload and the
+    cotangent download fall outside it, as in the single-context line)."""
+    import torch
+    import torch.distributed as dist
+
+    try:
+        sel = np.arange(0, n_total, 100, dtype=np.int64)
+        x0 = st.particles.x[sel % n].copy()  # every rank's column is the same seeding, shifted in x
+        x0[:, 0] += 256 * (sel // n - rank) * s.config.dh
+        seeder = {"field": "x", "obs_steps": [steps], "sel": sel, "target": x0[None] + 1e-3}
+        nseg, plan = hbm_plan(s, n, steps, 0.14 * n)
+        rk.backprop(steps, nseg, seeder, n_total)  # allocates the checkpoint / replay slots and the tape
+        t0 = time.perf_counter()
+        _, _, pg, res = rk.backprop(steps, nseg, seeder, n_total)
+        wall = time.perf_counter() - t0
+        t = torch.tensor([res.device_ms, wall], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, wall = float(t[0].item()), float(t[1].item())
+        L = steps // nseg
+        return {"value": n_total * steps / (ms / 1e3), "unit": UNIT, "steps": steps, "n_segments": nseg, "plan": plan,
+                "ms_per_step": ms / steps, "device_ms": ms, "wall_s": wall, "loss": res.loss,
+                "forward_passes_per_step": 1 + (steps - L) / steps,
+                "timing": "CUDA events on each rank's library stream around mpm_dist_backprop, max over ranks"}
+    except Exception as e:  # reported, the forward line still prints
+        return {"value": None, "error": f"{type(e).__name__}: {str(e)[:200]}"}
 
 
 def SimState_take(full, ids):

@@ -337,6 +337,21 @@ int mpm_dist_advance(mpm_ctx* ctx, int64_t n_steps, uint32_t flags, double* devi
  * is rank r of bounds[r]..bounds[r+1]; exchanges are device copies ordered by events. */
 int mpm_dist_attach_local(mpm_ctx* const* ctxs, int nranks, const int* bounds, int64_t mig_cap);
 int mpm_dist_advance_local(mpm_ctx* const* ctxs, int nranks, int64_t n_steps, uint32_t flags);
+/* backprop_trajectory (checkpoint.hpp:72-143) over the decomposition, device-resident: per-rank
+ * HBM checkpoints and replay slots, rank-local digests (a mismatch on any rank fails all), the
+ * Lagrangian least-squares seeder on global particle ids in [0, id_space), the cotangent rows of
+ * migrants returned to their step-t owner, the decomposed step_vjp with two halo exchanges.
+ * Out: this rank's cotangent of S^0 (c0, storage order, c0->n rows; size the view with
+ * mpm_local_count) with the rows' global ids, and the rank-ordered sums of the loss and the
+ * ParamGrads (every rank gets the same). */
+int mpm_dist_backprop(mpm_ctx* ctx, int64_t total_steps, int n_segments, const mpm_seeder_desc* seeder,
+                      int64_t id_space, mpm_cot_view* c0, int64_t* c0_ids, mpm_param_grads* pg,
+                      mpm_backprop_result* res);
+/* the same for same-process ranks (one host thread per rank inside the call): c0s[r] / c0_ids[r]
+ * per rank, pg / res once */
+int mpm_dist_backprop_local(mpm_ctx* const* ctxs, int nranks, int64_t total_steps, int n_segments,
+                            const mpm_seeder_desc* seeder, int64_t id_space, mpm_cot_view* c0s,
+                            int64_t* const* c0_ids, mpm_param_grads* pg, mpm_backprop_result* res);
 
 /* ---- instrumentation (bench / tests) --------------------------------------------------- */
 /* enable per-kernel CUDA-event timing on the context stream */

@@ -232,6 +232,12 @@ _PROTOS = {
     "mpm_dist_advance": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint32, C.POINTER(C.c_double)]),
     "mpm_dist_attach_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_int), C.c_int64]),
     "mpm_dist_advance_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, C.c_uint32]),
+    "mpm_dist_backprop": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.POINTER(SeederDesc), C.c_int64,
+                                    C.POINTER(CotView), C.c_void_p, C.POINTER(ParamGradsView),
+                                    C.POINTER(BackpropResultView)]),
+    "mpm_dist_backprop_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, C.c_int, C.POINTER(SeederDesc),
+                                          C.c_int64, C.POINTER(CotView), C.POINTER(C.c_void_p),
+                                          C.POINTER(ParamGradsView), C.POINTER(BackpropResultView)]),
 }
 DIST_ID_BYTES = 128
 

@@ -21,6 +21,9 @@
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -77,6 +80,8 @@ struct ApiError : std::runtime_error {
                                              + __FILE__ + ":" + std::to_string(__LINE__));         \
     } while (0)
 
+struct LocalHub;
+
 struct ProfEvent {
     const char* name;
     cudaEvent_t a, b;
@@ -132,12 +137,165 @@ struct CtxBase {
     virtual int dist_device() const = 0;
     virtual void dist_enqueue_local(std::vector<CtxBase*>& all, int64_t n, uint32_t flags) = 0;
     virtual void dist_finish() = 0;
+    virtual void dist_backprop_nccl(int64_t total, int nseg, const mpm_seeder_desc* sd, int64_t id_space,
+                                    mpm_cot_view* c0, int64_t* c0_ids, mpm_param_grads* pg, mpm_backprop_result* res) = 0;
+    virtual void dist_backprop_local(LocalHub* hub, int64_t total, int nseg, const mpm_seeder_desc* sd,
+                                     int64_t id_space, mpm_cot_view* c0, int64_t* c0_ids, mpm_param_grads* pg,
+                                     mpm_backprop_result* res) = 0;
 
     // profiling
     bool prof = false;
     std::vector<ProfEvent> events;
     std::vector<std::pair<std::string, std::pair<double, int64_t>>> prof_acc;
     int64_t launches = 0;
+};
+
+// ---- transports of the library-owned decomposition --------------------------------------------
+// An exchange is a list of (send, recv, bytes, peer) pairs; every rank lists its pairs with a peer
+// in the same order as the peer lists its pairs with it. begin() puts the transfers on the
+// timeline of `stream` (sends read after the work enqueued so far), end() orders the work enqueued
+// after it behind the receives. NCCL: grouped ncclSend / ncclRecv on a communication stream,
+// ordered by events (capturable in a CUDA graph). Same-process ranks (one host thread per rank):
+// a rendezvous publishes the send buffers, then device copies from the peers' buffers, ordered by
+// events; nothing waits for the device on the host.
+struct XItem {
+    const void* send;
+    void* recv;
+    size_t bytes;
+    int peer;
+};
+struct DistTransport {
+    virtual ~DistTransport() = default;
+    virtual void begin(cudaStream_t s, const std::vector<XItem>& items) = 0;
+    virtual void end(cudaStream_t s) = 0;
+    // recv[nranks * bytes] <- every rank's send[bytes], rank order
+    virtual void allgather(cudaStream_t s, const void* send, void* recv, size_t bytes) = 0;
+};
+
+struct NcclX : DistTransport {
+    ncclComm_t comm;
+    cudaStream_t cs;
+    cudaEvent_t ea, eb;
+    NcclX(ncclComm_t c, cudaStream_t s, cudaEvent_t a, cudaEvent_t b) : comm(c), cs(s), ea(a), eb(b) {}
+    void begin(cudaStream_t s, const std::vector<XItem>& items) override
+    {
+        CK(cudaEventRecord(ea, s));
+        CK(cudaStreamWaitEvent(cs, ea, 0));
+        NCK(ncclGroupStart());
+        for (const XItem& it : items) {
+            NCK(ncclSend(it.send, it.bytes, ncclUint8, it.peer, comm, cs));
+            NCK(ncclRecv(it.recv, it.bytes, ncclUint8, it.peer, comm, cs));
+        }
+        NCK(ncclGroupEnd());
+        CK(cudaEventRecord(eb, cs));
+    }
+    void end(cudaStream_t s) override { CK(cudaStreamWaitEvent(s, eb, 0)); }
+    void allgather(cudaStream_t s, const void* send, void* recv, size_t bytes) override
+    {
+        CK(cudaEventRecord(ea, s));
+        CK(cudaStreamWaitEvent(cs, ea, 0));
+        NCK(ncclAllGather(send, recv, bytes, ncclUint8, comm, cs));
+        CK(cudaEventRecord(eb, cs));
+        CK(cudaStreamWaitEvent(s, eb, 0));
+    }
+};
+
+struct LocalHub {
+    int R;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long gen = 0;
+    std::vector<std::vector<XItem>> items;
+    std::vector<const void*> gsend;
+    std::vector<cudaEvent_t> ready, done;
+    std::vector<std::string> err; // a rank that failed on the host side releases the others
+    bool failed = false;
+    explicit LocalHub(int r) : R(r), items(r), gsend(r), ready(r), done(r), err(r)
+    {
+        for (int k = 0; k < R; ++k) {
+            CK(cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+        }
+    }
+    ~LocalHub()
+    {
+        for (int k = 0; k < R; ++k) {
+            cudaEventDestroy(ready[k]);
+            cudaEventDestroy(done[k]);
+        }
+    }
+    void barrier()
+    {
+        std::unique_lock<std::mutex> lk(m);
+        if (failed)
+            throw ApiError(MPM_ERR_CUDA, "dist: another same-process rank failed");
+        const long long g = gen;
+        if (++arrived == R) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g || failed; });
+            if (failed)
+                throw ApiError(MPM_ERR_CUDA, "dist: another same-process rank failed");
+        }
+    }
+    void fail()
+    {
+        std::lock_guard<std::mutex> lk(m);
+        failed = true;
+        cv.notify_all();
+    }
+};
+
+struct LocalX : DistTransport {
+    LocalHub* hub;
+    int rank;
+    LocalX(LocalHub* h, int r) : hub(h), rank(r) {}
+    void settle(cudaStream_t s)
+    {
+        CK(cudaEventRecord(hub->done[rank], s));
+        hub->barrier();
+        for (int p = 0; p < hub->R; ++p) // peers' copies out of this rank's buffers come first
+            if (p != rank)
+                CK(cudaStreamWaitEvent(s, hub->done[p], 0));
+        hub->barrier(); // every rank has queued its waits before the events are recorded again
+    }
+    void begin(cudaStream_t s, const std::vector<XItem>& items) override
+    {
+        hub->items[rank] = items;
+        CK(cudaEventRecord(hub->ready[rank], s));
+        hub->barrier();
+        std::vector<int> seen(hub->R, 0);
+        for (const XItem& it : items) {
+            const int p = it.peer;
+            int j = seen[p]++, k = -1;
+            for (size_t q = 0; q < hub->items[p].size(); ++q)
+                if (hub->items[p][q].peer == rank && j-- == 0) {
+                    k = int(q);
+                    break;
+                }
+            if (k < 0 || hub->items[p][k].bytes != it.bytes)
+                throw ApiError(MPM_ERR_CUDA, "dist: mismatched same-process exchange");
+            CK(cudaStreamWaitEvent(s, hub->ready[p], 0));
+            CK(cudaMemcpyAsync(it.recv, hub->items[p][k].send, it.bytes, cudaMemcpyDeviceToDevice, s));
+        }
+        settle(s);
+    }
+    void end(cudaStream_t) override {}
+    void allgather(cudaStream_t s, const void* send, void* recv, size_t bytes) override
+    {
+        hub->gsend[rank] = send;
+        CK(cudaEventRecord(hub->ready[rank], s));
+        hub->barrier();
+        for (int p = 0; p < hub->R; ++p) {
+            CK(cudaStreamWaitEvent(s, hub->ready[p], 0));
+            CK(cudaMemcpyAsync(static_cast<char*>(recv) + size_t(p) * bytes, hub->gsend[p], bytes,
+                               cudaMemcpyDeviceToDevice, s));
+        }
+        settle(s);
+    }
 };
 
 template <class T> T* dalloc(size_t n)
@@ -1383,12 +1541,19 @@ template <class T, int D> struct Ctx : CtxBase {
             halo(sc.slab_hi, 2, dist.halo_send[1], 0);
     }
     bool dist_has_peers() const { return dist.lo_peer >= 0 || dist.hi_peer >= 0; }
+    bool dist_store = false; // keep m, p, f in the grid (a replay step whose grid goes to the tape)
     void dist_grid_interior()
     {
-        if (dist_has_peers())
-            step_grid_interior();
-        else
+        if (dist_has_peers()) {
+            if (dist_store)
+                grid_kernel<G_INTERIOR | G_SUM | G_MOM | G_CORR | G_STORE>();
+            else
+                step_grid_interior();
+        } else if (dist_store) {
+            grid_kernel<G_SUM | G_MOM | G_CORR | G_STORE>();
+        } else {
             grid_kernel<G_SUM | G_MOM | G_CORR>();
+        }
     }
     void dist_phase_b(bool guard)
     {
@@ -1553,6 +1718,515 @@ template <class T, int D> struct Ctx : CtxBase {
         }
     }
     void dist_finish() override { dist_finish_call(); }
+    // ---- decomposed backprop_trajectory on the library-owned path (checkpoint.hpp:72-143) --------
+    // Every rank runs the same sequence with its own particles: a forward sweep with per-rank HBM
+    // checkpoints at segment starts (and rank-local digests), then per segment (reversed) a replay
+    // into per-rank slots recording each step's migration (export lists with the vacated slots,
+    // import layout), a digest check (any rank's mismatch fails every rank), and per step: the
+    // device seeder on global particle ids, the return of migrants' cotangent rows to their step-t
+    // owner, and the decomposed step_vjp (adjoint.hpp:328-525) with its two halo exchanges. Loss and
+    // ParamGrads are per-rank device sums, gathered and added in rank order at the end.
+    struct DistTape {
+        int64_t n_before = 0, n_after = 0; // counts of S^j and S^{j+1}
+        long long* ex_cnt = nullptr; // [2] exports toward lo / hi during the step
+        int* ex_pid[2] = {nullptr, nullptr};
+        int* ex_slot[2] = {nullptr, nullptr};
+        int* nlive = nullptr;         // the step's G2P output count
+        long long* im_cnt = nullptr;  // [2] imports from lo / hi
+    };
+    std::vector<DistTape> dtape;
+    T* cot_xbuf[4] = {nullptr, nullptr, nullptr, nullptr}; // cotangent-row messages: send lo / hi, recv lo / hi
+    int* dist_sop = nullptr;   // slot of a global particle id
+    int64_t dist_sop_n = 0;
+    int* abort_all = nullptr;  // [nranks]
+    double* dist_gather = nullptr;
+
+    std::vector<XItem> halo_items(size_t bytes)
+    {
+        std::vector<XItem> v;
+        if (dist.lo_peer >= 0)
+            v.push_back({dist.halo_send[0], dist.halo_recv[0], bytes, dist.lo_peer});
+        if (dist.hi_peer >= 0)
+            v.push_back({dist.halo_send[1], dist.halo_recv[1], bytes, dist.hi_peer});
+        return v;
+    }
+    std::vector<XItem> mig_items()
+    {
+        const size_t rb = sizeof(T) * size_t(mig.rec) * mig.cap, pb = sizeof(int) * size_t(mig.cap);
+        std::vector<XItem> v;
+        for (int side = 0; side < 2; ++side) {
+            const int peer = side == 0 ? dist.lo_peer : dist.hi_peer;
+            if (peer < 0)
+                continue;
+            v.push_back({dist.cnt_send + side, dist.cnt_recv + side, sizeof(long long), peer});
+            v.push_back({side == 0 ? mig.lo : mig.hi, dist.recs_recv[side], rb, peer});
+            v.push_back({side == 0 ? mig.lo_pid : mig.hi_pid, dist.pid_recv[side], pb, peer});
+        }
+        return v;
+    }
+    void dist_abort_reduce(DistTransport& X)
+    {
+        X.allgather(stream, dist.abort_red, abort_all, sizeof(int));
+        AbortPtrs ap{};
+        ap.R = dist.nranks;
+        for (int r = 0; r < dist.nranks; ++r)
+            ap.p[r] = abort_all + r;
+        launch("k_dist", [&] { k_dist_abort_max<<<1, 1, 0, stream>>>(ap, dist.abort_red + 1); });
+    }
+    // one decomposed forward step over any transport (eager)
+    void dist_step_x(DistTransport& X, bool guard)
+    {
+        dist_phase_a();
+        if (dist_has_peers())
+            X.begin(stream, halo_items(sizeof(T) * dist.halo_elems));
+        dist_grid_interior();
+        if (dist_has_peers())
+            X.end(stream);
+        dist_phase_b(guard);
+        if (dist.nranks > 1) {
+            X.begin(stream, mig_items());
+            X.end(stream);
+            dist_abort_reduce(X);
+        }
+        dist_phase_c(dist.abort_red + 1);
+    }
+    // the decomposed step_vjp of the state in buf[cur] (host n valid): cot[bo] -> cot[bi]
+    void dist_vjp_x(DistTransport& X, int bo, int bi)
+    {
+        sort_and_segment();
+        p2g_kernel();
+        if (!dist_has_peers()) {
+            grid_kernel<G_SUM | G_MOM | G_CORR | G_STORE>();
+            aw.vjp_reverse(*this, bo, bi);
+            return;
+        }
+        grid_kernel<G_BANDONLY | G_SUM | G_NOGRAV | G_STORE>();
+        if (dist.lo_peer >= 0)
+            halo(sc.slab_lo, 2, dist.halo_send[0], 0);
+        if (dist.hi_peer >= 0)
+            halo(sc.slab_hi, 2, dist.halo_send[1], 0);
+        X.begin(stream, halo_items(sizeof(T) * dist.halo_elems));
+        grid_kernel<G_INTERIOR | G_SUM | G_MOM | G_CORR | G_STORE>();
+        X.end(stream);
+        if (dist.lo_peer >= 0)
+            halo(sc.slab_lo, 2, dist.halo_recv[0], 1);
+        if (dist.hi_peer >= 0)
+            halo(sc.slab_hi, 2, dist.halo_recv[1], 2);
+        grid_kernel<G_BANDONLY | G_GRAV | G_ZEROV | G_MOM | G_CORR | G_STORE>();
+        dist_vjp_reverse_x(X, bo, bi);
+    }
+    // the reverse part of the decomposed step_vjp, on the step's sort and full forward grid (from
+    // the replay's tape, or just recomputed by dist_vjp_x)
+    void dist_vjp_reverse_x(DistTransport& X, int bo, int bi)
+    {
+        if (!dist_has_peers()) {
+            aw.vjp_reverse(*this, bo, bi);
+            return;
+        }
+        aw.k5(*this, bo, bi);
+        launch("k_adj_grid", [&] {
+            k_adj_grid<T, D, ADJ_BAND_SUM><<<persistent(4), C::NB, 0, stream>>>(sc, G, aw.gc, aw.partials, bstart, act,
+                                                                               counts + 1, aw.fr_block, st);
+        });
+        const HaloFields<T> H = aw.cot_halo_fields();
+        int64_t plane = 1;
+        for (int a = 1; a < D; ++a)
+            plane *= sc.cells[a] + 1;
+        if (dist.lo_peer >= 0)
+            halo_fields(H, sc.slab_lo, 2, dist.halo_send[0], 0);
+        if (dist.hi_peer >= 0)
+            halo_fields(H, sc.slab_hi, 2, dist.halo_send[1], 0);
+        X.begin(stream, halo_items(sizeof(T) * 2 * plane * 2 * D));
+        X.end(stream);
+        if (dist.lo_peer >= 0)
+            halo_fields(H, sc.slab_lo, 2, dist.halo_recv[0], 1);
+        if (dist.hi_peer >= 0)
+            halo_fields(H, sc.slab_hi, 2, dist.halo_recv[1], 2);
+        launch("k_adj_grid", [&] {
+            k_adj_grid<T, D, ADJ_INTERIOR><<<persistent(4), C::NB, 0, stream>>>(sc, G, aw.gc, aw.partials, bstart, act,
+                                                                               counts + 1, aw.fr_block, st);
+        });
+        launch("k_adj_grid", [&] {
+            k_adj_grid<T, D, ADJ_BAND_LOAD><<<persistent(4), C::NB, 0, stream>>>(sc, G, aw.gc, aw.partials, bstart, act,
+                                                                                counts + 1, aw.fr_block, st);
+        });
+        aw.k7(*this, bi);
+    }
+    int cot_values() const { return 2 * D + 2 + (D == 2 ? 1 : 0) + 2 * D * D + (has_aff ? D * D : 0); }
+    // migrants' cotangent rows back to their step-t owners (kernels_dist.cuh)
+    void dist_cot_return(DistTransport& X, const DistTape& tp, int cb)
+    {
+        if (!dist_has_peers())
+            return;
+        const int nv = cot_values();
+        const size_t bytes = sizeof(T) * size_t(nv) * mig.cap;
+        const unsigned g = grid_for(mig.cap, 256);
+        const int gz = aw.gvz[cb] ? 1 : 0;
+        std::vector<XItem> items;
+        for (int side = 0; side < 2; ++side) {
+            const int peer = side == 0 ? dist.lo_peer : dist.hi_peer;
+            if (peer < 0)
+                continue;
+            launch("k_cot_pack", [&] {
+                k_cot_pack<T, D><<<g, 256, 0, stream>>>(aw.cot[cb], tp.nlive, tp.im_cnt, tp.im_cnt + side, side,
+                                                        cot_xbuf[side], gz, has_aff);
+            });
+            items.push_back({cot_xbuf[side], cot_xbuf[2 + side], bytes, peer});
+        }
+        X.begin(stream, items);
+        X.end(stream);
+        for (int side = 0; side < 2; ++side) {
+            const int peer = side == 0 ? dist.lo_peer : dist.hi_peer;
+            if (peer < 0)
+                continue;
+            launch("k_cot_unpack", [&] {
+                k_cot_unpack<T, D><<<g, 256, 0, stream>>>(aw.cot[cb], tp.ex_cnt + side, tp.ex_pid[side], tp.ex_slot[side],
+                                                          cot_xbuf[2 + side], gz, has_aff);
+            });
+        }
+    }
+    void dist_bp_alloc(int64_t Lmax, int64_t id_space)
+    {
+        while (int64_t(dtape.size()) < Lmax) {
+            DistTape t;
+            t.ex_cnt = alloc<long long>(2);
+            t.im_cnt = alloc<long long>(2);
+            t.nlive = alloc<int>(1);
+            for (int s2 = 0; s2 < 2; ++s2) {
+                t.ex_pid[s2] = alloc<int>(mig.cap);
+                t.ex_slot[s2] = alloc<int>(mig.cap);
+            }
+            dtape.push_back(t);
+        }
+        if (!cot_xbuf[0])
+            for (auto& b : cot_xbuf)
+                b = alloc<T>(size_t(cot_values()) * mig.cap);
+        if (id_space > dist_sop_n) {
+            dist_sop = alloc<int>(id_space);
+            dist_sop_n = id_space;
+        }
+        if (!abort_all) {
+            abort_all = alloc<int>(dist.nranks);
+            dist_gather = alloc<double>(size_t(dist.nranks) * (PG_SLOTS + 1));
+        }
+    }
+    void dist_backprop(DistTransport& X, int64_t total, int nseg, const mpm_seeder_desc* sd, int64_t id_space,
+                       mpm_cot_view* c0, int64_t* c0_ids, mpm_param_grads* pg, mpm_backprop_result* res)
+    {
+        if (!dist.on)
+            throw ApiError(MPM_ERR_USAGE, "dist: context not attached");
+        if (!has_state)
+            throw ApiError(MPM_ERR_USAGE, "no state uploaded");
+        if (total < 1 || nseg < 1 || int64_t(nseg) > total)
+            throw ApiError(MPM_ERR_VALIDATION, "checkpoint plan: n_segments must lie in [1, N_t]");
+        if (sd && sd->kind != MPM_SEEDER_LAGRANGIAN_LS && sd->n_obs > 0)
+            throw ApiError(MPM_ERR_USAGE, "dist backprop: the Lagrangian least-squares seeder only");
+        std::vector<int64_t> bnd(nseg + 1, 0);
+        {
+            const int64_t base = total / nseg, rem = total % nseg;
+            for (int k = 0; k < nseg; ++k)
+                bnd[k + 1] = bnd[k] + base + (k < rem ? 1 : 0);
+        }
+        int64_t Lmax = 0;
+        for (int k = 0; k < nseg; ++k)
+            Lmax = std::max(Lmax, bnd[k + 1] - bnd[k]);
+        aw.ensure(*this);
+        dist_bp_alloc(Lmax, std::max<int64_t>(id_space, 1));
+        const bool seeding = sd && sd->n_obs > 0;
+        const int64_t nsel = seeding ? (sd->sel ? sd->n_sel : id_space) : 0;
+        struct Owned {
+            std::vector<void*> v;
+            ~Owned()
+            {
+                for (void* p : v)
+                    cudaFree(p);
+            }
+        } owned;
+        long long* d_sel = nullptr;
+        T* d_tgt = nullptr;
+        T* d_lblk = nullptr;
+        if (seeding) {
+            if (sd->sel) {
+                CK(cudaMalloc(&d_sel, nsel * sizeof(long long)));
+                owned.v.push_back(d_sel);
+                for (int64_t l = 0; l < nsel; ++l)
+                    if (sd->sel[l] < 0 || sd->sel[l] >= id_space)
+                        throw ApiError(MPM_ERR_VALIDATION, "seeder: particle id out of range");
+                h2d_raw(d_sel, sd->sel, nsel * sizeof(long long));
+            }
+            CK(cudaMalloc(&d_tgt, (size_t)sd->n_obs * nsel * D * sizeof(T)));
+            owned.v.push_back(d_tgt);
+            h2d_raw(d_tgt, sd->target, (size_t)sd->n_obs * nsel * D * sizeof(T));
+            CK(cudaMalloc(&d_lblk, sizeof(T) * std::max<int64_t>(1, grid_for(nsel, 256))));
+            owned.v.push_back(d_lblk);
+        }
+        auto obs_index = [&](int64_t t) {
+            if (!seeding)
+                return -1;
+            for (int k = 0; k < sd->n_obs; ++k)
+                if (sd->obs_steps[k] == t)
+                    return k;
+            return -1;
+        };
+        auto seed = [&](const PBuf<T, D>& P, int64_t nP, int k, int cb, int do_cot) {
+            CK(cudaMemsetAsync(dist_sop, 0xff, sizeof(int) * dist_sop_n, stream));
+            launch("k_slot_of_pid", [&] { k_slot_of_pid<T, D><<<grid_for(nP, 256), 256, 0, stream>>>(P, int(nP), dist_sop); });
+            const int sb = int(grid_for(nsel, 256));
+            launch("k_seed", [&] {
+                k_seed_lagrangian<T, D><<<sb, 256, 0, stream>>>(P, int(nP), dist_sop, d_sel, nsel,
+                                                                d_tgt + (size_t)k * nsel * D, sd->field, aw.cot[cb],
+                                                                do_cot, d_lblk);
+            });
+            launch("k_seed", [&] { k_seed_sum<T><<<1, 1024, 0, stream>>>(d_lblk, sb, aw.loss_acc); });
+        };
+        const PBuf<T, D> own0 = buf[0], own1 = buf[1];
+        const int cur0 = cur;
+        const int64_t step0 = step;
+        struct Ev {
+            cudaEvent_t e{};
+            Ev() { CK(cudaEventCreate(&e)); }
+            ~Ev() { cudaEventDestroy(e); }
+        } ev0, ev1;
+        std::vector<int64_t> ckn(nseg);
+        std::vector<uint64_t> bhash(nseg + 1);
+        int cb = 0;
+        const SortSet own_ss0 = sort_set();
+        try {
+            std::vector<PBuf<T, D>> ckpt(nseg), replay(Lmax + 1);
+            for (int k = 0; k < nseg; ++k)
+                ckpt[k] = pool_buf(size_t(k));
+            for (int64_t j = 0; j <= Lmax; ++j)
+                replay[j] = pool_buf(size_t(nseg + j));
+            // the replay tape (the step's sort arrays and forward grid kept, as backprop_run does): the
+            // VJP then skips its forward replay; slots sized from S0's active node blocks (+25 %),
+            // a step that outgrows its slot falls back to the recompute
+            const SortSet own_ss = sort_set();
+            bool use_tape = false;
+            {
+                keys_valid = false;
+                inc_invalidate();
+                sort_and_segment();
+                keys_valid = false;
+                int n_act_now = 0;
+                d2h_raw(&n_act_now, counts + 1, sizeof(int));
+                const char* cap_env = std::getenv("MPM_TAPE_CAP"); // test hook: force slot overflows
+                const int64_t grid_cap = cap_env ? std::max<int64_t>(1, std::atoll(cap_env))
+                                                 : std::min<int64_t>(sc.nnb_total, (int64_t(n_act_now) * 5 / 4 + 255) / 256 * 256);
+                use_tape = tape_enabled && tape_reserve(Lmax, grid_cap);
+                if (use_tape)
+                    CK(cudaMemsetAsync(tape_over, 0, sizeof(int) * Lmax, stream));
+            }
+            CK(cudaMemsetAsync(aw.loss_acc, 0, sizeof(double), stream));
+            aw.pg_reset(*this, nullptr);
+            reset_status();
+            CK(cudaEventRecord(ev0.e, stream));
+            // the steps of segment k run in the replay slots (state j in replay[j]), each step's
+            // migration recorded for the reverse sweep; `fwd_seed`: evaluate the loss at observed
+            // steps (the forward sweep's run of the last segment)
+            std::vector<int> over(Lmax, 1);
+            auto run_in_slots = [&](int k, bool fwd_seed) {
+                const int64_t b0 = bnd[k], len = bnd[k + 1] - b0;
+                n = ckn[k]; // (pbuf_copy moves n rows)
+                pbuf_copy(replay[0], ckpt[k]);
+                if (use_tape)
+                    CK(cudaMemsetAsync(tape_over, 0, sizeof(int) * len, stream));
+                for (int64_t j = 0; j < len; ++j) {
+                    DistTape& tp = dtape[size_t(j)];
+                    tp.n_before = n;
+                    buf[0] = replay[j];
+                    buf[1] = replay[j + 1];
+                    cur = 0;
+                    keys_valid = false;
+                    inc_invalidate();
+                    dist_step_begin();
+                    if (use_tape) {
+                        use_sort_set(tape[j].ss);
+                        dist_store = true;
+                    }
+                    dist_step_x(X, false);
+                    if (use_tape) {
+                        tape_grid<true>(int(j));
+                        dist_store = false;
+                        use_sort_set(own_ss);
+                    }
+                    CK(cudaMemcpyAsync(tp.nlive, dist.d_nlive, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+                    CK(cudaMemcpyAsync(tp.im_cnt, dist.cnt_recv, 2 * sizeof(long long), cudaMemcpyDeviceToDevice, stream));
+                    launch("k_dist", [&] { k_dist_export_counts<<<1, 1, 0, stream>>>(st, tp.ex_cnt, mig.cap); });
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        CK(cudaMemcpyAsync(tp.ex_pid[s2], s2 ? mig.hi_pid : mig.lo_pid, sizeof(int) * mig.cap,
+                                           cudaMemcpyDeviceToDevice, stream));
+                        CK(cudaMemcpyAsync(tp.ex_slot[s2], s2 ? mig.hi_slot : mig.lo_slot, sizeof(int) * mig.cap,
+                                           cudaMemcpyDeviceToDevice, stream));
+                    }
+                    if (dist.nranks == 1) // no imports: the recorded counts are zero
+                        CK(cudaMemsetAsync(tp.im_cnt, 0, 2 * sizeof(long long), stream));
+                    dist_sync_count();
+                    tp.n_after = n;
+                    if (fwd_seed && obs_index(b0 + j + 1) >= 0)
+                        seed(buf[cur], n, obs_index(b0 + j + 1), 0, 0);
+                }
+                if (use_tape)
+                    d2h_raw(over.data(), tape_over, sizeof(int) * len);
+            };
+            // forward sweep; the last segment runs directly in the replay slots: its states are the
+            // ones a replay would recompute bit for bit, so the reverse sweep starts without
+            // replaying it (with one segment: 1 forward pass + 1 VJP per step)
+            if (obs_index(0) >= 0)
+                seed(buf[cur], n, obs_index(0), 0, 0);
+            for (int k = 0; k < nseg; ++k) {
+                pbuf_copy(ckpt[k], buf[cur]);
+                ckn[k] = n;
+                if (k >= 1)
+                    bhash[k] = digest_of(buf[cur]);
+                if (k == nseg - 1) {
+                    run_in_slots(k, true);
+                    break;
+                }
+                dist_step_begin();
+                for (int64_t t = bnd[k]; t < bnd[k + 1]; ++t) {
+                    dist_step_x(X, false);
+                    if (obs_index(t + 1) >= 0) {
+                        dist_sync_count();
+                        seed(buf[cur], n, obs_index(t + 1), 0, 0);
+                    }
+                }
+                dist_sync_count();
+            }
+            check_status(step0);
+            double loss_local = 0;
+            d2h_raw(&loss_local, aw.loss_acc, sizeof(double));
+            // reverse sweep
+            n = dtape[size_t(bnd[nseg] - bnd[nseg - 1] - 1)].n_after; // S^N: the last slot
+            aw.cot_zero(*this, 0);
+            int64_t peak = 0;
+            for (int k = nseg - 1; k >= 0; --k) {
+                const int64_t b0 = bnd[k], b1 = bnd[k + 1], len = b1 - b0;
+                const bool kept = k == nseg - 1;
+                if (!kept) // replay into the slots, recording every step's migration
+                    run_in_slots(k, false);
+                peak = std::max(peak, len + 1);
+                // digest check of a replayed segment; any rank's mismatch fails every rank
+                int bad = !kept && digest_of(replay[len]) != bhash[k + 1] ? 1 : 0;
+                h2d_raw(dist.abort_red, &bad, sizeof(int));
+                if (dist.nranks > 1)
+                    dist_abort_reduce(X);
+                else
+                    CK(cudaMemcpyAsync(dist.abort_red + 1, dist.abort_red, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+                int any = 0;
+                d2h_raw(&any, dist.abort_red + 1, sizeof(int));
+                if (any)
+                    throw ApiError(MPM_ERR_CHECKPOINT, "checkpoint mismatch: recomputed segment end differs from the "
+                                                       "recorded state at step " + std::to_string(step0 + b1));
+                for (int64_t t = b1; t > b0; --t) {
+                    const int64_t j = t - b0 - 1;
+                    const DistTape& tp = dtape[size_t(j)];
+                    if (obs_index(t) >= 0) // cotangent of S^t, storage order of replay[j + 1]
+                        seed(replay[j + 1], tp.n_after, obs_index(t), cb, 1);
+                    dist_cot_return(X, tp, cb);
+                    buf[0] = replay[j];
+                    buf[1] = replay[j + 1];
+                    cur = 0;
+                    n = tp.n_before;
+                    keys_valid = false;
+                    inc_invalidate();
+                    if (use_tape && !over[size_t(j)]) { // the replay's sort and grid
+                        use_sort_set(tape[size_t(j)].ss);
+                        tape_grid<false>(int(j));
+                        dist_vjp_reverse_x(X, cb, cb ^ 1);
+                        use_sort_set(own_ss);
+                    } else {
+                        dist_vjp_x(X, cb, cb ^ 1);
+                    }
+                    cb ^= 1;
+                }
+                check_status(step);
+            }
+            n = ckn[0];
+            if (obs_index(0) >= 0)
+                seed(ckpt[0], n, obs_index(0), cb, 1);
+            CK(cudaEventRecord(ev1.e, stream));
+            // rank-ordered sums of the loss and the ParamGrads
+            double mine[PG_SLOTS + 1];
+            d2h_raw(mine, aw.pg_acc, sizeof(double) * PG_SLOTS);
+            mine[PG_SLOTS] = loss_local;
+            h2d_raw(dist_gather, mine, sizeof(mine));
+            std::vector<double> all(size_t(dist.nranks) * (PG_SLOTS + 1));
+            if (dist.nranks > 1) {
+                double* gbuf = nullptr;
+                CK(cudaMalloc(&gbuf, sizeof(double) * all.size()));
+                owned.v.push_back(gbuf);
+                X.allgather(stream, dist_gather, gbuf, sizeof(double) * (PG_SLOTS + 1));
+                d2h_raw(all.data(), gbuf, sizeof(double) * all.size());
+            } else {
+                std::memcpy(all.data(), mine, sizeof(mine));
+            }
+            double tot[PG_SLOTS + 1] = {0};
+            for (int r = 0; r < dist.nranks; ++r)
+                for (int q = 0; q <= PG_SLOTS; ++q)
+                    tot[q] += all[size_t(r) * (PG_SLOTS + 1) + q];
+            h2d_raw(aw.pg_acc, tot, sizeof(double) * PG_SLOTS);
+            aw.pg_download(*this, pg);
+            float dev_ms = 0;
+            CK(cudaEventElapsedTime(&dev_ms, ev0.e, ev1.e));
+            // this rank's cotangent of S^0 (storage order of the checkpoint) and the particle ids
+            buf[0] = ckpt[0];
+            cur = 0;
+            aw.cot_download(*this, c0, cb);
+            std::vector<int> pids(std::max<int64_t>(n, 1));
+            d2h_raw(pids.data(), ckpt[0].pid, sizeof(int) * n);
+            for (int64_t i = 0; i < n; ++i)
+                c0_ids[i] = pids[i];
+            c0->n = n;
+            if (res) {
+                res->loss = tot[PG_SLOTS];
+                res->checkpoints_stored = nseg;
+                res->peak_replay_states = peak;
+                res->device_ms = dev_ms;
+            }
+            buf[0] = own0;
+            buf[1] = own1;
+            cur = cur0;
+            n = ckn[0];
+            pbuf_copy(buf[cur], ckpt[0]);
+            step = step0;
+            keys_valid = false;
+            inc_invalidate();
+            CK(cudaStreamSynchronize(stream));
+        } catch (...) {
+            buf[0] = own0;
+            buf[1] = own1;
+            cur = cur0;
+            keys_valid = false;
+            dist_store = false;
+            use_sort_set(own_ss0);
+            inc_invalidate();
+            cudaStreamSynchronize(stream);
+            throw;
+        }
+    }
+    void dist_backprop_nccl(int64_t total, int nseg, const mpm_seeder_desc* sd, int64_t id_space, mpm_cot_view* c0,
+                            int64_t* c0_ids, mpm_param_grads* pg, mpm_backprop_result* res) override
+    {
+        if (!dist.comm)
+            throw ApiError(MPM_ERR_USAGE, "dist: context not attached to an NCCL communicator");
+        NcclX X(dist.comm, dist.comm_stream, dist.ev_a, dist.ev_b);
+        dist_backprop(X, total, nseg, sd, id_space, c0, c0_ids, pg, res);
+    }
+    void dist_backprop_local(LocalHub* hub, int64_t total, int nseg, const mpm_seeder_desc* sd, int64_t id_space,
+                             mpm_cot_view* c0, int64_t* c0_ids, mpm_param_grads* pg, mpm_backprop_result* res) override
+    {
+        CK(cudaSetDevice(device));
+        LocalX X(hub, dist.rank);
+        dist_backprop(X, total, nseg, sd, id_space, c0, c0_ids, pg, res);
+    }
+    void dist_sync_count()
+    {
+        int dn = 0;
+        CK(cudaMemcpyAsync(&dn, dist.d_n, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        n = dn;
+    }
+
     // n decomposed steps on an NCCL rank; graph-replayed after the first (its radix sort and the
     // count upload run eagerly), no host synchronisation until the status check at the end
     void dist_advance(int64_t nsteps, uint32_t flags, double* ms) override
@@ -1649,6 +2323,8 @@ template <class T, int D> struct Ctx : CtxBase {
             mig.hi = alloc<T>((size_t)mig_cap * mig.rec);
             mig.lo_pid = alloc<int>(mig_cap);
             mig.hi_pid = alloc<int>(mig_cap);
+            mig.lo_slot = alloc<int>(mig_cap);
+            mig.hi_slot = alloc<int>(mig_cap);
         }
         for (auto& g : graphs)
             for (auto& h : g)
@@ -2666,6 +3342,58 @@ int mpm_dist_advance_local(mpm_ctx* const* ctxs, int nranks, int64_t n_steps, ui
             rc = e;
     }
     return rc;
+}
+
+int mpm_dist_backprop(mpm_ctx* c, int64_t total, int nseg, const mpm_seeder_desc* sd, int64_t id_space,
+                      mpm_cot_view* c0, int64_t* c0_ids, mpm_param_grads* pg, mpm_backprop_result* res)
+{
+    MPM_CALL(c, c->impl->dist_backprop_nccl(total, nseg, sd, id_space, c0, c0_ids, pg, res));
+}
+int mpm_dist_backprop_local(mpm_ctx* const* ctxs, int nranks, int64_t total, int nseg, const mpm_seeder_desc* sd,
+                            int64_t id_space, mpm_cot_view* c0s, int64_t* const* c0_ids, mpm_param_grads* pg,
+                            mpm_backprop_result* res)
+{
+    if (!ctxs || nranks < 1 || !c0s || !c0_ids || !pg)
+        return MPM_ERR_USAGE;
+    for (int r = 0; r < nranks; ++r)
+        if (!ctxs[r])
+            return MPM_ERR_USAGE;
+    std::unique_ptr<LocalHub> hub;
+    int rc = guarded(ctxs[0], [&] { hub = std::make_unique<LocalHub>(nranks); });
+    if (rc)
+        return rc;
+    // ranks other than 0 write their (identical, rank-ordered) ParamGrads into scratch copies
+    std::vector<std::vector<std::vector<double>>> fr(nranks, std::vector<std::vector<double>>(6));
+    std::vector<mpm_param_grads> pgs(nranks, *pg);
+    for (int r = 1; r < nranks; ++r)
+        for (int w = 0; w < 6; ++w)
+            if (pg->wall_friction[w]) {
+                fr[r][w].assign(MAX_FRIC, 0.0);
+                pgs[r].wall_friction[w] = fr[r][w].data();
+            }
+    std::vector<mpm_backprop_result> rs(nranks);
+    std::vector<int> codes(nranks, 0);
+    std::vector<std::thread> th;
+    for (int r = 0; r < nranks; ++r)
+        th.emplace_back([&, r] {
+            codes[r] = guarded(ctxs[r], [&] {
+                try {
+                    ctxs[r]->impl->dist_backprop_local(hub.get(), total, nseg, sd, id_space, &c0s[r], c0_ids[r],
+                                                       r == 0 ? pg : &pgs[r], &rs[r]);
+                } catch (...) {
+                    hub->fail();
+                    throw;
+                }
+            });
+        });
+    for (auto& t : th)
+        t.join();
+    if (res)
+        *res = rs[0];
+    for (int r = 0; r < nranks; ++r)
+        if (codes[r])
+            return codes[r];
+    return MPM_OK;
 }
 
 int mpm_grid_stats(mpm_ctx* c, int64_t* an, int64_t* ob, int64_t* anb) { MPM_CALL(c, c->impl->grid_stats(an, ob, anb)); }

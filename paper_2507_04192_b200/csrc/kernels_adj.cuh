@@ -2020,9 +2020,11 @@ __global__ void __launch_bounds__(256) k_seed_lagrangian(PBuf<T, D> P, int n, co
     const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (l < nsel) {
         const int pid = sel ? int(sel[l]) : int(l);
-        const int s = slot_of_pid[pid];
+        const int s = slot_of_pid[pid]; // -1: not on this rank (slab decomposition)
 #pragma unroll
         for (int a = 0; a < D; ++a) {
+            if (s < 0)
+                break;
             const T z = field == 0 ? P.x[a][s] : P.v[a][s];
             const T r = z - target[l * D + a];
             acc += r * r;
@@ -2226,7 +2228,7 @@ __global__ void k_cot_out(Stage<T, D> S, CBuf<T, D> k, int n, int has_aff, int g
 template <class T, int D> __global__ void k_slot_of_pid(PBuf<T, D> P, int n, int* slot_of_pid)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n)
+    if (i < n && P.pid[i] >= 0) // vacated slots (exported particles) carry pid -1
         slot_of_pid[P.pid[i]] = i;
 }
 

@@ -13,6 +13,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "kernels_adj.cuh"
 #include "kernels_fwd.cuh"
 
 namespace mpmgpu {
@@ -138,6 +139,89 @@ __global__ void k_dist_import(DevScene<T, D> sc, PBuf<T, D> P, const int* __rest
     }
     keys[i] = key;
     okeys[i] = -1;
+}
+
+// ---- decomposed adjoint: the cotangent rows of migrants go back to their step-t owner ----------
+// A particle exported by rank r during step t sits, at t+1, on the neighbour (appended after the
+// neighbour's G2P output in particle-id order). The VJP of step t runs on r, which holds the particle
+// in S^t; it needs the particle's cotangent of S^{t+1}, i.e. the neighbour's row. The neighbour packs
+// the rows of its imports from r (fixed capacity, count in front) and r writes them into the slots
+// its G2P vacated (export list sorted by particle id = the neighbour's import order).
+template <class T, int D> __device__ __forceinline__ int cot_row_values(int has_aff) { return 2 * D + 2 + (D == 2 ? 1 : 0) + 2 * D * D + (has_aff ? D * D : 0); }
+
+template <class T, int D>
+__device__ __forceinline__ void cot_row_io(CBuf<T, D>& c, int i, T* row, bool load, int gv_zero, int has_aff)
+{
+    int q = 0;
+    auto io = [&](T* a) {
+        if (load)
+            row[q] = a ? a[i] : T(0);
+        else if (a)
+            a[i] = row[q];
+        ++q;
+    };
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        io(c.x[a]);
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        io(c.v[a]);
+    io(c.rho);
+    io(c.V);
+    if (D == 2)
+        io(c.szz);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k)
+        io(c.sig[k]);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k)
+        io(gv_zero ? nullptr : c.gv[k]);
+    if (has_aff)
+        for (int k = 0; k < D * D; ++k)
+            io(c.aff[k]);
+}
+
+// rows [base + off, base + off + k) of cot -> out (k = *cnt, base = *nlive); off = 0 for the imports
+// from the lower neighbour, *cnt_lo for those from the upper one
+template <class T, int D>
+__global__ void k_cot_pack(CBuf<T, D> c, const int* __restrict__ nlive, const long long* __restrict__ cnt_lo,
+                           const long long* __restrict__ cnt, int upper, T* __restrict__ out, int gv_zero, int has_aff)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = int(*cnt);
+    if (j >= k)
+        return;
+    const int i = *nlive + (upper ? int(*cnt_lo) : 0) + j;
+    const int nv = cot_row_values<T, D>(has_aff);
+    cot_row_io<T, D>(c, i, out + (size_t)j * nv, true, gv_zero, has_aff);
+}
+
+// in (rows in particle-id order of this rank's exports to one side) -> cot at the vacated slots
+template <class T, int D>
+__global__ void k_cot_unpack(CBuf<T, D> c, const long long* __restrict__ ex_cnt, const int* __restrict__ ex_pid,
+                             const int* __restrict__ ex_slot, const T* __restrict__ in, int gv_zero, int has_aff)
+{
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = int(*ex_cnt);
+    if (e >= k)
+        return;
+    const int me = ex_pid[e];
+    int rank = 0;
+    for (int l = 0; l < k; ++l)
+        rank += ex_pid[l] < me;
+    const int nv = cot_row_values<T, D>(has_aff);
+    T row[2 * D + 3 + 3 * D * D];
+    const T* r = in + (size_t)rank * nv;
+    for (int q = 0; q < nv; ++q)
+        row[q] = r[q];
+    cot_row_io<T, D>(c, ex_slot[e], row, false, gv_zero, has_aff);
+}
+
+// the export counts of the step just taken (G2P's counters; capped like the messages)
+__global__ void k_dist_export_counts(const DevStatus* st, long long* cnt, int cap)
+{
+    cnt[0] = st->mig_lo < cap ? st->mig_lo : cap;
+    cnt[1] = st->mig_hi < cap ? st->mig_hi : cap;
 }
 
 } // namespace mpmgpu

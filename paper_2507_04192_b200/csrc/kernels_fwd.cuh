@@ -1655,6 +1655,8 @@ template <class T> struct MigBuf {
     T* hi;
     int* lo_pid;
     int* hi_pid;
+    int* lo_slot; // the vacated output slot of each export (the decomposed adjoint returns
+    int* hi_slot; // the particle's cotangent row there)
 };
 
 // per-thread staging of a particle's G2P inputs (x, v, m, V, rho, eps, [szz], sigma, [F])
@@ -2019,6 +2021,7 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                                 rec[q++] = Fm[k2];
                         }
                         (side ? MG.hi_pid : MG.lo_pid)[k] = pid;
+                        (side ? MG.hi_slot : MG.lo_slot)[k] = i;
                     } else {
                         st->mig_over = 1;
                         st->abort = 1;

@@ -860,6 +860,35 @@ def _dist_capacity(n_local: int, n_total: int, n_ranks: int, mig_cap: int) -> in
     return max(1024, int(1.25 * n_local) + n_total // (4 * n_ranks) + 2 * mig_cap)
 
 
+def _dist_cot_views(ctxs, template: SimState):
+    """per rank: a writable cotangent view sized for its live particles, plus the id array"""
+    from .state import StateCotangent
+
+    outs = []
+    p = template.particles
+    for c in ctxs:
+        k = int(c.lib.mpm_local_count(c.h))
+        prt = ParticleSoA(k, p.dim, p.dtype, p.affine is not None, False)
+        cot = StateCotangent.zeros_like(prt)
+        v, keep = cot.to_view()
+        ids = np.empty(max(k, 1), np.int64)
+        outs.append((cot, v, keep, ids))
+    return outs
+
+
+def _dist_cot_assemble(outs, n_total: int, template: SimState):
+    """rows of every rank (c0.n of them, storage order) -> the global cotangent in id order"""
+    from .state import StateCotangent
+
+    glob = StateCotangent.zeros_like(template.particles)
+    for cot, v, keep, ids in outs:
+        k = int(v.n)
+        cot.sync_from(keep)
+        live = np.nonzero(ids[:k] >= 0)[0]  # vacated slots (exported particles) carry id -1
+        glob.put(ids[live], cot.take(live))
+    return glob
+
+
 class NcclSlabRank:
     """This process's rank of the decomposition (one process per GPU): a context owning particles
     [lo, hi) of the plan and an NCCL communicator (mpm_dist_attach_nccl)."""
@@ -891,6 +920,27 @@ class NcclSlabRank:
         self.ctx.check(self.lib.mpm_dist_advance(self.h, int(n), capi.MPM_ADV_NAN_GUARD if nan_guard else 0,
                                                  C.byref(ms)))
         return ms.value
+
+    def backprop(self, total: int, nseg: int, seeder: dict, id_space: int):
+        """backprop_trajectory over the decomposition (mpm_dist_backprop): returns (this rank's cotangent
+        rows with their global ids, ParamGrads (rank-ordered sum, identical on every rank), result)"""
+        from . import capi
+        from .seeders import make_seeder_desc
+        from .state import ParamGrads
+
+        sd, keep_sd = make_seeder_desc(seeder, self.scene.np_dtype)
+        (cot, v, keep, ids), = _dist_cot_views([self.ctx], self._template)
+        pg = ParamGrads(self.scene.boundary)
+        pv = pg.to_view()
+        res = capi.BackpropResultView()
+        self.ctx.check(self.lib.mpm_dist_backprop(self.h, int(total), int(nseg), C.byref(sd), int(id_space),
+                                                  C.byref(v), ids.ctypes.data_as(C.c_void_p), C.byref(pv),
+                                                  C.byref(res)))
+        k = int(v.n)
+        cot.sync_from(keep)
+        pg.sync_from(pv)
+        live = np.nonzero(ids[:k] >= 0)[0]  # vacated slots carry id -1
+        return cot.take(live), ids[live], pg, res
 
     def gather(self):
         """(particles, global ids, (step, time)) of this rank's live particles"""
@@ -955,6 +1005,43 @@ class LocalSlabGroup:
             if errs:
                 errs[0][1].check(errs[0][2])
             self.ctxs[0].check(rc)
+
+    def backprop(self, total: int, nseg: int, seeder: dict):
+        """backprop_trajectory (checkpoint.hpp:72-143) over the decomposition, device-resident
+        (mpm_dist_backprop_local): (global cotangent of S^0 in id order, ParamGrads, result)"""
+        from . import capi
+        from .seeders import make_seeder_desc
+        from .state import ParamGrads
+
+        sd, keep_sd = make_seeder_desc(seeder, self.scene.np_dtype)
+        outs = _dist_cot_views(self.ctxs, self._template)
+        R = len(self.ctxs)
+        views = (capi.CotView * R)(*[o[1] for o in outs])
+        idp = (C.c_void_p * R)(*[o[3].ctypes.data for o in outs])
+        pg = ParamGrads(self.scene.boundary)
+        pv = pg.to_view()
+        res = capi.BackpropResultView()
+        rc = self.lib.mpm_dist_backprop_local(self._arr, R, int(total), int(nseg), C.byref(sd), int(self.n_total),
+                                              views, idp, C.byref(pv), C.byref(res))
+        if rc:
+            self._raise(rc)
+        for k, o in enumerate(outs):
+            o[1].n = views[k].n
+        pg.sync_from(pv)
+        return _dist_cot_assemble(outs, self.n_total, self._template), pg, res
+
+    def _raise(self, rc):
+        errs = []
+        for c in self.ctxs:
+            code = C.c_int()
+            buf = C.create_string_buffer(1024)
+            c.lib.mpm_last_error(c.h, C.byref(code), None, None, buf, 1024)
+            if code.value:
+                errs.append((b"another" in buf.value, c, code.value))
+        errs.sort(key=lambda e: e[0])
+        if errs:
+            errs[0][1].check(errs[0][2])
+        self.ctxs[0].check(rc)
 
     def gather(self) -> SimState:
         """the global state in particle-id order"""

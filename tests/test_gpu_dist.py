@@ -146,3 +146,124 @@ def test_c4_two_slabs_close_to_single_context():
     g.close()
     ref = plain_gpu(s, st, 6, [1, 5])
     assert_state_close(got, ref, 1e-10, what="C4 R=2")
+
+
+# ---- decomposed backprop_trajectory, device-resident (mpm_dist_backprop[_local]) ---------------
+def single_backprop(s, st, N, nseg, seeder):
+    ctx = Context(s, st.particles.size())
+    c0, pg, res = ctx.backprop(st, N, nseg, seeder)
+    ctx.close()
+    return c0, pg, res
+
+
+def _lag_seeder(s, st, N):
+    ctx = Context(s, st.particles.size())
+    ctx.upload(st)
+    ctx.advance(N)
+    xf = ctx.download(st.copy()).particles.x
+    ctx.close()
+    rng = np.random.default_rng(4)
+    sel = np.sort(rng.choice(len(xf), len(xf) // 3, replace=False)).astype(np.int64)
+    return {"field": "x", "obs_steps": [N // 2, N], "sel": sel,
+            "target": np.stack([xf[sel] + 0.002, xf[sel] - 0.001])}
+
+
+def _assert_cot_close(got, want, tol, what):
+    from helpers import rel_err
+    for f in ("x", "v", "rho", "volume", "sigma"):
+        e = rel_err(getattr(got, f), getattr(want, f))
+        assert e <= tol, (what, f, e)
+
+
+@pytest.mark.parametrize("dim,R,nseg", [(2, 1, 1), (2, 2, 1), (2, 3, 2), (3, 2, 3), (3, 4, 1)])
+def test_dist_backprop_matches_single_context(dim, R, nseg):
+    """migrating fluid block: the decomposed gradient (device-resident, cotangent rows of migrants
+    returned to their owners) equals the single context's to round-off"""
+    s = moving_fluid_scene(dim)
+    st = init_scene(s)
+    N = 24 if dim == 2 else 12
+    seeder = _lag_seeder(s, st, N)
+    want_c0, want_pg, want_res = single_backprop(s, st, N, nseg, seeder)
+    plan = SlabPlan.make(s, R, st.particles.x)
+    g = LocalSlabGroup(s, plan, st)
+    got_c0, got_pg, got_res = g.backprop(N, nseg, seeder)
+    after = g.gather()
+    g.close()
+    assert abs(got_res.loss - want_res.loss) <= 1e-10 * abs(want_res.loss)
+    _assert_cot_close(got_c0, want_c0, 1e-8 if R > 1 else 1e-12, f"R={R}")
+    assert abs(got_pg.sound_speed - want_pg.sound_speed) <= 1e-8 * abs(want_pg.sound_speed)
+    for f in FIELDS:  # the group's state is S^0 again
+        assert np.array_equal(getattr(after.particles, f), getattr(st.particles, f)), f
+
+
+def test_dist_backprop_friction_and_segment_invariance():
+    """a fluid block sliding over a 4-segment Coulomb floor in 2 slabs: friction gradients vs the
+    single context; the gradient is bit-identical for 1, 2 and 4 checkpoint segments. (A fluid:
+    a Drucker-Prager block seeded at sigma = 0 sits on the cone's apex, where round-off differences
+    of the halo sums legitimately select other return-map branches in the VJP.)"""
+    from paper_2507_04192_b200 import Wall
+    s = moving_fluid_scene(3)
+    s.boundary.walls[2] = Wall("coulomb", [0.1, 0.3, 0.2, 0.4])
+    s.geometry[0].lo[1] = 2 * s.config.dh  # the lowest nodes lie in the wall band
+    st = init_scene(s)
+    N = 8
+    seeder = _lag_seeder(s, st, N)
+    want_c0, want_pg, want_res = single_backprop(s, st, N, 1, seeder)
+    plan = SlabPlan([0, 16, 32], 8)
+    outs = []
+    for nseg in (1, 2, 4):
+        g = LocalSlabGroup(s, plan, st)
+        outs.append(g.backprop(N, nseg, seeder))
+        g.close()
+    c0, pg, res = outs[0]
+    fr_want, fr_got = want_pg.wall_friction[2], pg.wall_friction[2]
+    assert np.abs(fr_want).max() > 0
+    assert np.abs(fr_got - fr_want).max() <= 1e-8 * np.abs(fr_want).max()
+    _assert_cot_close(c0, want_c0, 1e-8, "coulomb fluid R=2")
+    for c_k, pg_k, res_k in outs[1:]:
+        assert res_k.loss == res.loss
+        assert np.array_equal(pg_k.flat(), pg.flat())
+        for f in ("x", "v", "sigma"):
+            assert np.array_equal(getattr(c_k, f), getattr(c0, f)), f
+
+
+def test_dist_backprop_nccl_single_rank():
+    s = moving_fluid_scene(2)
+    st = init_scene(s)
+    N = 10
+    seeder = _lag_seeder(s, st, N)
+    want_c0, want_pg, want_res = single_backprop(s, st, N, 2, seeder)
+    plan = SlabPlan([0, s.config.cells[0]], 16)
+    ids = np.arange(st.particles.size(), dtype=np.int64)
+    rk = NcclSlabRank(s, plan, 0, st, ids, dist_unique_id())
+    cot, gid, pg, res = rk.backprop(N, 2, seeder, st.particles.size())
+    rk.close()
+    got = want_c0.copy()
+    got.put(gid, cot)
+    assert abs(res.loss - want_res.loss) <= 1e-12 * abs(want_res.loss)
+    _assert_cot_close(got, want_c0, 1e-12, "nccl R=1")
+
+
+@pytest.mark.parametrize("cap", [None, "1"])
+def test_dist_backprop_tape_bitwise(cap, monkeypatch):
+    """the replay tape (each replay step's sort arrays and forward grid kept for its VJP) changes
+    nothing: bit-identical to recomputing the forward replay inside every decomposed step_vjp;
+    cap=1 forces every step to overflow its slot (the recompute fallback)"""
+    s = moving_fluid_scene(2)
+    st = init_scene(s)
+    N = 16
+    seeder = _lag_seeder(s, st, N)
+    plan = SlabPlan.make(s, 3, st.particles.x)
+    res = []
+    for tape in ("1", "0"):
+        monkeypatch.setenv("MPM_TAPE", tape)
+        if cap:
+            monkeypatch.setenv("MPM_TAPE_CAP", cap)
+        g = LocalSlabGroup(s, plan, st)
+        res.append(g.backprop(N, 2, seeder))
+        g.close()
+    (a, pa, ra), (b, pb, rb) = res
+    assert ra.loss == rb.loss
+    assert np.array_equal(pa.flat(), pb.flat())
+    for f in ("x", "v", "sigma", "rho", "volume"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
