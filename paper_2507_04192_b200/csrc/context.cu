@@ -859,10 +859,14 @@ template <class T, int D> struct Ctx : CtxBase {
         last_sort_full = !inc_ok;
         if (inc_ok) {
             const IncSrc o = inc_src;
-            CK(cudaMemsetAsync(counts, 0, sizeof(int) * 4, stream));
-            CK(cudaMemsetAsync(nflag, 0, sc.nnb_total, stream));
             IncSort is = inc;
             is.d_n = dist.on ? dist.d_n : nullptr; // decomposed steps: the count lives on the device
+            is.nflag = nflag;
+            is.nnb_total = sc.nnb_total;
+            is.nb = d_nb;
+            is.nnb = d_nnb;
+            is.act = act;
+            is.counts = counts;
             const int64_t nthr = dist.on ? cap : n;
             launch("k_sort_classify", [&] {
                 k_inc_classify<D><<<grid_for((nthr + 3) / 4, 256), 256, 0, stream>>>(keys, o.ks, int(n), sc.nb_total, is);
@@ -870,17 +874,17 @@ template <class T, int D> struct Ctx : CtxBase {
             const bool lpt = occ_lpt && D == 3;
             const unsigned nbc = unsigned((sc.nb_total + 255) / 256);
             launch("k_sort_count", [&] {
-                k_inc_count<D><<<nbc, 256, 0, stream>>>(sc.nb_total, o.bs, o.be, inc, bend);
+                k_inc_count<D><<<nbc, 256, 0, stream>>>(sc.nb_total, o.bs, o.be, is, bend);
             });
             launch("k_sort_offsets", [&] {
                 if (lpt)
-                    k_inc_offsets<D, true><<<nbc, 256, 0, stream>>>(sc.nb_total, inc, bstart, bend, occ, counts);
+                    k_inc_offsets<D, true><<<nbc, 256, 0, stream>>>(sc.nb_total, is, bstart, bend, occ, counts);
                 else
-                    k_inc_offsets<D, false><<<nbc, 256, 0, stream>>>(sc.nb_total, inc, bstart, bend, occ, counts);
+                    k_inc_offsets<D, false><<<nbc, 256, 0, stream>>>(sc.nb_total, is, bstart, bend, occ, counts);
             });
-            launch("k_sort_place", [&] { k_inc_place<D><<<nsm, 256, 0, stream>>>(keys, inc, nsm * 256); });
+            launch("k_sort_place", [&] { k_inc_place<D><<<nsm, 256, 0, stream>>>(keys, is, nsm * 256); });
             launch("k_sort_block", [&] {
-                k_inc_block<D><<<persistent(8), INC_THREADS, 0, stream>>>(keys, o.ks, o.bs, o.be, inc, bstart, bend,
+                k_inc_block<D><<<persistent(8), INC_THREADS, 0, stream>>>(keys, o.ks, o.bs, o.be, is, bstart, bend,
                                                                           occ, counts, perm, keys_sorted, lstart);
             });
         } else {
@@ -906,8 +910,10 @@ template <class T, int D> struct Ctx : CtxBase {
                 launch("k_compact", [&] { k_compact_pos<<<grid_for(sc.nb_total, 256), 256, 0, stream>>>(bstart, sc.nb_total, occ, counts); });
             }
         }
-        launch("k_mark_nodes", [&] { k_mark_nodes<D><<<grid_for(sc.nb_total, 128), 128, 0, stream>>>(occ, counts, d_nb, d_nnb, nflag); });
-        launch("k_compact", [&] { k_compact_flag<<<grid_for(sc.nnb_total, 256), 256, 0, stream>>>(nflag, sc.nnb_total, act, counts + 1); });
+        if (!inc_ok) { // (the incremental sort's kernels mark and list the node blocks themselves)
+            launch("k_mark_nodes", [&] { k_mark_nodes<D><<<grid_for(sc.nb_total, 128), 128, 0, stream>>>(occ, counts, d_nb, d_nnb, nflag); });
+            launch("k_compact", [&] { k_compact_flag<<<grid_for(sc.nnb_total, 256), 256, 0, stream>>>(nflag, sc.nnb_total, act, counts + 1); });
+        }
     }
 
     void p2g_kernel()

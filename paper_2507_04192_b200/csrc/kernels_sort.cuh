@@ -54,6 +54,14 @@ struct IncSort {
     int* bcur;    // [OCC_NBUCKET] bucket cursors (zeroed by k_inc_block)
     int* nlive;   // [1] particles the sort placed (= the count G2P writes)
     const int* d_n; // device particle count (decomposed steps) or nullptr (the host's n)
+    // the step's active-node bookkeeping, folded into the sort's kernels (fewer graph nodes per
+    // step: the 2-D scenes are launch-latency bound)
+    unsigned char* nflag; // [nnb_total] node blocks touched (zeroed by k_inc_classify, set by k_inc_offsets)
+    int nnb_total;
+    const int* nb;        // [D] particle blocks per axis (device)
+    const int* nnb;       // [D] node blocks per axis (device)
+    int* act;             // active node-block list (k_inc_place)
+    int* counts;          // [4] counts[0] occupied blocks, counts[1] active node blocks
 };
 
 // 4 particles per thread (two 16-byte loads per thread keep enough bytes in flight)
@@ -64,6 +72,19 @@ __global__ void __launch_bounds__(256) k_inc_classify(const int* __restrict__ ke
     using C = Cfg<D>;
     if (S.d_n)
         n = *S.d_n;
+    { // zero this step's node-block flags (16 bytes per thread) and the list counters
+        const int t = blockIdx.x * blockDim.x + threadIdx.x;
+        const int nq = (S.nnb_total + 15) / 16;
+        for (int q = t; q < nq; q += gridDim.x * blockDim.x) {
+            if (16 * q + 16 <= S.nnb_total)
+                reinterpret_cast<uint4*>(S.nflag)[q] = make_uint4(0, 0, 0, 0);
+            else
+                for (int c = 16 * q; c < S.nnb_total; ++c)
+                    S.nflag[c] = 0;
+        }
+        if (t == 0)
+            S.counts[1] = 0;
+    }
     const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
     int k[4], o[4];
     if (i0 + 3 < n) {
@@ -230,10 +251,31 @@ __global__ void __launch_bounds__(256) k_inc_offsets(int nb_total, IncSort S, in
             } else {
                 occ[po + o - 1] = b;
             }
+            // node blocks touched by block b: b + s, s in {0,1}^D (k_mark_nodes)
+            int q[D], rem = b;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+                q[a] = rem % S.nb[a];
+                rem /= S.nb[a];
+            }
+#pragma unroll
+            for (int sft = 0; sft < (1 << D); ++sft) {
+                int id = 0;
+                bool ok = true;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const int c2 = q[a] + ((sft >> (D - 1 - a)) & 1);
+                    ok &= c2 < S.nnb[a];
+                    id = id * S.nnb[a] + c2;
+                }
+                if (ok)
+                    S.nflag[id] = 1;
+            }
         }
     }
 }
 
+// movers into their buckets, and the active node-block list (k_compact_flag's compaction)
 template <int D>
 __global__ void __launch_bounds__(256) k_inc_place(const int* __restrict__ keys, IncSort S, int grid_threads)
 {
@@ -243,6 +285,18 @@ __global__ void __launch_bounds__(256) k_inc_place(const int* __restrict__ keys,
         const int i = S.xlist[j];
         const int b = keys[i] >> C::LOGNB;
         S.inbuf[S.in_off[b] + atomicAdd(&S.cnt_out[b], 1)] = i;
+    }
+    const int lane = threadIdx.x & 31;
+    for (int q0 = blockIdx.x * blockDim.x; q0 < S.nnb_total; q0 += grid_threads) {
+        const int q = q0 + threadIdx.x;
+        const bool p = q < S.nnb_total && S.nflag[q] != 0;
+        const unsigned m = __ballot_sync(0xffffffffu, p);
+        int base = 0;
+        if (lane == 0 && m)
+            base = atomicAdd(S.counts + 1, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (p)
+            S.act[base + __popc(m & ((1u << lane) - 1))] = q;
     }
 }
 
