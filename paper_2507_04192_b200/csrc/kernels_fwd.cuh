@@ -1510,6 +1510,9 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
         }
     }
     unsigned long long nact_nodes = 0;
+    // the (up to 2^D) source tiles of the current node block, resolved once per CTA: the per-node
+    // loop then issues its tile loads without a dependent bstart load per source
+    __shared__ const T* s_part[1 << D];
     for (int w = blockIdx.x; w < nact; w += gridDim.x) {
         const int q = act[w];
         int qc[D], n[D];
@@ -1518,6 +1521,21 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
             const int x0 = qc[0] * C::B;
             if (!((sc.band_lo + 1 >= x0 && sc.band_lo < x0 + C::B) || (sc.band_hi + 1 >= x0 && sc.band_hi < x0 + C::B)))
                 continue;
+        }
+        if (MODE & G_SUM) {
+            __syncthreads(); // the previous node block's readers are done
+            if (tid < (1 << D)) {
+                int Qid = 0;
+                bool ok = true;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const int Qa = qc[a] - ((tid >> (D - 1 - a)) & 1);
+                    ok &= Qa >= 0 && Qa < sc.nb[a];
+                    Qid = Qid * sc.nb[a] + Qa;
+                }
+                s_part[tid] = ok && bstart[Qid] >= 0 ? partials + (size_t)Qid * C::NF * C::TN : nullptr;
+            }
+            __syncthreads();
         }
         bool inside = true;
 #pragma unroll
@@ -1542,32 +1560,23 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
             // fixed order over source blocks Q = q - s, s lexicographic in {0,1}^D
 #pragma unroll
             for (int s = 0; s < (1 << D); ++s) {
-                int Qid = 0, tl = 0;
-                bool ok = true;
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    const int sa = (s >> (D - 1 - a)) & 1;
-                    const int Qa = qc[a] - sa;
-                    const int t = n[a] - Qa * C::B;
-                    ok &= Qa >= 0 && Qa < sc.nb[a] && t < C::TE;
-                    Qid = Qid * sc.nb[a] + Qa;
-                    (void)t;
-                }
-                if (!ok || bstart[Qid] < 0)
-                    continue;
+                const T* base = s_part[s];
+                bool ok = base != nullptr;
                 // tile index: last axis slowest, columns row-major over the other axes
                 int colx = 0, z = 0;
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
                     const int sa = (s >> (D - 1 - a)) & 1;
-                    const int t = n[a] - (qc[a] - sa) * C::B;
+                    const int t = lc[a] + sa * C::B; // n[a] - (qc[a] - sa) B
+                    ok &= t < C::TE;
                     if (a == D - 1)
                         z = t;
                     else
                         colx = colx * C::TE + t;
                 }
-                tl = ptile<D>(z, colx);
-                const T* part = partials + (size_t)Qid * C::NF * C::TN + tl;
+                if (!ok)
+                    continue;
+                const T* part = base + ptile<D>(z, colx);
                 m += part[0];
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
