@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--slab-adj", action="store_true",
                     help="slab mode: also time the host-orchestrated decomposed backprop (slow; DESIGN.md §7)")
     ap.add_argument("--adj-steps", type=int, default=20, help="fwd+adjoint sample: backprop steps (0: skip)")
+    ap.add_argument("--long-adj", type=int, default=1000,
+                    help="also time a backprop over this many steps with the HBM-sized checkpoint plan (0: skip)")
     ap.add_argument("--adj-segments", type=int, default=0,
                     help="checkpoint segments of the fwd+adjoint sample (0: fewest that fit in HBM)")
     ap.add_argument("--mode", default="auto", choices=["auto", "plain", "slab", "pyslab"],
@@ -318,7 +320,7 @@ def cpu_baseline_adj(cfg, dtype, steps=2, nseg=1):
     return cpu_sample(cfg, dtype, steps, mode="adj", nseg=nseg)
 
 
-def bench_fwd_adj(ctx, s, st, n, steps, nseg):
+def bench_fwd_adj(ctx, s, st, n, steps, nseg, profile=True):
     """fwd+adjoint (BASELINE metric, second half): one checkpointed backprop_trajectory through the
     C ABI -- forward sweep, segment replays, step_vjp per step (checkpoint.hpp:72-143) -- with the
     device Lagrangian least-squares seeder on the final positions. Device time from CUDA events on
@@ -332,10 +334,14 @@ def bench_fwd_adj(ctx, s, st, n, steps, nseg):
     _, _, res = ctx.backprop(st0, steps, nseg, sd.desc())
     wall = time.perf_counter() - t0
     ms = res.device_ms
+    kern = {}
+    if not profile:
+        return {"value": n * steps / (ms / 1e3), "unit": UNIT, "steps": steps, "n_segments": nseg, "device_ms": ms,
+                "ms_per_step": ms / steps, "wall_s_incl_host_transfers": wall, "loss": res.loss,
+                "forward_passes_per_step": 1 + (steps - (steps // nseg)) / steps}
     ctx.profile(True)
     ctx.profile_reset()
     ctx.backprop(st0, steps, nseg, sd.desc())
-    kern = {}
     for k in ("k_p2g", "k_grid", "k_g2p", "k_adj_g2pT_gather", "k_adj_scatter", "k_adj_grid", "k_adj_p2gT",
               "k_seed"):
         t, c = ctx.profile_query(k)
@@ -367,7 +373,8 @@ def vjp_bytes(s, n, active_nodes_step, B_fwd, IN, fwd_passes=2.0):
 # CPU samples of the sub-lines (BASELINE.md §2 horizons where they fit a few minutes of wall
 # time; the reference is serial, so each is run as concurrent replicas on the host cores):
 #   (cfg, mode, steps, n_segments)
-CPU_SUBLINE = {"C2": {"fwd": ("C2", "fwd", 100, 1)},
+CPU_SUBLINE = {"C1": {"fwd": ("C1", "fwd", 1000, 1)},
+               "C2": {"fwd": ("C2", "fwd", 100, 1)},
                "C3": {"fwd": ("C3", "fwd", 100, 1), "fwd_adj": ("C3", "adj", 20, 1)},
                "C5": {"fwd": ("C5", "fwd", 1, 1), "fwd_adj": ("C5/8", "adj", 1, 1)}}
 
@@ -398,7 +405,7 @@ def bench_workloads(peak, names, cpu=True):
             ctx = Context(s, n)
             ctx.upload(st0)
             ctx.advance(3)
-            k_fwd = {"C2": 200, "C3": 200, "C5": 20}[name]
+            k_fwd = {"C1": 1000, "C2": 200, "C3": 200, "C5": 20}[name]
             ms = ctx.advance_timed(k_fwd, nan_guard=True)
             act, _, _ = ctx.grid_stats()
             B_fwd, IN, _ = bytes_model(s, n, act / k_fwd)
@@ -589,6 +596,12 @@ def bench_b200(a, rank, world, local):
         if nseg != 2 and a.adj_steps >= 2:  # the two-segment plan beside it (same loss, more replay)
             alt = bench_fwd_adj(ctx, s, st, n, a.adj_steps, 2)
             fwd_adj["two_segments"] = {k: alt[k] for k in ("value", "ms_per_step", "forward_passes_per_step", "loss")}
+        if a.long_adj > 0:  # the horizon an inverse run sustains (C3 / C5: 1000 steps), HBM-sized plan
+            nl, pl = hbm_plan(s, n, a.long_adj, active_nodes_step)
+            lg = bench_fwd_adj(ctx, s, st, n, a.long_adj, nl, profile=False)
+            fwd_adj["long_horizon"] = {k: lg[k] for k in ("value", "ms_per_step", "steps", "n_segments",
+                                                         "forward_passes_per_step", "loss", "device_ms")}
+            fwd_adj["long_horizon"]["plan"] = pl
         B_fa = vjp_bytes(s, n, active_nodes_step, B_fwd1, IN)
         B_ex = vjp_bytes(s, n, active_nodes_step, B_fwd1, IN, fwd_adj["forward_passes_per_step"])
         gbs = n * B_fa / (fwd_adj["ms_per_step"] / 1e3) / 1e9
@@ -602,7 +615,7 @@ def bench_b200(a, rank, world, local):
     ctx.close()
     workloads = None
     if world == 1 and a.config == "C4" and not a.no_workloads:
-        workloads = bench_workloads(peak, ["C2", "C3", "C5"], cpu=not a.no_cpu_baseline)
+        workloads = bench_workloads(peak, ["C1", "C2", "C3", "C5"], cpu=not a.no_cpu_baseline)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
