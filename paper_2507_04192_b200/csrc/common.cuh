@@ -206,6 +206,13 @@ template <> __device__ __forceinline__ float dsqrt<float>(float x) { return sqrt
 
 template <class T> __device__ __forceinline__ bool finite_(T x) { return isfinite(x); }
 
+// Programmatic dependent launch (the step's kernels are launched with it, context.cu launch_pdl):
+// a kernel may be scheduled while its predecessor drains; it waits here before touching any of
+// the predecessor's outputs, and lets its own successor be scheduled. Both are no-ops for a
+// kernel launched the ordinary way.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // quadratic B-spline weights along one axis (bspline.hpp:76-108): base = floor(u - 1/2),
 // fx = u - base in [1/2, 3/2); returns false when out of the valid interior.
 template <class T> struct Axis {

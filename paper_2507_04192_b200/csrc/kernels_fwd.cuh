@@ -269,6 +269,8 @@ __global__ void __launch_bounds__(256) k_p2g(DevScene<T, D> sc, PBuf<T, D> P, co
                                              const int* __restrict__ n_occ, T* __restrict__ partials,
                                              const DevStatus* st)
 {
+    pdl_wait();
+    pdl_trigger();
     using C = Cfg<D>;
     constexpr int B = C::B, TE = C::TE, NF = C::NF;
     static_assert(!STAGED || (D == 2 && !AFF), "staged P2G: 2-D without affine transfer");
@@ -537,6 +539,8 @@ __global__ void __launch_bounds__(StageCfg<T, D>::THREADS, 1)
                  const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ occ,
                  const int* __restrict__ n_occ, T* __restrict__ partials, const DevStatus* st)
 {
+    pdl_wait();
+    pdl_trigger();
     using C = Cfg<D>;
     using S = StageCfg<T, D>;
     constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NSRC = S::NSRC, NBC = S::NBC;
@@ -871,6 +875,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
                 const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials, DevStatus* st,
                 int* __restrict__ wq)
 {
+    pdl_wait();
+    pdl_trigger();
     using C = Cfg<3>;
     using S = Pipe3Cfg<T, WIDE, NGR>;
     constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW;
@@ -1150,6 +1156,8 @@ __global__ void __launch_bounds__(Lane3Cfg<T>::THREADS, 1)
                  const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ lstart,
                  const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials, DevStatus* st)
 {
+    pdl_wait();
+    pdl_trigger();
     using C = Cfg<3>;
     using S = Lane3Cfg<T>;
     using PL = PLay<3>;
@@ -1495,6 +1503,8 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_grid(DevScene<T, D> sc, GBuf<T, 
                                                      const int* __restrict__ bstart, const int* __restrict__ act,
                                                      const int* __restrict__ n_act, DevStatus* st)
 {
+    pdl_wait();
+    pdl_trigger();
     using C = Cfg<D>;
     if (st->abort)
         return;
@@ -1686,6 +1696,8 @@ __global__ void __launch_bounds__(256, 2) k_g2p(DevScene<T, D> sc, PBuf<T, D> Pi
                                              int* __restrict__ keys_out, DevStatus* st, MigBuf<T> MG,
                                              int* __restrict__ wq)
 {
+    pdl_wait();
+    pdl_trigger();
     using C = Cfg<D>;
     using SG = G2PStage<T, D, TRACKF>;
     constexpr int TE = C::TE, TN = C::TN, NSF = SG::NSF, NT = SG::THREADS;
@@ -2099,6 +2111,8 @@ __global__ void k_constitutive(DevScene<T, D> sc, PBuf<T, D> P, int n, DevStatus
 // forming the next step's keys) did complete -- the reference throws in the next step's P2G
 __global__ void k_step_end(DevStatus* st)
 {
+    pdl_wait();
+    pdl_trigger();
     if (!st->abort) {
         st->step += 1;
     } else if (st->ood_flag == 2 && !st->den_flag && !st->nan_flag && !st->ood_counted) {

@@ -69,6 +69,8 @@ template <int D>
 __global__ void __launch_bounds__(256) k_inc_classify(const int* __restrict__ keys, const int* __restrict__ okeys, int n,
                                                       int nb_total, IncSort S)
 {
+    pdl_wait();
+    pdl_trigger();
     using C = Cfg<D>;
     if (S.d_n)
         n = *S.d_n;
@@ -128,6 +130,8 @@ template <int D>
 __global__ void __launch_bounds__(256) k_inc_count(int nb_total, const int* __restrict__ obstart,
                                                    const int* __restrict__ obend, IncSort S, int* __restrict__ bend)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int ws[8][3];
     const int b = blockIdx.x * 256 + threadIdx.x;
     int cnt = 0, cin = 0;
@@ -169,6 +173,8 @@ __global__ void __launch_bounds__(256) k_inc_offsets(int nb_total, IncSort S, in
                                                      int* __restrict__ bend, int* __restrict__ occ,
                                                      int* __restrict__ counts)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int ws[8][3];
     __shared__ int pre[3];
     __shared__ int boff[OCC_NBUCKET];
@@ -279,6 +285,8 @@ __global__ void __launch_bounds__(256) k_inc_offsets(int nb_total, IncSort S, in
 template <int D>
 __global__ void __launch_bounds__(256) k_inc_place(const int* __restrict__ keys, IncSort S, int grid_threads)
 {
+    pdl_wait();
+    pdl_trigger();
     using C = Cfg<D>;
     const int nx = *S.nx;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nx; j += grid_threads) {
@@ -326,6 +334,8 @@ __global__ void __launch_bounds__(INC_THREADS) k_inc_block(const int* __restrict
                                                            int* __restrict__ perm, int* __restrict__ keys_sorted,
                                                            int* __restrict__ lstart)
 {
+    pdl_wait();
+    pdl_trigger();
     using C = Cfg<D>;
     constexpr int NB = C::NB;
     constexpr int LVLBITS = (D - 1) * C::LOGB;
