@@ -373,7 +373,7 @@ def vjp_bytes(s, n, active_nodes_step, B_fwd, IN, fwd_passes=2.0):
 # CPU samples of the sub-lines (BASELINE.md §2 horizons where they fit a few minutes of wall
 # time; the reference is serial, so each is run as concurrent replicas on the host cores):
 #   (cfg, mode, steps, n_segments)
-CPU_SUBLINE = {"C1": {"fwd": ("C1", "fwd", 1000, 1)},
+CPU_SUBLINE = {"C1": {"fwd": ("C1", "fwd", 1000, 1)}, "C4/f32": {"fwd": ("C4", "fwd", 1, 1, "f32")},
                "C2": {"fwd": ("C2", "fwd", 100, 1)},
                "C3": {"fwd": ("C3", "fwd", 100, 1), "fwd_adj": ("C3", "adj", 20, 1)},
                "C5": {"fwd": ("C5", "fwd", 1, 1), "fwd_adj": ("C5/8", "adj", 1, 1)}}
@@ -399,17 +399,18 @@ def bench_workloads(peak, names, cpu=True):
             if name == "C5" and _mem_available_gb() < 48:
                 out[name] = {"skipped": "host memory below 48 GB for the 7.3 GB host copies"}
                 continue
-            s = CONFIGS[name](dtype="f64")
+            cname, dt = (name.split("/") + ["f64"])[:2]
+            s = CONFIGS[cname](dtype=dt)
             st0 = init_scene(s)
             n = st0.particles.size()
             ctx = Context(s, n)
             ctx.upload(st0)
             ctx.advance(3)
-            k_fwd = {"C1": 1000, "C2": 200, "C3": 200, "C5": 20}[name]
+            k_fwd = {"C1": 1000, "C2": 200, "C3": 200, "C4/f32": 50, "C5": 20}[name]
             ms = ctx.advance_timed(k_fwd, nan_guard=True)
             act, _, _ = ctx.grid_stats()
             B_fwd, IN, _ = bytes_model(s, n, act / k_fwd)
-            w = {"particles": n, "grid_cells": s.config.cells, "dtype": "f64",
+            w = {"particles": n, "grid_cells": s.config.cells, "dtype": dt,
                  "fwd": {"value": n * k_fwd / (ms / 1e3), "unit": UNIT, "steps": k_fwd, "ms_per_step": ms / k_fwd,
                          "roofline_frac": n * B_fwd / (ms / k_fwd / 1e3) / 1e9 / peak,
                          "bytes_per_particle_step": B_fwd}}
@@ -463,10 +464,12 @@ def bench_workloads(peak, names, cpu=True):
             ctx.close()
             torch.cuda.empty_cache()
             if cpu:
-                for leg, (ccfg, mode, steps, cseg) in CPU_SUBLINE.get(name, {}).items():
+                for leg, spec in CPU_SUBLINE.get(name, {}).items():
+                    ccfg, mode, steps, cseg = spec[:4]
+                    cdt = spec[4] if len(spec) > 4 else "f64"
                     if leg in w:
                         try:
-                            w[leg]["cpu_baseline"] = cpu_sample(ccfg, "f64", steps, mode=mode, nseg=cseg)
+                            w[leg]["cpu_baseline"] = cpu_sample(ccfg, cdt, steps, mode=mode, nseg=cseg)
                         except Exception as e:
                             w[leg]["cpu_baseline"] = {"value": None, "error": f"{type(e).__name__}: {str(e)[:160]}"}
             out[name] = w
@@ -615,7 +618,7 @@ def bench_b200(a, rank, world, local):
     ctx.close()
     workloads = None
     if world == 1 and a.config == "C4" and not a.no_workloads:
-        workloads = bench_workloads(peak, ["C1", "C2", "C3", "C5"], cpu=not a.no_cpu_baseline)
+        workloads = bench_workloads(peak, ["C1", "C2", "C3", "C4/f32", "C5"], cpu=not a.no_cpu_baseline)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
