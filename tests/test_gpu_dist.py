@@ -267,3 +267,28 @@ def test_dist_backprop_tape_bitwise(cap, monkeypatch):
     assert np.array_equal(pa.flat(), pb.flat())
     for f in ("x", "v", "sigma", "rho", "volume"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
+def test_dist_c2_three_slabs_backprop_and_c5_forward():
+    """scale: C2 (250,000 fluid particles) in 3 slabs, a 12-step decomposed backprop against the
+    single context; the 1/8-particle C5 (4.06 M particles, 32 Coulomb segments) forward in 2 slabs"""
+    from paper_2507_04192_b200.presets import c2_dam_break, c5_landslide_eighth
+    s = c2_dam_break()
+    st = init_scene(s)
+    N = 12
+    seeder = _lag_seeder(s, st, N)
+    want_c0, want_pg, want_res = single_backprop(s, st, N, 3, seeder)
+    g = LocalSlabGroup(s, SlabPlan.make(s, 3, st.particles.x), st)
+    got_c0, got_pg, got_res = g.backprop(N, 3, seeder)
+    g.close()
+    assert abs(got_res.loss - want_res.loss) <= 1e-10 * abs(want_res.loss)
+    _assert_cot_close(got_c0, want_c0, 1e-8, "C2 R=3")
+    s5 = c5_landslide_eighth()
+    st5 = init_scene(s5)
+    g5 = LocalSlabGroup(s5, SlabPlan([0, 256, 512], 8), st5)
+    g5.advance(1)
+    g5.advance(3)
+    got5 = g5.gather()
+    g5.close()
+    ref5 = plain_gpu(s5, st5, 4, [1, 3])
+    assert_state_close(got5, ref5, 1e-10, what="C5/8 R=2")
