@@ -1664,9 +1664,9 @@ template <class T, int D> struct Ctx : CtxBase {
             NCK(ncclRecv(dist.recs_recv[side], rb, ncclUint8, peer, dist.comm, dist.comm_stream));
             NCK(ncclRecv(dist.pid_recv[side], pb, ncclUint8, peer, dist.comm, dist.comm_stream));
         }
-        if (dist.nranks > 1)
-            NCK(ncclAllReduce(dist.abort_red, dist.abort_red, 1, ncclInt32, ncclMax, dist.comm, dist.comm_stream));
         NCK(ncclGroupEnd());
+        if (dist.nranks > 1) // (a collective of its own, after the point-to-point group)
+            NCK(ncclAllReduce(dist.abort_red, dist.abort_red, 1, ncclInt32, ncclMax, dist.comm, dist.comm_stream));
         CK(cudaEventRecord(dist.ev_b, dist.comm_stream));
         CK(cudaStreamWaitEvent(stream, dist.ev_b, 0));
     }
@@ -2286,8 +2286,14 @@ template <class T, int D> struct Ctx : CtxBase {
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0, stream));
         }
+        // NCCL calls inside a captured graph are supported, but untested here beyond one rank (this
+        // pool gives one GPU per call): with peers the steps are enqueued eagerly unless
+        // MPM_DIST_GRAPH=1 (the host runs ahead asynchronously, so C4-sized steps stay GPU-bound);
+        // MPM_DIST_GRAPH=0 forces the eager path on one rank too (tests compare the two)
+        const char* dg = std::getenv("MPM_DIST_GRAPH");
+        const bool graph_ok = dg ? dg[0] == '1' : dist.nranks == 1;
         for (int64_t k = 0; k < nsteps; ++k) {
-            const bool eager = prof || !inc_source_ok();
+            const bool eager = prof || !inc_source_ok() || !graph_ok;
             if (eager) {
                 dist_step_nccl(guard);
                 continue;

@@ -116,7 +116,10 @@ def test_failure_raises_on_every_rank():
 
 
 @pytest.mark.parametrize("dim", [2, 3])
-def test_nccl_single_rank_bitwise_plain(dim):
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_nccl_single_rank_bitwise_plain(dim, graph, monkeypatch):
+    """graph "0": the eager step path multi-rank NCCL groups take by default"""
+    monkeypatch.setenv("MPM_DIST_GRAPH", graph)
     s = moving_fluid_scene(dim)
     st = init_scene(s)
     plan = SlabPlan([0, s.config.cells[0]], 16 if dim == 2 else 8)
