@@ -13,7 +13,9 @@
 #include "kernels_sort.cuh"
 #include "kernels_dist.cuh"
 
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h> // types only: the functions are resolved at run time (dyn::api)
+#include <type_traits>
 #include "kernels_util.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -66,11 +68,88 @@ struct ApiError : std::runtime_error {
     }
 };
 
+// NCCL is resolved at run time, on the first decomposed call, so the library carries no load-time
+// dependency on a particular libnccl: a process that loads it before torch (which needs its own
+// bundled, newer libnccl.so.2) keeps working, and single-GPU use never touches NCCL. An already
+// loaded libnccl.so.2 (torch's) is preferred; otherwise the loader's search path decides.
+namespace dyn {
+struct Api {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    std::string error;
+};
+inline const Api& api()
+{
+    static const Api a = [] {
+        Api r;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h)
+            h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) {
+            const char* e = dlerror();
+            r.error = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+            return r;
+        }
+        auto sym = [&](auto& fp, const char* name) {
+            fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+            if (!fp && r.error.empty())
+                r.error = std::string("libnccl.so.2 lacks ") + name;
+        };
+        sym(r.GetUniqueId, "ncclGetUniqueId");
+        sym(r.CommInitRank, "ncclCommInitRank");
+        sym(r.CommDestroy, "ncclCommDestroy");
+        sym(r.GetErrorString, "ncclGetErrorString");
+        sym(r.GroupStart, "ncclGroupStart");
+        sym(r.GroupEnd, "ncclGroupEnd");
+        sym(r.Send, "ncclSend");
+        sym(r.Recv, "ncclRecv");
+        sym(r.AllReduce, "ncclAllReduce");
+        sym(r.AllGather, "ncclAllGather");
+        return r;
+    }();
+    if (!a.error.empty())
+        throw ApiError(MPM_ERR_USAGE, "dist: " + a.error);
+    return a;
+}
+inline ncclResult_t ncclGetUniqueId(ncclUniqueId* id) { return api().GetUniqueId(id); }
+inline ncclResult_t ncclCommInitRank(ncclComm_t* c, int n, ncclUniqueId id, int r) { return api().CommInitRank(c, n, id, r); }
+inline ncclResult_t ncclCommDestroy(ncclComm_t c) { return api().CommDestroy(c); }
+inline const char* ncclGetErrorString(ncclResult_t e) { return api().GetErrorString(e); }
+inline ncclResult_t ncclGroupStart() { return api().GroupStart(); }
+inline ncclResult_t ncclGroupEnd() { return api().GroupEnd(); }
+inline ncclResult_t ncclSend(const void* b, size_t n, ncclDataType_t t, int p, ncclComm_t c, cudaStream_t s)
+{
+    return api().Send(b, n, t, p, c, s);
+}
+inline ncclResult_t ncclRecv(void* b, size_t n, ncclDataType_t t, int p, ncclComm_t c, cudaStream_t s)
+{
+    return api().Recv(b, n, t, p, c, s);
+}
+inline ncclResult_t ncclAllReduce(const void* a, void* b, size_t n, ncclDataType_t t, ncclRedOp_t o, ncclComm_t c,
+                                  cudaStream_t s)
+{
+    return api().AllReduce(a, b, n, t, o, c, s);
+}
+inline ncclResult_t ncclAllGather(const void* a, void* b, size_t n, ncclDataType_t t, ncclComm_t c, cudaStream_t s)
+{
+    return api().AllGather(a, b, n, t, c, s);
+}
+} // namespace dyn
+
 #define NCK(call)                                                                                  \
     do {                                                                                           \
         ncclResult_t r_ = (call);                                                                  \
         if (r_ != ncclSuccess)                                                                     \
-            throw ApiError(MPM_ERR_CUDA, std::string("NCCL error: ") + ncclGetErrorString(r_) + " at " \
+            throw ApiError(MPM_ERR_CUDA, std::string("NCCL error: ") + dyn::ncclGetErrorString(r_) + " at " \
                                              + __FILE__ + ":" + std::to_string(__LINE__));         \
     } while (0)
 
@@ -183,12 +262,12 @@ struct NcclX : DistTransport {
     {
         CK(cudaEventRecord(ea, s));
         CK(cudaStreamWaitEvent(cs, ea, 0));
-        NCK(ncclGroupStart());
+        NCK(dyn::ncclGroupStart());
         for (const XItem& it : items) {
-            NCK(ncclSend(it.send, it.bytes, ncclUint8, it.peer, comm, cs));
-            NCK(ncclRecv(it.recv, it.bytes, ncclUint8, it.peer, comm, cs));
+            NCK(dyn::ncclSend(it.send, it.bytes, ncclUint8, it.peer, comm, cs));
+            NCK(dyn::ncclRecv(it.recv, it.bytes, ncclUint8, it.peer, comm, cs));
         }
-        NCK(ncclGroupEnd());
+        NCK(dyn::ncclGroupEnd());
         CK(cudaEventRecord(eb, cs));
     }
     void end(cudaStream_t s) override { CK(cudaStreamWaitEvent(s, eb, 0)); }
@@ -196,7 +275,7 @@ struct NcclX : DistTransport {
     {
         CK(cudaEventRecord(ea, s));
         CK(cudaStreamWaitEvent(cs, ea, 0));
-        NCK(ncclAllGather(send, recv, bytes, ncclUint8, comm, cs));
+        NCK(dyn::ncclAllGather(send, recv, bytes, ncclUint8, comm, cs));
         CK(cudaEventRecord(eb, cs));
         CK(cudaStreamWaitEvent(s, eb, 0));
     }
@@ -600,7 +679,7 @@ template <class T, int D> struct Ctx : CtxBase {
                 if (e)
                     cudaGraphExecDestroy(e);
         if (dist.comm)
-            ncclCommDestroy(dist.comm);
+            dyn::ncclCommDestroy(dist.comm);
         if (dist.comm_stream)
             cudaStreamDestroy(dist.comm_stream);
         if (dist.ev_a)
@@ -1556,7 +1635,7 @@ template <class T, int D> struct Ctx : CtxBase {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
             CK(cudaSetDevice(device));
-            NCK(ncclCommInitRank(&dist.comm, nranks, id, rank));
+            NCK(dyn::ncclCommInitRank(&dist.comm, nranks, id, rank));
         }
         CK(cudaStreamSynchronize(stream));
     }
@@ -1635,16 +1714,16 @@ template <class T, int D> struct Ctx : CtxBase {
         const size_t hb = sizeof(T) * dist.halo_elems;
         CK(cudaEventRecord(dist.ev_a, stream));
         CK(cudaStreamWaitEvent(dist.comm_stream, dist.ev_a, 0));
-        NCK(ncclGroupStart());
+        NCK(dyn::ncclGroupStart());
         if (dist.lo_peer >= 0) {
-            NCK(ncclSend(dist.halo_send[0], hb, ncclUint8, dist.lo_peer, dist.comm, dist.comm_stream));
-            NCK(ncclRecv(dist.halo_recv[0], hb, ncclUint8, dist.lo_peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclSend(dist.halo_send[0], hb, ncclUint8, dist.lo_peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclRecv(dist.halo_recv[0], hb, ncclUint8, dist.lo_peer, dist.comm, dist.comm_stream));
         }
         if (dist.hi_peer >= 0) {
-            NCK(ncclSend(dist.halo_send[1], hb, ncclUint8, dist.hi_peer, dist.comm, dist.comm_stream));
-            NCK(ncclRecv(dist.halo_recv[1], hb, ncclUint8, dist.hi_peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclSend(dist.halo_send[1], hb, ncclUint8, dist.hi_peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclRecv(dist.halo_recv[1], hb, ncclUint8, dist.hi_peer, dist.comm, dist.comm_stream));
         }
-        NCK(ncclGroupEnd());
+        NCK(dyn::ncclGroupEnd());
         CK(cudaEventRecord(dist.ev_b, dist.comm_stream));
     }
     void dist_exchange_mig_nccl()
@@ -1652,21 +1731,21 @@ template <class T, int D> struct Ctx : CtxBase {
         const size_t rb = sizeof(T) * size_t(mig.rec) * mig.cap, pb = sizeof(int) * size_t(mig.cap);
         CK(cudaEventRecord(dist.ev_a, stream));
         CK(cudaStreamWaitEvent(dist.comm_stream, dist.ev_a, 0));
-        NCK(ncclGroupStart());
+        NCK(dyn::ncclGroupStart());
         for (int side = 0; side < 2; ++side) {
             const int peer = side == 0 ? dist.lo_peer : dist.hi_peer;
             if (peer < 0)
                 continue;
-            NCK(ncclSend(dist.cnt_send + side, sizeof(long long), ncclUint8, peer, dist.comm, dist.comm_stream));
-            NCK(ncclSend(side == 0 ? mig.lo : mig.hi, rb, ncclUint8, peer, dist.comm, dist.comm_stream));
-            NCK(ncclSend(side == 0 ? mig.lo_pid : mig.hi_pid, pb, ncclUint8, peer, dist.comm, dist.comm_stream));
-            NCK(ncclRecv(dist.cnt_recv + side, sizeof(long long), ncclUint8, peer, dist.comm, dist.comm_stream));
-            NCK(ncclRecv(dist.recs_recv[side], rb, ncclUint8, peer, dist.comm, dist.comm_stream));
-            NCK(ncclRecv(dist.pid_recv[side], pb, ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclSend(dist.cnt_send + side, sizeof(long long), ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclSend(side == 0 ? mig.lo : mig.hi, rb, ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclSend(side == 0 ? mig.lo_pid : mig.hi_pid, pb, ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclRecv(dist.cnt_recv + side, sizeof(long long), ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclRecv(dist.recs_recv[side], rb, ncclUint8, peer, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclRecv(dist.pid_recv[side], pb, ncclUint8, peer, dist.comm, dist.comm_stream));
         }
-        NCK(ncclGroupEnd());
+        NCK(dyn::ncclGroupEnd());
         if (dist.nranks > 1) // (a collective of its own, after the point-to-point group)
-            NCK(ncclAllReduce(dist.abort_red, dist.abort_red, 1, ncclInt32, ncclMax, dist.comm, dist.comm_stream));
+            NCK(dyn::ncclAllReduce(dist.abort_red, dist.abort_red, 1, ncclInt32, ncclMax, dist.comm, dist.comm_stream));
         CK(cudaEventRecord(dist.ev_b, dist.comm_stream));
         CK(cudaStreamWaitEvent(stream, dist.ev_b, 0));
     }
@@ -3340,7 +3419,7 @@ int mpm_dist_unique_id(void* id_out)
     if (!id_out)
         return MPM_ERR_USAGE;
     ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess)
+    if (dyn::ncclGetUniqueId(&id) != ncclSuccess)
         return MPM_ERR_CUDA;
     std::memcpy(id_out, &id, sizeof(id));
     return MPM_OK;

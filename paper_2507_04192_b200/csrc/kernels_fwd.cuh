@@ -13,6 +13,8 @@
 //             writes the new state in sorted order and the next step's cell keys
 #pragma once
 
+#include <cstdio>
+
 #include "common.cuh"
 #include "constit.cuh"
 
@@ -866,7 +868,8 @@ template <class T> __device__ __forceinline__ void cp_async_t(T* smem, const T* 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// ABL != 0: timing ablation only (1 skip reduce, 2 skip convert, 4 skip march), launched in
+// ABL != 0: timing ablation only (1 skip reduce, 2 skip convert, 4 skip march, 32 phase clocks:
+// thread 0 of CTAs 0..3 prints cycles per phase, with a barrier after the march), launched in
 // front of the real kernel by ablation builds (-DP2G_ABL=...), never on its own
 template <class T, bool WIDE, int ABL = 0, int NGR = 2>
 __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
@@ -912,12 +915,25 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
     using PL = PLay<3>;
     static_assert(PL::M == RM && PL::VOL == RVOL && PL::SIG == RS + 2 && RS + 6 == NRAW, "raw row map");
     const long long SI = P.S;
+    constexpr bool CLK = (ABL & 32) != 0;
+    long long ck[16] = {}, t0 = 0;
+    auto mark = [&](int ph) {
+        if constexpr (CLK) {
+            const long long t = clock64();
+            ck[ph] += t - t0;
+            t0 = t;
+        }
+    };
+    if constexpr (CLK)
+        t0 = clock64();
 
     for (;;) {
         __syncthreads(); // w_s published; the previous block's shared-memory readers are done
         const int w = w_s;
         if (w >= nocc)
             break;
+        if constexpr (CLK)
+            ck[7] += 1;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
         int qc[3];
@@ -956,6 +972,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
         const int nit = nit_s;
         if (tid == 0) // every thread read w_s before the barrier above
             w_s = wq_next(wq, w);
+        mark(8);
         auto issue_pk = [&](int j) {
             int* dp = pk + (j % 3) * 2 * CAP;
             const int b = s0 + it_start[j];
@@ -989,6 +1006,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
         if (nit > 0)
             issue_fields(0);
         cp_async_commit();
+        mark(0);
 
         T* part = partials + (size_t)Q * NF * C::TN;
         T acc[NO1][3][NA];
@@ -1014,7 +1032,9 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
                     acc[i1][2][f] = T(0);
                 }
             }
+            mark(11);
             __syncthreads(); // slots complete
+            mark(12);
             // one (node column, field) per task: 700 short fixed-order sums over all threads
             for (int t = tid; t < ((ABL & 1) ? 0 : C::NCOL * NF); t += blockDim.x) {
                 const int c = t / NF, f = t - c * NF;
@@ -1035,11 +1055,24 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
         for (int j = 0; j < nit; ++j) {
             cp_async_wait_all();
             __syncthreads(); // fields(j) and pk(j+1) have landed for every thread
-            if (j + 1 < nit)
-                issue_fields(j + 1);
+            mark(1);
             if (j + 2 < nit)
                 issue_pk(j + 2);
-            cp_async_commit();
+            // fields(j+1) are issued one row per march iteration below, so the LDGSTS traffic
+            // overlaps the FP64 march instead of stalling every warp at once (MEASURED C4 f64: the
+            // up-front issue took 17% of the kernel's cycles); the commit follows the march
+            const int nrow1 = j + 1 < nit ? it_len[j + 1] : 0;
+            int prow = tid;
+            const int* pp1 = pk + ((j + 1) % 3) * 2 * CAP;
+            T* rb1 = raw + ((j + 1) & 1) * NRAW * CAP;
+            auto issue_row = [&]() {
+                const T* q = P.base + pp1[prow];
+#pragma unroll
+                for (int f = 0; f < NRAW; ++f)
+                    cp_async_t<T>(rb1 + f * CAP + prow, q + (f < RS ? f : f + 2) * SI);
+                prow += blockDim.x;
+            };
+            mark(9);
             // item j: convert each staged particle once (x -> fractional offset, v -> m v,
             // sigma -> V sigma) and count its column (records are column-sorted inside a level)
             const int len = it_len[j];
@@ -1067,7 +1100,9 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
                         Rw[(RS + q) * CAP + r] *= V;
                 }
             }
+            mark(10);
             __syncthreads(); // converted records and the counts are complete
+            mark(2);
             // every warp scans the 64 column counts itself (no extra barrier): lane l holds the
             // exclusive prefix of columns 2l and 2l+1
             int kb, ke;
@@ -1116,16 +1151,38 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
                     else if constexpr (NG > 2)
                         p2g_visit<S::fb(2), S::fb(3)>(acc, wx, dwx, wy, dwy, wz, dwz, R, k, CAP);
                 }
+                if (prow < nrow1)
+                    issue_row();
+            }
+            while (prow < nrow1)
+                issue_row();
+            cp_async_commit();
+            if constexpr (CLK) {
+                mark(3);
+                __syncthreads();
+                mark(4);
+                ck[6] += 1;
             }
             if (it_last[j]) // slots were last read before the previous emit's closing barrier
                 emit_and_reduce(it_lvl[j]);
+            mark(5);
         }
         cp_async_wait_all();
         __syncthreads();
         emit_and_reduce(B);
         __syncthreads(); // slots reused by the next emit right away
         emit_and_reduce(B + 1);
+        mark(0);
     }
+    if constexpr (CLK)
+        if (threadIdx.x == 0 && blockIdx.x < 4)
+            printf("p2g-clk cta %d blocks %lld items %lld setup+tail %lld wait %lld convert %lld march0 %lld "
+                   "march-imbalance %lld emit %lld\n",
+                   blockIdx.x, ck[7], ck[6], ck[0], ck[1], ck[2], ck[3], ck[4], ck[5]);
+    if constexpr (CLK)
+        if (threadIdx.x == 0 && blockIdx.x < 4)
+            printf("p2g-clk2 cta %d blocksetup %lld issue %lld convloop %lld slotwrite %lld slotbar %lld\n", blockIdx.x,
+                   ck[8], ck[9], ck[10], ck[11], ck[12]);
     wq_finish(wq);
 }
 

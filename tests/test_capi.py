@@ -42,3 +42,17 @@ def test_no_cpu_fallback_without_gpu():
     from paper_2507_04192_b200.solver import Context
     with pytest.raises(DeviceError):
         Context(small_fluid_scene(), 100)
+
+
+def test_library_loads_before_torch():
+    """NCCL is resolved at run time (dyn::api in context.cu): loading the library first must not pin
+    an older system libnccl.so.2 that torch's own libtorch_cuda.so then fails to link against"""
+    import subprocess
+    import sys
+    if not capi.LIB_PATH.exists():
+        pytest.fail("libmpm_b200.so is not built: run __graft_entry__.build()")
+    needed = subprocess.run(["readelf", "-d", str(capi.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "libnccl" not in needed
+    code = f"import ctypes; ctypes.CDLL({str(capi.LIB_PATH)!r}); import torch; print(torch.__version__)"
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
