@@ -394,7 +394,9 @@ template <class T, int D> struct Ctx : CtxBase {
     mpm_scene_desc desc{};
     cudaStream_t stream{};
     cudaStream_t own_stream{}; // stream may be a caller's (mpm_ctx_set_stream)
-    int p2g_impl = 1, p2g_lanes_per_sm = 1; // 3-D P2G: 1 pipe3 (default), 0 lanes3 (experimental)
+    // 3-D P2G: 2 warp-specialized (default), 1 pipe3, 0 lanes3 (experimental). MEASURED C4 (same
+    // box, bench): f64 ws 0.410-0.414 ms vs pipe3 0.472 ms
+    int p2g_impl = 2, p2g_lanes_per_sm = 1;
     int device = 0;
     int64_t cap = 0, n = 0;
     int64_t step = 0;
@@ -881,8 +883,12 @@ template <class T, int D> struct Ctx : CtxBase {
                                                              Lane3Cfg<T>::SMEM));
             if (p2g_lanes_per_sm < 1)
                 p2g_lanes_per_sm = 1;
+            CK(cudaFuncSetAttribute(k_p2g_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(WsCfg<T>::SMEM)));
+#if P2G_ABL == 64
+            CK(cudaFuncSetAttribute(k_p2g_ws<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(WsCfg<T>::SMEM)));
+#endif
             if (const char* e = std::getenv("MPM_P2G_IMPL")) // A/B measurement only
-                p2g_impl = std::string(e) == "lanes3" ? 0 : 1;
+                p2g_impl = std::string(e) == "lanes3" ? 0 : std::string(e) == "pipe3" ? 1 : 2;
         } else {
             CK(cudaFuncSetAttribute(k_p2g<T, D, false, D == 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(p2g2_smem<T>())));
@@ -1041,7 +1047,21 @@ template <class T, int D> struct Ctx : CtxBase {
             });
         } else {
             if constexpr (D == 3) {
-                if (p2g_impl == 1) {
+                if (p2g_impl == 2) {
+                    using S = WsCfg<T>;
+#if P2G_ABL == 64
+                    launch("k_p2g_abl", [&] {
+                        pdl(k_p2g_ws<T, true>, unsigned(nsm), S::THREADS, S::SMEM)(sc, buf[cur], perm, keys_sorted, bstart,
+                                                                                   bend, lstart, occ, counts, partials,
+                                                                                   st, wq_ptr(WQ_P2G));
+                    });
+#endif
+                    launch("k_p2g", [&] {
+                        pdl(k_p2g_ws<T>, unsigned(nsm), S::THREADS, S::SMEM)(sc, buf[cur], perm, keys_sorted, bstart,
+                                                                             bend, lstart, occ, counts, partials, st,
+                                                                             wq_ptr(WQ_P2G));
+                    });
+                } else if (p2g_impl == 1) {
                     using S = Pipe3Cfg<T, P2G_WIDE>;
 #if P2G_ABL == 16
                     launch("k_p2g_abl", [&] { pdl(k_spin_abl, nsm, 32, 0)(600000); });

@@ -782,6 +782,19 @@ template <class T> __device__ __forceinline__ void quad_w(T fx, int o, T inv_dh,
 #endif
 // SPLIT (f64 only; bit-identical sums): 12 warps of <= 45 accumulators instead of 6 warps of 63.
 // MEASURED C4: f64 k_p2g 0.517-0.523 -> 0.508 ms; f32 0.262 -> 0.318 ms (so f32 stays narrow).
+// 3-D slot buffer layout: value (node column c < 100, source lane q < 9, field f < 7) at
+// c + 107 q + 999 f. Strides from an exhaustive search over a bank model of the emit's writes
+// (lanes = (base column, x offset)) and the sums' reads (lanes = consecutive (c, f) tasks):
+// ~1.3x / ~1.0x the ideal wavefronts instead of 1.5x / 1.6x for the dense [c][q][f] layout
+// (ncu at C4 f64: the dense layout's slot traffic was 32% of the kernel's shared wavefronts,
+// half of it bank conflicts).
+#ifndef SLOT3_DENSE
+#define SLOT3_DENSE 0
+#endif
+__host__ __device__ constexpr int slot3(int c, int q, int f) { return SLOT3_DENSE ? (c * 9 + q) * 7 + f : c + 107 * q + 999 * f; }
+constexpr int SLOT3_SIZE = 99 + 107 * 8 + 999 * 6 + 1;
+static_assert(Cfg<3>::NCOL == 100 && Cfg<3>::NF == 7, "slot3 strides assume B = 8");
+
 template <class T, bool WIDE = true, int NGR = 2> struct Pipe3Cfg {
     // NG thread groups of 192 lanes split the 7 node fields (m, p[3], f[3]); f64 only
     static constexpr int NG = (!WIDE && P2G_SPLIT && sizeof(T) == 8) ? NGR : 1;
@@ -791,7 +804,7 @@ template <class T, bool WIDE = true, int NGR = 2> struct Pipe3Cfg {
     static constexpr int CAP = 640;
     static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
     static constexpr size_t SMEM_PK = sizeof(int) * 3 * 2 * CAP;
-    static constexpr size_t SMEM_SLOT = sizeof(T) * Cfg<3>::NCOL * NSRC * Cfg<3>::NF;
+    static constexpr size_t SMEM_SLOT = sizeof(T) * SLOT3_SIZE;
     static constexpr size_t SMEM = SMEM_RAW + SMEM_PK + SMEM_SLOT;
     // field range [fb(g), fb(g + 1)) of group g in the order m, p0..2, f0..2.
     // NG 2: {m, p, f_x} {f_y, f_z}; NG 3: {m, p} {f_x, f_y} {f_z} (FP64 work per lane-particle
@@ -916,6 +929,12 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
     static_assert(PL::M == RM && PL::VOL == RVOL && PL::SIG == RS + 2 && RS + 6 == NRAW, "raw row map");
     const long long SI = P.S;
     constexpr bool CLK = (ABL & 32) != 0;
+    // staged record r lives at column rsw(r) of its field row: an XOR swizzle inside each group of
+    // 16 (a bank-width of doubles), so the march's lanes -- different node columns, whose records
+    // sit a column count apart (8 at a uniform 8 per column: C4's lattice) -- hit different banks
+    // instead of 4-6-way conflicting. A permutation of [0, CAP) since CAP % 16 == 0.
+    static_assert(CAP % 16 == 0, "swizzle groups");
+    auto rsw = [](int r) { return r ^ ((r >> 4) & 15); };
     long long ck[16] = {}, t0 = 0;
     auto mark = [&](int ph) {
         if constexpr (CLK) {
@@ -989,7 +1008,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
                 const T* q = P.base + pp[r];
 #pragma unroll
                 for (int f = 0; f < NRAW; ++f)
-                    cp_async_t<T>(rb + f * CAP + r, q + (f < RS ? f : f + 2) * SI);
+                    cp_async_t<T>(rb + f * CAP + rsw(r), q + (f < RS ? f : f + 2) * SI);
             }
         };
         if (tid < NBC) {
@@ -1026,7 +1045,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
 #pragma unroll
                 for (int f = 0; f < NA; ++f) {
                     if (f < gfn)
-                        slots[(ncol * NSRC + o0 * 3 + o1) * NF + gfb + f] = acc[i1][0][f];
+                        slots[slot3(ncol, o0 * 3 + o1, gfb + f)] = acc[i1][0][f];
                     acc[i1][0][f] = acc[i1][1][f];
                     acc[i1][1][f] = acc[i1][2][f];
                     acc[i1][2][f] = T(0);
@@ -1044,7 +1063,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
                 for (int q = 0; q < NSRC; ++q) {
                     const int b0 = n0 - q / 3, b1 = n1 - q % 3;
                     if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
-                        sum += slots[(c * NSRC + q) * NF + f];
+                        sum += slots[slot3(c, q, f)];
                 }
                 part[f * C::TN + ptile<3>(z, c)] = sum;
             }
@@ -1069,7 +1088,7 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
                 const T* q = P.base + pp1[prow];
 #pragma unroll
                 for (int f = 0; f < NRAW; ++f)
-                    cp_async_t<T>(rb1 + f * CAP + prow, q + (f < RS ? f : f + 2) * SI);
+                    cp_async_t<T>(rb1 + f * CAP + rsw(prow), q + (f < RS ? f : f + 2) * SI);
                 prow += blockDim.x;
             };
             mark(9);
@@ -1082,10 +1101,11 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
                 ccount[(j + 1) & 1][tid] = 0;
             {
                 T* Rw = raw + (j & 1) * NRAW * CAP;
-                for (int r = tid; r < len; r += blockDim.x) {
-                    atomicAdd(&cnt[col[r] & (NBC - 1)], 1);
+                for (int r0 = tid; r0 < len; r0 += blockDim.x) {
+                    atomicAdd(&cnt[col[r0] & (NBC - 1)], 1);
                     if (ABL & 2)
                         continue;
+                    const int r = rsw(r0);
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         const T u = (Rw[(RX + a) * CAP + r] - sc.origin[a]) * sc.inv_dh;
@@ -1125,7 +1145,8 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
                 ke = kb + ((bc & 1) ? a1 : a0);
             }
             const T* R = raw + (j & 1) * NRAW * CAP;
-            for (int k = kb; k < ((ABL & 4) ? kb : ke); ++k) {
+            for (int k0 = kb; k0 < ((ABL & 4) ? kb : ke); ++k0) {
+                const int k = rsw(k0);
                 T f[3];
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
@@ -1184,6 +1205,490 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
             printf("p2g-clk2 cta %d blocksetup %lld issue %lld convloop %lld slotwrite %lld slotbar %lld\n", blockIdx.x,
                    ck[8], ck[9], ck[10], ck[11], ck[12]);
     wq_finish(wq);
+}
+
+// ---- 3-D P2G, warp-specialized (PIC / FLIP / blend) ---------------------------------------
+// The same per-particle arithmetic, node fields, partial tiles and fixed combine order as
+// k_p2g_pipe3 (bit-identical output), with the work split by role instead of by phase:
+//   producer warpgroup (4 warps, 56 registers): pulls occupied blocks from the work counter,
+//     builds their (level, chunk) item lists, gathers each item's particle fields through the
+//     sort permutation with cp.async into one of two record buffers, and -- while those copies
+//     land -- does the fixed-order 9-source sums of the node planes the consumers finished (slot
+//     buffer -> the block's partial tile); then converts the records (fractional offset, m v,
+//     V sigma), counts the node columns and publishes the item on an mbarrier;
+//   consumer warps (the pipe3 lane mapping, 152 registers): wait for an item, march it (FP64),
+//     release the buffer; after a finished node plane, write their accumulators to one of two
+//     slot buffers and release it to the producers.
+// No CTA-wide barrier after the setup: the roles meet only on mbarriers (full/empty pairs for the
+// record buffers and for the slot buffers).
+// Registers (f64): 512 threads start at 128; setmaxnreg moves the producers' release (128 x 72)
+// to the consumers (384 x 24). The register file is split over the 4 SM sub-partitions (16384
+// each, warps assigned round-robin), so each holds 3 consumer warps and 1 producer warp:
+// 3 x 152 + 56 = 512 registers per lane slot. (A 17th warp would put 5 warps on one sub-partition
+// and cap every thread at 96: MEASURED, a separate reducer warp needs a 5th warp there.)
+// MEASURED (C4 f64): pipe3 0.47 ms with the FP64 pipe 37% busy, the march ~60% of its cycles.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b)
+{
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b)) : "memory");
+}
+// a protocol bug must not hang the GPU: after ~2^22 polls (legitimate waits are microseconds) the
+// kernel reports the barrier and traps, which surfaces as a launch failure
+#ifndef MBAR_ASM_LOOP
+#define MBAR_ASM_LOOP 0
+#endif
+#ifndef WS_SLEEP_NS
+#define WS_SLEEP_NS 128
+#endif
+// SLEEP: back off between polls (a waiting producer warp shares its sub-partition's issue slots
+// with three consumer warps)
+template <bool SLEEP = false> __device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity)
+{
+    if (MBAR_ASM_LOOP) {
+        asm volatile("{\n .reg .pred P1;\n"
+                     "WAIT_%=:\n"
+                     " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                     " @!P1 bra WAIT_%=;\n"
+                     "}\n" ::"r"(smem_u32(b)),
+                     "r"(parity)
+                     : "memory");
+        return;
+    }
+    const unsigned a = smem_u32(b);
+    unsigned ok = 0, spins = 0;
+    for (;;) {
+        asm volatile("{\n .reg .pred P1;\n"
+                     " mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, P1;\n"
+                     "}\n"
+                     : "=r"(ok)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+        if (ok)
+            return;
+        if (SLEEP && WS_SLEEP_NS > 0)
+            __nanosleep(WS_SLEEP_NS);
+        if (++spins == (1u << 22)) {
+            printf("mbarrier wait timed out: block %d thread %d barrier smem+%u parity %d\n", blockIdx.x, threadIdx.x,
+                   a, parity);
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ void named_bar(int id, int count)
+{
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+#ifndef WS_REALLOC
+#define WS_REALLOC 1
+#endif
+#ifndef WS_PRED
+#define WS_PRED 0
+#endif
+#ifndef WS_PROD_REGS
+#define WS_PROD_REGS 56
+#endif
+#ifndef WS_LB
+#define WS_LB 0
+#endif
+#ifndef WS_PREFETCH_LATE
+#define WS_PREFETCH_LATE 0
+#endif
+template <class T> struct WsCfg {
+    using P3 = Pipe3Cfg<T, false>;
+    static constexpr int NG = P3::NG, NA = P3::NA;
+    static constexpr int CONS = 192 * NG;  // consumer threads (f64: 12 warps, f32: 6)
+    static constexpr int PROD = 128; // one warpgroup
+    static constexpr int THREADS = CONS + PROD;
+    static constexpr bool REALLOC = WS_REALLOC && CONS % 128 == 0;
+    static constexpr int WPS = (THREADS / 32 + 3) / 4; // warps per SM sub-partition
+    static constexpr int BASE_REGS = (512 / WPS) / 8 * 8, PROD_REGS = WS_PROD_REGS, CONS_REGS = 152;
+    static_assert(!REALLOC || CONS * (CONS_REGS - BASE_REGS) <= PROD * (BASE_REGS - PROD_REGS), "register pool");
+    static_assert(!REALLOC || (WPS == 4 && 3 * CONS_REGS + PROD_REGS <= 512), "sub-partition register file");
+    // PRED: the producers sum the finished node planes (two slot buffers, so CAP 512: f64
+    // 2 x 14 x 512 x 8 + 2 x 55600 B = 226 KB); otherwise the consumers do, between two named
+    // barriers of their own, from one slot buffer. MEASURED C4 f64: consumers 0.388 ms, producers
+    // 0.402 ms (their sums' shared-memory traffic slows the overlapping march by ~25%).
+    static constexpr bool PRED = WS_PRED;
+    static constexpr int NBC = 64, NSRC = 9, NRAW = 14, MAXIT = 64, CAP = PRED ? 512 : 640, NSLOT = PRED ? 2 : 1;
+    static constexpr int SLOT = SLOT3_SIZE; // values per slot buffer
+    static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
+    static constexpr size_t SMEM = SMEM_RAW + sizeof(T) * NSLOT * SLOT;
+};
+
+// CLK: timing build only (tools/p2g_clocks.py): thread 0 of each role in CTAs 0..3 prints cycles per phase
+template <class T, bool CLK = false>
+__global__ void
+#if WS_LB
+__launch_bounds__(WsCfg<T>::THREADS, 1)
+#else
+__maxnreg__(WsCfg<T>::BASE_REGS)
+#endif
+    k_p2g_ws(DevScene<T, 3> sc, PBuf<T, 3> P, const int* __restrict__ perm, const int* __restrict__ keys,
+             const int* __restrict__ bstart, const int* __restrict__ bend, const int* __restrict__ lstart,
+             const int* __restrict__ occ, const int* __restrict__ n_occ, T* __restrict__ partials, DevStatus* st,
+             int* __restrict__ wq)
+{
+    pdl_wait();
+    pdl_trigger();
+    using C = Cfg<3>;
+    using S = WsCfg<T>;
+    constexpr int B = C::B, TE = C::TE, NF = C::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW;
+    constexpr int NO1 = 3, NG = S::NG, NA = S::NA, CONS = S::CONS;
+    constexpr int RX = 0, RV = 3, RM = 6, RVOL = 7, RS = 8;
+    extern __shared__ unsigned char smem_raw[];
+    T* raw = reinterpret_cast<T*>(smem_raw);                      // [2][NRAW][CAP]
+    T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_RAW);      // [2][NCOL][NSRC][NF]
+    __shared__ int cnt_s[2][NBC];                                 // per-item column counts
+    __shared__ int4 desc_s[2];                                    // (Q, level, flags, -): 1 level done, 2 block done, 4 end
+    __shared__ int2 em_s[2];                                      // slot buffer: (Q, node plane)
+    __shared__ __align__(8) unsigned long long bar_full[2], bar_empty[2], sl_full[2], sl_empty[2];
+    __shared__ int it_start[S::MAXIT], it_len[S::MAXIT], it_lvl[S::MAXIT], it_last[S::MAXIT]; // producers only
+    __shared__ int blk_s[4];                                      // producers only: w, Q, s0, nit
+    const int tid = threadIdx.x;
+    const int nocc = st->abort ? 0 : *n_occ;
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar_full[i], S::PROD);
+            mbar_init(&bar_empty[i], CONS / 32);
+            mbar_init(&sl_full[i], CONS / 32);
+            mbar_init(&sl_empty[i], S::PROD);
+        }
+    }
+    __syncthreads();
+    // staged record r at column rsw(r) of its field row (bank swizzle, as in k_p2g_pipe3)
+    auto rsw = [](int r) { return r ^ ((r >> 4) & 15); };
+    using PL = PLay<3>;
+    static_assert(PL::M == RM && PL::VOL == RVOL && PL::SIG == RS + 2 && RS + 6 == NRAW, "raw row map");
+    long long ck[6] = {}, t0 = 0;
+    auto mark = [&](int ph) {
+        if constexpr (CLK) {
+            const long long t = clock64();
+            ck[ph] += t - t0;
+            t0 = t;
+        }
+    };
+    if constexpr (CLK)
+        t0 = clock64();
+
+    if (tid >= CONS) { // ================= producer warpgroup =================
+        if constexpr (S::REALLOC) // registers to the consumers
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(S::PROD_REGS));
+        const int pt = tid - CONS;
+        const long long SI = P.S;
+        // the plane sums of slot buffer (e & 1): one (node column, field) per task, fixed order
+        // over the 9 source lanes; emits are reduced in the consumers' order
+        int nred = 0;
+        auto reduce_one = [&]() {
+            const int sb = nred & 1;
+            mbar_wait(&sl_full[sb], (nred >> 1) & 1);
+            const int2 em = em_s[sb];
+            const T* sl = slots + sb * S::SLOT;
+            T* part = partials + (size_t)em.x * NF * C::TN;
+            constexpr int NT = C::NCOL * NF, UR = 2;
+            for (int t0 = pt; t0 < NT; t0 += UR * S::PROD) {
+                T sum[UR];
+#pragma unroll
+                for (int x = 0; x < UR; ++x) {
+                    const int t = t0 + x * S::PROD;
+                    const int c = t / NF, f = t - c * NF;
+                    const int n0 = c / TE, n1 = c - n0 * TE;
+                    sum[x] = T(0);
+#pragma unroll
+                    for (int q = 0; q < NSRC; ++q) {
+                        const int b0 = n0 - q / 3, b1 = n1 - q % 3;
+                        if (t < NT && b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
+                            sum[x] += sl[slot3(c, q, f)];
+                    }
+                }
+#pragma unroll
+                for (int x = 0; x < UR; ++x) {
+                    const int t = t0 + x * S::PROD;
+                    if (t < NT) {
+                        const int c = t / NF, f = t - c * NF;
+                        part[f * C::TN + ptile<3>(em.y, c)] = sum[x];
+                    }
+                }
+            }
+            mbar_arrive(&sl_empty[sb]);
+            ++nred;
+        };
+        int em_prev2 = 0, em_prev1 = 0; // node planes the consumers emit after items j-2, j-1
+        int w = 0;
+        if (pt == 0)
+            w = wq_first(wq);
+        int j = 0; // items published so far (both buffers)
+        for (;;) {
+            if (pt == 0) {
+                blk_s[0] = w;
+                if (w < nocc) { // level starts (suffix minimum) -> work items, as k_p2g_pipe3
+                    const int Q = occ[w];
+                    const int s0 = bstart[Q], s1 = bend[Q];
+                    int lv[B + 1];
+                    int nxt = s1;
+                    lv[B] = s1 - s0;
+                    for (int z = B - 1; z >= 0; --z) {
+                        const int v = lstart[Q * (B + 1) + z];
+                        nxt = (v >= s0 && v < s1) ? v : nxt;
+                        lv[z] = nxt - s0;
+                    }
+                    int k = 0;
+                    for (int z = 0; z < B; ++z) {
+                        const int nl = lv[z + 1] - lv[z];
+                        const int nch = nl > 0 ? (nl + CAP - 1) / CAP : 1;
+                        for (int c = 0; c < nch; ++c) {
+                            if (k < S::MAXIT) {
+                                it_start[k] = lv[z] + c * CAP;
+                                it_len[k] = min(CAP, nl - c * CAP);
+                                it_lvl[k] = z;
+                                it_last[k] = c == nch - 1;
+                            }
+                            ++k;
+                        }
+                    }
+                    if (k > S::MAXIT) { // pathological compression: refuse loudly
+                        st->far_flag = 1;
+                        st->abort = 1;
+                        k = S::MAXIT;
+                    }
+                    blk_s[1] = Q;
+                    blk_s[2] = s0;
+                    blk_s[3] = k;
+                    w = wq_next(wq, w);
+                }
+            }
+            named_bar(2, S::PROD);
+            mark(0);
+            const bool done = blk_s[0] >= nocc;
+            const int Q = blk_s[1], s0 = blk_s[2], nit = done ? 1 : blk_s[3];
+            for (int i = 0; i < nit; ++i, ++j) {
+                const int b = j & 1, u = j >> 1;
+                // this item's permutation and keys are loaded before the buffer is free
+                constexpr int RPT = (CAP + S::PROD - 1) / S::PROD; // rows per producer thread
+                const int len = done ? 0 : it_len[i], base = s0 + (done ? 0 : it_start[i]);
+                int pr[RPT], kr[RPT];
+                if (WS_PREFETCH_LATE && u > 0)
+                    mbar_wait<true>(&bar_empty[b], (u - 1) & 1);
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) {
+                    const int r = pt + e * S::PROD;
+                    pr[e] = r < len ? perm[base + r] : 0;
+                    kr[e] = r < len ? keys[base + r] : 0;
+                }
+                if (!WS_PREFETCH_LATE && u > 0) // the consumers are done with this buffer's previous item (j - 2)
+                    mbar_wait<true>(&bar_empty[b], (u - 1) & 1);
+                mark(1);
+                if (done) { // end marker; then the planes of the last two items
+                    if (pt == 0)
+                        desc_s[b] = make_int4(-1, 0, 4, 0);
+                    mbar_arrive(&bar_full[b]);
+                    if constexpr (S::PRED)
+                        for (int e = 0; e < em_prev2 + em_prev1; ++e)
+                            reduce_one();
+                    break;
+                }
+                if (pt < NBC)
+                    cnt_s[b][pt] = 0;
+                named_bar(2, S::PROD); // counts zeroed before any producer adds to them
+                T* rb = raw + b * NRAW * CAP;
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) {
+                    const int r = pt + e * S::PROD;
+                    if (r < len) {
+                        const T* q = P.base + pr[e];
+                        const int rs = rsw(r);
+#pragma unroll
+                        for (int f = 0; f < NRAW; ++f)
+                            cp_async_t<T>(rb + f * CAP + rs, q + (f < RS ? f : f + 2) * SI);
+                        atomicAdd(&cnt_s[b][kr[e] & (NBC - 1)], 1);
+                    }
+                }
+                cp_async_commit();
+                mark(2);
+                if constexpr (S::PRED)
+                    for (int e = 0; e < em_prev2; ++e) // while the copies land: item j-2's node planes
+                        reduce_one();
+                cp_async_wait_all(); // this thread's rows have landed; it converts only those
+                mark(3);
+                for (int r0 = pt; r0 < len; r0 += S::PROD) {
+                    const int r = rsw(r0);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const T uu = (rb[(RX + a) * CAP + r] - sc.origin[a]) * sc.inv_dh;
+                        rb[(RX + a) * CAP + r] = uu - dfloor<T>(uu - T(0.5));
+                    }
+                    const T m = rb[RM * CAP + r], V = rb[RVOL * CAP + r];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                        rb[(RV + a) * CAP + r] *= m;
+#pragma unroll
+                    for (int q = 0; q < 6; ++q)
+                        rb[(RS + q) * CAP + r] *= V;
+                }
+                if (pt == 0)
+                    desc_s[b] = make_int4(Q, it_lvl[i], (it_last[i] ? 1 : 0) | (i == nit - 1 ? 2 : 0), 0);
+                mbar_arrive(&bar_full[b]); // release: records, counts and descriptor
+                em_prev2 = em_prev1;
+                em_prev1 = (it_last[i] ? 1 : 0) + (i == nit - 1 ? 2 : 0);
+                mark(4);
+            }
+            if (done)
+                break;
+            named_bar(2, S::PROD); // every producer has read it_* / blk_s before they are rewritten
+        }
+        if constexpr (CLK)
+            if (pt == 0 && blockIdx.x < 4)
+                printf("ws-prod cta %d blocklist %lld wait_empty %lld issue %lld landed %lld convert %lld\n", blockIdx.x,
+                       ck[0], ck[1], ck[2], ck[3], ck[4]);
+        if (wq && pt == 0) { // the work counter pair resets after the last CTA (wq_finish)
+            __threadfence();
+            if (atomicAdd(wq + 1, 1) == int(gridDim.x) - 1) {
+                atomicExch(wq, 0);
+                atomicExch(wq + 1, 0);
+            }
+        }
+        return;
+    }
+
+    // ================= consumers (k_p2g_pipe3's narrow lane mapping) =================
+    if constexpr (S::REALLOC)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(S::CONS_REGS));
+    const int grp = NG > 1 ? tid / 192 : 0; // warp-uniform
+    const int lt = tid - 192 * grp;
+    const int gfb = S::P3::fb(grp), gfn = S::P3::fb(grp + 1) - gfb;
+    const int bc = lt / 3, o0 = lt % 3;
+    const bool mid = o0 == 1;
+    const T xoff = o0 == 0 ? T(1.5) : (o0 == 1 ? T(1) : T(0.5)); // h = fx - xoff (bspline.hpp:94-99)
+    const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
+    const int lane = tid & 31;
+    T acc[NO1][3][NA];
+#pragma unroll
+    for (int a = 0; a < NO1; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int f = 0; f < NA; ++f)
+                acc[a][k][f] = T(0);
+    int ne = 0; // slot buffers filled so far
+    // node plane z of block Q is final in acc[.][0]: write it to a slot buffer and roll the window;
+    // the 9-source sums follow (PRED: by the producers, here: by the consumers)
+    auto emit = [&](int z, int Q) {
+        const int sb = S::NSLOT == 2 ? ne & 1 : 0, u = ne >> 1;
+        if constexpr (S::PRED) {
+            if (u > 0) // the producers have summed this buffer's previous plane
+                mbar_wait(&sl_empty[sb], (u - 1) & 1);
+        } else {
+            named_bar(1, CONS); // the previous sums are done reading the slots
+        }
+        T* sl = slots + sb * S::SLOT;
+#pragma unroll
+        for (int o1 = 0; o1 < NO1; ++o1) {
+            const int ncol = (bc0 + o0) * TE + bc1 + o1;
+#pragma unroll
+            for (int f = 0; f < NA; ++f) {
+                if (f < gfn)
+                    sl[slot3(ncol, o0 * 3 + o1, gfb + f)] = acc[o1][0][f];
+                acc[o1][0][f] = acc[o1][1][f];
+                acc[o1][1][f] = acc[o1][2][f];
+                acc[o1][2][f] = T(0);
+            }
+        }
+        if constexpr (S::PRED) {
+            if (tid == 0)
+                em_s[sb] = make_int2(Q, z);
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive(&sl_full[sb]);
+        } else {
+            named_bar(1, CONS); // slots complete
+            T* part = partials + (size_t)Q * NF * C::TN;
+            for (int t = tid; t < C::NCOL * NF; t += CONS) {
+                const int c = t / NF, f = t - c * NF;
+                const int n0 = c / TE, n1 = c - n0 * TE;
+                T sum = T(0);
+#pragma unroll
+                for (int q = 0; q < NSRC; ++q) {
+                    const int b0 = n0 - q / 3, b1 = n1 - q % 3;
+                    if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
+                        sum += sl[slot3(c, q, f)];
+                }
+                part[f * C::TN + ptile<3>(z, c)] = sum;
+            }
+        }
+        ++ne;
+    };
+    for (int j = 0;; ++j) {
+        const int b = j & 1;
+        mark(5);
+        mbar_wait(&bar_full[b], (j >> 1) & 1);
+        mark(0);
+        const int4 d = desc_s[b];
+        if (d.z & 4)
+            break;
+        int kb, ke; // this column's records (lane l of each warp scans columns 2l, 2l+1)
+        {
+            const int* cnt = cnt_s[b];
+            const int c0 = cnt[2 * lane], c1 = cnt[2 * lane + 1];
+            int v = c0 + c1;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, v, dd);
+                if (lane >= dd)
+                    v += t;
+            }
+            const int excl = v - c0 - c1;
+            const int src = bc >> 1;
+            const int e = __shfl_sync(0xffffffffu, excl, src);
+            const int a0 = __shfl_sync(0xffffffffu, c0, src);
+            const int a1 = __shfl_sync(0xffffffffu, c1, src);
+            kb = (bc & 1) ? e + a0 : e;
+            ke = kb + ((bc & 1) ? a1 : a0);
+        }
+        const T* R = raw + b * NRAW * CAP;
+        for (int k0 = kb; k0 < ke; ++k0) {
+            const int k = rsw(k0);
+            T f[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                f[a] = R[(RX + a) * CAP + k];
+            T wx, dwx, wy[NO1], dwy[NO1], wz[3], dwz[3];
+            {
+                const T h = f[0] - xoff;
+                const T hh = h * h;
+                wx = mid ? T(0.75) - hh : T(0.5) * hh;
+                dwx = (mid ? -T(2) * h : h) * sc.inv_dh;
+            }
+#pragma unroll
+            for (int i1 = 0; i1 < NO1; ++i1)
+                quad_w<T>(f[1], i1, sc.inv_dh, wy[i1], dwy[i1]);
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                quad_w<T>(f[2], q, sc.inv_dh, wz[q], dwz[q]);
+            if (grp == 0)
+                p2g_visit<S::P3::fb(0), S::P3::fb(1)>(acc, wx, dwx, wy, dwy, wz, dwz, R, k, CAP);
+            else if constexpr (NG > 1)
+                p2g_visit<S::P3::fb(1), S::P3::fb(2)>(acc, wx, dwx, wy, dwy, wz, dwz, R, k, CAP);
+        }
+        __syncwarp();
+        if (lane == 0)
+            mbar_arrive(&bar_empty[b]); // this warp is done with the buffer
+        mark(1);
+        if (d.z & 1)
+            emit(d.y, d.x);
+        if (d.z & 2) {
+            emit(B, d.x);
+            emit(B + 1, d.x);
+        }
+        mark(2);
+    }
+    if constexpr (CLK)
+        if (tid == 0 && blockIdx.x < 4)
+            printf("ws-cons cta %d wait_full %lld march %lld emit %lld\n", blockIdx.x, ck[0], ck[1], ck[2]);
 }
 
 // 3-D P2G, lane-per-stencil-offset (PIC / FLIP / blend). A warp owns 4 particle columns of

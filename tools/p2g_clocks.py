@@ -28,6 +28,9 @@ out = subprocess.run([sys.executable, __file__, sys.argv[1], os.environ.get("DT"
 lines = [l for l in out.splitlines() if l.startswith("p2g-clk ")][-4:]
 for l in [l for l in out.splitlines() if l.startswith("p2g-clk2")][-4:]:
     print(l)
+for pre in ("ws-prod", "ws-cons", "ws-red"):  # -DP2G_ABL=64 builds with MPM_P2G_IMPL=ws
+    for l in [l for l in out.splitlines() if l.startswith(pre)][-4:]:
+        print(l)
 names = ["setup+tail", "wait", "convert", "march0", "march-imbalance", "emit"]
 for l in lines:
     nums = dict(re.findall(r"([a-z+-]+\d?) (\d+)", l))
