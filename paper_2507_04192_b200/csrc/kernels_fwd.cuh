@@ -1226,7 +1226,13 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
 // each, warps assigned round-robin), so each holds 3 consumer warps and 1 producer warp:
 // 3 x 152 + 56 = 512 registers per lane slot. (A 17th warp would put 5 warps on one sub-partition
 // and cap every thread at 96: MEASURED, a separate reducer warp needs a 5th warp there.)
-// MEASURED (C4 f64): pipe3 0.47 ms with the FP64 pipe 37% busy, the march ~60% of its cycles.
+// MEASURED (C4 f64): pipe3 0.47 ms with the FP64 pipe 37% busy, the march ~60% of its cycles;
+// this kernel 0.41 ms, FP64 45%, shared wavefronts 34% of peak. Tried and slower (same-box A/B,
+// phase clocks in tools/p2g_clocks.py): the sums on the producers (PRED, 0.402 vs 0.388 ms), on
+// a separate reducer warp (0.415), on the lighter consumer group only (0.45); releasing the record
+// buffer after the sums (0.417 vs 0.406: the producers' gather burst then slows the march as much
+// as it sped up the sums -- the LSU/MIO traffic of the gathers is paid by whichever phase it
+// overlaps); unconditional slot loads in the sums (0.414).
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, int count)
 {
