@@ -1224,6 +1224,283 @@ __global__ void __launch_bounds__(AdjScatterCfg<T>::THREADS, 1)
     wq_finish(wq);
 }
 
+// ---- K5b, warp-specialized (3-D PIC / FLIP / blend): k_adj_scatter_pipe3's arithmetic, tiles
+// and fixed sum order (bit-identical), with k_p2g_ws's split by role: 2 producer warps pull the
+// blocks, gather fx through the permutation and copy the (sorted-order) scatter records a, inc, L
+// with cp.async into one of two record buffers, convert fx, count the columns and publish the item
+// on an mbarrier; the 6 consumer warps (up to 255 registers: 8 warps, 2 per SM sub-partition) only
+// march and emit node planes (slots + fixed-order sums between named barriers of their own).
+template <class T> struct AdjScatterWsCfg {
+    static constexpr int CONS = 192, PROD = 64, THREADS = CONS + PROD;
+    static constexpr int NBC = 64, NSRC = 9, NRAW = 18, MAXIT = 64, CAP = 512, NF = 6;
+    static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
+    static constexpr size_t SMEM = SMEM_RAW + sizeof(T) * Cfg<3>::NCOL * NSRC * NF;
+};
+
+template <class T>
+__global__ void __launch_bounds__(AdjScatterWsCfg<T>::THREADS, 1)
+    k_adj_scatter_ws(DevScene<T, 3> sc, PBuf<T, 3> P, SBuf<T, 3> Sb, const int* __restrict__ perm,
+                     const int* __restrict__ keys, const int* __restrict__ bstart, const int* __restrict__ bend,
+                     const int* __restrict__ lstart, const int* __restrict__ occ, const int* __restrict__ n_occ,
+                     T* __restrict__ partials, const DevStatus* st, int* __restrict__ wq)
+{
+    using C = Cfg<3>;
+    using S = AdjScatterWsCfg<T>;
+    constexpr int B = C::B, TE = C::TE, NF = S::NF, CAP = S::CAP, NBC = S::NBC, NSRC = S::NSRC, NRAW = S::NRAW;
+    constexpr int CONS = S::CONS;
+    constexpr int RX = 0, RA = 3, RI = 6, RL = 9; // raw rows: fx, a, inc, L (row-major a*3+b)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* raw = reinterpret_cast<T*>(smem_raw);                 // [2][NRAW][CAP]
+    T* slots = reinterpret_cast<T*>(smem_raw + S::SMEM_RAW); // [NCOL][NSRC][NF]
+    __shared__ int cnt_s[2][NBC];
+    __shared__ int4 desc_s[2]; // (Q, level, flags: 1 level done, 2 block done, 4 end, -)
+    __shared__ __align__(8) unsigned long long bar_full[2], bar_empty[2];
+    __shared__ int it_start[S::MAXIT], it_len[S::MAXIT], it_lvl[S::MAXIT], it_last[S::MAXIT]; // producers only
+    __shared__ int blk_s[4];                                                                   // w, Q, s0, nit
+    const int tid = threadIdx.x;
+    const int nocc = st->abort ? 0 : *n_occ;
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar_full[i], S::PROD);
+            mbar_init(&bar_empty[i], CONS / 32);
+        }
+    }
+    __syncthreads();
+
+    if (tid >= CONS) { // ================= producer warps =================
+        const int pt = tid - CONS;
+        const long long SI = P.S;
+        int w = 0;
+        if (pt == 0)
+            w = wq_first(wq);
+        int j = 0;
+        for (;;) {
+            if (pt == 0) {
+                blk_s[0] = w;
+                if (w < nocc) { // level starts -> work items (as k_adj_scatter_pipe3)
+                    const int Q = occ[w];
+                    const int s0 = bstart[Q], s1 = bend[Q];
+                    int lv[B + 1];
+                    int nxt = s1;
+                    lv[B] = s1 - s0;
+                    for (int z = B - 1; z >= 0; --z) {
+                        const int v = lstart[Q * (B + 1) + z];
+                        nxt = (v >= s0 && v < s1) ? v : nxt;
+                        lv[z] = nxt - s0;
+                    }
+                    int k = 0;
+                    for (int z = 0; z < B; ++z) {
+                        const int nl = lv[z + 1] - lv[z];
+                        const int nch = nl > 0 ? (nl + CAP - 1) / CAP : 1;
+                        for (int c = 0; c < nch; ++c) {
+                            if (k < S::MAXIT) {
+                                it_start[k] = lv[z] + c * CAP;
+                                it_len[k] = min(CAP, nl - c * CAP);
+                                it_lvl[k] = z;
+                                it_last[k] = c == nch - 1;
+                            }
+                            ++k;
+                        }
+                    }
+                    blk_s[1] = Q;
+                    blk_s[2] = s0;
+                    blk_s[3] = k > S::MAXIT ? 0 : k; // the forward refused this block already (far_flag)
+                    w = wq_next(wq, w);
+                }
+            }
+            named_bar(2, S::PROD);
+            const bool done = blk_s[0] >= nocc;
+            const int Q = blk_s[1], s0 = blk_s[2], nit = done ? 1 : blk_s[3];
+            for (int i = 0; i < nit; ++i, ++j) {
+                const int b = j & 1, u = j >> 1;
+                constexpr int RPT = CAP / S::PROD;
+                const int len = done ? 0 : it_len[i], base = s0 + (done ? 0 : it_start[i]);
+                int pr[RPT], kr[RPT];
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) {
+                    const int r = pt + e * S::PROD;
+                    pr[e] = r < len ? perm[base + r] : 0;
+                    kr[e] = r < len ? keys[base + r] : 0;
+                }
+                if (u > 0)
+                    mbar_wait<true>(&bar_empty[b], (u - 1) & 1);
+                if (done) {
+                    if (pt == 0)
+                        desc_s[b] = make_int4(-1, 0, 4, 0);
+                    mbar_arrive(&bar_full[b]);
+                    break;
+                }
+                cnt_s[b][pt] = 0; // PROD == NBC
+                named_bar(2, S::PROD);
+                T* rb = raw + b * NRAW * CAP;
+#pragma unroll
+                for (int e = 0; e < RPT; ++e) {
+                    const int r = pt + e * S::PROD;
+                    if (r < len) {
+                        const T* q = P.base + pr[e];
+                        const int g = base + r;
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            cp_async_t<T>(rb + (RX + a) * CAP + r, q + a * SI); // x (PLay field 0..2)
+                            cp_async_t<T>(rb + (RA + a) * CAP + r, Sb.a[a] + g);
+                            cp_async_t<T>(rb + (RI + a) * CAP + r, Sb.inc[a] + g);
+                        }
+#pragma unroll
+                        for (int k = 0; k < 9; ++k)
+                            cp_async_t<T>(rb + (RL + k) * CAP + r, Sb.L[k] + g);
+                        atomicAdd(&cnt_s[b][kr[e] & (NBC - 1)], 1);
+                    }
+                }
+                cp_async_commit();
+                cp_async_wait_all();
+                for (int r = pt; r < len; r += S::PROD) {
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const T uu = (rb[(RX + a) * CAP + r] - sc.origin[a]) * sc.inv_dh;
+                        rb[(RX + a) * CAP + r] = uu - dfloor<T>(uu - T(0.5));
+                    }
+                }
+                if (pt == 0)
+                    desc_s[b] = make_int4(Q, it_lvl[i], (it_last[i] ? 1 : 0) | (i == nit - 1 ? 2 : 0), 0);
+                mbar_arrive(&bar_full[b]);
+            }
+            if (done)
+                break;
+            named_bar(2, S::PROD);
+        }
+        if (wq && pt == 0) { // wq_finish
+            __threadfence();
+            if (atomicAdd(wq + 1, 1) == int(gridDim.x) - 1) {
+                atomicExch(wq, 0);
+                atomicExch(wq + 1, 0);
+            }
+        }
+        return;
+    }
+
+    // ================= consumers (k_adj_scatter_pipe3's lane mapping) =================
+    const int bc = tid / 3, o0 = tid % 3;
+    const bool mid = o0 == 1;
+    const T xoff = o0 == 0 ? T(1.5) : (o0 == 1 ? T(1) : T(0.5));
+    const int bc0 = bc >> C::LOGB, bc1 = bc & (B - 1);
+    const int lane = tid & 31;
+    T acc[3][3][NF];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+                acc[a][k][f] = T(0);
+    auto emit = [&](int z, int Q) {
+        named_bar(1, CONS); // the previous sums are done reading the slots
+#pragma unroll
+        for (int o1 = 0; o1 < 3; ++o1) {
+            const int ncol = (bc0 + o0) * TE + bc1 + o1;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                slots[(ncol * NSRC + o0 * 3 + o1) * NF + f] = acc[o1][0][f];
+                acc[o1][0][f] = acc[o1][1][f];
+                acc[o1][1][f] = acc[o1][2][f];
+                acc[o1][2][f] = T(0);
+            }
+        }
+        named_bar(1, CONS); // slots complete
+        T* part = partials + (size_t)Q * NF * C::TN;
+        for (int t = tid; t < C::NCOL * NF; t += CONS) {
+            const int c = t / NF, f = t - c * NF;
+            const int n0 = c / TE, n1 = c - n0 * TE;
+            T sum = T(0);
+#pragma unroll
+            for (int q = 0; q < NSRC; ++q) {
+                const int b0 = n0 - q / 3, b1 = n1 - q % 3;
+                if (b0 >= 0 && b0 < B && b1 >= 0 && b1 < B)
+                    sum += slots[(c * NSRC + q) * NF + f];
+            }
+            part[f * C::TN + z * C::NCOL + c] = sum; // the adjoint partial-tile layout (k_adj_grid)
+        }
+    };
+    for (int j = 0;; ++j) {
+        const int b = j & 1;
+        mbar_wait(&bar_full[b], (j >> 1) & 1);
+        const int4 d = desc_s[b];
+        if (d.z & 4)
+            break;
+        int kb, ke;
+        {
+            const int* cnt = cnt_s[b];
+            const int c0 = cnt[2 * lane], c1 = cnt[2 * lane + 1];
+            int v = c0 + c1;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, v, dd);
+                if (lane >= dd)
+                    v += t;
+            }
+            const int excl = v - c0 - c1;
+            const int src = bc >> 1;
+            const int e = __shfl_sync(0xffffffffu, excl, src);
+            const int a0 = __shfl_sync(0xffffffffu, c0, src);
+            const int a1 = __shfl_sync(0xffffffffu, c1, src);
+            kb = (bc & 1) ? e + a0 : e;
+            ke = kb + ((bc & 1) ? a1 : a0);
+        }
+        const T* R = raw + b * NRAW * CAP;
+        for (int k = kb; k < ke; ++k) {
+            const T fx = R[(RX + 0) * CAP + k], fy = R[(RX + 1) * CAP + k], fz = R[(RX + 2) * CAP + k];
+            T wx, dwx, wy[3], dwy[3], wz[3], dwz[3];
+            {
+                const T h = fx - xoff;
+                const T hh = h * h;
+                wx = mid ? T(0.75) - hh : T(0.5) * hh;
+                dwx = (mid ? -T(2) * h : h) * sc.inv_dh;
+            }
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                quad_w<T>(fy, q, sc.inv_dh, wy[q], dwy[q]);
+                quad_w<T>(fz, q, sc.inv_dh, wz[q], dwz[q]);
+            }
+            T av[3], iv[3], L[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                av[a] = R[(RA + a) * CAP + k];
+                iv[a] = R[(RI + a) * CAP + k];
+            }
+#pragma unroll
+            for (int q = 0; q < 9; ++q)
+                L[q] = R[(RL + q) * CAP + k];
+#pragma unroll
+            for (int o1 = 0; o1 < 3; ++o1) {
+                // grad phi = (p1 wz, p2 wz, pw dwz) with pw = wx wy, p1 = dwx wy, p2 = wx dwy
+                const T pw = wx * wy[o1], p1 = dwx * wy[o1], p2 = wx * dwy[o1];
+                T u[3], t[3], ui[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    u[a] = pw * av[a] + L[a * 3 + 0] * p1 + L[a * 3 + 1] * p2;
+                    t[a] = L[a * 3 + 2] * pw;
+                    ui[a] = pw * iv[a];
+                }
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        acc[o1][q][a] = acc[o1][q][a] + wz[q] * u[a] + dwz[q] * t[a];
+                        acc[o1][q][3 + a] = acc[o1][q][3 + a] - wz[q] * ui[a];
+                    }
+            }
+        }
+        __syncwarp();
+        if (lane == 0)
+            mbar_arrive(&bar_empty[b]);
+        if (d.z & 1)
+            emit(d.y, d.x);
+        if (d.z & 2) {
+            emit(B, d.x);
+            emit(B + 1, d.x);
+        }
+    }
+}
+
 // ---- K6: per node: sum partials, correction-chain VJP, momentum-update transpose ------------
 // a node's friction-gradient terms: at most one segment per Coulomb wall it lies in the band of
 template <class T, int D> struct FricAcc {
@@ -2289,6 +2566,8 @@ template <class T, int D> struct AdjWork {
     double* loss_acc = nullptr;
     int* slot_of_pid = nullptr;
     bool gvz[2] = {true, true}; // cot[b].grad_v is known zero (not stored)
+    // 3-D K5b: the warp-specialized march (default) or k_adj_scatter_pipe3 (MPM_K5B=pipe3, A/B)
+    bool k5b_ws = !(std::getenv("MPM_K5B") && std::getenv("MPM_K5B")[0] == 'p');
     std::vector<void*> allocs;
     bool ready = false;
     int64_t cap = 0;
@@ -2366,9 +2645,12 @@ template <class T, int D> struct AdjWork {
         cudaFuncSetAttribute(k_adj_g2pT_gather<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm5);
         cudaFuncSetAttribute(k_adj_p2gT<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm7);
         cudaFuncSetAttribute(k_adj_p2gT<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm7);
-        if constexpr (D == 3)
+        if constexpr (D == 3) {
             cudaFuncSetAttribute(k_adj_scatter_pipe3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(AdjScatterCfg<T>::SMEM));
+            cudaFuncSetAttribute(k_adj_scatter_ws<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(AdjScatterWsCfg<T>::SMEM));
+        }
         (void)c;
     }
 
@@ -2532,6 +2814,15 @@ template <class T, int D> struct AdjWork {
             });
         const int tpb = D == 2 ? 160 : 256;
         if constexpr (D == 3) {
+            if (!c.has_aff && k5b_ws) { // warp-specialized column march (as the forward P2G)
+                using SW = AdjScatterWsCfg<T>;
+                c.launch("k_adj_scatter", [&] {
+                    k_adj_scatter_ws<T><<<c.nsm, SW::THREADS, SW::SMEM, c.stream>>>(
+                        c.sc, Pin, sb, c.perm, c.keys_sorted, c.bstart, c.bend, c.lstart, c.occ, c.counts, partials,
+                        c.st, c.wq_ptr(WQ_K5B));
+                });
+                return;
+            }
             if (!c.has_aff) { // pipelined column march (as the forward P2G)
                 using SC = AdjScatterCfg<T>;
                 c.launch("k_adj_scatter", [&] {

@@ -1,7 +1,8 @@
-"""3-D P2G implementations agree bit for bit: the warp-specialized kernel (k_p2g_ws, producer
-warpgroup + consumer warps on mbarriers) against k_p2g_pipe3 -- same per-particle arithmetic, same
-partial tiles, same fixed combine order. Both are checked against the oracle through
-the pipe3 default elsewhere (test_gpu_forward.py), so equality here carries parity over."""
+"""3-D column-march implementations agree bit for bit: the warp-specialized kernels (k_p2g_ws and
+K5b's k_adj_scatter_ws: producer warps + consumer warps on mbarriers) against the CTA-barrier
+pipelines k_p2g_pipe3 / k_adj_scatter_pipe3 -- same per-particle arithmetic, same partial tiles,
+same fixed combine order. The defaults are checked against the oracle elsewhere
+(test_gpu_forward.py, test_gpu_adjoint.py), so equality here covers the A/B paths too."""
 import numpy as np
 import pytest
 
@@ -77,3 +78,26 @@ def test_ws_bitwise_equals_pipe3_c4(monkeypatch):
     b = run(s, st, "ws", 4, monkeypatch)
     for f in FIELDS:
         assert np.array_equal(getattr(a.particles, f), getattr(b.particles, f)), f
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("case", ["dp3-coulomb-obstacle", "fluid3-flip", "dense-chunks"])
+def test_k5b_ws_bitwise_equals_pipe3(case, dtype, monkeypatch):
+    """backprop_trajectory (forward sweep, replays, VJPs) with K5b on either kernel"""
+    s, st = CASES[case](dtype)
+    N = 4
+    got = []
+    for impl in ("ws", "pipe3"):
+        monkeypatch.setenv("MPM_K5B", impl)
+        c = Context(s, st.particles.size())
+        c.upload(st)
+        c.advance(N)
+        tgt = c.download(st.copy()).particles.x + 0.01
+        c0, pg, r = c.backprop(st, N, 2, {"field": "x", "obs_steps": [N], "sel": None, "target": tgt[None]})
+        got.append((c0, pg, r.loss))
+        c.close()
+    (a, pa, la), (b, pb, lb) = got
+    assert la == lb
+    for f in ("x", "v", "sigma", "rho", "volume"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert np.array_equal(pa.flat(), pb.flat())
