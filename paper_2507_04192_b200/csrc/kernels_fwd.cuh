@@ -1210,22 +1210,18 @@ __global__ void __launch_bounds__(Pipe3Cfg<T, WIDE, NGR>::THREADS, 1)
 // ---- 3-D P2G, warp-specialized (PIC / FLIP / blend) ---------------------------------------
 // The same per-particle arithmetic, node fields, partial tiles and fixed combine order as
 // k_p2g_pipe3 (bit-identical output), with the work split by role instead of by phase:
-//   producer warpgroup (4 warps, 56 registers): pulls occupied blocks from the work counter,
-//     builds their (level, chunk) item lists, gathers each item's particle fields through the
-//     sort permutation with cp.async into one of two record buffers, and -- while those copies
-//     land -- does the fixed-order 9-source sums of the node planes the consumers finished (slot
-//     buffer -> the block's partial tile); then converts the records (fractional offset, m v,
-//     V sigma), counts the node columns and publishes the item on an mbarrier;
-//   consumer warps (the pipe3 lane mapping, 152 registers): wait for an item, march it (FP64),
-//     release the buffer; after a finished node plane, write their accumulators to one of two
-//     slot buffers and release it to the producers.
-// No CTA-wide barrier after the setup: the roles meet only on mbarriers (full/empty pairs for the
-// record buffers and for the slot buffers).
-// Registers (f64): 512 threads start at 128; setmaxnreg moves the producers' release (128 x 72)
-// to the consumers (384 x 24). The register file is split over the 4 SM sub-partitions (16384
-// each, warps assigned round-robin), so each holds 3 consumer warps and 1 producer warp:
-// 3 x 152 + 56 = 512 registers per lane slot. (A 17th warp would put 5 warps on one sub-partition
-// and cap every thread at 96: MEASURED, a separate reducer warp needs a 5th warp there.)
+//   producer warps (f64: 2, f32: 4): pull occupied blocks from the work counter, build their
+//     (level, chunk) item lists, gather each item's particle fields through the sort permutation
+//     with cp.async into one of two record buffers, convert them (fractional offset, m v, V sigma),
+//     count the node columns and publish the item on an mbarrier (full/empty pair per buffer);
+//   consumer warps (the pipe3 lane mapping, 6 warps): wait for an item, march it (FP64), release
+//     the buffer, and emit finished node planes: slot writes, then the fixed-order 9-source sums
+//     into the block's partial tile, between two named barriers of the consumers only.
+// No CTA-wide barrier after the setup. Variants kept for A/B (macros): WS_NG=2 splits the 7 node
+// fields over two consumer groups (12 warps at 152 registers: setmaxnreg moves 128 x 72 registers
+// from a 4-warp producer warpgroup; the register file is split over the 4 SM sub-partitions,
+// 16384 each, warps round-robin, so 3 x 152 + 56 = 512 per lane slot); WS_PRED=1 has the
+// producers do the plane sums (two slot buffers).
 // MEASURED (C4 f64): pipe3 0.47 ms with the FP64 pipe 37% busy, the march ~60% of its cycles;
 // this kernel 0.41 ms, FP64 45%, shared wavefronts 34% of peak. Tried and slower (same-box A/B,
 // phase clocks in tools/p2g_clocks.py): the sums on the producers (PRED, 0.402 vs 0.388 ms), on
@@ -1305,15 +1301,25 @@ __device__ __forceinline__ void named_bar(int id, int count)
 #ifndef WS_PREFETCH_LATE
 #define WS_PREFETCH_LATE 0
 #endif
+// Shape (A/B on one box, C4): f64 one field group (6 consumer warps, 63 accumulators, ~200
+// registers) + 2 producer warps 0.378 ms; two field groups (12 consumer warps at 152 registers via
+// setmaxnreg) + 4 producer warps 0.406 ms; one group + 4 producer warps 0.531 ms (320 threads cap
+// the consumers at 168 registers: spills). f32: one group + 4 producer warps 0.268 ms, + 2: 0.285.
+#ifndef WS_NG
+#define WS_NG 1
+#endif
+#ifndef WS_PROD1
+#define WS_PROD1 0 // 0: 64 (f64) / 128 (f32)
+#endif
 template <class T> struct WsCfg {
-    using P3 = Pipe3Cfg<T, false>;
+    using P3 = Pipe3Cfg<T, false, WS_NG>;
     static constexpr int NG = P3::NG, NA = P3::NA;
     static constexpr int CONS = 192 * NG;  // consumer threads (f64: 12 warps, f32: 6)
-    static constexpr int PROD = 128; // one warpgroup
+    static constexpr int PROD = NG == 1 ? (WS_PROD1 ? WS_PROD1 : sizeof(T) == 8 ? 64 : 128) : 128; // producer threads
     static constexpr int THREADS = CONS + PROD;
     static constexpr bool REALLOC = WS_REALLOC && CONS % 128 == 0;
     static constexpr int WPS = (THREADS / 32 + 3) / 4; // warps per SM sub-partition
-    static constexpr int BASE_REGS = (512 / WPS) / 8 * 8, PROD_REGS = WS_PROD_REGS, CONS_REGS = 152;
+    static constexpr int BASE_REGS = (512 / WPS) / 8 * 8 > 255 ? 255 : (512 / WPS) / 8 * 8, PROD_REGS = WS_PROD_REGS, CONS_REGS = 152;
     static_assert(!REALLOC || CONS * (CONS_REGS - BASE_REGS) <= PROD * (BASE_REGS - PROD_REGS), "register pool");
     static_assert(!REALLOC || (WPS == 4 && 3 * CONS_REGS + PROD_REGS <= 512), "sub-partition register file");
     // PRED: the producers sum the finished node planes (two slot buffers, so CAP 512: f64
