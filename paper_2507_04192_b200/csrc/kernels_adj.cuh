@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
             break;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
+        int src_nx = s0 + int(threadIdx.x) < s1 ? perm[s0 + threadIdx.x] : 0; // in flight during the tile load
         int qc[D];
         block_coords<D>(Q, sc.nb, qc);
         for (int t = threadIdx.x; t < TN; t += blockDim.x) {
@@ -450,11 +451,14 @@ __global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf
             w_s = wq_next(wq, w);
         T c_acc = T(0), mu_acc = T(0);
         const T idh2 = sc.inv_dh * sc.inv_dh;
-        // process the segment in rounds so every thread reaches the block reductions
+        // process the segment in rounds so every thread reaches the block reductions; the next
+        // round's permutation entry is loaded one round ahead (the first one before the tile load)
         for (int base = s0; base < s1; base += blockDim.x) {
             const int i = base + threadIdx.x;
+            const int src_cur = src_nx;
+            src_nx = i + int(blockDim.x) < s1 ? perm[i + blockDim.x] : 0;
             if (i < s1) {
-                const int src = perm[i];
+                const int src = src_cur;
                 T x[D];
 #pragma unroll
                 for (int a = 0; a < D; ++a)
@@ -1914,6 +1918,7 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
             break;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
+        int src_nx = s0 + int(threadIdx.x) < s1 ? perm[s0 + threadIdx.x] : 0; // in flight during the tile load
         int qc[D];
         block_coords<D>(Q, sc.nb, qc);
         for (int t = threadIdx.x; t < TN; t += blockDim.x) {
@@ -1944,7 +1949,8 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
         if (threadIdx.x == 0) // every thread read w_s before the barrier above
             w_s = wq_next(wq, w);
         for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
-            const int src = perm[i];
+            const int src = src_nx; // perm[i], loaded one iteration ahead
+            src_nx = i + int(blockDim.x) < s1 ? perm[i + blockDim.x] : 0;
             T x[D], v[D], sig[D][D];
 #pragma unroll
             for (int a = 0; a < D; ++a) {
