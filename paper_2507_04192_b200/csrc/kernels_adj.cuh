@@ -394,8 +394,11 @@ __device__ __forceinline__ void stencil_moments(const T* __restrict__ f, int t0,
 // t) by src = perm[i] (the storage slot of S^t). Both are streamed, not gathered through ids.
 // GVZ: co.grad_v is known zero (FLIP/PIC chains and seeded losses) and ci.grad_v is left to the
 // caller's zero flag unless TPIC accumulates into it in K7.
+#ifndef K5A_MINB
+#define K5A_MINB 1 // MEASURED C4: 2 CTAs per SM (128 registers, 312 B of spills) 0.873 ms vs 0.837
+#endif
 template <class T, int D, bool APIC>
-__global__ void __launch_bounds__(256) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf<T, D> Pin, GBuf<T, D> G,
+__global__ void __launch_bounds__(256, K5A_MINB) k_adj_g2pT_gather(DevScene<T, D> sc, PBuf<T, D> Pin, GBuf<T, D> G,
                                                          const int* __restrict__ perm, const int* __restrict__ bstart,
                                                          const int* __restrict__ bend, const int* __restrict__ occ,
                                                          const int* __restrict__ n_occ, CBuf<T, D> co, CBuf<T, D> ci,
