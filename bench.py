@@ -179,6 +179,15 @@ class ClockSampler:
         self.index = index
         self.samples = []
         self.proc = None
+        self.first = 0
+
+    def ready(self, timeout=5.0):
+        """wait until nvidia-smi delivers its first line (its start-up can take longer than a short
+        timed region), then mark where the timed region's samples begin"""
+        t0 = time.time()
+        while self.proc and not self.samples and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        self.first = len(self.samples)
 
     def start(self):
         try:
@@ -203,16 +212,20 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
-        sm = [float(p[0]) for p in self.samples if p[0].replace(".", "").isdigit()]
-        mx = [float(p[1]) for p in self.samples if p[1].replace(".", "").isdigit()]
+        # the samples taken during the timed region (plus the one just before it when the region
+        # was shorter than the 100 ms sampling period)
+        region = self.samples[max(self.first - 1, 0):] if self.samples else []
+        sm = [float(p[0]) for p in region if p[0].replace(".", "").isdigit()]
+        mx = [float(p[1]) for p in region if p[1].replace(".", "").isdigit()]
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for p in self.samples:
+        for p in region:
             for k, nme in enumerate(names):
                 if p[3 + k].lower() in ("active", "1"):
                     reasons.add(nme)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+                "reasons": sorted(reasons), "samples": len(region),
+                "samples_in_region": len(self.samples) - self.first}
 
 
 # ---- CPU baseline (the reference on host cores) --------------------------------------------
@@ -527,7 +540,7 @@ def bench_b200(a, rank, world, local):
     # ---- device-resident timed region
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.3)
+    clocks.ready()
     l0 = ctx.launch_count()
     barrier()
     ms = ctx.advance_timed(a.steps, nan_guard=True)  # run()'s per-step all_finite guard (stepper.hpp:106-109)
@@ -686,7 +699,7 @@ def bench_slab(a, rank, world, local):
     stp.advance(a.warmup)
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.3)
+    clocks.ready()
     l0 = dom.ctx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
@@ -790,7 +803,7 @@ def bench_dist(a, rank, world, local):
     rk.advance(a.warmup)
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.3)
+    clocks.ready()
     l0 = rk.ctx.launch_count()
     dist.barrier()
     torch.cuda.synchronize()
