@@ -1790,6 +1790,20 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf
                 }
             }
         }
+        // every source's bstart entry loaded up front (independent loads in flight together)
+        int bsrc[1 << D];
+#pragma unroll
+        for (int s = 0; s < (1 << D); ++s) {
+            int Qid = 0;
+            bool okb = MODE != ADJ_BAND_LOAD && mine;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int Qa = qc[a] - ((s >> (D - 1 - a)) & 1);
+                okb &= Qa >= 0 && Qa < sc.nb[a];
+                Qid = Qid * sc.nb[a] + Qa;
+            }
+            bsrc[s] = okb ? bstart[Qid] : -1;
+        }
 #pragma unroll
         for (int s = 0; s < (MODE == ADJ_BAND_LOAD ? 0 : (1 << D)); ++s) {
             if (!mine)
@@ -1808,7 +1822,7 @@ __global__ void __launch_bounds__(Cfg<D>::NB) k_adj_grid(DevScene<T, D> sc, GBuf
                 else
                     colx = colx * C::TE + t;
             }
-            if (!ok || bstart[Qid] < 0)
+            if (!ok || bsrc[s] < 0)
                 continue;
             const T* part = partials + (size_t)Qid * NF * C::TN + z * C::NCOL + colx;
 #pragma unroll
