@@ -389,6 +389,11 @@ __device__ __forceinline__ void stencil_moments(const T* __restrict__ f, int t0,
 }
 
 // ---- K5a: G2P-transpose gather + constitutive VJP ------------------------------------------
+template <int D> struct K5aStage { // staged rows per thread (K5a, below)
+    static constexpr int CSIG = 0, CRHO = D * D, CV = CRHO + 1, RHO = CV + 1, VOL = RHO + 1, SIG = VOL + 1,
+                         SZZ = SIG + Cfg<D>::NS, CSZZ = SZZ + 1, N = CSZZ + 1;
+    template <class T> static constexpr size_t smem() { return sizeof(T) * (2 * D * Cfg<D>::TN + N * 256); }
+};
 // Cotangents live in state-storage order: co (cot at t+1) is indexed by the sorted slot i (the
 // storage order of S^{t+1}, which the forward G2P wrote in this step's sort order) and ci (cot at
 // t) by src = perm[i] (the storage slot of S^t). Both are streamed, not gathered through ids.
@@ -409,6 +414,12 @@ __global__ void __launch_bounds__(256, K5A_MINB) k_adj_g2pT_gather(DevScene<T, D
     constexpr int TE = C::TE, TN = C::TN;
     extern __shared__ unsigned char smem_raw[];
     T* tile = reinterpret_cast<T*>(smem_raw); // [2D][TN]: v, v - v_old
+    // the constitutive-transpose inputs of the thread's particle (co.sigma, co.rho, co.V, rho, V,
+    // sigma[, szz]) are fetched with cp.async at the top of the iteration into this thread's column
+    // and read after the stencil moments, so their latency overlaps the moments without holding
+    // registers (K5a runs one CTA per SM at ~216 registers)
+    using KS = K5aStage<D>;
+    T* kst = tile + 2 * D * TN + threadIdx.x; // [KS::N][256]
     __shared__ T red[256];
     __shared__ int w_s; // next list entry (work counter, common.cuh)
     const int nocc = st->abort ? 0 : *n_occ; // every CTA still passes wq_finish
@@ -462,6 +473,25 @@ __global__ void __launch_bounds__(256, K5A_MINB) k_adj_g2pT_gather(DevScene<T, D
             src_nx = i + int(blockDim.x) < s1 ? perm[i + blockDim.x] : 0;
             if (i < s1) {
                 const int src = src_cur;
+                {
+#pragma unroll
+                    for (int k = 0; k < D * D; ++k)
+                        cp_async_t<T>(kst + (KS::CSIG + k) * 256, co.sig[k] + i);
+                    cp_async_t<T>(kst + KS::CRHO * 256, co.rho + i);
+                    cp_async_t<T>(kst + KS::CV * 256, co.V + i);
+                    cp_async_t<T>(kst + KS::RHO * 256, Pin.rho + src);
+                    cp_async_t<T>(kst + KS::VOL * 256, Pin.V + src);
+                    if (sc.material != 0) {
+#pragma unroll
+                        for (int q = 0; q < Cfg<D>::NS; ++q)
+                            cp_async_t<T>(kst + (KS::SIG + q) * 256, Pin.sig[q] + src);
+                        if constexpr (D == 2)
+                            cp_async_t<T>(kst + KS::SZZ * 256, Pin.szz + src);
+                    }
+                    if constexpr (D == 2)
+                        cp_async_t<T>(kst + KS::CSZZ * 256, co.szz + i);
+                    cp_async_commit();
+                }
                 T x[D];
 #pragma unroll
                 for (int a = 0; a < D; ++a)
@@ -555,28 +585,29 @@ __global__ void __launch_bounds__(256, K5A_MINB) k_adj_g2pT_gather(DevScene<T, D
                     }
                 }
                 // (1) constitutive transpose (adjoint.hpp:374-400)
+                cp_async_wait_all(); // the staged inputs above
                 T sgc[D * D], gvn_c[D * D], sig_in_c[D * D];
 #pragma unroll
                 for (int k = 0; k < D * D; ++k) {
-                    sgc[k] = co.sig[k][i];
+                    sgc[k] = kst[(KS::CSIG + k) * 256];
                     gvn_c[k] = T(0);
                     sig_in_c[k] = T(0);
                 }
                 T rho_in_c = T(0), V_in_c = T(0), szz_in_c = T(0);
-                const T rho = Pin.rho[src], V = Pin.V[src];
+                const T rho = kst[KS::RHO * 256], V = kst[KS::VOL * 256];
+                const T co_rho = kst[KS::CRHO * 256], co_V = kst[KS::CV * 256];
                 if (sc.material == 0) {
-                    fluid_vjp_dev<T, D>(sc, rho, V, L, sgc, co.rho[i], co.V[i], gvn_c, rho_in_c, V_in_c, c_acc,
-                                        mu_acc);
+                    fluid_vjp_dev<T, D>(sc, rho, V, L, sgc, co_rho, co_V, gvn_c, rho_in_c, V_in_c, c_acc, mu_acc);
                 } else {
                     T Sm[3][3];
 #pragma unroll
                     for (int a = 0; a < 3; ++a)
 #pragma unroll
                         for (int b = 0; b < 3; ++b)
-                            Sm[a][b] = (a < D && b < D) ? Pin.sig[sym_idx<D>(a, b)][src] : T(0);
-                    if (D == 2)
-                        Sm[2][2] = Pin.szz[src];
-                    dp_vjp_dev<T, D>(sc, Sm, L, sgc, D == 2 ? co.szz[i] : T(0), co.rho[i], co.V[i], rho, V,
+                            Sm[a][b] = (a < D && b < D) ? kst[(KS::SIG + sym_idx<D>(a, b)) * 256] : T(0);
+                    if constexpr (D == 2)
+                        Sm[2][2] = kst[KS::SZZ * 256];
+                    dp_vjp_dev<T, D>(sc, Sm, L, sgc, D == 2 ? kst[KS::CSZZ * 256] : T(0), co_rho, co_V, rho, V,
                                      gvn_c, sig_in_c, szz_in_c, rho_in_c, V_in_c);
                 }
                 // cot_out.grad_v joins (adjoint.hpp:398-400)
@@ -2663,7 +2694,7 @@ template <class T, int D> struct AdjWork {
     {
         if (!ready)
             return;
-        const int sm5 = int(sizeof(T) * 2 * D * C::TN), sm7 = int(sizeof(T) * (1 + 2 * D) * C::TN);
+        const int sm5 = int(K5aStage<D>::template smem<T>()), sm7 = int(sizeof(T) * (1 + 2 * D) * C::TN);
         cudaFuncSetAttribute(k_adj_g2pT_gather<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm5);
         cudaFuncSetAttribute(k_adj_g2pT_gather<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm5);
         cudaFuncSetAttribute(k_adj_p2gT<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm7);
@@ -2820,7 +2851,7 @@ template <class T, int D> struct AdjWork {
     {
         auto& Pin = c.buf[c.cur];
         const unsigned gr = c.persistent(4);
-        const size_t sm5 = sizeof(T) * 2 * D * C::TN;
+        const size_t sm5 = K5aStage<D>::template smem<T>();
         const int gvw = c.sc.tpic ? 1 : 0; // only TPIC accumulates a grad_v cotangent (K7)
         gvz[bi] = !gvw;
         if (c.has_aff)
