@@ -392,7 +392,8 @@ __device__ __forceinline__ void stencil_moments(const T* __restrict__ f, int t0,
 template <int D> struct K5aStage { // staged rows per thread (K5a, below)
     static constexpr int CSIG = 0, CRHO = D * D, CV = CRHO + 1, RHO = CV + 1, VOL = RHO + 1, SIG = VOL + 1,
                          SZZ = SIG + Cfg<D>::NS, CSZZ = SZZ + 1, N = CSZZ + 1;
-    template <class T> static constexpr size_t smem() { return sizeof(T) * (2 * D * Cfg<D>::TN + N * 256); }
+    static constexpr int NX = 3 * D; // + 2 slots of (x, co.v, co.x) of the next round's particle
+    template <class T> static constexpr size_t smem() { return sizeof(T) * (2 * D * Cfg<D>::TN + (N + 2 * NX) * 256); }
 };
 // Cotangents live in state-storage order: co (cot at t+1) is indexed by the sorted slot i (the
 // storage order of S^{t+1}, which the forward G2P wrote in this step's sort order) and ci (cot at
@@ -426,14 +427,27 @@ __global__ void __launch_bounds__(256, K5A_MINB) k_adj_g2pT_gather(DevScene<T, D
     if (threadIdx.x == 0)
         w_s = wq_first(wq);
     const T alpha = sc.alpha;
+    // x, co.v and co.x of the thread's next particle: cp.async one round ahead into slot (slot ^ 1)
+    auto issue_x = [&](int slot, int src, int i) {
+        T* b = kst + (KS::N + slot * KS::NX) * 256;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            cp_async_t<T>(b + a * 256, Pin.x[a] + src);
+            cp_async_t<T>(b + (D + a) * 256, co.v[a] + i);
+            cp_async_t<T>(b + (2 * D + a) * 256, co.x[a] + i);
+        }
+    };
     for (;;) {
+        cp_async_wait_all();
         __syncthreads(); // w_s published; the previous block's shared-memory readers are done
         const int w = w_s;
         if (w >= nocc)
             break;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
-        int src_nx = s0 + int(threadIdx.x) < s1 ? perm[s0 + threadIdx.x] : 0; // in flight during the tile load
+        // the first two rounds' permutation entries in flight during the tile load
+        const int i0 = s0 + int(threadIdx.x);
+        int src_a = i0 < s1 ? perm[i0] : 0, src_b = i0 + int(blockDim.x) < s1 ? perm[i0 + blockDim.x] : 0;
         int qc[D];
         block_coords<D>(Q, sc.nb, qc);
         for (int t = threadIdx.x; t < TN; t += blockDim.x) {
@@ -460,17 +474,27 @@ __global__ void __launch_bounds__(256, K5A_MINB) k_adj_g2pT_gather(DevScene<T, D
                 tile[(D + a) * TN + t] = vn - vo;
             }
         }
+        if (i0 < s1)
+            issue_x(0, src_a, i0);
+        cp_async_commit();
         __syncthreads();
         if (threadIdx.x == 0) // every thread read w_s before the barrier above
             w_s = wq_next(wq, w);
         T c_acc = T(0), mu_acc = T(0);
+        int xslot = 0;
         const T idh2 = sc.inv_dh * sc.inv_dh;
         // process the segment in rounds so every thread reaches the block reductions; the next
         // round's permutation entry is loaded one round ahead (the first one before the tile load)
         for (int base = s0; base < s1; base += blockDim.x) {
             const int i = base + threadIdx.x;
-            const int src_cur = src_nx;
-            src_nx = i + int(blockDim.x) < s1 ? perm[i + blockDim.x] : 0;
+            const int src_cur = src_a;
+            src_a = src_b;
+            src_b = i + 2 * int(blockDim.x) < s1 ? perm[i + 2 * blockDim.x] : 0;
+            if (i + int(blockDim.x) < s1)
+                issue_x(xslot ^ 1, src_a, i + blockDim.x);
+            cp_async_commit();
+            const T* xs = kst + (KS::N + xslot * KS::NX) * 256;
+            xslot ^= 1;
             if (i < s1) {
                 const int src = src_cur;
                 {
@@ -492,10 +516,12 @@ __global__ void __launch_bounds__(256, K5A_MINB) k_adj_g2pT_gather(DevScene<T, D
                         cp_async_t<T>(kst + KS::CSZZ * 256, co.szz + i);
                     cp_async_commit();
                 }
+                // pending: this particle's x group, the next one's, and the group above
+                asm volatile("cp.async.wait_group 2;\n" ::: "memory");
                 T x[D];
 #pragma unroll
                 for (int a = 0; a < D; ++a)
-                    x[a] = Pin.x[a][src];
+                    x[a] = xs[a * 256];
                 T w[D][3], dw[D][3];
                 int tb[D];
 #pragma unroll
@@ -516,8 +542,8 @@ __global__ void __launch_bounds__(256, K5A_MINB) k_adj_g2pT_gather(DevScene<T, D
                 T vc[D], xc[D], pic[D], inc[D], xp[D];
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
-                    vc[a] = co.v[a][i];
-                    xc[a] = co.x[a][i];
+                    vc[a] = xs[(D + a) * 256];
+                    xc[a] = xs[(2 * D + a) * 256];
                     pic[a] = (T(1) - alpha) * vc[a] + sc.dt * xc[a];
                     inc[a] = alpha * vc[a];
                     xp[a] = T(0);
