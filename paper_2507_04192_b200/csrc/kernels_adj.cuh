@@ -1981,18 +1981,31 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
     constexpr int TE = C::TE, TN = C::TN; // tile fields: 1 + 2 D
     extern __shared__ unsigned char smem_raw[];
     T* tile = reinterpret_cast<T*>(smem_raw); // [NF][TN]: gm, gmom[D], gf[D]
+    // x and v of the thread's next particle: cp.async one iteration ahead into slot (slot ^ 1)
+    constexpr int NT = 256;
+    T* xst = tile + (1 + 2 * D) * TN + threadIdx.x; // [2][2D][NT]
+    auto issue_x = [&](int slot, int src) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            cp_async_t<T>(xst + (slot * 2 * D + a) * NT, Pin.x[a] + src);
+            cp_async_t<T>(xst + (slot * 2 * D + D + a) * NT, Pin.v[a] + src);
+        }
+    };
     __shared__ int w_s; // next list entry (work counter, common.cuh)
     const int nocc = st->abort ? 0 : *n_occ; // every CTA still passes wq_finish
     if (threadIdx.x == 0)
         w_s = wq_first(wq);
     for (;;) {
+        cp_async_wait_all();
         __syncthreads(); // w_s published; the previous block's shared-memory readers are done
         const int w = w_s;
         if (w >= nocc)
             break;
         const int Q = occ[w];
         const int s0 = bstart[Q], s1 = bend[Q];
-        int src_nx = s0 + int(threadIdx.x) < s1 ? perm[s0 + threadIdx.x] : 0; // in flight during the tile load
+        // the first two particles' permutation entries in flight during the tile load
+        const int i0 = s0 + int(threadIdx.x);
+        int src_a = i0 < s1 ? perm[i0] : 0, src_b = i0 + NT < s1 ? perm[i0 + NT] : 0;
         int qc[D];
         block_coords<D>(Q, sc.nb, qc);
         for (int t = threadIdx.x; t < TN; t += blockDim.x) {
@@ -2019,17 +2032,28 @@ __global__ void __launch_bounds__(256) k_adj_p2gT(DevScene<T, D> sc, PBuf<T, D> 
                 tile[(1 + D + a) * TN + t] = ok ? GC.gf[a][gi] : T(0);
             }
         }
+        if (i0 < s1)
+            issue_x(0, src_a);
+        cp_async_commit();
         __syncthreads();
         if (threadIdx.x == 0) // every thread read w_s before the barrier above
             w_s = wq_next(wq, w);
-        for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
-            const int src = src_nx; // perm[i], loaded one iteration ahead
-            src_nx = i + int(blockDim.x) < s1 ? perm[i + blockDim.x] : 0;
+        int xslot = 0;
+        for (int i = i0; i < s1; i += NT) {
+            const int src = src_a; // perm[i]
+            src_a = src_b;
+            src_b = i + 2 * NT < s1 ? perm[i + 2 * NT] : 0;
+            if (i + NT < s1)
+                issue_x(xslot ^ 1, src_a);
+            cp_async_commit();
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory"); // this particle's x, v landed
+            const T* xs = xst + xslot * 2 * D * NT;
+            xslot ^= 1;
             T x[D], v[D], sig[D][D];
 #pragma unroll
             for (int a = 0; a < D; ++a) {
-                x[a] = Pin.x[a][src];
-                v[a] = Pin.v[a][src];
+                x[a] = xs[a * NT];
+                v[a] = xs[(D + a) * NT];
             }
 #pragma unroll
             for (int a = 0; a < D; ++a)
@@ -2720,7 +2744,7 @@ template <class T, int D> struct AdjWork {
     {
         if (!ready)
             return;
-        const int sm5 = int(K5aStage<D>::template smem<T>()), sm7 = int(sizeof(T) * (1 + 2 * D) * C::TN);
+        const int sm5 = int(K5aStage<D>::template smem<T>()), sm7 = int(sizeof(T) * ((1 + 2 * D) * C::TN + 2 * 2 * D * 256));
         cudaFuncSetAttribute(k_adj_g2pT_gather<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm5);
         cudaFuncSetAttribute(k_adj_g2pT_gather<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm5);
         cudaFuncSetAttribute(k_adj_p2gT<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm7);
@@ -2932,7 +2956,7 @@ template <class T, int D> struct AdjWork {
     {
         auto& Pin = c.buf[c.cur];
         const unsigned gr = c.persistent(4);
-        const size_t sm7 = sizeof(T) * (1 + 2 * D) * C::TN;
+        const size_t sm7 = sizeof(T) * ((1 + 2 * D) * C::TN + 2 * 2 * D * 256); // tile + 2 slots of (x, v)
         const bool aff = c.has_aff || c.sc.tpic;
         if (aff)
             c.launch("k_adj_p2gT", [&] {
