@@ -38,6 +38,9 @@
 namespace mpmgpu {
 
 constexpr int INC_THREADS = 256; // k_inc_block CTA size
+#ifndef INC_UNR
+#define INC_UNR 4 // old-range keys in flight per thread in k_inc_block (MEASURED C4: 8 is slower, 21.0 vs 18.9 us)
+#endif
 constexpr int INC_WARPS = INC_THREADS / 32;
 
 // scratch of the incremental sort, owned by the context (self-cleaning: every counter the
@@ -371,16 +374,16 @@ __global__ void __launch_bounds__(INC_THREADS) k_inc_block(const int* __restrict
                 sm.m.cu_k[q] = keys[idx];
             }
         }
-        for (int r0 = 0; r0 < nrange; r0 += 4 * INC_THREADS) {
-            int kk[4], oo[4];
+        for (int r0 = 0; r0 < nrange; r0 += INC_UNR * INC_THREADS) {
+            int kk[INC_UNR], oo[INC_UNR];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) { // four independent loads in flight per thread
+            for (int j = 0; j < INC_UNR; ++j) { // independent loads in flight per thread
                 const int r = r0 + j * INC_THREADS + tid;
                 kk[j] = r < nrange ? keys[os + r] : 0;
                 oo[j] = r < nrange ? okeys[os + r] : 0;
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < INC_UNR; ++j) {
                 const int r = r0 + j * INC_THREADS + tid;
                 const int k = kk[j];
                 const bool ex = r < nrange && k != oo[j];
