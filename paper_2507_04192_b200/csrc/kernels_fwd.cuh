@@ -1293,6 +1293,9 @@ __device__ __forceinline__ void named_bar(int id, int count)
 #ifndef WS_PRED
 #define WS_PRED 0
 #endif
+#ifndef WS_CAP
+#define WS_CAP 576 // records per item (a multiple of 16: the swizzle groups). MEASURED C4 f64 P2G: 640 0.378 ms, 576 0.347, 512 0.347, 448 0.435, 384 0.451 (a C4 level holds 512 particles: below that every level splits), 256 0.392
+#endif
 #ifndef WS_PREFETCH_REC
 #define WS_PREFETCH_REC 0 // next record in registers during the march: MEASURED f64 0.390 vs 0.380 ms, f32 equal
 #endif
@@ -1331,7 +1334,7 @@ template <class T> struct WsCfg {
     // barriers of their own, from one slot buffer. MEASURED C4 f64: consumers 0.388 ms, producers
     // 0.402 ms (their sums' shared-memory traffic slows the overlapping march by ~25%).
     static constexpr bool PRED = WS_PRED;
-    static constexpr int NBC = 64, NSRC = 9, NRAW = 14, MAXIT = 64, CAP = PRED ? 512 : 640, NSLOT = PRED ? 2 : 1;
+    static constexpr int NBC = 64, NSRC = 9, NRAW = 14, MAXIT = 64, CAP = PRED ? 512 : WS_CAP, NSLOT = PRED ? 2 : 1;
     static constexpr int SLOT = SLOT3_SIZE; // values per slot buffer
     static constexpr size_t SMEM_RAW = sizeof(T) * 2 * NRAW * CAP;
     static constexpr size_t SMEM = SMEM_RAW + sizeof(T) * NSLOT * SLOT;
